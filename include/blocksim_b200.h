@@ -1,0 +1,292 @@
+/*
+ * blocksim_b200.h — C-ABI of the B200-native what-if simulation core.
+ *
+ * This is the drop-in boundary for Block's predictive-dispatch hot path
+ * (arXiv 2508.03611, reference implementation "blocksim"):
+ *
+ *   reference interface                                   replaced by
+ *   ----------------------------------------------------  ------------------------------
+ *   predict()            core/src/predictor.cpp:76-137     bsg_predict_batch[_device]
+ *   predict_across()     core/src/predictor.cpp:139-157    bsg_predict_batch (1 scenario
+ *                                                          per snapshot, same candidate)
+ *   PredictorClient::predict_across (scheduler.h:56-61)    bsg_predict_batch via the C++
+ *                                                          GpuPredictorClient
+ *   Dispatcher::dispatch BlockPredictive argmin
+ *                        core/src/scheduler.cpp:115-152    bsg_dispatch / bsg_dispatch_mc
+ *   Instance::execute_step loop (per-step StepResult)
+ *                        core/src/backend.cpp:338-349      bsg_trace (parity/trace mode)
+ *   InstanceConfig + CostModelParams  types.h:46-66         bsg_instance_cfg
+ *   LatencyCache modes   core/src/predictor.cpp:26-54      bsg_instance_cfg.cache_mode
+ *   SnapshotRequest / InstanceSnapshot types.h:75-94        bsg_entries (SoA) + bsg_scenario
+ *   PredictionResult     predictor.h:28-36                 bsg_result (integer ns ticks)
+ *
+ * Conventions: plain pointers and sizes, no exceptions, no torch types.
+ * Every call returns a bsg_status; per-scenario failures are reported in
+ * bsg_result.status with the reference's error taxonomy (error.h:31-56).
+ * Times are integer nanosecond ticks (SimTime, time.h:14-42); the reference's
+ * double seconds are ticks * 1e-9 (time.h:25), reproduced bit-exactly by
+ * bsg_ticks_to_seconds().
+ */
+#ifndef BLOCKSIM_B200_H
+#define BLOCKSIM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BSG_ABI_VERSION 1
+
+typedef enum bsg_status {
+  BSG_OK = 0,
+  /* RequestTooLargeError("snapshot running set exceeds total memory blocks")
+   * backend.cpp:42-44 -> PredictionError("candidate does not fit ...") predictor.cpp:134-135 */
+  BSG_TOO_LARGE_RUNNING = 1,
+  /* RequestTooLargeError from Instance::admit of the candidate, backend.cpp:76-83 */
+  BSG_TOO_LARGE_CANDIDATE = 2,
+  /* DeadlockError backend.cpp:274-277 -> PredictionError predictor.cpp:132-133;
+   * detail = origin index of the deadlocked member */
+  BSG_DEADLOCK = 3,
+  /* PredictionError("forward simulation exceeded the step limit") predictor.cpp:125-127 */
+  BSG_STEP_LIMIT = 4,
+  /* PredictionError("candidate vanished from the forward simulation") predictor.cpp:102-104 */
+  BSG_VANISHED = 5,
+  /* EmptyPlanError backend.cpp:245 (not caught by predict: propagates as EmptyPlanError) */
+  BSG_EMPTY_PLAN = 6,
+  /* input outside the supported integer domain */
+  BSG_BAD_INPUT = 7,
+  /* ConfigError from validate_instance_config, types.cpp:47-61; detail = field code */
+  BSG_BAD_CONFIG = 8,
+  BSG_CUDA_ERROR = 9,
+  /* NoInstancesError, predictor.cpp:144 / scheduler.cpp:116 */
+  BSG_NO_INSTANCES = 10,
+  BSG_INVALID_ARGUMENT = 11
+} bsg_status;
+
+typedef enum bsg_local_policy {
+  BSG_CHUNKED_PREFILL = 0,  /* LocalPolicy::kChunkedPrefill, backend.cpp:113-149 */
+  BSG_PREFILL_PRIORITY = 1  /* LocalPolicy::kPrefillPriority, backend.cpp:151-182 */
+} bsg_local_policy;
+
+typedef enum bsg_cache_mode {
+  BSG_CACHE_OFF = 0,      /* predict(req, nullptr)                        */
+  BSG_CACHE_EXACT = 1,    /* transparent: identical to OFF (predictor.cpp:43-47) */
+  BSG_CACHE_BUCKETED = 2  /* context rounded to (C + b/2)/b*b (predictor.cpp:29-32) */
+} bsg_cache_mode;
+
+/* InstanceConfig + CostModelParams (types.h:46-66) + predictor cache mode.
+ * 64 bytes, naturally aligned. */
+typedef struct bsg_instance_cfg {
+  int32_t total_blocks;    /* 1056 */
+  int32_t block_size;      /* 16   */
+  int32_t max_batch_size;  /* 48   */
+  int32_t chunk_budget;    /* 512  */
+  int32_t local_policy;    /* bsg_local_policy */
+  int32_t cache_mode;      /* bsg_cache_mode   */
+  int32_t context_bucket;  /* 256; clamped to >= 1 like LatencyCache (predictor.cpp:23-24) */
+  int32_t reserved;
+  double c0_s;                 /* 0.01 */
+  double prefill_s_per_token;  /* 1e-4 */
+  double decode_s_per_seq;     /* 1e-3 */
+  double context_s_per_token;  /* 1e-7 */
+} bsg_instance_cfg;
+
+/* Snapshot entries (SnapshotRequest, types.h:75-81) as SoA columns.
+ * `id` is optional (may be NULL); it is only used host-side for messages. */
+typedef struct bsg_entries {
+  const uint64_t* id;
+  const int32_t* prompt;     /* prompt_tokens            */
+  const int32_t* est;        /* estimated_output_tokens  */
+  const int32_t* prefill;    /* prefill_progress         */
+  const int32_t* decoded;    /* decoded_tokens           */
+} bsg_entries;
+
+/* One what-if scenario: snapshot (running + waiting slices of the entry
+ * columns) + candidate + instance config index. 32 bytes. */
+typedef struct bsg_scenario {
+  int32_t run_off, run_n;    /* InstanceSnapshot::running, oldest admission first */
+  int32_t wait_off, wait_n;  /* InstanceSnapshot::waiting, head first            */
+  int32_t cand_prompt;       /* CandidateRequest::prompt_tokens                   */
+  int32_t cand_est;          /* CandidateRequest::estimated_output_tokens         */
+  int32_t cfg;               /* index into the configs set by bsg_set_configs     */
+  int32_t reserved;
+} bsg_scenario;
+
+/* PredictionResult (predictor.h:28-36) in integer ticks. 40 bytes. */
+typedef struct bsg_result {
+  int64_t e2e_ticks;     /* predicted_e2e_latency    */
+  int64_t ttft_ticks;    /* predicted_ttft           */
+  int64_t qdelay_ticks;  /* predicted_queueing_delay */
+  int64_t steps;         /* simulated_steps          */
+  int32_t status;        /* bsg_status               */
+  int32_t detail;        /* status-specific (origin index, field code, ...) */
+} bsg_result;
+
+/* One simulated step in trace mode (Instance::execute_step's StepResult,
+ * backend.h:40-47, reduced to exact integer fingerprints). 56 bytes.
+ * Origins: running entry i -> i, waiting entry j -> run_n + j, candidate -> -1. */
+typedef struct bsg_step_record {
+  int64_t duration_ticks;    /* SimTime::from_seconds(latency(plan))      */
+  int64_t context_tokens;    /* BatchPlan::context_tokens                 */
+  int32_t n_decode;          /* |BatchPlan::decode_ids|                   */
+  int32_t prefill_tokens;    /* BatchPlan::total_prefill_tokens           */
+  int32_t n_prefill;         /* |BatchPlan::prefill_segments|             */
+  int32_t n_preempted;       /* |StepResult::preempted|                   */
+  int32_t n_completed;       /* |StepResult::completed|                   */
+  int32_t free_blocks_after; /* Instance::free_blocks() after finish_step */
+  uint64_t plan_hash;        /* bsg_hash over (k, origin, chunk) of plan items in order */
+  uint64_t event_hash;       /* bsg_hash over preempted (in order), started, first tokens, completed */
+} bsg_step_record;
+
+#if defined(__CUDACC__)
+#define BSG_HD __host__ __device__
+#else
+#define BSG_HD
+#endif
+
+/* Mixing function shared by the kernel, the oracle and the reference shim
+ * (SplitMix64 finaliser, rand.h:16-21). */
+static inline BSG_HD uint64_t bsg_mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+/* Fingerprint term of item k of list `tag` with origin o and value v; lists
+ * hash as the wrapping SUM of their terms (order enters through k). */
+static inline BSG_HD uint64_t bsg_hash_term(uint32_t tag, uint32_t k, int32_t origin, int32_t v) {
+  return bsg_mix64(((uint64_t)tag << 56) ^ ((uint64_t)k << 32) ^ (uint64_t)(uint32_t)(origin + 1)) +
+         bsg_mix64((uint64_t)(uint32_t)v + 0x9e3779b97f4a7c15ULL * (uint64_t)(k + 1));
+}
+#define BSG_TAG_PLAN 1u
+#define BSG_TAG_PREEMPT 2u
+#define BSG_TAG_STARTED 3u
+#define BSG_TAG_FIRST 4u
+#define BSG_TAG_COMPLETED 5u
+
+/* ---- context ------------------------------------------------------------ */
+typedef struct bsg_ctx bsg_ctx;
+
+int bsg_abi_version(void);
+/* SimTime::seconds (time.h:25): ticks * 1e-9 in double. */
+double bsg_ticks_to_seconds(int64_t ticks);
+/* Creates a context bound to CUDA device `device`. Fails loudly with
+ * BSG_CUDA_ERROR when no device is present: there is no CPU path. */
+bsg_status bsg_ctx_create(int device, bsg_ctx** out);
+void bsg_ctx_destroy(bsg_ctx* ctx);
+const char* bsg_last_error(const bsg_ctx* ctx);
+/* Number of kernel launches issued by this context so far. */
+int64_t bsg_launch_count(const bsg_ctx* ctx);
+
+/* Validates (validate_instance_config, types.cpp:47-61) and uploads configs.
+ * On BSG_BAD_CONFIG, bad_index and field_code identify the first offender
+ * (field codes: 1 total_blocks, 2 block_size, 3 max_batch_size, 4 chunk_budget,
+ *  5 c0_s, 6 prefill_s_per_token, 7 decode_s_per_seq, 8 context_s_per_token). */
+bsg_status bsg_set_configs(bsg_ctx* ctx, const bsg_instance_cfg* cfgs, int32_t n,
+                           int32_t* bad_index, int32_t* field_code);
+
+/* predict() over n scenarios, HOST buffers; synchronous. Copies the entry
+ * columns and scenarios host->device, runs the scenario kernel, copies the
+ * results device->host. */
+bsg_status bsg_predict_batch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries,
+                             const bsg_scenario* scenarios, int64_t n, bsg_result* out);
+
+/* Same, with DEVICE pointers (entries columns, scenarios, out), enqueued on
+ * `stream` (a cudaStream_t, NULL = the context stream); asynchronous. */
+bsg_status bsg_predict_batch_device(bsg_ctx* ctx, const bsg_entries* dev_entries,
+                                    const bsg_scenario* dev_scenarios, int64_t n,
+                                    bsg_result* dev_out, void* stream);
+
+/* Trace mode: runs ONE scenario (host buffers) and writes one record per
+ * simulated step (up to `cap`); *n_steps receives the total step count. */
+bsg_status bsg_trace(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries,
+                     const bsg_scenario* scenario, bsg_step_record* records, int64_t cap,
+                     int64_t* n_steps, bsg_result* out);
+
+/* BlockPredictive dispatch (scheduler.cpp:115-152): for each of n_requests
+ * arrivals, scenarios [r*n_inst, (r+1)*n_inst) are the per-instance what-ifs
+ * (instance ids given in `instance_ids`, per request block, any order).
+ * chosen[r] = argmin over e2e (objective 0) or ttft (objective 1) with the
+ * lowest-id tie-break. per_instance may be NULL. HOST buffers. If any
+ * scenario of a request fails, chosen[r] = -1 and status reports it. */
+bsg_status bsg_dispatch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries,
+                        const bsg_scenario* scenarios, const int32_t* instance_ids,
+                        int32_t n_inst, int32_t n_requests, int32_t objective,
+                        int32_t* chosen, bsg_result* per_instance);
+
+/* ---- closed-loop replay (the scenario source; driver.cpp:134-289) -------- */
+
+/* Synthetic ShareGPT-shaped workload: make_synthetic_trace (workload.cpp:172-191,
+ * SyntheticTraceSpec workload.h:63-75), estimate_length (workload.cpp:113-139),
+ * generate_arrivals (workload.cpp:141-170). */
+typedef struct bsg_workload {
+  int32_t count;              /* 1000 */
+  int32_t min_tokens;         /* 4 */
+  int32_t max_prompt_tokens;  /* 4096 */
+  int32_t max_output_tokens;  /* 8192 */
+  uint64_t trace_seed;        /* SyntheticTraceSpec::seed */
+  double prompt_median, prompt_sigma;  /* 230, 0.7 */
+  double output_median, output_sigma;  /* 160, 1.0 */
+  int32_t estimator_kind;     /* 0 oracle, 1 fixed, 2 noisy (EstimatorKind) */
+  int32_t fixed_tokens;       /* 256 */
+  double mean_abs_rel_error;  /* 0.244 */
+  uint64_t estimator_seed;
+  double qps;
+  uint64_t arrival_seed;      /* workload.seed */
+  int32_t request_cap;        /* < 0: none */
+  int32_t reserved;
+} bsg_workload;
+
+/* PolicyKind order (scheduler.h:16-23). */
+typedef enum bsg_policy {
+  BSG_POLICY_RANDOM = 0,
+  BSG_POLICY_ROUND_ROBIN = 1,
+  BSG_POLICY_MIN_QPM = 2,
+  BSG_POLICY_INFAAS_PP = 3,
+  BSG_POLICY_LLUMNIX_MINUS = 4,
+  BSG_POLICY_BLOCK_PREDICTIVE = 5
+} bsg_policy;
+
+/* Static-provisioning, zero-overhead, probe-free closed loop
+ * (ExperimentSpec driver.h / config.h:58-70 subset). */
+typedef struct bsg_replay_spec {
+  int32_t n_instances;
+  int32_t policy;        /* bsg_policy */
+  int32_t objective;     /* 0 e2e, 1 ttft */
+  int32_t capture;       /* nonzero: record every BlockPredictive what-if scenario */
+  uint64_t policy_seed;  /* PolicyConfig::seed (Random's stream) */
+} bsg_replay_spec;
+
+/* Per-request outcome (Request, types.h:30-42). Unset times are -1. */
+typedef struct bsg_request_outcome {
+  int64_t arrival_ticks, dispatch_ticks, first_token_ticks, finish_ticks;
+  int32_t instance;
+  int32_t preempt_count;
+} bsg_request_outcome;
+
+/* Captured scenario set (opaque, owned by the library). */
+typedef struct bsg_capture bsg_capture;
+
+/* Runs the closed loop on host C++ live instances; every BlockPredictive
+ * dispatch evaluates its per-instance what-ifs on the GPU (bsg_dispatch).
+ * outcomes must hold min(count, request_cap) rows. *capture (optional)
+ * receives the what-if scenarios in arrival order (n_instances per arrival). */
+bsg_status bsg_replay(bsg_ctx* ctx, const bsg_workload* w, const bsg_instance_cfg* cfg,
+                      const bsg_replay_spec* spec, bsg_request_outcome* outcomes,
+                      int64_t* total_preemptions, bsg_capture** capture);
+void bsg_capture_sizes(const bsg_capture* c, int64_t* n_entries, int64_t* n_scenarios);
+/* Copies the capture into caller buffers (entries columns of n_entries,
+ * scenarios of n_scenarios); the `cfg` field of every scenario is 0. */
+void bsg_capture_copy(const bsg_capture* c, uint64_t* id, int32_t* prompt, int32_t* est,
+                      int32_t* prefill, int32_t* decoded, bsg_scenario* scenarios);
+void bsg_capture_free(bsg_capture* c);
+
+/* Synthetic trace + estimates + Poisson arrival ticks (no GPU needed). */
+bsg_status bsg_make_workload(const bsg_workload* w, int32_t* prompt, int32_t* output,
+                             int32_t* est, int64_t* arrival_ticks);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BLOCKSIM_B200_H */

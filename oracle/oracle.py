@@ -1,0 +1,180 @@
+"""ctypes loaders for the two CPU checkers — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and
+--impl reference) import this module. The product package never does.
+
+  CRestatement  -> oracle/build/liboracle.so       (oracle/blocksim_oracle.c)
+  Reference     -> oracle/_ref/libblocksim_ref.so  (the reference compiled from
+                   /root/reference by oracle/Makefile + oracle/ref_shim.cpp)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+from paper_2508_03611_b200 import abi
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+C_LIB = os.path.join(HERE, "build", "liboracle.so")
+REF_LIB = os.path.join(HERE, "_ref", "libblocksim_ref.so")
+REF_SRC = "/root/reference/proj/core"
+
+
+def build(ref: bool | None = None) -> None:
+    """Compile the C restatement, and the reference shim when its sources exist."""
+    targets = ["c"]
+    if ref is None:
+        ref = os.path.isdir(REF_SRC)
+    if ref:
+        targets.append("ref")
+    subprocess.run(["make", "-s", "-C", HERE, f"-j{os.cpu_count() or 4}", *targets], check=True)
+
+
+def _vp(a):
+    return abi.ptr(a)
+
+
+class CRestatement:
+    def __init__(self, path: str = C_LIB):
+        if not os.path.exists(path):
+            build(ref=False)
+        self.lib = C.CDLL(path)
+        L = self.lib
+        L.oracle_predict.restype = C.c_int32
+        L.oracle_predict.argtypes = [C.c_void_p, C.POINTER(abi.Entries), C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
+        L.oracle_predict_batch.restype = None
+        L.oracle_predict_batch.argtypes = [C.c_void_p, C.POINTER(abi.Entries), C.c_void_p,
+                                           C.c_int64, C.c_void_p]
+        L.oracle_blocks_needed.restype = C.c_int64
+        L.oracle_blocks_needed.argtypes = [C.c_int64, C.c_int32]
+        L.oracle_llround_1e9.restype = C.c_int64
+        L.oracle_llround_1e9.argtypes = [C.c_double]
+        L.oracle_batch_latency.restype = C.c_double
+        L.oracle_batch_latency.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int64]
+        L.oracle_validate_config.restype = C.c_int32
+        L.oracle_validate_config.argtypes = [C.c_void_p]
+
+    def predict_batch(self, cfgs: np.ndarray, ss: abi.ScenarioSet) -> np.ndarray:
+        out = np.zeros(len(ss), abi.result_dtype)
+        e = ss.entries()
+        self.lib.oracle_predict_batch(_vp(cfgs), C.byref(e), _vp(ss.scenarios), len(ss), _vp(out))
+        return out
+
+    def trace(self, cfgs: np.ndarray, ss: abi.ScenarioSet, i: int = 0, cap: int = 1 << 20):
+        rec = np.zeros(cap, abi.step_dtype)
+        out = np.zeros(1, abi.result_dtype)
+        n = C.c_int64(0)
+        e = ss.entries()
+        sc = np.ascontiguousarray(ss.scenarios[i:i + 1])
+        cfg = np.ascontiguousarray(cfgs[int(sc["cfg"][0]):int(sc["cfg"][0]) + 1])
+        self.lib.oracle_predict(_vp(cfg), C.byref(e), _vp(sc), _vp(out), _vp(rec), cap, C.byref(n))
+        return out[0], rec[:min(n.value, cap)]
+
+
+class Reference:
+    def __init__(self, path: str = REF_LIB):
+        if not os.path.exists(path):
+            if not os.path.isdir(REF_SRC):
+                raise FileNotFoundError(
+                    f"{path} missing and reference sources absent; run oracle.build() where "
+                    "/root/reference exists (the built .so travels with the repo snapshot)")
+            build(ref=True)
+        self.lib = C.CDLL(path)
+        L = self.lib
+        E = C.POINTER(abi.Entries)
+        L.ref_predict_batch.restype = C.c_int
+        L.ref_predict_batch.argtypes = [C.c_void_p, E, C.c_void_p, C.c_int64, C.c_void_p, C.c_int]
+        L.ref_time_predict.restype = C.c_double
+        L.ref_time_predict.argtypes = [C.c_void_p, E, C.c_void_p, C.c_int64, C.c_int, C.c_int]
+        L.ref_trace.restype = C.c_int
+        L.ref_trace.argtypes = [C.c_void_p, E, C.c_void_p, C.c_void_p, C.c_int64,
+                                C.POINTER(C.c_int64), C.c_void_p]
+        L.ref_make_workload.restype = C.c_int
+        L.ref_make_workload.argtypes = [C.c_void_p] + [C.c_void_p] * 4
+        L.ref_run_experiment.restype = C.c_int
+        L.ref_run_experiment.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.POINTER(C.c_int64)]
+        L.ref_replay.restype = C.c_int
+        L.ref_replay.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.POINTER(C.c_int64), C.POINTER(C.c_void_p)]
+        L.ref_capture_sizes.restype = None
+        L.ref_capture_sizes.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.ref_capture_copy.restype = None
+        L.ref_capture_copy.argtypes = [C.c_void_p] * 7
+        L.ref_capture_free.restype = None
+        L.ref_capture_free.argtypes = [C.c_void_p]
+
+    def predict_batch(self, cfgs, ss: abi.ScenarioSet, threads: int = 1) -> np.ndarray:
+        out = np.zeros(len(ss), abi.ref_result_dtype)
+        e = ss.entries()
+        self.lib.ref_predict_batch(_vp(cfgs), C.byref(e), _vp(ss.scenarios), len(ss), _vp(out),
+                                   threads)
+        return out
+
+    def time_predict(self, cfgs, ss: abi.ScenarioSet, threads: int, reps: int = 1) -> float:
+        e = ss.entries()
+        return self.lib.ref_time_predict(_vp(cfgs), C.byref(e), _vp(ss.scenarios), len(ss),
+                                         threads, reps)
+
+    def trace(self, cfgs, ss: abi.ScenarioSet, i: int = 0, cap: int = 1 << 20):
+        rec = np.zeros(cap, abi.step_dtype)
+        out = np.zeros(1, abi.ref_result_dtype)
+        n = C.c_int64(0)
+        e = ss.entries()
+        sc = np.ascontiguousarray(ss.scenarios[i:i + 1])
+        cfg = np.ascontiguousarray(cfgs[int(sc["cfg"][0]):int(sc["cfg"][0]) + 1])
+        self.lib.ref_trace(_vp(cfg), C.byref(e), _vp(sc), _vp(rec), cap, C.byref(n), _vp(out))
+        return out[0], rec[:min(n.value, cap)]
+
+    def make_workload(self, w):
+        n = int(w["count"][0]) if w["request_cap"][0] < 0 else min(int(w["count"][0]),
+                                                                    int(w["request_cap"][0]))
+        p, o, e = (np.zeros(n, np.int32) for _ in range(3))
+        t = np.zeros(n, np.int64)
+        self.lib.ref_make_workload(_vp(w), _vp(p), _vp(o), _vp(e), _vp(t))
+        return p, o, e, t
+
+    def run_experiment(self, w, cfg, spec):
+        n = int(w["count"][0]) if w["request_cap"][0] < 0 else min(int(w["count"][0]),
+                                                                    int(w["request_cap"][0]))
+        out = np.zeros(n, abi.outcome_dtype)
+        tp = C.c_int64(0)
+        self.lib.ref_run_experiment(_vp(w), _vp(cfg), _vp(spec), _vp(out), C.byref(tp))
+        return out, tp.value
+
+    def replay(self, w, cfg, spec, capture: bool = True):
+        n = int(w["count"][0]) if w["request_cap"][0] < 0 else min(int(w["count"][0]),
+                                                                    int(w["request_cap"][0]))
+        out = np.zeros(n, abi.outcome_dtype)
+        tp = C.c_int64(0)
+        h = C.c_void_p(None)
+        self.lib.ref_replay(_vp(w), _vp(cfg), _vp(spec), _vp(out), C.byref(tp),
+                            C.byref(h) if capture else None)
+        ss = None
+        if capture:
+            ne, ns = C.c_int64(0), C.c_int64(0)
+            self.lib.ref_capture_sizes(h, C.byref(ne), C.byref(ns))
+            ids = np.zeros(ne.value, np.uint64)
+            cols = [np.zeros(ne.value, np.int32) for _ in range(4)]
+            sc = np.zeros(ns.value, abi.scenario_dtype)
+            self.lib.ref_capture_copy(h, _vp(ids), *[_vp(c) for c in cols], _vp(sc))
+            self.lib.ref_capture_free(h)
+            ss = abi.ScenarioSet(*cols, sc, ids=ids)
+        return out, tp.value, ss
+
+
+def compare_to_ref(gpu_res: np.ndarray, ref_res: np.ndarray) -> np.ndarray:
+    """Boolean mask of scenarios whose product result (ticks) differs from the
+    reference's (double seconds): status, steps, and e2e/ttft/qdelay compared
+    bit-exactly as ticks * 1e-9 (time.h:25)."""
+    ok = gpu_res["status"] == ref_res["status"]
+    good = ok & (gpu_res["status"] == abi.OK)
+    for tk, sk in (("e2e_ticks", "e2e_s"), ("ttft_ticks", "ttft_s"), ("qdelay_ticks", "qdelay_s")):
+        sec = abi.ticks_to_seconds(gpu_res[tk])
+        ok &= ~good | (sec.view(np.int64) == ref_res[sk].view(np.int64))
+    ok &= ~good | (gpu_res["steps"] == ref_res["steps"])
+    return ~ok

@@ -1,0 +1,193 @@
+"""numpy/ctypes mirror of the C-ABI structs in include/blocksim_b200.h.
+
+Layouts are asserted against the header's stated sizes; every array passed
+across the boundary is a C-contiguous numpy array of one of these dtypes.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+# bsg_status (include/blocksim_b200.h)
+OK = 0
+TOO_LARGE_RUNNING = 1
+TOO_LARGE_CANDIDATE = 2
+DEADLOCK = 3
+STEP_LIMIT = 4
+VANISHED = 5
+EMPTY_PLAN = 6
+BAD_INPUT = 7
+BAD_CONFIG = 8
+CUDA_ERROR = 9
+NO_INSTANCES = 10
+INVALID_ARGUMENT = 11
+STATUS_NAMES = {
+    0: "OK", 1: "TOO_LARGE_RUNNING", 2: "TOO_LARGE_CANDIDATE", 3: "DEADLOCK",
+    4: "STEP_LIMIT", 5: "VANISHED", 6: "EMPTY_PLAN", 7: "BAD_INPUT", 8: "BAD_CONFIG",
+    9: "CUDA_ERROR", 10: "NO_INSTANCES", 11: "INVALID_ARGUMENT",
+}
+
+CHUNKED_PREFILL = 0
+PREFILL_PRIORITY = 1
+CACHE_OFF, CACHE_EXACT, CACHE_BUCKETED = 0, 1, 2
+POLICY_RANDOM, POLICY_ROUND_ROBIN, POLICY_MIN_QPM, POLICY_INFAAS_PP, POLICY_LLUMNIX_MINUS, \
+    POLICY_BLOCK_PREDICTIVE = range(6)
+
+cfg_dtype = np.dtype([
+    ("total_blocks", "<i4"), ("block_size", "<i4"), ("max_batch_size", "<i4"),
+    ("chunk_budget", "<i4"), ("local_policy", "<i4"), ("cache_mode", "<i4"),
+    ("context_bucket", "<i4"), ("reserved", "<i4"),
+    ("c0_s", "<f8"), ("prefill_s_per_token", "<f8"), ("decode_s_per_seq", "<f8"),
+    ("context_s_per_token", "<f8"),
+])
+scenario_dtype = np.dtype([
+    ("run_off", "<i4"), ("run_n", "<i4"), ("wait_off", "<i4"), ("wait_n", "<i4"),
+    ("cand_prompt", "<i4"), ("cand_est", "<i4"), ("cfg", "<i4"), ("reserved", "<i4"),
+])
+result_dtype = np.dtype([
+    ("e2e_ticks", "<i8"), ("ttft_ticks", "<i8"), ("qdelay_ticks", "<i8"), ("steps", "<i8"),
+    ("status", "<i4"), ("detail", "<i4"),
+])
+ref_result_dtype = np.dtype([
+    ("e2e_s", "<f8"), ("ttft_s", "<f8"), ("qdelay_s", "<f8"), ("steps", "<i8"),
+    ("status", "<i4"), ("detail", "<i4"),
+])
+step_dtype = np.dtype([
+    ("duration_ticks", "<i8"), ("context_tokens", "<i8"), ("n_decode", "<i4"),
+    ("prefill_tokens", "<i4"), ("n_prefill", "<i4"), ("n_preempted", "<i4"),
+    ("n_completed", "<i4"), ("free_blocks_after", "<i4"), ("plan_hash", "<u8"),
+    ("event_hash", "<u8"),
+])
+workload_dtype = np.dtype([
+    ("count", "<i4"), ("min_tokens", "<i4"), ("max_prompt_tokens", "<i4"),
+    ("max_output_tokens", "<i4"), ("trace_seed", "<u8"), ("prompt_median", "<f8"),
+    ("prompt_sigma", "<f8"), ("output_median", "<f8"), ("output_sigma", "<f8"),
+    ("estimator_kind", "<i4"), ("fixed_tokens", "<i4"), ("mean_abs_rel_error", "<f8"),
+    ("estimator_seed", "<u8"), ("qps", "<f8"), ("arrival_seed", "<u8"),
+    ("request_cap", "<i4"), ("reserved", "<i4"),
+])
+replay_spec_dtype = np.dtype([
+    ("n_instances", "<i4"), ("policy", "<i4"), ("objective", "<i4"), ("capture", "<i4"),
+    ("policy_seed", "<u8"),
+])
+outcome_dtype = np.dtype([
+    ("arrival_ticks", "<i8"), ("dispatch_ticks", "<i8"), ("first_token_ticks", "<i8"),
+    ("finish_ticks", "<i8"), ("instance", "<i4"), ("preempt_count", "<i4"),
+])
+
+assert cfg_dtype.itemsize == 64
+assert scenario_dtype.itemsize == 32
+assert result_dtype.itemsize == 40
+assert step_dtype.itemsize == 56
+assert outcome_dtype.itemsize == 40
+
+
+class Entries(C.Structure):
+    """bsg_entries: SoA column pointers."""
+    _fields_ = [("id", C.c_void_p), ("prompt", C.c_void_p), ("est", C.c_void_p),
+                ("prefill", C.c_void_p), ("decoded", C.c_void_p)]
+
+
+def ptr(a: np.ndarray | None) -> C.c_void_p | None:
+    if a is None:
+        return None
+    assert a.flags["C_CONTIGUOUS"], "arrays crossing the C-ABI must be contiguous"
+    return C.c_void_p(a.ctypes.data)
+
+
+def make_config(total_blocks=1056, block_size=16, max_batch_size=48, chunk_budget=512,
+                local_policy=CHUNKED_PREFILL, cache_mode=CACHE_OFF, context_bucket=256,
+                c0_s=0.01, prefill_s_per_token=1e-4, decode_s_per_seq=1e-3,
+                context_s_per_token=1e-7) -> np.ndarray:
+    """InstanceConfig defaults (types.h:46-66) — the 'Llama-2-7B profile' of BASELINE.json."""
+    c = np.zeros(1, cfg_dtype)
+    c["total_blocks"], c["block_size"] = total_blocks, block_size
+    c["max_batch_size"], c["chunk_budget"] = max_batch_size, chunk_budget
+    c["local_policy"], c["cache_mode"], c["context_bucket"] = local_policy, cache_mode, context_bucket
+    c["c0_s"], c["prefill_s_per_token"] = c0_s, prefill_s_per_token
+    c["decode_s_per_seq"], c["context_s_per_token"] = decode_s_per_seq, context_s_per_token
+    return c
+
+
+def make_workload(count=1000, trace_seed=1234, prompt_median=230.0, prompt_sigma=0.7,
+                  output_median=160.0, output_sigma=1.0, min_tokens=4, max_prompt_tokens=4096,
+                  max_output_tokens=8192, estimator_kind=0, fixed_tokens=256,
+                  mean_abs_rel_error=0.244, estimator_seed=0, qps=1.0, arrival_seed=0,
+                  request_cap=-1) -> np.ndarray:
+    """SyntheticTraceSpec (workload.h:63-75) + LengthEstimator + arrivals."""
+    w = np.zeros(1, workload_dtype)
+    for k, v in dict(count=count, trace_seed=trace_seed, prompt_median=prompt_median,
+                     prompt_sigma=prompt_sigma, output_median=output_median,
+                     output_sigma=output_sigma, min_tokens=min_tokens,
+                     max_prompt_tokens=max_prompt_tokens, max_output_tokens=max_output_tokens,
+                     estimator_kind=estimator_kind, fixed_tokens=fixed_tokens,
+                     mean_abs_rel_error=mean_abs_rel_error, estimator_seed=estimator_seed,
+                     qps=qps, arrival_seed=arrival_seed, request_cap=request_cap).items():
+        w[k] = v
+    return w
+
+
+def make_replay_spec(n_instances, policy=POLICY_BLOCK_PREDICTIVE, objective=0, capture=1,
+                     policy_seed=0) -> np.ndarray:
+    s = np.zeros(1, replay_spec_dtype)
+    s["n_instances"], s["policy"], s["objective"] = n_instances, policy, objective
+    s["capture"], s["policy_seed"] = capture, policy_seed
+    return s
+
+
+class ScenarioSet:
+    """A batch of what-if scenarios: SoA entry columns + scenario rows."""
+
+    def __init__(self, prompt, est, prefill, decoded, scenarios, ids=None):
+        self.prompt = np.ascontiguousarray(prompt, dtype=np.int32)
+        self.est = np.ascontiguousarray(est, dtype=np.int32)
+        self.prefill = np.ascontiguousarray(prefill, dtype=np.int32)
+        self.decoded = np.ascontiguousarray(decoded, dtype=np.int32)
+        self.ids = None if ids is None else np.ascontiguousarray(ids, dtype=np.uint64)
+        self.scenarios = np.ascontiguousarray(scenarios, dtype=scenario_dtype)
+
+    @property
+    def n_entries(self) -> int:
+        return int(self.prompt.shape[0])
+
+    def __len__(self) -> int:
+        return int(self.scenarios.shape[0])
+
+    def entries(self) -> Entries:
+        return Entries(ptr(self.ids), ptr(self.prompt), ptr(self.est), ptr(self.prefill),
+                       ptr(self.decoded))
+
+    def subset(self, idx) -> "ScenarioSet":
+        return ScenarioSet(self.prompt, self.est, self.prefill, self.decoded,
+                           self.scenarios[idx], self.ids)
+
+    def nbytes_in(self) -> int:
+        return (self.prompt.nbytes + self.est.nbytes + self.prefill.nbytes + self.decoded.nbytes
+                + self.scenarios.nbytes)
+
+    @staticmethod
+    def from_snapshots(snapshots, candidates, cfg_index=None) -> "ScenarioSet":
+        """snapshots: list of (running, waiting) with entries (prompt, est, prefill, decoded);
+        candidates: list of (prompt, est)."""
+        cols = [[], [], [], []]
+        sc = np.zeros(len(snapshots), scenario_dtype)
+        for i, ((running, waiting), (cp, ce)) in enumerate(zip(snapshots, candidates)):
+            sc[i]["run_off"] = len(cols[0])
+            sc[i]["run_n"] = len(running)
+            for r in running:
+                for c, v in zip(cols, r):
+                    c.append(v)
+            sc[i]["wait_off"] = len(cols[0])
+            sc[i]["wait_n"] = len(waiting)
+            for r in waiting:
+                for c, v in zip(cols, r):
+                    c.append(v)
+            sc[i]["cand_prompt"], sc[i]["cand_est"] = cp, ce
+            sc[i]["cfg"] = 0 if cfg_index is None else cfg_index[i]
+        return ScenarioSet(*[np.array(c, dtype=np.int32) for c in cols], sc)
+
+
+def ticks_to_seconds(ticks) -> np.ndarray:
+    """SimTime::seconds (time.h:25): ticks * 1e-9 in double."""
+    return np.asarray(ticks, dtype=np.int64).astype(np.float64) * 1e-9

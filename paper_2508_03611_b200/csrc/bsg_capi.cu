@@ -1,0 +1,448 @@
+// bsg_capi.cu — C-ABI (include/blocksim_b200.h) over the sm_100a kernels.
+//
+// Host-side responsibilities only: config validation (validate_instance_config,
+// types.cpp:47-61), device buffer management, kernel selection by member
+// capacity, and stream-ordered launches. No simulation happens on the host;
+// without a CUDA device every entry point fails with BSG_CUDA_ERROR.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "bsg_internal.h"
+#include "scenario_sim.cuh"
+
+namespace bsg {
+
+constexpr int kWarpsPerBlock = 4;
+
+template <int K>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    predict_kernel(const DevCfg* __restrict__ cfgs, int32_t ncfg,
+                   const int32_t* __restrict__ prompt, const int32_t* __restrict__ est,
+                   const int32_t* __restrict__ prefill, const int32_t* __restrict__ decoded,
+                   const bsg_scenario* __restrict__ scen, int64_t n,
+                   const int32_t* __restrict__ order, bsg_result* __restrict__ out) {
+  __shared__ int32_t smem[kWarpsPerBlock * 5 * 32 * K];
+  const int warp = threadIdx.x >> 5;
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + warp;
+  if (w >= n) return;
+  const int64_t i = order ? order[w] : w;
+  const bsg_scenario sc = scen[i];
+  bsg_result* o = out + i;
+  if (sc.cfg < 0 || sc.cfg >= ncfg) {
+    if ((threadIdx.x & 31) == 0) {
+      bsg_result r{};
+      r.status = BSG_INVALID_ARGUMENT;
+      *o = r;
+    }
+    return;
+  }
+  const DevCfg cfg = cfgs[sc.cfg];
+  const int32_t need = max(sc.run_n, min(cfg.max_batch_size, sc.run_n + sc.wait_n + 1));
+  if (need > 32 * K || sc.run_n < 0 || sc.wait_n < 0) {
+    if ((threadIdx.x & 31) == 0) {
+      bsg_result r{};
+      r.status = BSG_BAD_INPUT;
+      *o = r;
+    }
+    return;
+  }
+  simulate_scenario<K, false>(cfg, prompt, est, prefill, decoded, sc,
+                              smem + warp * 5 * 32 * K, o, TraceSink{nullptr, 0});
+}
+
+template <int K>
+__global__ void __launch_bounds__(32)
+    trace_kernel(const DevCfg* __restrict__ cfgs, const int32_t* __restrict__ prompt,
+                 const int32_t* __restrict__ est, const int32_t* __restrict__ prefill,
+                 const int32_t* __restrict__ decoded, const bsg_scenario* __restrict__ scen,
+                 bsg_result* __restrict__ out, bsg_step_record* rec, int64_t cap) {
+  __shared__ int32_t smem[5 * 32 * K];
+  const bsg_scenario sc = scen[0];
+  const DevCfg cfg = cfgs[sc.cfg];
+  simulate_scenario<K, true>(cfg, prompt, est, prefill, decoded, sc, smem, out,
+                             TraceSink{rec, cap});
+}
+
+// BlockPredictive argmin (scheduler.cpp:138-150): one warp per request, value
+// compared as int64 ticks (== comparing ticks*1e-9 doubles),
+// ties to the lowest instance id. A failing scenario poisons its request.
+__global__ void argmin_kernel(const bsg_result* __restrict__ res,
+                              const int32_t* __restrict__ inst_ids, int32_t n_inst,
+                              int32_t n_req, int32_t objective, int32_t* __restrict__ chosen) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= n_req) return;
+  const int lane = threadIdx.x & 31;
+  int64_t best_v = INT64_MAX;
+  int32_t best_id = INT32_MAX;
+  bool fail = false;
+  for (int32_t i = lane; i < n_inst; i += 32) {
+    const bsg_result& x = res[r * n_inst + i];
+    const int32_t id = inst_ids[r * n_inst + i];
+    if (x.status != BSG_OK) fail = true;
+    const int64_t v = objective == 1 ? x.ttft_ticks : x.e2e_ticks;
+    if (v < best_v || (v == best_v && id < best_id)) {
+      best_v = v;
+      best_id = id;
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const int64_t ov = __shfl_xor_sync(kFull, best_v, d);
+    const int32_t oi = __shfl_xor_sync(kFull, best_id, d);
+    if (ov < best_v || (ov == best_v && oi < best_id)) {
+      best_v = ov;
+      best_id = oi;
+    }
+  }
+  fail = __any_sync(kFull, fail);
+  if (lane == 0) chosen[r] = fail ? -1 : best_id;
+}
+
+}  // namespace bsg
+
+using namespace bsg;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  bool ensure(size_t bytes) {
+    if (bytes <= cap) return true;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 1 << 16);
+    if (cudaMalloc(&p, want) != cudaSuccess) return false;
+    cap = want;
+    return true;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+struct bsg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string last_error;
+  int64_t launches = 0;
+  std::vector<bsg_instance_cfg> host_cfgs;
+  std::vector<DevCfg> dev_cfgs_host;
+  DevBuf cfgs, prompt, est, prefill, decoded, scen, res, rec, ids, chosen, order;
+  int32_t ncfg = 0;
+  int32_t max_batch_all = 0;
+  std::mutex mu;
+};
+
+namespace {
+
+bsg_status cuda_fail(bsg_ctx* ctx, cudaError_t e, const char* what) {
+  if (ctx) ctx->last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return BSG_CUDA_ERROR;
+}
+
+#define BSG_CUDA(ctx, call)                                  \
+  do {                                                       \
+    cudaError_t _e = (call);                                 \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, #call); \
+  } while (0)
+
+DevCfg to_dev(const bsg_instance_cfg& c) {
+  DevCfg d{};
+  d.total_blocks = c.total_blocks;
+  d.block_size = c.block_size;
+  d.max_batch_size = c.max_batch_size;
+  d.chunk_budget = c.chunk_budget;
+  d.local_policy = c.local_policy;
+  d.cache_mode = c.cache_mode;
+  d.context_bucket = c.context_bucket;
+  const uint32_t bs = static_cast<uint32_t>(c.block_size);
+  if ((bs & (bs - 1)) == 0) {
+    d.div_magic = 0;
+    d.div_shift = __builtin_ctz(bs);
+  } else {
+    // N = 31-bit dividends: l = ceil(log2 bs), m = floor(2^(31+l)/bs) + 1 < 2^32,
+    // q = umulhi(n, m) >> (l - 1).
+    int l = 0;
+    while ((1u << l) < bs) ++l;
+    const unsigned __int128 two = static_cast<unsigned __int128>(1) << (31 + l);
+    d.div_magic = static_cast<uint32_t>(two / bs + 1);
+    d.div_shift = l - 1;
+  }
+  d.c0 = c.c0_s;
+  d.cp = c.prefill_s_per_token;
+  d.cd = c.decode_s_per_seq;
+  d.cc = c.context_s_per_token;
+  return d;
+}
+
+int capacity_k(int32_t need) {
+  if (need <= 32) return 1;
+  if (need <= 64) return 2;
+  if (need <= 128) return 4;
+  if (need <= 256) return 8;
+  return 0;
+}
+
+template <int K>
+void launch_predict(bsg_ctx* ctx, int64_t n, const bsg_entries& e, const bsg_scenario* sc,
+                    const int32_t* order, bsg_result* out, cudaStream_t s) {
+  const int64_t blocks = (n + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  predict_kernel<K><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
+      static_cast<const DevCfg*>(ctx->cfgs.p), ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded,
+      sc, n, order, out);
+  ctx->launches += 1;
+}
+
+bsg_status launch_predict_k(bsg_ctx* ctx, int k, int64_t n, const bsg_entries& e,
+                            const bsg_scenario* sc, const int32_t* order, bsg_result* out,
+                            cudaStream_t s) {
+  if (n == 0) return BSG_OK;
+  switch (k) {
+    case 1: launch_predict<1>(ctx, n, e, sc, order, out, s); break;
+    case 2: launch_predict<2>(ctx, n, e, sc, order, out, s); break;
+    case 4: launch_predict<4>(ctx, n, e, sc, order, out, s); break;
+    case 8: launch_predict<8>(ctx, n, e, sc, order, out, s); break;
+    default:
+      ctx->last_error = "member capacity beyond 256 is outside the supported domain";
+      return BSG_BAD_INPUT;
+  }
+  BSG_CUDA(ctx, cudaGetLastError());
+  return BSG_OK;
+}
+
+int32_t host_need(const bsg_scenario* sc, int64_t n, const std::vector<bsg_instance_cfg>& cfgs) {
+  int32_t need = 1;
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t c = sc[i].cfg;
+    const int32_t maxb = (c >= 0 && c < static_cast<int32_t>(cfgs.size())) ? cfgs[c].max_batch_size : 1;
+    const int32_t tot = sc[i].run_n + sc[i].wait_n + 1;
+    need = std::max(need, std::max(sc[i].run_n, std::min(maxb, tot)));
+  }
+  return need;
+}
+
+// Uploads host entry columns + scenarios into the context's device buffers.
+bsg_status upload(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries,
+                  const bsg_scenario* sc, int64_t n, bsg_entries* dev) {
+  const size_t eb = static_cast<size_t>(std::max<int64_t>(n_entries, 1)) * sizeof(int32_t);
+  if (!ctx->prompt.ensure(eb) || !ctx->est.ensure(eb) || !ctx->prefill.ensure(eb) ||
+      !ctx->decoded.ensure(eb) || !ctx->scen.ensure(n * sizeof(bsg_scenario)) ||
+      !ctx->res.ensure(n * sizeof(bsg_result))) {
+    ctx->last_error = "device allocation failed";
+    return BSG_CUDA_ERROR;
+  }
+  cudaStream_t s = ctx->stream;
+  if (n_entries > 0) {
+    BSG_CUDA(ctx, cudaMemcpyAsync(ctx->prompt.p, entries->prompt, n_entries * 4, cudaMemcpyHostToDevice, s));
+    BSG_CUDA(ctx, cudaMemcpyAsync(ctx->est.p, entries->est, n_entries * 4, cudaMemcpyHostToDevice, s));
+    BSG_CUDA(ctx, cudaMemcpyAsync(ctx->prefill.p, entries->prefill, n_entries * 4, cudaMemcpyHostToDevice, s));
+    BSG_CUDA(ctx, cudaMemcpyAsync(ctx->decoded.p, entries->decoded, n_entries * 4, cudaMemcpyHostToDevice, s));
+  }
+  BSG_CUDA(ctx, cudaMemcpyAsync(ctx->scen.p, sc, n * sizeof(bsg_scenario), cudaMemcpyHostToDevice, s));
+  dev->id = nullptr;
+  dev->prompt = static_cast<const int32_t*>(ctx->prompt.p);
+  dev->est = static_cast<const int32_t*>(ctx->est.p);
+  dev->prefill = static_cast<const int32_t*>(ctx->prefill.p);
+  dev->decoded = static_cast<const int32_t*>(ctx->decoded.p);
+  return BSG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bsg_abi_version(void) { return BSG_ABI_VERSION; }
+
+double bsg_ticks_to_seconds(int64_t ticks) { return static_cast<double>(ticks) * 1e-9; }
+
+bsg_status bsg_ctx_create(int device, bsg_ctx** out) {
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) return BSG_CUDA_ERROR;
+  if (device < 0 || device >= count) return BSG_INVALID_ARGUMENT;
+  if (cudaSetDevice(device) != cudaSuccess) return BSG_CUDA_ERROR;
+  auto* ctx = new bsg_ctx();
+  ctx->device = device;
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return BSG_CUDA_ERROR;
+  }
+  *out = ctx;
+  return BSG_OK;
+}
+
+void bsg_ctx_destroy(bsg_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* bsg_last_error(const bsg_ctx* ctx) { return ctx ? ctx->last_error.c_str() : ""; }
+
+int64_t bsg_launch_count(const bsg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+bsg_status bsg_set_configs(bsg_ctx* ctx, const bsg_instance_cfg* cfgs, int32_t n,
+                           int32_t* bad_index, int32_t* field_code) {
+  if (!ctx || !cfgs || n <= 0) return BSG_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaSetDevice(ctx->device);
+  std::vector<DevCfg> dev(n);
+  int32_t maxb = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    const bsg_instance_cfg& c = cfgs[i];
+    int32_t f = 0;  // validate_instance_config, types.cpp:47-61 (same order)
+    if (c.total_blocks < 1) f = 1;
+    else if (c.block_size < 1) f = 2;
+    else if (c.max_batch_size < 1) f = 3;
+    else if (c.chunk_budget < c.block_size) f = 4;
+    else if (!(c.c0_s > 0)) f = 5;
+    else if (c.prefill_s_per_token < 0) f = 6;
+    else if (c.decode_s_per_seq < 0) f = 7;
+    else if (c.context_s_per_token < 0) f = 8;
+    if (f) {
+      if (bad_index) *bad_index = i;
+      if (field_code) *field_code = f;
+      ctx->last_error = "invalid config";
+      return BSG_BAD_CONFIG;
+    }
+    // Supported integer domain: all token sums fit in int32.
+    if (static_cast<int64_t>(c.total_blocks) * c.block_size > (1LL << 30) ||
+        c.block_size > (1 << 20) || c.chunk_budget > (1 << 30)) {
+      if (bad_index) *bad_index = i;
+      if (field_code) *field_code = 0;
+      ctx->last_error = "config outside the supported integer domain";
+      return BSG_BAD_INPUT;
+    }
+    dev[i] = to_dev(c);
+    maxb = std::max(maxb, c.max_batch_size);
+  }
+  if (!ctx->cfgs.ensure(n * sizeof(DevCfg))) return BSG_CUDA_ERROR;
+  BSG_CUDA(ctx, cudaMemcpyAsync(ctx->cfgs.p, dev.data(), n * sizeof(DevCfg), cudaMemcpyHostToDevice,
+                                ctx->stream));
+  BSG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->host_cfgs.assign(cfgs, cfgs + n);
+  ctx->dev_cfgs_host = dev;
+  ctx->ncfg = n;
+  ctx->max_batch_all = maxb;
+  return BSG_OK;
+}
+
+bsg_status bsg_predict_batch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries,
+                             const bsg_scenario* scenarios, int64_t n, bsg_result* out) {
+  if (!ctx || !entries || !scenarios || !out || n < 0) return BSG_INVALID_ARGUMENT;
+  if (ctx->ncfg == 0) return BSG_INVALID_ARGUMENT;
+  if (n == 0) return BSG_OK;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaSetDevice(ctx->device);
+  bsg_entries dev{};
+  bsg_status st = upload(ctx, entries, n_entries, scenarios, n, &dev);
+  if (st != BSG_OK) return st;
+  const int k = capacity_k(host_need(scenarios, n, ctx->host_cfgs));
+  st = launch_predict_k(ctx, k == 0 ? 8 : k, n, dev, static_cast<const bsg_scenario*>(ctx->scen.p),
+                        nullptr, static_cast<bsg_result*>(ctx->res.p), ctx->stream);
+  if (st != BSG_OK) return st;
+  BSG_CUDA(ctx, cudaMemcpyAsync(out, ctx->res.p, n * sizeof(bsg_result), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+  BSG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return BSG_OK;
+}
+
+bsg_status bsg_predict_batch_device(bsg_ctx* ctx, const bsg_entries* dev_entries,
+                                    const bsg_scenario* dev_scenarios, int64_t n,
+                                    bsg_result* dev_out, void* stream) {
+  if (!ctx || !dev_entries || !dev_scenarios || !dev_out || n < 0) return BSG_INVALID_ARGUMENT;
+  if (ctx->ncfg == 0) return BSG_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  // Capacity from the configs (scenarios are device-resident); scenarios that
+  // need more report BSG_BAD_INPUT from the kernel.
+  int k = capacity_k(std::max(1, ctx->max_batch_all));
+  if (k == 0) k = 8;
+  return launch_predict_k(ctx, k, n, *dev_entries, dev_scenarios, nullptr, dev_out, s);
+}
+
+bsg_status bsg_trace(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries,
+                     const bsg_scenario* scenario, bsg_step_record* records, int64_t cap,
+                     int64_t* n_steps, bsg_result* out) {
+  if (!ctx || !entries || !scenario || !out || cap < 0) return BSG_INVALID_ARGUMENT;
+  if (ctx->ncfg == 0) return BSG_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaSetDevice(ctx->device);
+  bsg_entries dev{};
+  bsg_status st = upload(ctx, entries, n_entries, scenario, 1, &dev);
+  if (st != BSG_OK) return st;
+  if (!ctx->rec.ensure(std::max<int64_t>(cap, 1) * sizeof(bsg_step_record))) return BSG_CUDA_ERROR;
+  BSG_CUDA(ctx, cudaMemsetAsync(ctx->rec.p, 0, std::max<int64_t>(cap, 1) * sizeof(bsg_step_record),
+                                ctx->stream));
+  const int k = capacity_k(host_need(scenario, 1, ctx->host_cfgs));
+  auto* rec = static_cast<bsg_step_record*>(ctx->rec.p);
+  auto* res = static_cast<bsg_result*>(ctx->res.p);
+  auto* sc = static_cast<const bsg_scenario*>(ctx->scen.p);
+  auto* cf = static_cast<const DevCfg*>(ctx->cfgs.p);
+  switch (k) {
+    case 1: trace_kernel<1><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap); break;
+    case 2: trace_kernel<2><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap); break;
+    case 4: trace_kernel<4><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap); break;
+    case 8: trace_kernel<8><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap); break;
+    default: ctx->last_error = "member capacity beyond 256"; return BSG_BAD_INPUT;
+  }
+  ctx->launches += 1;
+  BSG_CUDA(ctx, cudaGetLastError());
+  BSG_CUDA(ctx, cudaMemcpyAsync(out, res, sizeof(bsg_result), cudaMemcpyDeviceToHost, ctx->stream));
+  BSG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  *n_steps = out->steps;
+  const int64_t got = std::min<int64_t>(cap, out->steps);
+  if (got > 0) {
+    BSG_CUDA(ctx, cudaMemcpy(records, rec, got * sizeof(bsg_step_record), cudaMemcpyDeviceToHost));
+  }
+  return BSG_OK;
+}
+
+bsg_status bsg_dispatch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries,
+                        const bsg_scenario* scenarios, const int32_t* instance_ids,
+                        int32_t n_inst, int32_t n_requests, int32_t objective, int32_t* chosen,
+                        bsg_result* per_instance) {
+  if (!ctx || !entries || !scenarios || !instance_ids || !chosen) return BSG_INVALID_ARGUMENT;
+  if (n_inst <= 0) return BSG_NO_INSTANCES;  // scheduler.cpp:116
+  if (n_requests <= 0) return BSG_OK;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaSetDevice(ctx->device);
+  const int64_t n = static_cast<int64_t>(n_inst) * n_requests;
+  bsg_entries dev{};
+  bsg_status st = upload(ctx, entries, n_entries, scenarios, n, &dev);
+  if (st != BSG_OK) return st;
+  if (!ctx->ids.ensure(n * sizeof(int32_t)) || !ctx->chosen.ensure(n_requests * sizeof(int32_t)))
+    return BSG_CUDA_ERROR;
+  BSG_CUDA(ctx, cudaMemcpyAsync(ctx->ids.p, instance_ids, n * sizeof(int32_t),
+                                cudaMemcpyHostToDevice, ctx->stream));
+  const int k = capacity_k(host_need(scenarios, n, ctx->host_cfgs));
+  auto* res = static_cast<bsg_result*>(ctx->res.p);
+  st = launch_predict_k(ctx, k == 0 ? 8 : k, n, dev, static_cast<const bsg_scenario*>(ctx->scen.p),
+                        nullptr, res, ctx->stream);
+  if (st != BSG_OK) return st;
+  const int warps = 4;
+  argmin_kernel<<<(n_requests + warps - 1) / warps, warps * 32, 0, ctx->stream>>>(
+      res, static_cast<const int32_t*>(ctx->ids.p), n_inst, n_requests, objective,
+      static_cast<int32_t*>(ctx->chosen.p));
+  ctx->launches += 1;
+  BSG_CUDA(ctx, cudaGetLastError());
+  BSG_CUDA(ctx, cudaMemcpyAsync(chosen, ctx->chosen.p, n_requests * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+  if (per_instance) {
+    BSG_CUDA(ctx, cudaMemcpyAsync(per_instance, res, n * sizeof(bsg_result),
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  BSG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return BSG_OK;
+}
+
+}  // extern "C"

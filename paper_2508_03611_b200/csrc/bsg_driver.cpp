@@ -1,0 +1,627 @@
+// bsg_driver.cpp — closed-loop replay: the scenario source and sweep driver.
+//
+// Replays a synthetic trace through N live serving instances; every arrival
+// is dispatched by the configured policy, and BlockPredictive dispatches run
+// their per-instance what-if simulations on the GPU (bsg_dispatch). This is
+// the behaviour of SimulationDriver (core/src/driver.cpp:134-289) for static
+// provisioning, zero dispatch overhead and no probes, over the same
+// workload generators (core/src/workload.cpp:113-191) and dispatcher
+// heuristics (core/src/scheduler.cpp:33-113).
+//
+// The live instances here are host C++ (they are the simulated backends the
+// snapshots come from, not the prediction path). Their state is kept in the
+// same "resident list" form as the GPU kernel (scenario_sim.cuh): running
+// members [0,n) in admission order, preemption victims [n,L) = the waiting
+// front, then never-scheduled arrivals in FIFO order.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <limits>
+#include <memory>
+#include <queue>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "bsg_internal.h"
+
+namespace {
+
+// ---- fully specified RNG (SplitMix64 + helpers, rand.h:11-56) -------------
+struct Rng {
+  uint64_t s;
+  explicit Rng(uint64_t seed) : s(seed) {}
+  uint64_t next() {
+    uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+  }
+  double u01() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+  double u01_open_low() { return 1.0 - u01(); }
+  uint64_t below(uint64_t n) {
+    const uint64_t limit = UINT64_MAX - UINT64_MAX % n;
+    uint64_t r;
+    do r = next(); while (r >= limit);
+    return r % n;
+  }
+  double exponential(double rate) { return -std::log(u01_open_low()) / rate; }
+  double normal() {
+    const double u1 = u01_open_low();
+    const double u2 = u01();
+    return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * 3.14159265358979323846 * u2);
+  }
+};
+uint64_t mix_seed(uint64_t seed, uint64_t id) {
+  Rng s(id * 0x9e3779b97f4a7c15ULL + 0x1b873593ULL);
+  return seed ^ s.next();
+}
+
+int64_t ticks_from_seconds(double s) { return static_cast<int64_t>(std::llround(s * 1e9)); }
+
+struct Record {
+  int32_t prompt, output, est;
+  int64_t arrival;
+};
+
+// make_synthetic_trace (workload.cpp:172-191) + estimate_length
+// (workload.cpp:113-139) + generate_arrivals (workload.cpp:141-170).
+bsg_status make_records(const bsg_workload& w, std::vector<Record>* out) {
+  if (!(w.qps > 0)) return BSG_INVALID_ARGUMENT;
+  Rng rng(w.trace_seed);
+  int n = w.count;
+  std::vector<Record> recs;
+  recs.reserve(n);
+  for (int i = 0; i < n; ++i) {
+    const double p = w.prompt_median * std::exp(w.prompt_sigma * rng.normal());
+    const double o = w.output_median * std::exp(w.output_sigma * rng.normal());
+    Record r{};
+    r.prompt = static_cast<int32_t>(std::clamp<double>(std::round(p), w.min_tokens, w.max_prompt_tokens));
+    r.output = static_cast<int32_t>(std::clamp<double>(std::round(o), w.min_tokens, w.max_output_tokens));
+    recs.push_back(r);
+  }
+  if (w.request_cap >= 0 && w.request_cap < n) recs.resize(w.request_cap);
+  Rng arr(w.arrival_seed);
+  int64_t t = 0;
+  for (size_t i = 0; i < recs.size(); ++i) {
+    Record& r = recs[i];
+    switch (w.estimator_kind) {
+      case 1: r.est = w.fixed_tokens; break;
+      case 2: {
+        Rng e(mix_seed(w.estimator_seed, static_cast<uint64_t>(i)));
+        const double half = std::abs(e.normal());
+        const double sign = (e.next() & 1) ? 1.0 : -1.0;
+        const double scale = w.mean_abs_rel_error * std::sqrt(3.14159265358979323846 / 2.0);
+        const double est = std::round(static_cast<double>(r.output) * (1.0 + sign * half * scale));
+        r.est = static_cast<int32_t>(std::max(1.0, est));
+        break;
+      }
+      default: r.est = r.output;
+    }
+    t += ticks_from_seconds(arr.exponential(w.qps));
+    r.arrival = t;
+  }
+  *out = std::move(recs);
+  return BSG_OK;
+}
+
+int64_t blocks(int64_t t, int32_t bs) { return t <= 0 ? 0 : (t + bs - 1) / bs; }
+
+// ---- live serving instance ------------------------------------------------
+struct Member {
+  int32_t prompt, target, est, prefill, decoded;
+  int32_t rid;
+  bool ever;
+  int32_t stored() const { return prefill + decoded; }
+  bool ready() const { return prefill == prompt; }
+};
+
+class LiveInstance {
+ public:
+  explicit LiveInstance(const bsg_instance_cfg& c) : c_(c), free_(c.total_blocks) {}
+
+  void admit(int32_t rid, int32_t prompt, int32_t target, int32_t est) {
+    fifo_.push_back(Member{prompt, target, est, 0, 0, rid, false});
+  }
+  bool has_work() const { return n_ > 0 || res_.size() > static_cast<size_t>(n_) || !fifo_.empty(); }
+  bool mid_step() const { return mid_; }
+
+  // Status snapshot (Instance::snapshot semantics, backend.cpp:351-373): running
+  // in admission order, waiting head first, free recomputed from stored tokens.
+  void snapshot(std::vector<Member>* running, std::vector<Member>* waiting, int32_t* free_blocks,
+                int32_t* batch) const {
+    running->assign(res_.begin(), res_.begin() + n_);
+    waiting->assign(res_.begin() + n_, res_.end());
+    waiting->insert(waiting->end(), fifo_.begin(), fifo_.end());
+    int64_t held = 0;
+    for (int32_t p = 0; p < n_; ++p) held += blocks(res_[p].stored(), c_.block_size);
+    *free_blocks = static_cast<int32_t>(c_.total_blocks - held);
+    *batch = n_;
+  }
+
+  // Forms the batch, admits, allocates with newest-member preemption and prices
+  // the step. Returns the step duration in ticks; appends victim request ids.
+  bsg_status begin_step(int64_t* duration, std::vector<int32_t>* preempted) {
+    const int32_t bs = c_.block_size;
+    const bool chunked = c_.local_policy == BSG_CHUNKED_PREFILL;
+    const int32_t L = static_cast<int32_t>(res_.size());
+    chunk_.assign(res_.size(), 0);
+    decode_.assign(res_.size(), 0);
+    std::vector<int32_t> delta(res_.size(), 0);
+    int32_t D = 0;
+    bool any_nonready = false;
+    for (int32_t p = 0; p < n_; ++p) {
+      if (res_[p].ready()) ++D;
+      else any_nonready = true;
+    }
+    const bool waiting = L > n_ || !fifo_.empty();
+    int64_t budget = 0;
+    bool prefill_step = false;
+    if (chunked) {
+      budget = std::max<int64_t>(0, static_cast<int64_t>(c_.chunk_budget) - D);
+      for (int32_t p = 0; p < n_; ++p) decode_[p] = res_[p].ready();
+      for (int32_t p = 0; p < n_ && budget > 0; ++p) {
+        if (!res_[p].ready()) {
+          chunk_[p] = static_cast<int32_t>(std::min<int64_t>(res_[p].prompt - res_[p].prefill, budget));
+          budget -= chunk_[p];
+        }
+      }
+    } else {
+      prefill_step = waiting || any_nonready;
+      for (int32_t p = 0; p < n_; ++p) {
+        if (prefill_step && !res_[p].ready()) chunk_[p] = res_[p].prompt - res_[p].prefill;
+        decode_[p] = !prefill_step && res_[p].ready();
+      }
+    }
+    auto item_delta = [&](const Member& m, bool dec, int32_t ch) -> int32_t {
+      const int32_t s = m.stored();
+      int32_t ns = s;
+      if (dec) ns = s + 1;
+      else if (ch > 0) ns = m.prefill + ch + m.decoded + (m.prefill + ch == m.prompt ? 1 : 0);
+      return static_cast<int32_t>(blocks(ns, bs) - blocks(s, bs));
+    };
+    int64_t pf = free_;
+    for (int32_t p = 0; p < n_; ++p) {
+      if (decode_[p] || chunk_[p] > 0) {
+        delta[p] = item_delta(res_[p], decode_[p], chunk_[p]);
+        pf -= delta[p];
+      }
+    }
+    // waiting admissions: victim stack first, then FIFO arrivals
+    int32_t a = 0;
+    std::vector<int32_t> adm_chunk, adm_delta;
+    {
+      int32_t members = n_;
+      const size_t total_wait = static_cast<size_t>(L - n_) + fifo_.size();
+      for (size_t j = 0; j < total_wait; ++j) {
+        if ((chunked && budget == 0) || members >= c_.max_batch_size) break;
+        const Member& m = j < static_cast<size_t>(L - n_) ? res_[n_ + j] : fifo_[j - (L - n_)];
+        int32_t ch = m.prompt - m.prefill;
+        if (chunked) ch = static_cast<int32_t>(std::min<int64_t>(ch, budget));
+        const int32_t d = item_delta(m, false, ch);
+        if (d > pf) break;
+        adm_chunk.push_back(ch);
+        adm_delta.push_back(d);
+        if (chunked) budget -= ch;
+        pf -= d;
+        ++members;
+        ++a;
+      }
+    }
+    if (!chunked && prefill_step && !any_nonready && a == 0) {
+      for (int32_t p = 0; p < n_; ++p) {
+        decode_[p] = res_[p].ready();
+        delta[p] = decode_[p] ? item_delta(res_[p], true, 0) : 0;
+      }
+    }
+    if (n_ == 0 && a == 0) return BSG_EMPTY_PLAN;
+    // admissions move waiting heads into the running tail
+    const int32_t n_adm = n_ + a;
+    for (int32_t j = 0; j < a; ++j) {
+      if (n_ + j >= static_cast<int32_t>(res_.size())) {
+        res_.push_back(fifo_.front());
+        fifo_.pop_front();
+        chunk_.push_back(0);
+        decode_.push_back(0);
+        delta.push_back(0);
+      }
+      chunk_[n_ + j] = adm_chunk[j];
+      delta[n_ + j] = adm_delta[j];
+      res_[n_ + j].ever = true;
+    }
+    // allocation: survivors e* = max{e : F(e) >= 0} (see scenario_sim.cuh)
+    int64_t tot = 0;
+    for (int32_t p = 0; p < n_adm; ++p) tot += delta[p];
+    int32_t e_star = n_adm;
+    if (tot > free_) {
+      int64_t f = free_;
+      for (int32_t p = 0; p < n_; ++p) f += blocks(res_[p].stored(), bs);  // F(0)
+      // F(e+1) = F(e) - held_old[e] - delta[e]
+      e_star = 0;
+      for (int32_t p = 0; p < n_adm; ++p) {
+        const int64_t fn = f - (p < n_ ? blocks(res_[p].stored(), bs) : 0) - delta[p];
+        if (fn < 0) break;
+        f = fn;
+        e_star = p + 1;
+      }
+      if (e_star == 0) return BSG_DEADLOCK;
+      free_ = f;
+      for (int32_t p = n_adm - 1; p >= e_star; --p) {
+        preempted->push_back(res_[p].rid);
+        res_[p].prefill = 0;
+        res_[p].decoded = 0;
+        chunk_[p] = 0;
+        decode_[p] = 0;
+      }
+    } else {
+      free_ -= tot;
+    }
+    n_ = e_star;
+    int64_t ctx = 0, pt = 0, nd = 0;
+    for (int32_t p = 0; p < n_; ++p) {
+      if (decode_[p]) {
+        ++nd;
+        ctx += res_[p].stored();
+      } else if (chunk_[p] > 0) {
+        pt += chunk_[p];
+      }
+    }
+    if (c_.cache_mode == BSG_CACHE_BUCKETED) {
+      const int64_t b = std::max(1, c_.context_bucket);
+      ctx = (ctx + b / 2) / b * b;
+    }
+    const double x = c_.c0_s + c_.prefill_s_per_token * static_cast<double>(pt) +
+                     c_.decode_s_per_seq * static_cast<double>(nd) +
+                     c_.context_s_per_token * static_cast<double>(ctx);
+    *duration = ticks_from_seconds(x);
+    mid_ = true;
+    return BSG_OK;
+  }
+
+  void finish_step(std::vector<int32_t>* first_tokens, std::vector<int32_t>* completed) {
+    std::vector<char> done(res_.size(), 0);
+    for (int32_t p = 0; p < n_; ++p) {
+      Member& m = res_[p];
+      const bool item = decode_[p] || chunk_[p] > 0;
+      if (!item) continue;
+      const int32_t prev = m.decoded;
+      if (decode_[p]) {
+        m.decoded += 1;
+      } else {
+        m.prefill += chunk_[p];
+        if (m.prefill == m.prompt) m.decoded += 1;
+      }
+      if (prev == 0 && m.decoded >= 1) first_tokens->push_back(m.rid);
+      if (m.decoded >= m.target) {
+        completed->push_back(m.rid);
+        done[p] = 1;
+      }
+    }
+    std::vector<Member> keep;
+    keep.reserve(res_.size());
+    int32_t removed = 0;
+    for (size_t p = 0; p < res_.size(); ++p) {
+      if (done[p]) {
+        free_ += blocks(res_[p].stored(), c_.block_size);
+        ++removed;
+      } else {
+        keep.push_back(res_[p]);
+      }
+    }
+    res_.swap(keep);
+    n_ -= removed;
+    mid_ = false;
+  }
+
+ private:
+  bsg_instance_cfg c_;
+  std::vector<Member> res_;  // [0,n) running, [n, L) victims (waiting front)
+  int32_t n_ = 0;
+  std::deque<Member> fifo_;
+  int64_t free_;
+  bool mid_ = false;
+  std::vector<int32_t> chunk_;
+  std::vector<char> decode_;
+};
+
+// ---- DES kernel (event_loop.cpp:28-57 semantics) --------------------------
+struct Ev {
+  int64_t t;
+  uint64_t seq;
+  int32_t kind;  // 0 arrival, 1 batch complete
+  int32_t a;
+  bool operator>(const Ev& o) const { return t != o.t ? t > o.t : seq > o.seq; }
+};
+
+struct QpmWindow {  // QpmTracker (scheduler.cpp:48-63)
+  std::deque<int64_t> w;
+  void record(int64_t now) {
+    w.push_back(now);
+    const int64_t cutoff = now - ticks_from_seconds(60.0);
+    while (!w.empty() && w.front() <= cutoff) w.pop_front();
+  }
+  int qpm(int64_t now) const {
+    const int64_t cutoff = now - ticks_from_seconds(60.0);
+    return static_cast<int>(w.end() - std::upper_bound(w.begin(), w.end(), cutoff));
+  }
+};
+
+}  // namespace
+
+struct bsg_capture {
+  std::vector<uint64_t> id;
+  std::vector<int32_t> prompt, est, prefill, decoded;
+  std::vector<bsg_scenario> scenarios;
+};
+
+namespace {
+
+class Replay {
+ public:
+  Replay(bsg_ctx* ctx, const bsg_instance_cfg& cfg, const bsg_replay_spec& spec,
+         std::vector<Record> recs, bsg_capture* cap)
+      : ctx_(ctx), cfg_(cfg), spec_(spec), recs_(std::move(recs)), cap_(cap), rng_(spec.policy_seed) {
+    for (int i = 0; i < spec.n_instances; ++i) inst_.emplace_back(cfg);
+    qpm_.resize(spec.n_instances);
+    out_.resize(recs_.size());
+    for (size_t i = 0; i < recs_.size(); ++i) {
+      out_[i] = bsg_request_outcome{recs_[i].arrival, -1, -1, -1, -1, 0};
+      push(recs_[i].arrival, 0, static_cast<int32_t>(i));
+    }
+  }
+
+  bsg_status run() {
+    bool open = false;
+    for (;;) {
+      if (q_.empty() || (open && q_.top().t > now_)) {
+        if (open) {
+          open = false;
+          const bsg_status st = end_of_instant();
+          if (st != BSG_OK) return st;
+          continue;
+        }
+        if (q_.empty()) break;
+      }
+      const Ev ev = q_.top();
+      q_.pop();
+      now_ = ev.t;
+      const bsg_status st = ev.kind == 0 ? arrival(ev.a) : complete(ev.a);
+      if (st != BSG_OK) return st;
+      open = true;
+    }
+    return BSG_OK;
+  }
+
+  const std::vector<bsg_request_outcome>& outcomes() const { return out_; }
+  int64_t preemptions() const { return preemptions_; }
+
+ private:
+  void push(int64_t t, int32_t kind, int32_t a) { q_.push(Ev{t, seq_++, kind, a}); }
+
+  bsg_status end_of_instant() {  // driver.cpp:271-289
+    for (size_t i = 0; i < inst_.size(); ++i) {
+      LiveInstance& li = inst_[i];
+      if (li.mid_step() || !li.has_work()) continue;
+      int64_t dur = 0;
+      victims_.clear();
+      const bsg_status st = li.begin_step(&dur, &victims_);
+      if (st != BSG_OK) return st;
+      push(now_ + dur, 1, static_cast<int32_t>(i));
+      for (int32_t rid : victims_) {
+        out_[rid].preempt_count += 1;
+        preemptions_ += 1;
+      }
+    }
+    return BSG_OK;
+  }
+
+  bsg_status complete(int32_t iid) {  // driver.cpp:233-251
+    firsts_.clear();
+    dones_.clear();
+    inst_[iid].finish_step(&firsts_, &dones_);
+    for (int32_t rid : firsts_)
+      if (out_[rid].first_token_ticks < 0) out_[rid].first_token_ticks = now_;
+    for (int32_t rid : dones_) out_[rid].finish_ticks = now_;
+    return BSG_OK;
+  }
+
+  bsg_status arrival(int32_t rid) {  // driver.cpp:134-219 (static, no probes)
+    const int n = static_cast<int>(inst_.size());
+    snaps_run_.resize(n);
+    snaps_wait_.resize(n);
+    free_.resize(n);
+    batch_.resize(n);
+    for (int i = 0; i < n; ++i)
+      inst_[i].snapshot(&snaps_run_[i], &snaps_wait_[i], &free_[i], &batch_[i]);
+    int32_t chosen = 0;
+    const bsg_status st = decide(rid, &chosen);
+    if (st != BSG_OK) return st;
+    qpm_[chosen].record(now_);
+    const Record& r = recs_[rid];
+    inst_[chosen].admit(rid, r.prompt, r.output, r.est);
+    out_[rid].dispatch_ticks = now_;
+    out_[rid].instance = chosen;
+    return BSG_OK;
+  }
+
+  // Dispatcher::dispatch (scheduler.cpp:115-152) with the heuristics of
+  // pick_heuristic (scheduler.cpp:68-113).
+  bsg_status decide(int32_t rid, int32_t* chosen) {
+    const int n = static_cast<int>(inst_.size());
+    switch (spec_.policy) {
+      case BSG_POLICY_RANDOM: *chosen = static_cast<int32_t>(rng_.below(n)); return BSG_OK;
+      case BSG_POLICY_ROUND_ROBIN: *chosen = static_cast<int32_t>(rr_++ % n); return BSG_OK;
+      case BSG_POLICY_MIN_QPM:
+      case BSG_POLICY_INFAAS_PP:
+      case BSG_POLICY_LLUMNIX_MINUS: {
+        double best = std::numeric_limits<double>::infinity();
+        int32_t best_id = 0;
+        for (int i = 0; i < n; ++i) {
+          double score = 0;
+          const double used = static_cast<double>(cfg_.total_blocks - free_[i]);
+          const double bsz = static_cast<double>(std::max(batch_[i], 1));
+          if (spec_.policy == BSG_POLICY_MIN_QPM) {
+            score = static_cast<double>(qpm_[i].qpm(now_));
+          } else if (spec_.policy == BSG_POLICY_INFAAS_PP) {
+            score = used / bsz;  // load_infaas, scheduler.cpp:33-36
+          } else {
+            int64_t pm = 0;  // load_llumnix, scheduler.cpp:38-46
+            for (const Member& m : snaps_wait_[i]) pm += blocks(m.prompt - m.prefill, cfg_.block_size);
+            score = (used + static_cast<double>(pm)) / bsz;
+          }
+          if (i == 0 || score < best) {
+            best = score;
+            best_id = i;
+          }
+        }
+        *chosen = best_id;
+        return BSG_OK;
+      }
+      default: break;
+    }
+    // BlockPredictive: per-instance what-ifs on the GPU, argmin with lowest-id ties.
+    prompt_.clear();
+    est_.clear();
+    prefill_.clear();
+    decoded_.clear();
+    ids_.clear();
+    scen_.assign(n, bsg_scenario{});
+    inst_ids_.resize(n);
+    const Record& r = recs_[rid];
+    for (int i = 0; i < n; ++i) {
+      bsg_scenario& sc = scen_[i];
+      sc.run_off = static_cast<int32_t>(prompt_.size());
+      sc.run_n = static_cast<int32_t>(snaps_run_[i].size());
+      for (const Member& m : snaps_run_[i]) add(m);
+      sc.wait_off = static_cast<int32_t>(prompt_.size());
+      sc.wait_n = static_cast<int32_t>(snaps_wait_[i].size());
+      for (const Member& m : snaps_wait_[i]) add(m);
+      sc.cand_prompt = r.prompt;
+      sc.cand_est = r.est;
+      sc.cfg = 0;
+      inst_ids_[i] = i;
+    }
+    if (cap_) {
+      const int32_t base = static_cast<int32_t>(cap_->prompt.size());
+      for (bsg_scenario sc : scen_) {
+        sc.run_off += base;
+        sc.wait_off += base;
+        cap_->scenarios.push_back(sc);
+      }
+      cap_->id.insert(cap_->id.end(), ids_.begin(), ids_.end());
+      cap_->prompt.insert(cap_->prompt.end(), prompt_.begin(), prompt_.end());
+      cap_->est.insert(cap_->est.end(), est_.begin(), est_.end());
+      cap_->prefill.insert(cap_->prefill.end(), prefill_.begin(), prefill_.end());
+      cap_->decoded.insert(cap_->decoded.end(), decoded_.begin(), decoded_.end());
+    }
+    bsg_entries e{ids_.data(), prompt_.data(), est_.data(), prefill_.data(), decoded_.data()};
+    int32_t pick = -1;
+    per_.resize(n);
+    const bsg_status st = bsg_dispatch(ctx_, &e, static_cast<int64_t>(prompt_.size()), scen_.data(),
+                                       inst_ids_.data(), n, 1, spec_.objective, &pick, per_.data());
+    if (st != BSG_OK) return st;
+    if (pick < 0) {
+      for (const bsg_result& x : per_)
+        if (x.status != BSG_OK) return static_cast<bsg_status>(x.status);
+      return BSG_INVALID_ARGUMENT;
+    }
+    *chosen = pick;
+    return BSG_OK;
+  }
+
+  void add(const Member& m) {
+    ids_.push_back(static_cast<uint64_t>(m.rid));
+    prompt_.push_back(m.prompt);
+    est_.push_back(m.est);
+    prefill_.push_back(m.prefill);
+    decoded_.push_back(m.decoded);
+  }
+
+  bsg_ctx* ctx_;
+  bsg_instance_cfg cfg_;
+  bsg_replay_spec spec_;
+  std::vector<Record> recs_;
+  bsg_capture* cap_;
+  Rng rng_;
+  uint64_t rr_ = 0;
+  std::vector<LiveInstance> inst_;
+  std::vector<QpmWindow> qpm_;
+  std::vector<bsg_request_outcome> out_;
+  std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> q_;
+  uint64_t seq_ = 0;
+  int64_t now_ = 0;
+  int64_t preemptions_ = 0;
+  std::vector<int32_t> victims_, firsts_, dones_;
+  std::vector<std::vector<Member>> snaps_run_, snaps_wait_;
+  std::vector<int32_t> free_, batch_;
+  std::vector<int32_t> prompt_, est_, prefill_, decoded_, inst_ids_;
+  std::vector<uint64_t> ids_;
+  std::vector<bsg_scenario> scen_;
+  std::vector<bsg_result> per_;
+};
+
+}  // namespace
+
+extern "C" {
+
+bsg_status bsg_make_workload(const bsg_workload* w, int32_t* prompt, int32_t* output, int32_t* est,
+                             int64_t* arrival_ticks) {
+  if (!w) return BSG_INVALID_ARGUMENT;
+  std::vector<Record> recs;
+  const bsg_status st = make_records(*w, &recs);
+  if (st != BSG_OK) return st;
+  for (size_t i = 0; i < recs.size(); ++i) {
+    prompt[i] = recs[i].prompt;
+    output[i] = recs[i].output;
+    est[i] = recs[i].est;
+    arrival_ticks[i] = recs[i].arrival;
+  }
+  return BSG_OK;
+}
+
+bsg_status bsg_replay(bsg_ctx* ctx, const bsg_workload* w, const bsg_instance_cfg* cfg,
+                      const bsg_replay_spec* spec, bsg_request_outcome* outcomes,
+                      int64_t* total_preemptions, bsg_capture** capture) {
+  if (!ctx || !w || !cfg || !spec || spec->n_instances < 1) return BSG_INVALID_ARGUMENT;
+  int32_t bi = 0, fc = 0;
+  bsg_status st = bsg_set_configs(ctx, cfg, 1, &bi, &fc);
+  if (st != BSG_OK) return st;
+  std::vector<Record> recs;
+  st = make_records(*w, &recs);
+  if (st != BSG_OK) return st;
+  // Workload must be servable at all (config.cpp:197-205).
+  for (const Record& r : recs)
+    if (blocks(static_cast<int64_t>(r.prompt) + r.output, cfg->block_size) > cfg->total_blocks)
+      return BSG_TOO_LARGE_CANDIDATE;
+  std::unique_ptr<bsg_capture> cap(capture ? new bsg_capture() : nullptr);
+  Replay replay(ctx, *cfg, *spec, std::move(recs), cap.get());
+  st = replay.run();
+  if (st != BSG_OK) return st;
+  if (outcomes)
+    std::memcpy(outcomes, replay.outcomes().data(),
+                replay.outcomes().size() * sizeof(bsg_request_outcome));
+  if (total_preemptions) *total_preemptions = replay.preemptions();
+  if (capture) *capture = cap.release();
+  return BSG_OK;
+}
+
+void bsg_capture_sizes(const bsg_capture* c, int64_t* n_entries, int64_t* n_scenarios) {
+  *n_entries = static_cast<int64_t>(c->prompt.size());
+  *n_scenarios = static_cast<int64_t>(c->scenarios.size());
+}
+
+void bsg_capture_copy(const bsg_capture* c, uint64_t* id, int32_t* prompt, int32_t* est,
+                      int32_t* prefill, int32_t* decoded, bsg_scenario* scenarios) {
+  const size_t n = c->prompt.size();
+  if (id) std::memcpy(id, c->id.data(), n * sizeof(uint64_t));
+  std::memcpy(prompt, c->prompt.data(), n * sizeof(int32_t));
+  std::memcpy(est, c->est.data(), n * sizeof(int32_t));
+  std::memcpy(prefill, c->prefill.data(), n * sizeof(int32_t));
+  std::memcpy(decoded, c->decoded.data(), n * sizeof(int32_t));
+  std::memcpy(scenarios, c->scenarios.data(), c->scenarios.size() * sizeof(bsg_scenario));
+}
+
+void bsg_capture_free(bsg_capture* c) { delete c; }
+
+}  // extern "C"

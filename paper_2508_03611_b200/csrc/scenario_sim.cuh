@@ -1,0 +1,664 @@
+// scenario_sim.cuh — K1: warp-per-scenario what-if simulation (sm_100a).
+//
+// One warp replays one instance's continuous-batching engine forward from a
+// snapshot with the candidate appended to the waiting tail, until the
+// candidate completes: blocksim predict() (core/src/predictor.cpp:76-137)
+// driving Instance::execute_step (core/src/backend.cpp:238-331).
+//
+// State layout (per warp, in registers): the "resident list" of up to 32*K
+// members, position p held by lane p / K, register slot p % K (contiguous, so
+// prefix scans are lane-local + one warp scan):
+//   positions [0, n)  : running_ in admission order (backend.h:157)
+//   positions [n, L)  : preemption victims = the FRONT of waiting_, head first
+//   then, virtually   : snapshot.waiting[h..wait_n) (read-only, HBM/L2), then the
+//                       candidate if it was never admitted.
+// Because the victim of every preemption is the newest running member (the
+// running tail) and victims go to the waiting FRONT, preemption is
+// "n -= 1" and admission of a victim is "n += 1": both are boundary moves.
+//
+// Allocation with preemption (backend.cpp:263-288) is evaluated in parallel:
+// with F(e) = free + sum_{v>=e} held_old[v] - sum_{items at pos<e} delta, which
+// is non-increasing in e, the sequential victim loop ends with exactly
+// e* = max{e : F(e) >= 0} survivors, and deadlocks iff e* == 0 (DESIGN.md §4
+// derives this). One ballot finds e*.
+//
+// Floating point: batch_latency's unfused ((c0 + p*T) + d*D) + c*C in double
+// (backend.cpp:10-14) with __dmul_rn/__dadd_rn (no contraction), then llround
+// (time.h:20-22); elapsed is an int64 tick sum, so results are bit-exact.
+#pragma once
+
+#include <cstdint>
+
+#include "../../include/blocksim_b200.h"
+
+namespace bsg {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int64_t kMaxSimulatedSteps = 50000000LL;  // predictor.cpp:11
+
+// Device-side config: bsg_instance_cfg + precomputed block-size divisor.
+struct DevCfg {
+  int32_t total_blocks, block_size, max_batch_size, chunk_budget;
+  int32_t local_policy, cache_mode, context_bucket;
+  uint32_t div_magic;   // 0 => power of two
+  int32_t div_shift;
+  int32_t pad[3];
+  double c0, cp, cd, cc;
+};
+
+// floor(n / block_size) for 0 <= n < 2^31 (Granlund-Montgomery, N = 31).
+__device__ __forceinline__ int32_t div_bs(int32_t n, const DevCfg& c) {
+  if (c.div_magic == 0) return n >> c.div_shift;
+  return static_cast<int32_t>(__umulhi(static_cast<uint32_t>(n), c.div_magic) >> c.div_shift);
+}
+// blocks_needed (types.cpp:63-66): tokens <= 0 ? 0 : ceil(tokens / block_size).
+__device__ __forceinline__ int32_t bn(int32_t t, const DevCfg& c) {
+  return t <= 0 ? 0 : div_bs(t + c.block_size - 1, c);
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ int32_t warp_incl_scan(int32_t x) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int32_t y = __shfl_up_sync(kFull, x, d);
+    if (lane >= d) x += y;
+  }
+  return x;
+}
+
+// Exclusive prefix over positions (lane-contiguous layout); returns the total.
+template <int K>
+__device__ __forceinline__ int32_t excl_scan(const int32_t (&in)[K], int32_t (&out)[K]) {
+  int32_t s = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    out[k] = s;
+    s += in[k];
+  }
+  const int32_t incl = warp_incl_scan(s);
+  const int32_t base = incl - s;
+#pragma unroll
+  for (int k = 0; k < K; ++k) out[k] += base;
+  return __shfl_sync(kFull, incl, 31);
+}
+
+template <int K>
+__device__ __forceinline__ int32_t warp_sum(const int32_t (&in)[K]) {
+  int32_t s = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) s += in[k];
+  return static_cast<int32_t>(__reduce_add_sync(kFull, static_cast<uint32_t>(s)));
+}
+
+// Position of the first set flag (or `none`).
+template <int K>
+__device__ __forceinline__ int32_t first_pos(const bool (&f)[K], int32_t none) {
+  int32_t local = none;
+#pragma unroll
+  for (int k = K - 1; k >= 0; --k)
+    if (f[k]) local = lane_id() * K + k;
+  return static_cast<int32_t>(__reduce_min_sync(kFull, static_cast<uint32_t>(local)));
+}
+
+template <int K>
+__device__ __forceinline__ int32_t count(const bool (&f)[K]) {
+  int32_t c = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) c += __popc(__ballot_sync(kFull, f[k]));
+  return c;
+}
+
+// Reads position p's value of a per-lane register array (warp-uniform p).
+template <int K>
+__device__ __forceinline__ int32_t read_pos(const int32_t (&v)[K], int32_t p) {
+  int32_t mine = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if (k == p % K) mine = v[k];
+  return __shfl_sync(kFull, mine, p / K);
+}
+
+// The member "org" word: bit 31 = ever_scheduled (backend.h:124),
+// bits 0..30 = origin + 1 (origin: running i -> i, waiting j -> run_n + j,
+// candidate -> -1).
+__device__ __forceinline__ int32_t org_origin(int32_t w) { return (w & 0x7fffffff) - 1; }
+__device__ __forceinline__ bool org_ever(int32_t w) { return (w >> 31) & 1; }
+constexpr int32_t kEverBit = static_cast<int32_t>(0x80000000u);
+constexpr int32_t kCandOrg = 0;  // origin -1 -> org 0 (never scheduled)
+
+__device__ __forceinline__ uint64_t hash_term(uint32_t tag, uint32_t k, int32_t origin, int32_t v) {
+  return bsg_hash_term(tag, k, origin, v);
+}
+
+// latency (backend.cpp:10-14; bucketed context predictor.cpp:29-32) -> ticks (time.h:20-22)
+__device__ __forceinline__ int64_t step_ticks(const DevCfg& c, int32_t prefill_tokens,
+                                              int32_t n_decode, int32_t context) {
+  int64_t ctx = context;
+  if (c.cache_mode == BSG_CACHE_BUCKETED) {
+    const int64_t b = c.context_bucket < 1 ? 1 : c.context_bucket;
+    ctx = (ctx + b / 2) / b * b;
+  }
+  double x = __dadd_rn(c.c0, __dmul_rn(c.cp, static_cast<double>(prefill_tokens)));
+  x = __dadd_rn(x, __dmul_rn(c.cd, static_cast<double>(n_decode)));
+  x = __dadd_rn(x, __dmul_rn(c.cc, static_cast<double>(ctx)));
+  return llround(__dmul_rn(x, 1e9));
+}
+
+struct TraceSink {
+  bsg_step_record* rec;
+  int64_t cap;
+};
+
+// Simulates one scenario with the calling warp. All lanes return the same
+// result; lane 0 writes it.
+template <int K, bool TRACE>
+__device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__ g_prompt,
+                                  const int32_t* __restrict__ g_est,
+                                  const int32_t* __restrict__ g_prefill,
+                                  const int32_t* __restrict__ g_decoded, const bsg_scenario sc,
+                                  int32_t* __restrict__ smem,  // 5 * 32 * K int32 per warp
+                                  bsg_result* __restrict__ out, TraceSink trace) {
+  constexpr int CAP = 32 * K;
+  const int lane = lane_id();
+  bsg_result res{};
+
+  // ---- load running entries: from_snapshot (backend.cpp:24-41) with
+  // correct_lengths (predictor.cpp:65-74) applied to est -> target.
+  int32_t prompt[K], target[K], prefill[K], decoded[K], org[K];
+  const int32_t run_n = sc.run_n;
+  bool bad = false;
+  int32_t held[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int32_t p = lane * K + k;
+    prompt[k] = 1;
+    target[k] = 0;
+    prefill[k] = 0;
+    decoded[k] = 0;
+    org[k] = 0;
+    held[k] = 0;
+    if (p < run_n) {
+      const int32_t g = sc.run_off + p;
+      prompt[k] = __ldg(g_prompt + g);
+      const int32_t est = __ldg(g_est + g);
+      prefill[k] = __ldg(g_prefill + g);
+      decoded[k] = __ldg(g_decoded + g);
+      target[k] = decoded[k] >= est ? decoded[k] + 10 : est;
+      org[k] = (p + 1) | kEverBit;
+      bad |= prompt[k] < 1 || prompt[k] > (1 << 22) || prefill[k] < 0 || prefill[k] > prompt[k] ||
+             decoded[k] < 0 || decoded[k] > (1 << 22) || est > (1 << 24);
+      held[k] = bn(prefill[k] + decoded[k], cfg);
+    }
+  }
+  if (__any_sync(kFull, bad) || run_n > CAP) {
+    res.status = BSG_BAD_INPUT;
+    if (lane == 0) *out = res;
+    return;
+  }
+  int32_t free_blocks = cfg.total_blocks - warp_sum<K>(held);
+  if (free_blocks < 0) {  // backend.cpp:42-44
+    res.status = BSG_TOO_LARGE_RUNNING;
+    if (lane == 0) *out = res;
+    return;
+  }
+  // waiting entries: validated lazily as they are read; the candidate's admit check
+  // (backend.cpp:76-83):
+  {
+    const int64_t need = (static_cast<int64_t>(sc.cand_prompt) + sc.cand_est + cfg.block_size - 1) /
+                         cfg.block_size;
+    if (sc.cand_prompt < 1 || sc.cand_prompt > (1 << 22) || sc.cand_est < 0 ||
+        sc.cand_est > (1 << 24)) {
+      res.status = BSG_BAD_INPUT;
+      if (lane == 0) *out = res;
+      return;
+    }
+    if (need > cfg.total_blocks) {
+      res.status = BSG_TOO_LARGE_CANDIDATE;
+      res.detail = static_cast<int32_t>(need);
+      if (lane == 0) *out = res;
+      return;
+    }
+  }
+
+  int32_t n = run_n;   // running count
+  int32_t L = run_n;   // running + victim stack
+  int32_t h = 0;       // next unread snapshot.waiting index
+  bool cand_tail = true;
+  int64_t elapsed = 0, steps = 0;
+  bool qd_set = false, ttft_set = false;
+  const int32_t wait_n = sc.wait_n;
+  const bool chunked = cfg.local_policy == BSG_CHUNKED_PREFILL;
+  const int32_t maxb = cfg.max_batch_size;
+
+  for (;;) {
+    const bool waiting_nonempty = (L > n) || (h < wait_n) || cand_tail;
+    if (n == 0 && !waiting_nonempty) {  // predictor.cpp:102-104
+      res.status = BSG_VANISHED;
+      break;
+    }
+    // ---------------- plan (backend.cpp:113-182) ----------------
+    bool ready[K], nonready[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int32_t p = lane * K + k;
+      ready[k] = p < n && prefill[k] == prompt[k];
+      nonready[k] = p < n && prefill[k] != prompt[k];
+    }
+    const int32_t D = count<K>(ready);
+    bool any_local = false;
+#pragma unroll
+    for (int k = 0; k < K; ++k) any_local |= nonready[k];
+    const bool any_nonready = __any_sync(kFull, any_local);
+    int32_t chunk[K];
+    bool decode_item[K];
+    int32_t budget = 0;  // budget left for waiting admissions (chunked prefill)
+    bool prefill_step = false;  // prefill-priority pure-prefill step
+    if (chunked) {
+      int32_t b0 = cfg.chunk_budget - D;  // one budget token per decode (backend.cpp:116-121)
+      if (b0 < 0) b0 = 0;
+      budget = b0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        chunk[k] = 0;
+        decode_item[k] = ready[k];
+      }
+      if (any_nonready) {  // running partial prefills in order, break at budget 0 (122-130)
+        int32_t rem[K], S[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) rem[k] = nonready[k] ? prompt[k] - prefill[k] : 0;
+        const int32_t tot = excl_scan<K>(rem, S);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          int32_t c = b0 - S[k];
+          c = c < 0 ? 0 : c;
+          chunk[k] = nonready[k] ? (c < rem[k] ? c : rem[k]) : 0;
+        }
+        budget = b0 - tot;
+        if (budget < 0) budget = 0;
+      }
+    } else {
+      prefill_step = waiting_nonempty || any_nonready;  // backend.cpp:152-155
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        chunk[k] = (prefill_step && nonready[k]) ? prompt[k] - prefill[k] : 0;
+        decode_item[k] = !prefill_step && ready[k];
+      }
+    }
+    // deltas of running items (make_item, backend.cpp:94-111)
+    int32_t delta[K], stored[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      stored[k] = prefill[k] + decoded[k];
+      int32_t ns = stored[k];
+      if (decode_item[k]) {
+        ns = stored[k] + 1;
+      } else if (chunk[k] > 0) {
+        const int32_t np = prefill[k] + chunk[k];
+        ns = np + decoded[k] + (np == prompt[k] ? 1 : 0);
+      }
+      delta[k] = (decode_item[k] || chunk[k] > 0) ? bn(ns, cfg) - bn(stored[k], cfg) : 0;
+    }
+    const int32_t run_delta = warp_sum<K>(delta);
+
+    // ---------------- waiting admissions ----------------
+    int32_t a = 0;  // admitted waiting heads
+    const bool try_admit =
+        waiting_nonempty && n < maxb && (chunked ? budget > 0 : true);
+    if (try_admit) {
+      const int32_t pf = free_blocks - run_delta;  // projected_free (backend.cpp:131-133 / 158-164)
+      // Materialise waiting heads at positions [L, CAP): snapshot.waiting[h..], then candidate.
+      bool valid[K];
+      int32_t wprompt[K], fdelta[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int32_t p = lane * K + k;
+        valid[k] = p >= n && p < maxb;
+        if (p >= L) {
+          const int32_t j = h + (p - L);
+          if (j < wait_n) {
+            const int32_t g = sc.wait_off + j;
+            prompt[k] = __ldg(g_prompt + g);
+            const int32_t est = __ldg(g_est + g);
+            const int32_t dec = __ldg(g_decoded + g);
+            target[k] = dec >= est ? dec + 10 : est;  // correct_lengths on waiting too
+            org[k] = run_n + j + 1;
+          } else if (j == wait_n && cand_tail) {
+            prompt[k] = sc.cand_prompt;
+            target[k] = sc.cand_est;
+            org[k] = kCandOrg;
+          } else {
+            valid[k] = false;
+          }
+          prefill[k] = 0;
+          decoded[k] = 0;
+        }
+        wprompt[k] = valid[k] ? prompt[k] : 0;
+        fdelta[k] = valid[k] ? bn(prompt[k] + 1, cfg) : 0;
+      }
+      int32_t P[K], DX[K];
+      excl_scan<K>(wprompt, P);
+      excl_scan<K>(fdelta, DX);
+      bool stop[K];
+      bool badw = false;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int32_t p = lane * K + k;
+        bool ok = valid[k];
+        int32_t c = prompt[k];
+        if (chunked) {
+          const int32_t bj = budget - P[k];
+          ok = ok && bj > 0;
+          c = prompt[k] < bj ? prompt[k] : bj;
+        }
+        const int32_t dj = bn(c + (c == prompt[k] ? 1 : 0), cfg);
+        ok = ok && dj <= pf - DX[k];
+        if (ok) chunk[k] = c;
+        if (p >= L && valid[k])
+          badw |= prompt[k] < 1 || prompt[k] > (1 << 22) || target[k] > (1 << 24) + 10;
+        stop[k] = p >= n && !ok;
+        if (ok) delta[k] = dj;
+      }
+      if (__any_sync(kFull, badw)) {
+        res.status = BSG_BAD_INPUT;
+        break;
+      }
+      const int32_t first_stop = first_pos<K>(stop, CAP);
+      a = first_stop - n;
+      // entries that were not admitted keep chunk 0 / delta 0
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int32_t p = lane * K + k;
+        if (p >= n && p >= n + a) {
+          chunk[k] = 0;
+          delta[k] = 0;
+        }
+      }
+    }
+    if (!chunked && prefill_step && !any_nonready && a == 0) {
+      // nothing to prefill fits: fall back to decoding all ready (backend.cpp:176-181)
+      prefill_step = false;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        decode_item[k] = ready[k];
+        const int32_t ns = stored[k] + 1;
+        delta[k] = ready[k] ? bn(ns, cfg) - bn(stored[k], cfg) : 0;
+      }
+    }
+    if (n == 0 && a == 0) {  // backend.cpp:245
+      res.status = BSG_EMPTY_PLAN;
+      break;
+    }
+    // ---------------- begin_step: admissions (backend.cpp:249-261) ----------------
+    const int32_t n_adm = n + a;
+    if (a > 0) {
+      const int32_t from_tail = n_adm > L ? n_adm - L : 0;  // admitted beyond the victim stack
+      const int32_t avail_w = wait_n - h;
+      if (from_tail > avail_w) cand_tail = false;  // the candidate was admitted
+      h += from_tail < avail_w ? from_tail : avail_w;
+      if (n_adm > L) L = n_adm;
+      bool started[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int32_t p = lane * K + k;
+        started[k] = p >= n && p < n_adm && !org_ever(org[k]);
+      }
+      if constexpr (TRACE) {
+        int32_t one[K], rk[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) one[k] = started[k] ? 1 : 0;
+        excl_scan<K>(one, rk);
+        uint64_t hs = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+          if (started[k]) hs += hash_term(BSG_TAG_STARTED, rk[k], org_origin(org[k]), 0);
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) hs += __shfl_xor_sync(kFull, hs, d);
+        if (lane == 0 && steps < trace.cap) trace.rec[steps].event_hash = hs;
+      }
+      bool cand_started = false;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (started[k]) {
+          if (org[k] == kCandOrg) cand_started = true;
+          org[k] |= kEverBit;
+        }
+      }
+      if (!qd_set && __any_sync(kFull, cand_started)) {
+        res.qdelay_ticks = elapsed;  // predictor.cpp:111-115
+        qd_set = true;
+      }
+    } else if constexpr (TRACE) {
+      if (lane == 0 && steps < trace.cap) trace.rec[steps].event_hash = 0;
+    }
+
+    // ---------------- allocation + preemption (backend.cpp:263-288) ----------------
+    const int32_t tot_delta = warp_sum<K>(delta);
+    int32_t e_star = n_adm;
+    if (tot_delta > free_blocks) {
+      int32_t ho[K], hinc[K], dinc[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int32_t p = lane * K + k;
+        ho[k] = p < n ? bn(stored[k], cfg) : 0;
+      }
+      const int32_t htot = excl_scan<K>(ho, hinc);
+      excl_scan<K>(delta, dinc);
+      bool badp[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int32_t p = lane * K + k;
+        // F(p+1) = free + (htot - incl_held(p)) - incl_delta(p)
+        const int32_t f = free_blocks + (htot - hinc[k] - ho[k]) - (dinc[k] + delta[k]);
+        badp[k] = p < n_adm && f < 0;
+      }
+      e_star = first_pos<K>(badp, n_adm);
+      if (e_star == 0) {  // backend.cpp:274-277
+        res.status = BSG_DEADLOCK;
+        res.detail = org_origin(read_pos<K>(org, 0));
+        break;
+      }
+      // F(e*) = free + sum_{v>=e*} held_old - sum_{p<e*} delta
+      int32_t fe[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        fe[k] = free_blocks + (htot - hinc[k] - ho[k]) - (dinc[k] + delta[k]);
+      free_blocks = read_pos<K>(fe, e_star - 1);
+      if constexpr (TRACE) {
+        uint64_t hp = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const int32_t p = lane * K + k;
+          if (p >= e_star && p < n_adm)
+            hp += hash_term(BSG_TAG_PREEMPT, static_cast<uint32_t>(n_adm - 1 - p),
+                            org_origin(org[k]), 0);
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) hp += __shfl_xor_sync(kFull, hp, d);
+        if (lane == 0 && steps < trace.cap) {
+          trace.rec[steps].event_hash += hp;
+          trace.rec[steps].n_preempted = n_adm - e_star;
+        }
+      }
+      // victims: recompute semantics (preempt, backend.cpp:221-232)
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int32_t p = lane * K + k;
+        if (p >= e_star && p < n_adm) {
+          prefill[k] = 0;
+          decoded[k] = 0;
+          chunk[k] = 0;
+          decode_item[k] = false;
+          delta[k] = 0;
+        }
+      }
+    } else {
+      free_blocks -= tot_delta;
+      if constexpr (TRACE) {
+        if (lane == 0 && steps < trace.cap) trace.rec[steps].n_preempted = 0;
+      }
+    }
+    n = e_star;
+
+    // ---------------- price the surviving plan (to_batch_plan 194-209) ----------------
+    int32_t ctx[K], pt[K];
+    bool dec_s[K], pre_s[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int32_t p = lane * K + k;
+      dec_s[k] = p < n && decode_item[k];
+      pre_s[k] = p < n && chunk[k] > 0;
+      ctx[k] = dec_s[k] ? stored[k] : 0;
+      pt[k] = pre_s[k] ? chunk[k] : 0;
+    }
+    const int32_t n_dec = count<K>(dec_s);
+    const int32_t context = warp_sum<K>(ctx);
+    const int32_t prefill_tokens = warp_sum<K>(pt);
+    const int64_t dur = step_ticks(cfg, prefill_tokens, n_dec, context);
+    elapsed += dur;
+    steps += 1;
+    if constexpr (TRACE) {
+      int32_t od[K], rd[K], op[K], rp[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        od[k] = dec_s[k] ? 1 : 0;
+        op[k] = pre_s[k] ? 1 : 0;
+      }
+      excl_scan<K>(od, rd);
+      const int32_t n_pre = excl_scan<K>(op, rp);
+      uint64_t hplan = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (dec_s[k]) hplan += hash_term(BSG_TAG_PLAN, rd[k], org_origin(org[k]), 0);
+        if (pre_s[k]) hplan += hash_term(BSG_TAG_PLAN + 16u, rp[k], org_origin(org[k]), chunk[k]);
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) hplan += __shfl_xor_sync(kFull, hplan, d);
+      if (lane == 0 && steps - 1 < trace.cap) {
+        bsg_step_record& r = trace.rec[steps - 1];
+        r.duration_ticks = dur;
+        r.context_tokens = context;
+        r.n_decode = n_dec;
+        r.prefill_tokens = prefill_tokens;
+        r.n_prefill = n_pre;
+        r.plan_hash = hplan;
+      }
+    }
+
+    // ---------------- finish_step (backend.cpp:298-331) ----------------
+    bool first_tok[K], done[K];
+    int32_t freed[K];
+    bool cand_first = false, cand_done = false;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int32_t prev = decoded[k];
+      if (dec_s[k]) {
+        decoded[k] += 1;
+      } else if (pre_s[k]) {
+        prefill[k] += chunk[k];
+        if (prefill[k] == prompt[k]) decoded[k] += 1;
+      }
+      const bool item = dec_s[k] || pre_s[k];
+      first_tok[k] = item && prev == 0 && decoded[k] >= 1;
+      done[k] = item && decoded[k] >= target[k];
+      freed[k] = done[k] ? bn(prefill[k] + decoded[k], cfg) : 0;
+      if (org[k] == (kCandOrg | kEverBit)) {
+        cand_first |= first_tok[k];
+        cand_done |= done[k];
+      }
+    }
+    if constexpr (TRACE) {
+      // item order: decodes (position order), then prefill items (position order)
+      int32_t fd[K], fp[K], cd[K], cp[K], rfd[K], rfp[K], rcd[K], rcp[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        fd[k] = (first_tok[k] && dec_s[k]) ? 1 : 0;
+        fp[k] = (first_tok[k] && pre_s[k]) ? 1 : 0;
+        cd[k] = (done[k] && dec_s[k]) ? 1 : 0;
+        cp[k] = (done[k] && pre_s[k]) ? 1 : 0;
+      }
+      const int32_t nfd = excl_scan<K>(fd, rfd);
+      excl_scan<K>(fp, rfp);
+      const int32_t ncd = excl_scan<K>(cd, rcd);
+      const int32_t ncp = excl_scan<K>(cp, rcp);
+      uint64_t he = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int32_t o = org_origin(org[k]);
+        if (fd[k]) he += hash_term(BSG_TAG_FIRST, rfd[k], o, 0);
+        if (fp[k]) he += hash_term(BSG_TAG_FIRST, nfd + rfp[k], o, 0);
+        if (cd[k]) he += hash_term(BSG_TAG_COMPLETED, rcd[k], o, 0);
+        if (cp[k]) he += hash_term(BSG_TAG_COMPLETED, ncd + rcp[k], o, 0);
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) he += __shfl_xor_sync(kFull, he, d);
+      if (lane == 0 && steps - 1 < trace.cap) {
+        trace.rec[steps - 1].event_hash += he;
+        trace.rec[steps - 1].n_completed = ncd + ncp;
+      }
+    }
+    if (!ttft_set && __any_sync(kFull, cand_first)) {  // predictor.cpp:117-121
+      res.ttft_ticks = elapsed;
+      ttft_set = true;
+    }
+    const int32_t n_done = count<K>(done);
+    if (n_done > 0) {
+      free_blocks += warp_sum<K>(freed);
+      // stable erase of completed members from running_ (backend.cpp:319-322):
+      // compact positions [0, L) through shared memory.
+      int32_t keep[K], dst[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int32_t p = lane * K + k;
+        keep[k] = (p < L && !done[k]) ? 1 : 0;
+      }
+      excl_scan<K>(keep, dst);
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (keep[k]) {
+          int32_t* s = smem + dst[k];
+          s[0 * CAP] = prompt[k];
+          s[1 * CAP] = target[k];
+          s[2 * CAP] = prefill[k];
+          s[3 * CAP] = decoded[k];
+          s[4 * CAP] = org[k];
+        }
+      }
+      __syncwarp();
+      n -= n_done;
+      L -= n_done;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int32_t p = lane * K + k;
+        if (p < L) {
+          const int32_t* s = smem + p;
+          prompt[k] = s[0 * CAP];
+          target[k] = s[1 * CAP];
+          prefill[k] = s[2 * CAP];
+          decoded[k] = s[3 * CAP];
+          org[k] = s[4 * CAP];
+        }
+      }
+      __syncwarp();
+    }
+    if constexpr (TRACE) {
+      if (lane == 0 && steps - 1 < trace.cap) trace.rec[steps - 1].free_blocks_after = free_blocks;
+    }
+    if (__any_sync(kFull, cand_done)) {  // predictor.cpp:122-124
+      res.e2e_ticks = elapsed;
+      if (!ttft_set) res.ttft_ticks = elapsed;  // predictor.cpp:130
+      res.status = BSG_OK;
+      break;
+    }
+    if (steps > kMaxSimulatedSteps) {  // predictor.cpp:125-127
+      res.status = BSG_STEP_LIMIT;
+      break;
+    }
+  }
+  res.steps = steps;
+  if (lane == 0) *out = res;
+}
+
+}  // namespace bsg

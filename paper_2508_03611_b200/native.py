@@ -1,0 +1,191 @@
+"""ctypes binding of the product C-ABI (include/blocksim_b200.h).
+
+Loads paper_2508_03611_b200/_lib/libblocksim_b200.so (built in-tree by
+__graft_entry__.build() / `make -C paper_2508_03611_b200/csrc`). There is no
+fallback: a missing library or a missing CUDA device raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import abi
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libblocksim_b200.so")
+HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
+                      "blocksim_b200.h")
+
+_lib = None
+
+
+class BsgError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str = ""):
+        self.status = status
+        super().__init__(f"{where}: {abi.STATUS_NAMES.get(status, status)} {detail}".strip())
+
+
+def load() -> C.CDLL:
+    """Loads the native library (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} not built: run __graft_entry__.build() "
+                           "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    V, E = C.c_void_p, C.POINTER(abi.Entries)
+    sigs = {
+        "bsg_abi_version": (C.c_int, []),
+        "bsg_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+        "bsg_ctx_destroy": (None, [V]),
+        "bsg_last_error": (C.c_char_p, [V]),
+        "bsg_launch_count": (C.c_int64, [V]),
+        "bsg_set_configs": (C.c_int, [V, V, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+        "bsg_predict_batch": (C.c_int, [V, E, C.c_int64, V, C.c_int64, V]),
+        "bsg_predict_batch_device": (C.c_int, [V, E, V, C.c_int64, V, V]),
+        "bsg_trace": (C.c_int, [V, E, C.c_int64, V, V, C.c_int64, C.POINTER(C.c_int64), V]),
+        "bsg_dispatch": (C.c_int, [V, E, C.c_int64, V, V, C.c_int32, C.c_int32, C.c_int32, V, V]),
+        "bsg_replay": (C.c_int, [V, V, V, V, V, C.POINTER(C.c_int64), C.POINTER(C.c_void_p)]),
+        "bsg_capture_sizes": (None, [V, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+        "bsg_capture_copy": (None, [V] * 7),
+        "bsg_capture_free": (None, [V]),
+        "bsg_make_workload": (C.c_int, [V, V, V, V, V]),
+        "bsg_ticks_to_seconds": (C.c_double, [C.c_int64]),
+    }
+    for name, (res, args) in sigs.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    if L.bsg_abi_version() != 1:
+        raise RuntimeError("ABI version mismatch")
+    _lib = L
+    return L
+
+
+def exported_symbols_declared_in_header() -> list[str]:
+    """Function names declared in include/blocksim_b200.h (for the export check)."""
+    import re
+    txt = open(HEADER).read()
+    decl = re.compile(r"^\s*(?:bsg_status|void|int|int64_t|double|const char\*)\s+(bsg_[a-z_0-9]+)\s*\(",
+                      re.M)
+    return sorted(set(decl.findall(txt)))
+
+
+def _p(a):
+    return abi.ptr(a)
+
+
+def make_workload_host(w: np.ndarray):
+    """Synthetic trace + estimates + arrival ticks (host C++, no GPU needed)."""
+    L = load()
+    n = int(w["count"][0]) if w["request_cap"][0] < 0 else min(int(w["count"][0]),
+                                                                int(w["request_cap"][0]))
+    p, o, e = (np.zeros(n, np.int32) for _ in range(3))
+    t = np.zeros(n, np.int64)
+    st = L.bsg_make_workload(_p(w), _p(p), _p(o), _p(e), _p(t))
+    if st != abi.OK:
+        raise BsgError(st, "bsg_make_workload")
+    return p, o, e, t
+
+
+class Context:
+    """One CUDA device + stream + device buffers (bsg_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self.L = load()
+        h = C.c_void_p()
+        st = self.L.bsg_ctx_create(device, C.byref(h))
+        if st != abi.OK:
+            raise BsgError(st, "bsg_ctx_create", "(a CUDA device is required)")
+        self.h = h
+        self.cfgs = None
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.bsg_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st, where):
+        if st != abi.OK:
+            raise BsgError(st, where, self.L.bsg_last_error(self.h).decode())
+
+    @property
+    def launches(self) -> int:
+        return int(self.L.bsg_launch_count(self.h))
+
+    def set_configs(self, cfgs: np.ndarray):
+        cfgs = np.ascontiguousarray(cfgs, dtype=abi.cfg_dtype)
+        bi, fc = C.c_int32(-1), C.c_int32(0)
+        st = self.L.bsg_set_configs(self.h, _p(cfgs), len(cfgs), C.byref(bi), C.byref(fc))
+        if st != abi.OK:
+            raise BsgError(st, "bsg_set_configs", f"config {bi.value} field {fc.value}")
+        self.cfgs = cfgs
+
+    def predict_batch(self, ss: abi.ScenarioSet) -> np.ndarray:
+        out = np.zeros(len(ss), abi.result_dtype)
+        e = ss.entries()
+        self._check(self.L.bsg_predict_batch(self.h, C.byref(e), ss.n_entries, _p(ss.scenarios),
+                                             len(ss), _p(out)), "bsg_predict_batch")
+        return out
+
+    def predict_batch_device(self, dev_cols, dev_scen_ptr: int, n: int, dev_out_ptr: int,
+                             stream_ptr: int | None = None):
+        """dev_cols: (prompt, est, prefill, decoded) device pointers (ints)."""
+        e = abi.Entries(None, *[C.c_void_p(x) for x in dev_cols])
+        self._check(self.L.bsg_predict_batch_device(self.h, C.byref(e), C.c_void_p(dev_scen_ptr), n,
+                                                    C.c_void_p(dev_out_ptr),
+                                                    C.c_void_p(stream_ptr) if stream_ptr else None),
+                    "bsg_predict_batch_device")
+
+    def trace(self, ss: abi.ScenarioSet, i: int = 0, cap: int = 1 << 20):
+        rec = np.zeros(cap, abi.step_dtype)
+        out = np.zeros(1, abi.result_dtype)
+        n = C.c_int64(0)
+        e = ss.entries()
+        sc = np.ascontiguousarray(ss.scenarios[i:i + 1])
+        self._check(self.L.bsg_trace(self.h, C.byref(e), ss.n_entries, _p(sc), _p(rec), cap,
+                                     C.byref(n), _p(out)), "bsg_trace")
+        return out[0], rec[:min(n.value, cap)]
+
+    def dispatch(self, ss: abi.ScenarioSet, instance_ids: np.ndarray, n_inst: int,
+                 objective: int = 0):
+        n_req = len(ss) // n_inst
+        ids = np.ascontiguousarray(instance_ids, dtype=np.int32)
+        chosen = np.zeros(n_req, np.int32)
+        per = np.zeros(len(ss), abi.result_dtype)
+        e = ss.entries()
+        self._check(self.L.bsg_dispatch(self.h, C.byref(e), ss.n_entries, _p(ss.scenarios), _p(ids),
+                                        n_inst, n_req, objective, _p(chosen), _p(per)),
+                    "bsg_dispatch")
+        return chosen, per
+
+    def replay(self, w, cfg, spec):
+        """Closed-loop replay (host live instances, GPU what-ifs). Returns
+        (outcomes, total_preemptions, captured ScenarioSet or None)."""
+        n = int(w["count"][0]) if w["request_cap"][0] < 0 else min(int(w["count"][0]),
+                                                                    int(w["request_cap"][0]))
+        out = np.zeros(n, abi.outcome_dtype)
+        tp = C.c_int64(0)
+        h = C.c_void_p(None)
+        capture = bool(spec["capture"][0])
+        self._check(self.L.bsg_replay(self.h, _p(w), _p(cfg), _p(spec), _p(out), C.byref(tp),
+                                      C.byref(h) if capture else None), "bsg_replay")
+        ss = None
+        if capture:
+            ne, ns = C.c_int64(0), C.c_int64(0)
+            self.L.bsg_capture_sizes(h, C.byref(ne), C.byref(ns))
+            ids = np.zeros(ne.value, np.uint64)
+            cols = [np.zeros(ne.value, np.int32) for _ in range(4)]
+            sc = np.zeros(ns.value, abi.scenario_dtype)
+            self.L.bsg_capture_copy(h, _p(ids), *[_p(c) for c in cols], _p(sc))
+            self.L.bsg_capture_free(h)
+            ss = abi.ScenarioSet(*cols, sc, ids=ids)
+        return out, tp.value, ss

@@ -1,0 +1,82 @@
+"""CPU tests of the C-ABI library: it builds for sm_100a, loads, exports every
+symbol include/blocksim_b200.h declares, and its host-only parts (workload
+generators) match the reference. No compute call touches a GPU here."""
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2508_03611_b200 import abi, native
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(native.LIB_PATH):
+        import __graft_entry__
+        __graft_entry__.build()
+    return native.load()
+
+
+def test_exports_every_header_symbol(lib):
+    names = native.exported_symbols_declared_in_header()
+    assert len(names) >= 15
+    out = subprocess.run(["nm", "-D", "--defined-only", native.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if line.strip()}
+    missing = [n for n in names if n not in exported]
+    assert not missing, missing
+
+
+def test_kernels_are_sm100a(lib):
+    out = subprocess.run(["cuobjdump", "--list-elf", native.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_struct_layouts(lib):
+    assert abi.cfg_dtype.itemsize == 64 and abi.scenario_dtype.itemsize == 32
+    assert abi.result_dtype.itemsize == 40 and abi.step_dtype.itemsize == 56
+    assert lib.bsg_abi_version() == 1
+    assert lib.bsg_ticks_to_seconds(61_200_000) == 61_200_000 * 1e-9
+
+
+def test_no_cpu_fallback_without_device(lib):
+    # In this container there is no GPU: creating a context must fail loudly.
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a device is present")
+    h = C.c_void_p()
+    assert lib.bsg_ctx_create(0, C.byref(h)) == abi.CUDA_ERROR
+    with pytest.raises(native.BsgError):
+        native.Context(0)
+
+
+@pytest.mark.parametrize("kw", [
+    dict(count=5000, estimator_kind=2, estimator_seed=1, qps=27, arrival_seed=1),
+    dict(count=2000, prompt_median=600, output_median=600, qps=4.5, arrival_seed=3),
+    dict(count=300, estimator_kind=1, fixed_tokens=100, qps=5, request_cap=100),
+])
+def test_workload_generators_match_reference(lib, ref, kw):
+    # make_synthetic_trace / estimate_length / generate_arrivals (workload.cpp:113-191)
+    w = abi.make_workload(**kw)
+    a = native.make_workload_host(w)
+    b = ref.make_workload(w)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+
+
+def test_divisor_magic_matches_integer_division():
+    # The kernel divides by block_size with a 32-bit magic multiplier (bsg_capi.cu:
+    # to_dev); check the formula exhaustively on small n and randomly on large n.
+    rng = np.random.default_rng(0)
+    for bs in list(range(1, 70)) + [1000, 4095, 65537, (1 << 20) - 3]:
+        if bs & (bs - 1) == 0:
+            continue
+        l = (bs - 1).bit_length()
+        m = (1 << (31 + l)) // bs + 1
+        assert m < (1 << 32)
+        ns = np.concatenate([np.arange(0, 5000), rng.integers(0, 1 << 31, 20000)]).astype(np.uint64)
+        q = ((ns * np.uint64(m)) >> np.uint64(32)) >> np.uint64(l - 1)
+        assert np.array_equal(q, ns // np.uint64(bs)), bs

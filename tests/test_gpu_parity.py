@@ -1,0 +1,110 @@
+"""GPU parity tests proper: the sm_100a kernels, called through the C-ABI,
+against the reference (oracle/_ref/libblocksim_ref.so, travels prebuilt) and
+the committed golden vectors. Bit-exact on ticks, steps, statuses, per-step
+batch composition / allocation / preemption fingerprints, and decisions.
+(North star allows 1e-6 relative on latencies; we hold ourselves to equality.)"""
+import numpy as np
+import pytest
+
+from paper_2508_03611_b200 import abi
+from oracle.oracle import compare_to_ref
+from scenarios import fuzz_set, kat_set
+from test_oracle import load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def run(ctx, cfgs, ss):
+    ctx.set_configs(cfgs)
+    return ctx.predict_batch(ss)
+
+
+@pytest.mark.parametrize("fixture", ["reference_kats.json", "fuzz_400_seed7.json"])
+def test_gpu_matches_golden(ctx, fixture):
+    names, cfgs, ss, exp = load_golden(fixture)
+    got = run(ctx, cfgs, ss)
+    bad = compare_to_ref(got, exp)
+    assert not bad.any(), [(names[i], got[i], exp[i]) for i in np.nonzero(bad)[0][:5]]
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_gpu_matches_reference_fuzz(ctx, ref, seed):
+    cfgs, ss = fuzz_set(seed, 20000)
+    got = run(ctx, cfgs, ss)
+    exp = ref.predict_batch(cfgs, ss, threads=8)
+    bad = compare_to_ref(got, exp)
+    assert bad.sum() == 0, [(i, got[i], exp[i]) for i in np.nonzero(bad)[0][:5]]
+
+
+def test_gpu_trace_matches_reference(ctx, ref):
+    """Per-step batch composition, allocations, preemption victims, first
+    tokens, completions and durations (bsg_step_record) for every step."""
+    cfgs, ss = fuzz_set(12, 400)
+    ctx.set_configs(cfgs)
+    names, kc, ks = kat_set()
+    for cf, s in ((cfgs, ss), (kc, ks)):
+        ctx.set_configs(cf)
+        for i in range(len(s)):
+            a, ta = ctx.trace(s, i, cap=8192)
+            b, tb = ref.trace(cf, s, i, cap=8192)
+            assert a["status"] == b["status"], (i, a, b)
+            assert len(ta) == len(tb), (i, len(ta), len(tb))
+            assert np.array_equal(ta, tb), (i, np.nonzero(ta != tb)[0][:3])
+
+
+def test_gpu_kats(ctx):
+    names, cfgs, ss = kat_set()
+    r = run(ctx, cfgs, ss)
+    i = names.index("predictor_empty_instance")
+    prefill = round((0.01 + 512 * 1e-4) * 1e9)
+    total = prefill + sum(round((0.01 + 1e-3 + c * 1e-7) * 1e9) for c in range(513, 522))
+    assert r[i]["e2e_ticks"] == total and r[i]["ttft_ticks"] == prefill  # test_driver.cpp:16-36
+    assert r[names.index("predictor_impossible")]["status"] == abi.TOO_LARGE_CANDIDATE
+    assert r[names.index("predictor_across_0")]["e2e_ticks"] < r[names.index("predictor_across_2")]["e2e_ticks"]
+
+
+@pytest.mark.parametrize("cfgname,kw,n_inst", [
+    ("cfg1", dict(count=1000, estimator_kind=2, estimator_seed=1, qps=10, arrival_seed=1), 4),
+    ("cfg2", dict(count=5000, estimator_kind=0, qps=27, arrival_seed=1), 12),
+    ("cfg3", dict(count=600, prompt_median=600, output_median=600, qps=4.5, arrival_seed=1), 12),
+])
+def test_gpu_matches_reference_on_replay_captures(ctx, ref, cfgname, kw, n_inst):
+    """Scenario sets a BlockPredictive closed loop evaluates (captured by the
+    reference's own driver loop): identical per-scenario results."""
+    cfg = abi.make_config()
+    w = abi.make_workload(**kw)
+    _, _, ss = ref.replay(w, cfg, abi.make_replay_spec(n_inst))
+    got = run(ctx, cfg, ss)
+    exp = ref.predict_batch(cfg, ss, threads=8)
+    assert compare_to_ref(got, exp).sum() == 0
+
+
+@pytest.mark.parametrize("kw,n_inst,policy", [
+    (dict(count=1000, estimator_kind=2, estimator_seed=1, qps=10, arrival_seed=1), 4,
+     abi.POLICY_BLOCK_PREDICTIVE),
+    (dict(count=1500, qps=27, arrival_seed=2), 12, abi.POLICY_BLOCK_PREDICTIVE),
+    (dict(count=800, qps=9, arrival_seed=5), 4, abi.POLICY_LLUMNIX_MINUS),
+    (dict(count=800, qps=9, arrival_seed=5), 4, abi.POLICY_INFAAS_PP),
+    (dict(count=500, qps=9, arrival_seed=5), 3, abi.POLICY_RANDOM),
+])
+def test_closed_loop_decisions_match_reference(ctx, ref, kw, n_inst, policy):
+    """Per-arrival decisions, dispatch/first-token/finish ticks and preemption
+    counts of the GPU-driven closed loop equal the reference's run_experiment."""
+    cfg = abi.make_config()
+    w = abi.make_workload(**kw)
+    spec = abi.make_replay_spec(n_inst, policy=policy, capture=1, policy_seed=3)
+    got, gp, gss = ctx.replay(w, cfg, spec)
+    exp, ep = ref.run_experiment(w, cfg, spec)
+    assert np.array_equal(got["instance"], exp["instance"])
+    assert np.array_equal(got, exp) and gp == ep
+
+
+def test_dispatch_argmin_ties_lowest_id(ctx):
+    # test_scheduler.cpp:178-203: identical snapshots tie -> lowest id wins,
+    # whatever order the ids arrive in.
+    cfg = abi.make_config()
+    snap = ([(64, 100, 64, 3)] * 5, [])
+    ss = abi.ScenarioSet.from_snapshots([snap] * 4, [(256, 32)] * 4)
+    ctx.set_configs(cfg)
+    chosen, per = ctx.dispatch(ss, np.array([9, 4, 7, 11], np.int32), 4)
+    assert chosen[0] == 4 and len(set(per["e2e_ticks"].tolist())) == 1
