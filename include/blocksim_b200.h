@@ -113,12 +113,15 @@ typedef struct bsg_scenario {
   int32_t reserved;
 } bsg_scenario;
 
-/* PredictionResult (predictor.h:28-36) in integer ticks. 40 bytes. */
+/* PredictionResult (predictor.h:28-36) in integer ticks. 48 bytes.
+ * member_steps = sum over simulated steps of (surviving plan items + 1), the
+ * algorithmic work unit of SURVEY.md 8(d) (not part of the reference result). */
 typedef struct bsg_result {
   int64_t e2e_ticks;     /* predicted_e2e_latency    */
   int64_t ttft_ticks;    /* predicted_ttft           */
   int64_t qdelay_ticks;  /* predicted_queueing_delay */
   int64_t steps;         /* simulated_steps          */
+  int64_t member_steps;  /* work counter (roofline numerator) */
   int32_t status;        /* bsg_status               */
   int32_t detail;        /* status-specific (origin index, field code, ...) */
 } bsg_result;

@@ -448,6 +448,7 @@ int32_t oracle_predict(const bsg_instance_cfg* cfg, const bsg_entries* e,
       }
       elapsed += st.duration;
       steps += 1;
+      out->member_steps += st.n_decode + st.n_prefill + 1;
       if (trace && steps <= trace_cap) {
         bsg_step_record* r = &trace[steps - 1];
         r->duration_ticks = st.duration;

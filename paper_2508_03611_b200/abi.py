@@ -47,7 +47,7 @@ scenario_dtype = np.dtype([
 ])
 result_dtype = np.dtype([
     ("e2e_ticks", "<i8"), ("ttft_ticks", "<i8"), ("qdelay_ticks", "<i8"), ("steps", "<i8"),
-    ("status", "<i4"), ("detail", "<i4"),
+    ("member_steps", "<i8"), ("status", "<i4"), ("detail", "<i4"),
 ])
 ref_result_dtype = np.dtype([
     ("e2e_s", "<f8"), ("ttft_s", "<f8"), ("qdelay_s", "<f8"), ("steps", "<i8"),
@@ -78,7 +78,7 @@ outcome_dtype = np.dtype([
 
 assert cfg_dtype.itemsize == 64
 assert scenario_dtype.itemsize == 32
-assert result_dtype.itemsize == 40
+assert result_dtype.itemsize == 48
 assert step_dtype.itemsize == 56
 assert outcome_dtype.itemsize == 40
 

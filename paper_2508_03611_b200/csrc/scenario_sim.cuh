@@ -513,6 +513,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
       pt[k] = pre_s[k] ? chunk[k] : 0;
     }
     const int32_t n_dec = count<K>(dec_s);
+    res.member_steps += n_dec + count<K>(pre_s) + 1;
     const int32_t context = warp_sum<K>(ctx);
     const int32_t prefill_tokens = warp_sum<K>(pt);
     const int64_t dur = step_ticks(cfg, prefill_tokens, n_dec, context);

@@ -37,7 +37,7 @@ def test_kernels_are_sm100a(lib):
 
 def test_struct_layouts(lib):
     assert abi.cfg_dtype.itemsize == 64 and abi.scenario_dtype.itemsize == 32
-    assert abi.result_dtype.itemsize == 40 and abi.step_dtype.itemsize == 56
+    assert abi.result_dtype.itemsize == 48 and abi.step_dtype.itemsize == 56
     assert lib.bsg_abi_version() == 1
     assert lib.bsg_ticks_to_seconds(61_200_000) == 61_200_000 * 1e-9
 
