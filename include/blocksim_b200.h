@@ -195,10 +195,15 @@ bsg_status bsg_predict_batch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n
                              const bsg_scenario* scenarios, int64_t n, bsg_result* out);
 
 /* Same, with DEVICE pointers (entries columns, scenarios, out), enqueued on
- * `stream` (a cudaStream_t, NULL = the context stream); asynchronous. */
+ * `stream` (a cudaStream_t; NULL = the context's own stream); asynchronous.
+ * member_capacity: an upper bound the caller guarantees on
+ * max(run_n, min(max_batch_size, run_n + wait_n + 1)) over the scenarios
+ * (it selects the kernel's per-warp member capacity, 32/64/128/256); <= 0
+ * derives it from the configs' max_batch_size. Scenarios exceeding the
+ * capacity report BSG_BAD_INPUT. */
 bsg_status bsg_predict_batch_device(bsg_ctx* ctx, const bsg_entries* dev_entries,
                                     const bsg_scenario* dev_scenarios, int64_t n,
-                                    bsg_result* dev_out, void* stream);
+                                    int32_t member_capacity, bsg_result* dev_out, void* stream);
 
 /* Trace mode: runs ONE scenario (host buffers) and writes one record per
  * simulated step (up to `cap`); *n_steps receives the total step count. */

@@ -162,6 +162,13 @@ class ScenarioSet:
         return ScenarioSet(self.prompt, self.est, self.prefill, self.decoded,
                            self.scenarios[idx], self.ids)
 
+    def member_capacity(self, cfgs: np.ndarray) -> int:
+        """max(run_n, min(max_batch_size, run_n + wait_n + 1)) over the set."""
+        sc = self.scenarios
+        maxb = cfgs["max_batch_size"][sc["cfg"]]
+        need = np.maximum(sc["run_n"], np.minimum(maxb, sc["run_n"] + sc["wait_n"] + 1))
+        return int(need.max()) if len(sc) else 1
+
     def nbytes_in(self) -> int:
         return (self.prompt.nbytes + self.est.nbytes + self.prefill.nbytes + self.decoded.nbytes
                 + self.scenarios.nbytes)

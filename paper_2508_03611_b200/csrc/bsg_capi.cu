@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
                    const int32_t* __restrict__ prefill, const int32_t* __restrict__ decoded,
                    const bsg_scenario* __restrict__ scen, int64_t n,
                    const int32_t* __restrict__ order, bsg_result* __restrict__ out) {
-  __shared__ int32_t smem[kWarpsPerBlock * 5 * 32 * K];
+  __shared__ int32_t smem[kWarpsPerBlock * (5 * 32 * K + 32)];
   const int warp = threadIdx.x >> 5;
   const int64_t w = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + warp;
   if (w >= n) return;
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     return;
   }
   simulate_scenario<K, false>(cfg, prompt, est, prefill, decoded, sc,
-                              smem + warp * 5 * 32 * K, o, TraceSink{nullptr, 0});
+                              smem + warp * (5 * 32 * K + 32), o, TraceSink{nullptr, 0});
 }
 
 template <int K>
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(32)
                  const int32_t* __restrict__ est, const int32_t* __restrict__ prefill,
                  const int32_t* __restrict__ decoded, const bsg_scenario* __restrict__ scen,
                  bsg_result* __restrict__ out, bsg_step_record* rec, int64_t cap) {
-  __shared__ int32_t smem[5 * 32 * K];
+  __shared__ int32_t smem[5 * 32 * K + 32];
   const bsg_scenario sc = scen[0];
   const DevCfg cfg = cfgs[sc.cfg];
   simulate_scenario<K, true>(cfg, prompt, est, prefill, decoded, sc, smem, out,
@@ -358,14 +358,13 @@ bsg_status bsg_predict_batch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n
 
 bsg_status bsg_predict_batch_device(bsg_ctx* ctx, const bsg_entries* dev_entries,
                                     const bsg_scenario* dev_scenarios, int64_t n,
-                                    bsg_result* dev_out, void* stream) {
+                                    int32_t member_capacity, bsg_result* dev_out, void* stream) {
   if (!ctx || !dev_entries || !dev_scenarios || !dev_out || n < 0) return BSG_INVALID_ARGUMENT;
   if (ctx->ncfg == 0) return BSG_INVALID_ARGUMENT;
   cudaSetDevice(ctx->device);
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-  // Capacity from the configs (scenarios are device-resident); scenarios that
-  // need more report BSG_BAD_INPUT from the kernel.
-  int k = capacity_k(std::max(1, ctx->max_batch_all));
+  const int32_t cap = member_capacity > 0 ? member_capacity : std::max(1, ctx->max_batch_all);
+  int k = capacity_k(cap);
   if (k == 0) k = 8;
   return launch_predict_k(ctx, k, n, *dev_entries, dev_scenarios, nullptr, dev_out, s);
 }

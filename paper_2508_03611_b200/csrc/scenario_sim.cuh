@@ -158,7 +158,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
                                   const int32_t* __restrict__ g_est,
                                   const int32_t* __restrict__ g_prefill,
                                   const int32_t* __restrict__ g_decoded, const bsg_scenario sc,
-                                  int32_t* __restrict__ smem,  // 5 * 32 * K int32 per warp
+                                  int32_t* __restrict__ smem,  // (5 * 32 * K + 32) int32 per warp
                                   bsg_result* __restrict__ out, TraceSink trace) {
   constexpr int CAP = 32 * K;
   const int lane = lane_id();
@@ -390,6 +390,108 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
       res.status = BSG_EMPTY_PLAN;
       break;
     }
+    bool first_tok[K], done[K], dec_s[K], pre_s[K];
+    int32_t freed[K];
+    bool cand_first = false, cand_done = false;
+
+    // ---------------- event skipping: pure-decode window ----------------
+    // This step is pure decode with no admission. Until the first completion
+    // (t_c) or the first step whose cumulative block demand exceeds free
+    // (t_p), every following step has the same membership and is pure decode
+    // too (projected_free only shrinks, so a blocked waiting head stays
+    // blocked). Lane t prices step t of the window; block demand per step is
+    // a histogram of (-stored) mod block_size over the members.
+    int32_t T = 0;
+    if (a == 0 && D == n && n > 0 && !prefill_step) {
+      int32_t lc = 0x7fffffff;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int32_t p = lane * K + k;
+        if (p < n) lc = min(lc, target[k] - decoded[k] - 1);
+      }
+      const int32_t t_c = static_cast<int32_t>(__reduce_min_sync(kFull, static_cast<uint32_t>(lc)));
+      int32_t* hist = smem + 5 * CAP;
+      hist[lane] = 0;
+      __syncwarp();
+      const int32_t bs = cfg.block_size;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int32_t p = lane * K + k;
+        if (p < n) {
+          const int32_t m = stored[k] - div_bs(stored[k], cfg) * bs;
+          const int32_t r = m == 0 ? 0 : bs - m;
+          if (r < 32) atomicAdd(&hist[r], 1);
+        }
+      }
+      __syncwarp();
+      const int32_t dem = hist[bs <= 32 ? lane - div_bs(lane, cfg) * bs : lane];
+      __syncwarp();
+      const int32_t cum = warp_incl_scan(dem);
+      const unsigned over = __ballot_sync(kFull, cum > free_blocks);
+      const int32_t t_p = over ? __ffs(over) - 1 : 32;
+      const int64_t lim = kMaxSimulatedSteps + 1 - steps;
+      T = min(min(t_c + 1, t_p), 32);
+      if (lim < T) T = static_cast<int32_t>(lim);
+      if (T < 2) T = 0;
+      if (T > 0) {
+        int32_t st_run[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) st_run[k] = (lane * K + k) < n ? stored[k] : 0;
+        const int32_t c0 = warp_sum<K>(st_run);
+        const int64_t d = lane < T ? step_ticks(cfg, 0, D, c0 + lane * D) : 0;
+        int64_t sum = d;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
+        if constexpr (TRACE) {
+          uint64_t hplan = 0, hfirst = 0;
+          int32_t z[K], rz[K];
+#pragma unroll
+          for (int k = 0; k < K; ++k) z[k] = ((lane * K + k) < n && decoded[k] == 0) ? 1 : 0;
+          excl_scan<K>(z, rz);
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const int32_t p = lane * K + k;
+            if (p < n) hplan += hash_term(BSG_TAG_PLAN, p, org_origin(org[k]), 0);
+            if (z[k]) hfirst += hash_term(BSG_TAG_FIRST, rz[k], org_origin(org[k]), 0);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            hplan += __shfl_xor_sync(kFull, hplan, o);
+            hfirst += __shfl_xor_sync(kFull, hfirst, o);
+          }
+          if (lane < T && steps + lane < trace.cap) {
+            bsg_step_record& r = trace.rec[steps + lane];
+            r.duration_ticks = d;
+            r.context_tokens = c0 + lane * D;
+            r.n_decode = D;
+            r.prefill_tokens = 0;
+            r.n_prefill = 0;
+            r.n_preempted = 0;
+            r.n_completed = 0;
+            r.free_blocks_after = free_blocks - cum;
+            r.plan_hash = hplan;
+            r.event_hash = lane == 0 ? hfirst : 0;
+          }
+          __syncwarp();
+        }
+        elapsed += sum;
+        steps += T;
+        res.member_steps += static_cast<int64_t>(T) * (D + 1);
+        free_blocks -= __shfl_sync(kFull, cum, T - 1);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const int32_t p = lane * K + k;
+          dec_s[k] = p < n;
+          pre_s[k] = false;
+          first_tok[k] = false;  // only possible at window step 0; never the candidate
+          if (p < n) decoded[k] += T;
+          done[k] = p < n && decoded[k] >= target[k];
+          freed[k] = done[k] ? bn(prefill[k] + decoded[k], cfg) : 0;
+          if (org[k] == (kCandOrg | kEverBit)) cand_done |= done[k];
+        }
+      }
+    }
+    if (T == 0) {
     // ---------------- begin_step: admissions (backend.cpp:249-261) ----------------
     const int32_t n_adm = n + a;
     if (a > 0) {
@@ -503,7 +605,6 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
 
     // ---------------- price the surviving plan (to_batch_plan 194-209) ----------------
     int32_t ctx[K], pt[K];
-    bool dec_s[K], pre_s[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const int32_t p = lane * K + k;
@@ -548,9 +649,6 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
     }
 
     // ---------------- finish_step (backend.cpp:298-331) ----------------
-    bool first_tok[K], done[K];
-    int32_t freed[K];
-    bool cand_first = false, cand_done = false;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const int32_t prev = decoded[k];
@@ -569,6 +667,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
         cand_done |= done[k];
       }
     }
+    }  // general step (T == 0)
     if constexpr (TRACE) {
       // item order: decodes (position order), then prefill items (position order)
       int32_t fd[K], fp[K], cd[K], cp[K], rfd[K], rfp[K], rcd[K], rcp[K];

@@ -44,7 +44,7 @@ def load() -> C.CDLL:
         "bsg_launch_count": (C.c_int64, [V]),
         "bsg_set_configs": (C.c_int, [V, V, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
         "bsg_predict_batch": (C.c_int, [V, E, C.c_int64, V, C.c_int64, V]),
-        "bsg_predict_batch_device": (C.c_int, [V, E, V, C.c_int64, V, V]),
+        "bsg_predict_batch_device": (C.c_int, [V, E, V, C.c_int64, C.c_int32, V, V]),
         "bsg_trace": (C.c_int, [V, E, C.c_int64, V, V, C.c_int64, C.POINTER(C.c_int64), V]),
         "bsg_dispatch": (C.c_int, [V, E, C.c_int64, V, V, C.c_int32, C.c_int32, C.c_int32, V, V]),
         "bsg_replay": (C.c_int, [V, V, V, V, V, C.POINTER(C.c_int64), C.POINTER(C.c_void_p)]),
@@ -137,11 +137,12 @@ class Context:
         return out
 
     def predict_batch_device(self, dev_cols, dev_scen_ptr: int, n: int, dev_out_ptr: int,
-                             stream_ptr: int | None = None):
-        """dev_cols: (prompt, est, prefill, decoded) device pointers (ints)."""
+                             stream_ptr: int | None = None, member_capacity: int = 0):
+        """dev_cols: (prompt, est, prefill, decoded) device pointers (ints).
+        stream_ptr: a cudaStream_t (not the legacy default stream 0)."""
         e = abi.Entries(None, *[C.c_void_p(x) for x in dev_cols])
         self._check(self.L.bsg_predict_batch_device(self.h, C.byref(e), C.c_void_p(dev_scen_ptr), n,
-                                                    C.c_void_p(dev_out_ptr),
+                                                    member_capacity, C.c_void_p(dev_out_ptr),
                                                     C.c_void_p(stream_ptr) if stream_ptr else None),
                     "bsg_predict_batch_device")
 
