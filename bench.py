@@ -260,11 +260,53 @@ def run_gpu(args):
         }
         if args.cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(ss, cfg)
+        if args.latency:
+            line["dispatch_latency"] = mc_latency(ctx)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     ctx.close()
     return line
+
+
+def mc_latency(ctx, n_calls: int = 400, n_inst: int = 64, n_samples: int = 256):
+    """cfg4: p50/p99 wall time of ONE BlockPredictive dispatch call with 256
+    Monte-Carlo length samples per candidate over 64 instances (16,384 what-if
+    scenarios per call, prefix-shared into 64 simulations), through the public
+    C-ABI with host buffers (pack + H2D + kernel + fused argmin + D2H).
+    Snapshots come from a 64-instance, 3000-request, 130 QPS closed loop."""
+    import ctypes as C
+    from paper_2508_03611_b200 import abi, native
+    w = abi.make_workload(count=3000, qps=130.0, arrival_seed=1)
+    cfg = abi.make_config()
+    _, _, cap = ctx.replay(w, cfg, abi.make_replay_spec(n_inst))
+    ctx.set_configs(cfg)
+    n_arr = len(cap) // n_inst
+    picks = np.linspace(0, n_arr - 1, n_calls).astype(int)
+    calls = []
+    for g in picks:
+        one = cap.compact(np.arange(g * n_inst, (g + 1) * n_inst))
+        lens = native.mc_lengths(int(one.scenarios[0]["cand_est"]), int(g), n_samples, seed=1)
+        calls.append((one, one.entries(), lens))
+    ids = np.arange(n_inst, dtype=np.int32)
+    chosen = np.zeros(1, np.int32)
+    lat = []
+    for i, (one, ent, lens) in enumerate(calls * 2):
+        t0 = time.perf_counter()
+        st = ctx.L.bsg_dispatch_mc(ctx.h, C.byref(ent), one.n_entries, abi.ptr(one.scenarios),
+                                   abi.ptr(ids), n_inst, 1, abi.ptr(lens), n_samples, 0,
+                                   abi.ptr(chosen), None, None, None)
+        t1 = time.perf_counter()
+        assert st == abi.OK and chosen[0] >= 0
+        if i >= len(calls):  # first pass is warm-up
+            lat.append((t1 - t0) * 1e6)
+    lat = np.array(lat)
+    return {"p50_us": float(np.percentile(lat, 50)), "p99_us": float(np.percentile(lat, 99)),
+            "max_us": float(lat.max()), "calls": len(lat),
+            "config": f"cfg4: {n_inst} instances x {n_samples} MC length samples per candidate "
+                      "(16384 what-if scenarios per dispatch, 64 prefix-shared simulations), "
+                      "snapshots from a 3000-request 130 QPS closed loop; host buffers, "
+                      "wall clock per call"}
 
 
 def cpu_baseline(ss, cfg):
@@ -321,6 +363,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-latency", dest="latency", action="store_false")
     args = ap.parse_args()
     line = run_reference(args) if args.impl == "reference" else run_gpu(args)
     if line is not None:

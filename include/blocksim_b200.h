@@ -222,6 +222,30 @@ bsg_status bsg_dispatch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entr
                         int32_t n_inst, int32_t n_requests, int32_t objective,
                         int32_t* chosen, bsg_result* per_instance);
 
+/* Monte-Carlo BlockPredictive dispatch (BASELINE cfg4; an extension: the
+ * reference has no sampling loop). For each of n_requests arrivals,
+ * scenarios [r*n_inst, (r+1)*n_inst) are the per-instance what-ifs (the
+ * candidate's cand_est is ignored) and lengths[r*n_samples ...] are its sampled
+ * response lengths (bsg_mc_lengths). Per instance, score = sum over samples of
+ * the e2e ticks predict() would return with that sample as the candidate's
+ * length (objective 0), or n_samples * ttft (objective 1); chosen[r] = argmin,
+ * lowest instance id on ties, -1 if any (instance, sample) fails. One
+ * simulation per (request, instance) serves all samples (prefix sharing).
+ * Optional outputs: scores [n_req*n_inst], sample_e2e [n_req*n_inst*n_samples],
+ * per_instance [n_req*n_inst]. HOST buffers; 1 <= n_samples <= 1024. */
+bsg_status bsg_dispatch_mc(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries,
+                           const bsg_scenario* scenarios, const int32_t* instance_ids,
+                           int32_t n_inst, int32_t n_requests, const int32_t* lengths,
+                           int32_t n_samples, int32_t objective, int32_t* chosen,
+                           int64_t* scores, int64_t* sample_e2e, bsg_result* per_instance);
+
+/* Sampled response lengths for one request: estimate_length's Noisy formula
+ * (workload.cpp:126-136) applied to the predicted length `est`:
+ * L_s = max(1, round(est * (1 + sign * |N(0,1)| * err * sqrt(pi/2)))), with
+ * SplitMix64(mix_seed(seed, request_id * n_samples + s)) (rand.h:11-56). */
+bsg_status bsg_mc_lengths(int32_t est, uint64_t request_id, int32_t n_samples, uint64_t seed,
+                          double mean_abs_rel_error, int32_t* out);
+
 /* ---- closed-loop replay (the scenario source; driver.cpp:134-289) -------- */
 
 /* Synthetic ShareGPT-shaped workload: make_synthetic_trace (workload.cpp:172-191,

@@ -55,6 +55,9 @@ double ref_time_predict(const bsg_instance_cfg* cfgs, const bsg_entries* e,
 /* Per-step trace through the reference's public Instance::execute_step. */
 int ref_trace(const bsg_instance_cfg* cfg, const bsg_entries* e, const bsg_scenario* sc,
               bsg_step_record* rec, int64_t cap, int64_t* n_steps, ref_result* out);
+/* estimate_length(Noisy{err, seed}) of a record {id, output_tokens} (workload.cpp:126-136). */
+int32_t ref_estimate_noisy(int32_t output_tokens, uint64_t record_id, uint64_t seed,
+                           double mean_abs_rel_error);
 /* Reference workload generators. */
 int ref_make_workload(const bsg_workload* w, int32_t* prompt, int32_t* output, int32_t* est,
                       int64_t* arrival_ticks);

@@ -105,6 +105,8 @@ class Reference:
         L.ref_capture_sizes.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.ref_capture_copy.restype = None
         L.ref_capture_copy.argtypes = [C.c_void_p] * 7
+        L.ref_estimate_noisy.restype = C.c_int32
+        L.ref_estimate_noisy.argtypes = [C.c_int32, C.c_uint64, C.c_uint64, C.c_double]
         L.ref_capture_free.restype = None
         L.ref_capture_free.argtypes = [C.c_void_p]
 
@@ -165,6 +167,38 @@ class Reference:
             self.lib.ref_capture_free(h)
             ss = abi.ScenarioSet(*cols, sc, ids=ids)
         return out, tp.value, ss
+
+
+def seconds_to_ticks_exact(sec: np.ndarray) -> np.ndarray:
+    """Inverse of SimTime::seconds (ticks * 1e-9, time.h:25), exact for the
+    values it produces (the map is injective below ~52 days)."""
+    sec = np.asarray(sec, dtype=np.float64)
+    t = np.rint(sec * 1e9).astype(np.int64)
+    for adj in (0, -1, 1, -2, 2):
+        cand = t + adj
+        ok = (cand.astype(np.float64) * 1e-9) == sec
+        t = np.where(ok, cand, t)
+    assert ((t.astype(np.float64) * 1e-9) == sec).all()
+    return t
+
+
+def mc_reference_dispatch(ref, cfg, ss, n_inst, lengths, threads=8):
+    """The oracle for cfg4: loop the reference predict() over every (instance,
+    sample) with the sample as the candidate's length, sum e2e ticks per
+    instance, argmin with lowest-id ties (instance id = index). Returns
+    (chosen, scores, sample_e2e)."""
+    n_req = len(ss) // n_inst
+    S = lengths.shape[1]
+    rows = np.repeat(ss.scenarios, S)
+    rows["cand_est"] = np.repeat(lengths, n_inst, axis=0).reshape(-1)
+    big = abi.ScenarioSet(ss.prompt, ss.est, ss.prefill, ss.decoded, rows)
+    rr = ref.predict_batch(cfg, big, threads=threads)
+    ok = (rr["status"] == abi.OK).reshape(n_req, n_inst, S)
+    e2e = seconds_to_ticks_exact(np.where(rr["status"] == abi.OK, rr["e2e_s"], 0.0))
+    e2e = e2e.reshape(n_req, n_inst, S)
+    scores = e2e.sum(axis=2)
+    chosen = np.where(ok.all(axis=(1, 2)), scores.argmin(axis=1), -1)  # argmin: first (lowest id)
+    return chosen, scores.reshape(-1), e2e.reshape(n_req * n_inst, S)
 
 
 def compare_to_ref(gpu_res: np.ndarray, ref_res: np.ndarray) -> np.ndarray:

@@ -515,6 +515,18 @@ int ref_trace(const bsg_instance_cfg* cfg, const bsg_entries* e, const bsg_scena
   return 0;
 }
 
+int32_t ref_estimate_noisy(int32_t output_tokens, uint64_t record_id, uint64_t seed,
+                           double mean_abs_rel_error) {
+  LengthEstimator e;
+  e.kind = EstimatorKind::kNoisy;
+  e.seed = seed;
+  e.mean_abs_rel_error = mean_abs_rel_error;
+  TraceRecord r;
+  r.id = record_id;
+  r.output_tokens = output_tokens;
+  return estimate_length(e, r);
+}
+
 int ref_make_workload(const bsg_workload* w, int32_t* prompt, int32_t* output, int32_t* est,
                       int64_t* arrival_ticks) {
   const std::vector<TraceRecord> records = make_records(w);

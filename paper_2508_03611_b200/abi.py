@@ -162,6 +162,23 @@ class ScenarioSet:
         return ScenarioSet(self.prompt, self.est, self.prefill, self.decoded,
                            self.scenarios[idx], self.ids)
 
+    def compact(self, rows) -> "ScenarioSet":
+        """A self-contained copy holding only the entries the selected scenario
+        rows reference (what a caller packs for one dispatch call)."""
+        sc = np.array(self.scenarios[rows], dtype=scenario_dtype)
+        cols = [[], [], [], []]
+        src = (self.prompt, self.est, self.prefill, self.decoded)
+        off = 0
+        for r in sc:
+            for start_key, n_key in (("run_off", "run_n"), ("wait_off", "wait_n")):
+                a, b = int(r[start_key]), int(r[n_key])
+                for c, col in zip(cols, src):
+                    c.append(col[a:a + b])
+                r[start_key] = off
+                off += b
+        cat = [np.concatenate(c) if c else np.zeros(0, np.int32) for c in cols]
+        return ScenarioSet(*cat, sc)
+
     def member_capacity(self, cfgs: np.ndarray) -> int:
         """max(run_n, min(max_batch_size, run_n + wait_n + 1)) over the set."""
         sc = self.scenarios

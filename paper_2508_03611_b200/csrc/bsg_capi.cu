@@ -104,6 +104,94 @@ __global__ void argmin_kernel(const bsg_result* __restrict__ res,
   if (lane == 0) chosen[r] = fail ? -1 : best_id;
 }
 
+// Monte-Carlo BlockPredictive dispatch (cfg4): warp w simulates instance
+// w % n_inst of request w / n_inst once, with the request's sorted sample
+// lengths staged in shared memory (prefix sharing), and the
+// last warp of each request to finish takes the argmin over the per-instance
+// scores (sum of per-sample e2e ticks), lowest instance id on ties
+// (scheduler.cpp:138-150).
+template <int K>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    dispatch_mc_kernel(const DevCfg* __restrict__ cfgs, int32_t ncfg,
+                       const int32_t* __restrict__ prompt, const int32_t* __restrict__ est,
+                       const int32_t* __restrict__ prefill, const int32_t* __restrict__ decoded,
+                       const bsg_scenario* __restrict__ scen, const int32_t* __restrict__ inst_ids,
+                       int32_t n_inst, int32_t n_req, const int32_t* __restrict__ sorted_len,
+                       int32_t S, int32_t objective, int64_t* __restrict__ scores,
+                       int64_t* __restrict__ sample_e2e, bsg_result* __restrict__ res,
+                       unsigned* __restrict__ counters, int32_t* __restrict__ chosen) {
+  extern __shared__ int32_t dsm[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + warp;
+  if (w >= static_cast<int64_t>(n_inst) * n_req) return;
+  const int32_t r = static_cast<int32_t>(w / n_inst);
+  int32_t* smem = dsm + warp * (5 * 32 * K + 32 + S);
+  int32_t* len = smem + 5 * 32 * K + 32;
+  for (int32_t j = lane; j < S; j += 32) len[j] = sorted_len[static_cast<int64_t>(r) * S + j];
+  __syncwarp();
+  const bsg_scenario sc = scen[w];
+  bsg_result* o = res + w;
+  if (sc.cfg < 0 || sc.cfg >= ncfg) {
+    if (lane == 0) {
+      bsg_result x{};
+      x.status = BSG_INVALID_ARGUMENT;
+      *o = x;
+      scores[w] = INT64_MAX;
+    }
+  } else {
+    const DevCfg cfg = cfgs[sc.cfg];
+    const int32_t need = max(sc.run_n, min(cfg.max_batch_size, sc.run_n + sc.wait_n + 1));
+    if (need > 32 * K || sc.run_n < 0 || sc.wait_n < 0) {
+      if (lane == 0) {
+        bsg_result x{};
+        x.status = BSG_BAD_INPUT;
+        *o = x;
+        scores[w] = INT64_MAX;
+      }
+    } else {
+      simulate_scenario<K, false, true>(
+          cfg, prompt, est, prefill, decoded, sc, smem, o, TraceSink{nullptr, 0},
+          McArgs{len, S, sample_e2e ? sample_e2e + w * S : nullptr, scores + w, objective});
+    }
+  }
+  // fused per-request argmin by the last warp to finish
+  __threadfence();
+  unsigned prev = 0;
+  if (lane == 0) prev = atomicAdd(&counters[r], 1u);
+  prev = __shfl_sync(kFull, prev, 0);
+  if (prev != static_cast<unsigned>(n_inst - 1)) return;
+  __threadfence();
+  int64_t best_v = INT64_MAX;
+  int32_t best_id = INT32_MAX;
+  bool fail = false;
+  for (int32_t i = lane; i < n_inst; i += 32) {
+    const int64_t q = static_cast<int64_t>(r) * n_inst + i;
+    const int32_t st = __ldcg(&res[q].status);
+    const int64_t v = __ldcg(&scores[q]);
+    const int32_t id = inst_ids[q];
+    if (st != BSG_OK) fail = true;
+    if (v < best_v || (v == best_v && id < best_id)) {
+      best_v = v;
+      best_id = id;
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const int64_t ov = __shfl_xor_sync(kFull, best_v, d);
+    const int32_t oi = __shfl_xor_sync(kFull, best_id, d);
+    if (ov < best_v || (ov == best_v && oi < best_id)) {
+      best_v = ov;
+      best_id = oi;
+    }
+  }
+  fail = __any_sync(kFull, fail);
+  if (lane == 0) {
+    chosen[r] = fail ? -1 : best_id;
+    counters[r] = 0;  // ready for the next call
+  }
+}
+
 }  // namespace bsg
 
 using namespace bsg;
@@ -134,6 +222,9 @@ struct bsg_ctx {
   std::vector<bsg_instance_cfg> host_cfgs;
   std::vector<DevCfg> dev_cfgs_host;
   DevBuf cfgs, prompt, est, prefill, decoded, scen, res, rec, ids, chosen, order;
+  DevBuf blob, scores, samples, counters;
+  void* pinned = nullptr;   // host staging for single-copy uploads
+  size_t pinned_cap = 0;
   int32_t ncfg = 0;
   int32_t max_batch_all = 0;
   std::mutex mu;
@@ -283,6 +374,7 @@ void bsg_ctx_destroy(bsg_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   cudaStreamDestroy(ctx->stream);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
   delete ctx;
 }
 
@@ -441,6 +533,128 @@ bsg_status bsg_dispatch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entr
                                   cudaMemcpyDeviceToHost, ctx->stream));
   }
   BSG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return BSG_OK;
+}
+
+bsg_status bsg_dispatch_mc(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries,
+                           const bsg_scenario* scenarios, const int32_t* instance_ids,
+                           int32_t n_inst, int32_t n_requests, const int32_t* lengths,
+                           int32_t n_samples, int32_t objective, int32_t* chosen,
+                           int64_t* scores, int64_t* sample_e2e, bsg_result* per_instance) {
+  if (!ctx || !entries || !scenarios || !instance_ids || !lengths || !chosen)
+    return BSG_INVALID_ARGUMENT;
+  if (n_inst <= 0) return BSG_NO_INSTANCES;
+  if (n_samples < 1 || n_samples > 1024) return BSG_INVALID_ARGUMENT;
+  if (n_requests <= 0) return BSG_OK;
+  if (ctx->ncfg == 0) return BSG_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaSetDevice(ctx->device);
+  const int64_t n = static_cast<int64_t>(n_inst) * n_requests;
+  const int64_t S = n_samples;
+  // sort each request's samples, remembering the permutation for sample_e2e
+  std::vector<int32_t> sorted(static_cast<size_t>(n_requests * S));
+  std::vector<int32_t> perm(static_cast<size_t>(n_requests * S));
+  for (int32_t r = 0; r < n_requests; ++r) {
+    int32_t* pr = perm.data() + r * S;
+    for (int32_t j = 0; j < S; ++j) pr[j] = j;
+    const int32_t* lr = lengths + r * S;
+    std::stable_sort(pr, pr + S, [&](int32_t a, int32_t b) { return lr[a] < lr[b]; });
+    for (int32_t j = 0; j < S; ++j) sorted[r * S + j] = lr[pr[j]];
+  }
+  // one packed host->device copy: 4 entry columns | scenarios | ids | sorted lengths
+  const size_t ne = static_cast<size_t>(n_entries);
+  const size_t bytes = 4 * ne * 4 + n * sizeof(bsg_scenario) + n * 4 + sorted.size() * 4 + 64;
+  if (ctx->pinned_cap < bytes) {
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    ctx->pinned = nullptr;
+    ctx->pinned_cap = 0;
+    BSG_CUDA(ctx, cudaHostAlloc(&ctx->pinned, bytes * 2, cudaHostAllocDefault));
+    ctx->pinned_cap = bytes * 2;
+  }
+  if (!ctx->blob.ensure(bytes) || !ctx->scores.ensure(n * 8) || !ctx->res.ensure(n * sizeof(bsg_result)) ||
+      !ctx->chosen.ensure(n_requests * 4) || !ctx->ids.ensure(4)) {
+    ctx->last_error = "device allocation failed";
+    return BSG_CUDA_ERROR;
+  }
+  if (ctx->counters.cap < static_cast<size_t>(n_requests) * 4) {
+    if (!ctx->counters.ensure(n_requests * 4)) return BSG_CUDA_ERROR;
+    BSG_CUDA(ctx, cudaMemsetAsync(ctx->counters.p, 0, ctx->counters.cap, ctx->stream));
+  }
+  if (sample_e2e && !ctx->samples.ensure(n * S * 8)) return BSG_CUDA_ERROR;
+  char* h = static_cast<char*>(ctx->pinned);
+  size_t off = 0;
+  auto put = [&](const void* src, size_t b) {
+    std::memcpy(h + off, src, b);
+    const size_t at = off;
+    off += (b + 15) & ~size_t(15);
+    return at;
+  };
+  const size_t o_p = put(entries->prompt, ne * 4), o_e = put(entries->est, ne * 4),
+               o_f = put(entries->prefill, ne * 4), o_d = put(entries->decoded, ne * 4),
+               o_s = put(scenarios, n * sizeof(bsg_scenario)), o_i = put(instance_ids, n * 4),
+               o_l = put(sorted.data(), sorted.size() * 4);
+  BSG_CUDA(ctx, cudaMemcpyAsync(ctx->blob.p, h, off, cudaMemcpyHostToDevice, ctx->stream));
+  char* d = static_cast<char*>(ctx->blob.p);
+  int32_t cap = 1;
+  for (int64_t i = 0; i < n; ++i) {
+    const bsg_scenario& sc = scenarios[i];
+    const int32_t c = sc.cfg;
+    const int32_t maxb = (c >= 0 && c < ctx->ncfg) ? ctx->host_cfgs[c].max_batch_size : 1;
+    cap = std::max(cap, std::max(sc.run_n, std::min(maxb, sc.run_n + sc.wait_n + 1)));
+  }
+  int k = capacity_k(cap);
+  if (k == 0) k = 8;
+  const int64_t blocks = (n + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  auto* dp = reinterpret_cast<const int32_t*>(d + o_p);
+  auto* de = reinterpret_cast<const int32_t*>(d + o_e);
+  auto* df = reinterpret_cast<const int32_t*>(d + o_f);
+  auto* dd = reinterpret_cast<const int32_t*>(d + o_d);
+  auto* ds = reinterpret_cast<const bsg_scenario*>(d + o_s);
+  auto* di = reinterpret_cast<const int32_t*>(d + o_i);
+  auto* dl = reinterpret_cast<const int32_t*>(d + o_l);
+  auto* dsc = static_cast<int64_t*>(ctx->scores.p);
+  auto* dse = sample_e2e ? static_cast<int64_t*>(ctx->samples.p) : nullptr;
+  auto* dres = static_cast<bsg_result*>(ctx->res.p);
+  auto* dcnt = static_cast<unsigned*>(ctx->counters.p);
+  auto* dch = static_cast<int32_t*>(ctx->chosen.p);
+  auto* dcf = static_cast<const DevCfg*>(ctx->cfgs.p);
+#define BSG_LAUNCH_MC(KK)                                                                       \
+  {                                                                                             \
+    const size_t sm = static_cast<size_t>(kWarpsPerBlock) * (5 * 32 * KK + 32 + S) * 4;         \
+    if (sm > 48 * 1024)                                                                         \
+      cudaFuncSetAttribute(dispatch_mc_kernel<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                           static_cast<int>(sm));                                               \
+    dispatch_mc_kernel<KK><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, sm, ctx->stream>>>( \
+        dcf, ctx->ncfg, dp, de, df, dd, ds, di, n_inst, n_requests, dl, n_samples, objective,   \
+        dsc, dse, dres, dcnt, dch);                                                             \
+  }
+  switch (k) {
+    case 1: BSG_LAUNCH_MC(1); break;
+    case 2: BSG_LAUNCH_MC(2); break;
+    case 4: BSG_LAUNCH_MC(4); break;
+    default: BSG_LAUNCH_MC(8); break;
+  }
+#undef BSG_LAUNCH_MC
+  ctx->launches += 1;
+  BSG_CUDA(ctx, cudaGetLastError());
+  BSG_CUDA(ctx, cudaMemcpyAsync(chosen, dch, n_requests * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (scores)
+    BSG_CUDA(ctx, cudaMemcpyAsync(scores, dsc, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (per_instance)
+    BSG_CUDA(ctx, cudaMemcpyAsync(per_instance, dres, n * sizeof(bsg_result), cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+  std::vector<int64_t> tmp;
+  if (sample_e2e) {
+    tmp.resize(static_cast<size_t>(n * S));
+    BSG_CUDA(ctx, cudaMemcpyAsync(tmp.data(), dse, n * S * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  BSG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (sample_e2e) {
+    for (int64_t q = 0; q < n; ++q) {
+      const int32_t r = static_cast<int32_t>(q / n_inst);
+      for (int32_t j = 0; j < S; ++j) sample_e2e[q * S + perm[r * S + j]] = tmp[q * S + j];
+    }
+  }
   return BSG_OK;
 }
 

@@ -565,6 +565,22 @@ class Replay {
 
 extern "C" {
 
+bsg_status bsg_mc_lengths(int32_t est, uint64_t request_id, int32_t n_samples, uint64_t seed,
+                          double mean_abs_rel_error, int32_t* out) {
+  if (!out || n_samples < 0) return BSG_INVALID_ARGUMENT;
+  // estimate_length's Noisy branch (workload.cpp:126-136) applied to the
+  // predicted length, one SplitMix64 stream per sample.
+  const double scale = mean_abs_rel_error * std::sqrt(3.14159265358979323846 / 2.0);
+  for (int32_t s = 0; s < n_samples; ++s) {
+    Rng rng(mix_seed(seed, request_id * static_cast<uint64_t>(n_samples) + static_cast<uint64_t>(s)));
+    const double half = std::abs(rng.normal());
+    const double sign = (rng.next() & 1) ? 1.0 : -1.0;
+    const double v = std::round(static_cast<double>(est) * (1.0 + sign * half * scale));
+    out[s] = static_cast<int32_t>(std::max(1.0, v));
+  }
+  return BSG_OK;
+}
+
 bsg_status bsg_make_workload(const bsg_workload* w, int32_t* prompt, int32_t* output, int32_t* est,
                              int64_t* arrival_ticks) {
   if (!w) return BSG_INVALID_ARGUMENT;

@@ -151,16 +151,36 @@ struct TraceSink {
   int64_t cap;
 };
 
+// Monte-Carlo length samples of the candidate. The samples
+// are sorted ascending; the simulation runs once with target = len[S-1] and
+// sample j's e2e is the elapsed time at the end of the first step in which the
+// candidate's decoded count reaches len[j] (the candidate's target influences
+// nothing before its own completion, so this equals running predict() with
+// target len[j]; prefix sharing is exact).
+struct McArgs {
+  const int32_t* len;   // sorted sample lengths (shared memory), S >= 1
+  int32_t S;
+  int64_t* sample_e2e;  // optional, sorted order
+  int64_t* score;       // sum_j e2e_j (or S * ttft for the ttft objective)
+  int32_t objective;
+};
+
 // Simulates one scenario with the calling warp. All lanes return the same
 // result; lane 0 writes it.
-template <int K, bool TRACE>
+template <int K, bool TRACE, bool MC = false>
 __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__ g_prompt,
                                   const int32_t* __restrict__ g_est,
                                   const int32_t* __restrict__ g_prefill,
                                   const int32_t* __restrict__ g_decoded, const bsg_scenario sc,
                                   int32_t* __restrict__ smem,  // (5 * 32 * K + 32) int32 per warp
-                                  bsg_result* __restrict__ out, TraceSink trace) {
+                                  bsg_result* __restrict__ out, TraceSink trace,
+                                  McArgs mc = McArgs{}) {
   constexpr int CAP = 32 * K;
+  // candidate target: its estimate, or the largest MC sample
+  const int32_t cand_target = MC ? mc.len[mc.S - 1] : sc.cand_est;
+  int32_t cand_hi = 0;     // MC: highest decoded count the candidate has reached
+  int32_t mc_ptr = 0;      // MC: samples already completed (sorted prefix)
+  int64_t mc_sum = 0;      // MC: per-lane partial score
   const int lane = lane_id();
   bsg_result res{};
 
@@ -206,10 +226,10 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
   // waiting entries: validated lazily as they are read; the candidate's admit check
   // (backend.cpp:76-83):
   {
-    const int64_t need = (static_cast<int64_t>(sc.cand_prompt) + sc.cand_est + cfg.block_size - 1) /
+    const int64_t need = (static_cast<int64_t>(sc.cand_prompt) + cand_target + cfg.block_size - 1) /
                          cfg.block_size;
-    if (sc.cand_prompt < 1 || sc.cand_prompt > (1 << 22) || sc.cand_est < 0 ||
-        sc.cand_est > (1 << 24)) {
+    if (sc.cand_prompt < 1 || sc.cand_prompt > (1 << 22) || cand_target < 0 ||
+        cand_target > (1 << 24)) {
       res.status = BSG_BAD_INPUT;
       if (lane == 0) *out = res;
       return;
@@ -326,7 +346,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
             org[k] = run_n + j + 1;
           } else if (j == wait_n && cand_tail) {
             prompt[k] = sc.cand_prompt;
-            target[k] = sc.cand_est;
+            target[k] = cand_target;
             org[k] = kCandOrg;
           } else {
             valid[k] = false;
@@ -402,6 +422,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
     // blocked). Lane t prices step t of the window; block demand per step is
     // a histogram of (-stored) mod block_size over the members.
     int32_t T = 0;
+    int64_t win_pre = 0, win_base = 0;
     if (a == 0 && D == n && n > 0 && !prefill_step) {
       int32_t lc = 0x7fffffff;
 #pragma unroll
@@ -442,6 +463,17 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
         int64_t sum = d;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
+        if constexpr (MC) {
+          // inclusive prefix of step durations: elapsed at the end of window step `lane`
+          int64_t pre = d;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(kFull, pre, o);
+            if (lane >= o) pre += y;
+          }
+          win_pre = pre;
+          win_base = elapsed;
+        }
         if constexpr (TRACE) {
           uint64_t hplan = 0, hfirst = 0;
           int32_t z[K], rz[K];
@@ -702,6 +734,33 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
       res.ttft_ticks = elapsed;
       ttft_set = true;
     }
+    if constexpr (MC) {
+      // candidate's decoded count after this step / window (-1 when not running)
+      int32_t cd = -1;
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if ((lane * K + k) < n && org[k] == (kCandOrg | kEverBit)) cd = decoded[k];
+      cd = static_cast<int32_t>(__reduce_max_sync(kFull, static_cast<uint32_t>(cd + 1))) - 1;
+      if (cd > cand_hi) {
+        const int32_t dec0 = cd - (T > 0 ? T : 1);  // decoded before this step / window
+        for (;;) {
+          const int32_t j = mc_ptr + lane;
+          const int32_t lj = j < mc.S ? mc.len[j] : 0x7fffffff;
+          const bool hit = lj <= cd;
+          // step (within the window) at whose end decoded first reaches lj
+          const int32_t tj = hit ? lj - dec0 - 1 : 0;
+          const int64_t at = T > 0 ? win_base + __shfl_sync(kFull, win_pre, tj & 31) : elapsed;
+          if (hit) {
+            mc_sum += at;
+            if (mc.sample_e2e) mc.sample_e2e[j] = at;
+          }
+          const int32_t c = __popc(__ballot_sync(kFull, hit));
+          mc_ptr += c;
+          if (c < 32) break;
+        }
+        cand_hi = cd;
+      }
+    }
     const int32_t n_done = count<K>(done);
     if (n_done > 0) {
       free_blocks += warp_sum<K>(freed);
@@ -758,6 +817,13 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
     }
   }
   res.steps = steps;
+  if constexpr (MC) {
+    int64_t tot = mc_sum;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(kFull, tot, o);
+    if (mc.objective == 1) tot = static_cast<int64_t>(mc.S) * res.ttft_ticks;
+    if (lane == 0) *mc.score = res.status == BSG_OK ? tot : INT64_MAX;
+  }
   if (lane == 0) *out = res;
 }
 

@@ -53,6 +53,9 @@ def load() -> C.CDLL:
         "bsg_capture_free": (None, [V]),
         "bsg_make_workload": (C.c_int, [V, V, V, V, V]),
         "bsg_ticks_to_seconds": (C.c_double, [C.c_int64]),
+        "bsg_dispatch_mc": (C.c_int, [V, E, C.c_int64, V, V, C.c_int32, C.c_int32, V, C.c_int32,
+                                      C.c_int32, V, V, V, V]),
+        "bsg_mc_lengths": (C.c_int, [C.c_int32, C.c_uint64, C.c_int32, C.c_uint64, C.c_double, V]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -75,6 +78,17 @@ def exported_symbols_declared_in_header() -> list[str]:
 
 def _p(a):
     return abi.ptr(a)
+
+
+def mc_lengths(est: int, request_id: int, n_samples: int = 256, seed: int = 1,
+               mean_abs_rel_error: float = 0.244) -> np.ndarray:
+    """Sampled response lengths for one request (bsg_mc_lengths)."""
+    out = np.zeros(n_samples, np.int32)
+    st = load().bsg_mc_lengths(int(est), int(request_id), n_samples, seed, mean_abs_rel_error,
+                               _p(out))
+    if st != abi.OK:
+        raise BsgError(st, "bsg_mc_lengths")
+    return out
 
 
 def make_workload_host(w: np.ndarray):
@@ -167,6 +181,25 @@ class Context:
                                         n_inst, n_req, objective, _p(chosen), _p(per)),
                     "bsg_dispatch")
         return chosen, per
+
+    def dispatch_mc(self, ss: abi.ScenarioSet, instance_ids: np.ndarray, n_inst: int,
+                    lengths: np.ndarray, objective: int = 0, want_samples: bool = False,
+                    want_results: bool = False):
+        """Monte-Carlo BlockPredictive dispatch (bsg_dispatch_mc). lengths: [n_req, S]."""
+        n_req = len(ss) // n_inst
+        lengths = np.ascontiguousarray(lengths, dtype=np.int32).reshape(n_req, -1)
+        S = lengths.shape[1]
+        ids = np.ascontiguousarray(instance_ids, dtype=np.int32)
+        chosen = np.zeros(n_req, np.int32)
+        scores = np.zeros(len(ss), np.int64)
+        samples = np.zeros((len(ss), S), np.int64) if want_samples else None
+        per = np.zeros(len(ss), abi.result_dtype) if want_results else None
+        e = ss.entries()
+        self._check(self.L.bsg_dispatch_mc(self.h, C.byref(e), ss.n_entries, _p(ss.scenarios),
+                                           _p(ids), n_inst, n_req, _p(lengths), S, objective,
+                                           _p(chosen), _p(scores), _p(samples), _p(per)),
+                    "bsg_dispatch_mc")
+        return chosen, scores, samples, per
 
     def replay(self, w, cfg, spec):
         """Closed-loop replay (host live instances, GPU what-ifs). Returns

@@ -80,3 +80,13 @@ def test_divisor_magic_matches_integer_division():
         ns = np.concatenate([np.arange(0, 5000), rng.integers(0, 1 << 31, 20000)]).astype(np.uint64)
         q = ((ns * np.uint64(m)) >> np.uint64(32)) >> np.uint64(l - 1)
         assert np.array_equal(q, ns // np.uint64(bs)), bs
+
+
+def test_mc_lengths_match_reference_estimator(lib, ref):
+    """bsg_mc_lengths == the reference's estimate_length Noisy branch
+    (workload.cpp:126-136) applied to the predicted length, sample s drawn from
+    the stream of record id request_id * n_samples + s."""
+    for est, rid in [(160, 0), (7, 12345), (4000, 2), (1, 99)]:
+        got = native.mc_lengths(est, rid, 256, seed=1)
+        exp = [ref.lib.ref_estimate_noisy(est, rid * 256 + s, 1, 0.244) for s in range(256)]
+        assert got.tolist() == exp

@@ -108,3 +108,28 @@ def test_dispatch_argmin_ties_lowest_id(ctx):
     ctx.set_configs(cfg)
     chosen, per = ctx.dispatch(ss, np.array([9, 4, 7, 11], np.int32), 4)
     assert chosen[0] == 4 and len(set(per["e2e_ticks"].tolist())) == 1
+
+
+@pytest.mark.parametrize("n_inst,n_samples,qps", [(8, 64, 14.0), (64, 256, 130.0)])
+def test_mc_dispatch_matches_reference_loop(ctx, ref, n_inst, n_samples, qps):
+    """cfg4 semantics: per-instance score = sum over MC length samples of the
+    e2e ticks the reference predict() returns with that sample as the
+    candidate's length; prefix-shared GPU simulation must give identical
+    per-sample e2e, scores and decisions."""
+    from paper_2508_03611_b200 import native
+    from oracle.oracle import mc_reference_dispatch
+    cfg = abi.make_config()
+    w = abi.make_workload(count=400, qps=qps, arrival_seed=4)
+    _, _, cap = ref.replay(w, cfg, abi.make_replay_spec(n_inst))
+    groups = [50, 200, 399] if n_inst == 64 else list(range(100, 400, 25))
+    rows = np.concatenate([cap.scenarios[g * n_inst:(g + 1) * n_inst] for g in groups])
+    ss = abi.ScenarioSet(cap.prompt, cap.est, cap.prefill, cap.decoded, rows)
+    lengths = np.stack([native.mc_lengths(int(rows[i * n_inst]["cand_est"]), g, n_samples)
+                        for i, g in enumerate(groups)])
+    ctx.set_configs(cfg)
+    ids = np.tile(np.arange(n_inst, dtype=np.int32), len(groups))
+    chosen, scores, samples, _ = ctx.dispatch_mc(ss, ids, n_inst, lengths, want_samples=True)
+    e_chosen, e_scores, e_samples = mc_reference_dispatch(ref, cfg, ss, n_inst, lengths)
+    assert np.array_equal(samples, e_samples)
+    assert np.array_equal(scores, e_scores)
+    assert np.array_equal(chosen, e_chosen)
