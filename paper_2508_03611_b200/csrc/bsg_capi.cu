@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -217,6 +218,8 @@ struct DevBuf {
 struct bsg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};  // chunked host-buffer pipeline
+  cudaEvent_t pipe_done[3] = {nullptr, nullptr, nullptr};
   std::string last_error;
   int64_t launches = 0;
   std::vector<bsg_instance_cfg> host_cfgs;
@@ -365,6 +368,13 @@ bsg_status bsg_ctx_create(int device, bsg_ctx** out) {
     delete ctx;
     return BSG_CUDA_ERROR;
   }
+  for (int i = 0; i < 3; ++i) {
+    if (cudaStreamCreateWithFlags(&ctx->pipe[i], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->pipe_done[i], cudaEventDisableTiming) != cudaSuccess) {
+      delete ctx;
+      return BSG_CUDA_ERROR;
+    }
+  }
   *out = ctx;
   return BSG_OK;
 }
@@ -374,6 +384,13 @@ void bsg_ctx_destroy(bsg_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   cudaStreamDestroy(ctx->stream);
+  for (int i = 0; i < 3; ++i) {
+    if (ctx->pipe[i]) {
+      cudaStreamSynchronize(ctx->pipe[i]);
+      cudaStreamDestroy(ctx->pipe[i]);
+    }
+    if (ctx->pipe_done[i]) cudaEventDestroy(ctx->pipe_done[i]);
+  }
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   delete ctx;
 }
@@ -435,16 +452,72 @@ bsg_status bsg_predict_batch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n
   if (n == 0) return BSG_OK;
   std::lock_guard<std::mutex> lock(ctx->mu);
   cudaSetDevice(ctx->device);
+  const size_t eb = static_cast<size_t>(std::max<int64_t>(n_entries, 1)) * sizeof(int32_t);
+  if (!ctx->prompt.ensure(eb) || !ctx->est.ensure(eb) || !ctx->prefill.ensure(eb) ||
+      !ctx->decoded.ensure(eb) || !ctx->scen.ensure(n * sizeof(bsg_scenario)) ||
+      !ctx->res.ensure(n * sizeof(bsg_result))) {
+    ctx->last_error = "device allocation failed";
+    return BSG_CUDA_ERROR;
+  }
   bsg_entries dev{};
-  bsg_status st = upload(ctx, entries, n_entries, scenarios, n, &dev);
-  if (st != BSG_OK) return st;
-  const int k = capacity_k(host_need(scenarios, n, ctx->host_cfgs));
-  st = launch_predict_k(ctx, k == 0 ? 8 : k, n, dev, static_cast<const bsg_scenario*>(ctx->scen.p),
-                        nullptr, static_cast<bsg_result*>(ctx->res.p), ctx->stream);
-  if (st != BSG_OK) return st;
-  BSG_CUDA(ctx, cudaMemcpyAsync(out, ctx->res.p, n * sizeof(bsg_result), cudaMemcpyDeviceToHost,
-                                ctx->stream));
-  BSG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  dev.prompt = static_cast<const int32_t*>(ctx->prompt.p);
+  dev.est = static_cast<const int32_t*>(ctx->est.p);
+  dev.prefill = static_cast<const int32_t*>(ctx->prefill.p);
+  dev.decoded = static_cast<const int32_t*>(ctx->decoded.p);
+  auto* dsc = static_cast<bsg_scenario*>(ctx->scen.p);
+  auto* dres = static_cast<bsg_result*>(ctx->res.p);
+  // Chunked pipeline: chunk c (a contiguous scenario range) copies only the
+  // entry range its scenarios reference, runs, and copies its results back on
+  // stream c % 3, so H2D(c+1) overlaps the kernel on c and D2H(c-1).
+  const int64_t target_chunk = 16384;
+  const int64_t nchunks = std::min<int64_t>(8, std::max<int64_t>(1, n / target_chunk));
+  const int64_t per = (n + nchunks - 1) / nchunks;
+  auto cols_h = std::array<const int32_t*, 4>{entries->prompt, entries->est, entries->prefill,
+                                              entries->decoded};
+  auto cols_d = std::array<int32_t*, 4>{static_cast<int32_t*>(ctx->prompt.p), static_cast<int32_t*>(ctx->est.p),
+                                        static_cast<int32_t*>(ctx->prefill.p),
+                                        static_cast<int32_t*>(ctx->decoded.p)};
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t s0 = c * per, s1 = std::min(n, s0 + per);
+    if (s0 >= s1) break;
+    int64_t lo = INT64_MAX, hi = 0;
+    int32_t need = 1;
+    for (int64_t i = s0; i < s1; ++i) {
+      const bsg_scenario& x = scenarios[i];
+      if (x.run_n > 0) {
+        lo = std::min<int64_t>(lo, x.run_off);
+        hi = std::max<int64_t>(hi, static_cast<int64_t>(x.run_off) + x.run_n);
+      }
+      if (x.wait_n > 0) {
+        lo = std::min<int64_t>(lo, x.wait_off);
+        hi = std::max<int64_t>(hi, static_cast<int64_t>(x.wait_off) + x.wait_n);
+      }
+      const int32_t cf = x.cfg;
+      const int32_t maxb = (cf >= 0 && cf < ctx->ncfg) ? ctx->host_cfgs[cf].max_batch_size : 1;
+      need = std::max(need, std::max(x.run_n, std::min(maxb, x.run_n + x.wait_n + 1)));
+    }
+    if (lo < 0 || hi > n_entries) {
+      ctx->last_error = "scenario references entries outside [0, n_entries)";
+      return BSG_INVALID_ARGUMENT;
+    }
+    cudaStream_t st = ctx->pipe[c % 3];
+    if (c >= 3) BSG_CUDA(ctx, cudaStreamWaitEvent(st, ctx->pipe_done[c % 3], 0));
+    if (hi > lo) {
+      for (int q = 0; q < 4; ++q)
+        BSG_CUDA(ctx, cudaMemcpyAsync(cols_d[q] + lo, cols_h[q] + lo, (hi - lo) * 4,
+                                      cudaMemcpyHostToDevice, st));
+    }
+    BSG_CUDA(ctx, cudaMemcpyAsync(dsc + s0, scenarios + s0, (s1 - s0) * sizeof(bsg_scenario),
+                                  cudaMemcpyHostToDevice, st));
+    const int k = capacity_k(need);
+    const bsg_status ls = launch_predict_k(ctx, k == 0 ? 8 : k, s1 - s0, dev, dsc + s0, nullptr,
+                                           dres + s0, st);
+    if (ls != BSG_OK) return ls;
+    BSG_CUDA(ctx, cudaMemcpyAsync(out + s0, dres + s0, (s1 - s0) * sizeof(bsg_result),
+                                  cudaMemcpyDeviceToHost, st));
+    BSG_CUDA(ctx, cudaEventRecord(ctx->pipe_done[c % 3], st));
+  }
+  for (int i = 0; i < 3; ++i) BSG_CUDA(ctx, cudaStreamSynchronize(ctx->pipe[i]));
   return BSG_OK;
 }
 
