@@ -41,9 +41,9 @@ PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 
 def workload(rank: int):
-    from paper_2508_03611_b200 import abi
-    return (abi.make_workload(count=N_REQ, qps=QPS, arrival_seed=1 + rank), abi.make_config(),
-            abi.make_replay_spec(N_INST))
+    from paper_2508_03611_b200 import abi, shard
+    return (abi.make_workload(count=N_REQ, qps=QPS, arrival_seed=shard.weak_seed(rank)),
+            abi.make_config(), abi.make_replay_spec(N_INST))
 
 
 def workload_desc():
@@ -202,14 +202,11 @@ def run_gpu(args):
                 e2e_times.append(tb - ta)
     e2e_total = sum(e2e_times)
 
-    # ---- max over ranks ---------------------------------------------------------
+    # ---- max over ranks (NCCL only here: timings and counts) -------------------
+    from paper_2508_03611_b200 import shard
     if world > 1:
-        t = torch.tensor([total_ms, e2e_total], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, e2e_total = float(t[0]), float(t[1])
-        c = torch.tensor([n, member_steps, launches], dtype=torch.int64, device=dev)
-        dist.all_reduce(c, op=dist.ReduceOp.SUM)
-        n_all, ms_all, launches_all = int(c[0]), int(c[1]), int(c[2])
+        (total_ms, e2e_total), (n_all, ms_all, launches_all) = shard.reduce_max_sum(
+            [total_ms, e2e_total], [n, member_steps, launches], device=dev)
     else:
         n_all, ms_all, launches_all = n, member_steps, launches
 
@@ -260,8 +257,10 @@ def run_gpu(args):
         }
         if args.cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(ss, cfg)
-        if args.latency:
-            line["dispatch_latency"] = mc_latency(ctx)
+    if args.latency:
+        lat = mc_latency(ctx, world, rank, dev)
+        if rank == 0:
+            line["dispatch_latency"] = lat
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -269,44 +268,54 @@ def run_gpu(args):
     return line
 
 
-def mc_latency(ctx, n_calls: int = 400, n_inst: int = 64, n_samples: int = 256):
+def mc_latency(ctx, world: int = 1, rank: int = 0, device=None, n_calls: int = 400,
+               n_inst: int = 64, n_samples: int = 256):
     """cfg4: p50/p99 wall time of ONE BlockPredictive dispatch call with 256
     Monte-Carlo length samples per candidate over 64 instances (16,384 what-if
     scenarios per call, prefix-shared into 64 simulations), through the public
     C-ABI with host buffers (pack + H2D + kernel + fused argmin + D2H).
-    Snapshots come from a 64-instance, 3000-request, 130 QPS closed loop."""
+    Snapshots come from a 64-instance, 3000-request, 130 QPS closed loop.
+    With N GPUs, instance i is simulated on rank i % N and the per-request
+    argmin crosses ranks as one exact NCCL min-reduction pair (shard.py)."""
     import ctypes as C
-    from paper_2508_03611_b200 import abi, native
+    from paper_2508_03611_b200 import abi, native, shard
     w = abi.make_workload(count=3000, qps=130.0, arrival_seed=1)
     cfg = abi.make_config()
     _, _, cap = ctx.replay(w, cfg, abi.make_replay_spec(n_inst))
     ctx.set_configs(cfg)
     n_arr = len(cap) // n_inst
+    mine = shard.instance_shard(n_inst, world, rank)
     picks = np.linspace(0, n_arr - 1, n_calls).astype(int)
     calls = []
     for g in picks:
-        one = cap.compact(np.arange(g * n_inst, (g + 1) * n_inst))
+        one = cap.compact(g * n_inst + mine)
         lens = native.mc_lengths(int(one.scenarios[0]["cand_est"]), int(g), n_samples, seed=1)
         calls.append((one, one.entries(), lens))
-    ids = np.arange(n_inst, dtype=np.int32)
+    ids = np.ascontiguousarray(mine, dtype=np.int32)
     chosen = np.zeros(1, np.int32)
+    scores = np.zeros(len(mine), np.int64)
     lat = []
     for i, (one, ent, lens) in enumerate(calls * 2):
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
         t0 = time.perf_counter()
         st = ctx.L.bsg_dispatch_mc(ctx.h, C.byref(ent), one.n_entries, abi.ptr(one.scenarios),
-                                   abi.ptr(ids), n_inst, 1, abi.ptr(lens), n_samples, 0,
-                                   abi.ptr(chosen), None, None, None)
+                                   abi.ptr(ids), len(mine), 1, abi.ptr(lens), n_samples, 0,
+                                   abi.ptr(chosen), abi.ptr(scores), None, None)
+        pick = int(chosen[0]) if world == 1 else shard.global_argmin(scores, ids, device=device)
         t1 = time.perf_counter()
-        assert st == abi.OK and chosen[0] >= 0
+        assert st == abi.OK and pick >= 0
         if i >= len(calls):  # first pass is warm-up
             lat.append((t1 - t0) * 1e6)
     lat = np.array(lat)
     return {"p50_us": float(np.percentile(lat, 50)), "p99_us": float(np.percentile(lat, 99)),
-            "max_us": float(lat.max()), "calls": len(lat),
+            "max_us": float(lat.max()), "calls": len(lat), "gpus": world,
             "config": f"cfg4: {n_inst} instances x {n_samples} MC length samples per candidate "
                       "(16384 what-if scenarios per dispatch, 64 prefix-shared simulations), "
                       "snapshots from a 3000-request 130 QPS closed loop; host buffers, "
-                      "wall clock per call"}
+                      "wall clock per call" + (f"; instances sharded i % {world}, NCCL argmin"
+                                                if world > 1 else "")}
 
 
 def cpu_baseline(ss, cfg):

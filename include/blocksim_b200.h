@@ -61,7 +61,9 @@ typedef enum bsg_status {
   BSG_CUDA_ERROR = 9,
   /* NoInstancesError, predictor.cpp:144 / scheduler.cpp:116 */
   BSG_NO_INSTANCES = 10,
-  BSG_INVALID_ARGUMENT = 11
+  BSG_INVALID_ARGUMENT = 11,
+  /* NoCapacityError: the lowest swept qps already violates the SLO (metrics.cpp:153-155) */
+  BSG_NO_CAPACITY = 12
 } bsg_status;
 
 typedef enum bsg_local_policy {
@@ -279,15 +281,28 @@ typedef enum bsg_policy {
   BSG_POLICY_BLOCK_PREDICTIVE = 5
 } bsg_policy;
 
-/* Static-provisioning, zero-overhead, probe-free closed loop
- * (ExperimentSpec driver.h / config.h:58-70 subset). */
+/* Zero-overhead, probe-free closed loop (ExperimentSpec, config.h:58-70
+ * subset) with the autoscaler (ProvisionPolicy, autoscaler.h:10-27). */
 typedef struct bsg_replay_spec {
-  int32_t n_instances;
-  int32_t policy;        /* bsg_policy */
-  int32_t objective;     /* 0 e2e, 1 ttft */
-  int32_t capture;       /* nonzero: record every BlockPredictive what-if scenario */
-  uint64_t policy_seed;  /* PolicyConfig::seed (Random's stream) */
+  int32_t n_instances;     /* cluster.instances */
+  int32_t policy;          /* bsg_policy */
+  int32_t objective;       /* 0 e2e, 1 ttft */
+  int32_t capture;         /* nonzero: record every BlockPredictive what-if scenario */
+  uint64_t policy_seed;    /* PolicyConfig::seed (Random's stream) */
+  int32_t provision_kind;  /* 0 static, 1 preempt (predicted e2e), 2 relief (realized e2e) */
+  int32_t max_instances;   /* provision.max_instances (>= n_instances) */
+  double threshold_s;      /* provision.threshold_s (70) */
+  double cold_start_s;     /* provision.cold_start_s (30) */
+  double cooldown_s;       /* provision.cooldown_s (15) */
 } bsg_replay_spec;
+
+/* RunLog totals (metrics.h:18-54 subset). */
+typedef struct bsg_replay_summary {
+  int64_t total_preemptions;
+  int64_t end_ticks;              /* time of the last processed event */
+  int32_t instances_provisioned;  /* Autoscaler::provisioned_total */
+  int32_t final_instance_count;
+} bsg_replay_summary;
 
 /* Per-request outcome (Request, types.h:30-42). Unset times are -1. */
 typedef struct bsg_request_outcome {
@@ -305,13 +320,45 @@ typedef struct bsg_capture bsg_capture;
  * receives the what-if scenarios in arrival order (n_instances per arrival). */
 bsg_status bsg_replay(bsg_ctx* ctx, const bsg_workload* w, const bsg_instance_cfg* cfg,
                       const bsg_replay_spec* spec, bsg_request_outcome* outcomes,
-                      int64_t* total_preemptions, bsg_capture** capture);
+                      bsg_replay_summary* summary, bsg_capture** capture);
 void bsg_capture_sizes(const bsg_capture* c, int64_t* n_entries, int64_t* n_scenarios);
 /* Copies the capture into caller buffers (entries columns of n_entries,
  * scenarios of n_scenarios); the `cfg` field of every scenario is 0. */
 void bsg_capture_copy(const bsg_capture* c, uint64_t* id, int32_t* prompt, int32_t* est,
                       int32_t* prefill, int32_t* decoded, bsg_scenario* scenarios);
 void bsg_capture_free(bsg_capture* c);
+
+/* RunReport subset (metrics.h:80-108) of aggregate (metrics.cpp:21-124):
+ * TTFT = first token - dispatch, e2e = finish - arrival over finished
+ * requests; nearest-rank percentiles (metrics.cpp:11-19); throughput =
+ * finished / (last finish - first arrival). */
+typedef struct bsg_run_report {
+  int32_t finished_requests, censored_requests;
+  double throughput_rps;
+  double mean_ttft_s, p50_ttft_s, p99_ttft_s;
+  double mean_e2e_s, p50_e2e_s, p99_e2e_s;
+  int64_t total_preemptions;
+  int32_t instances_provisioned, final_instance_count;
+} bsg_run_report;
+bsg_status bsg_aggregate(const bsg_request_outcome* outcomes, int64_t n,
+                         const bsg_replay_summary* summary, bsg_run_report* out);
+
+/* capacity_search (metrics.cpp:139-178) over run_experiment cells built like
+ * spec_for_cell (driver.cpp:321-331: policy seed = workload seed = estimator
+ * seed = seed, qps swept): every integer qps in [qps_min, qps_max], then
+ * tenths inside the bracket; pass iff p99 TTFT < slo. BSG_NO_CAPACITY when
+ * qps_min already fails. tested_qps/tested_pass (capacity tested_cap) receive
+ * the (qps, passed) sequence in test order. */
+typedef struct bsg_capacity_result {
+  double capacity_qps;
+  int32_t bracket_pass, bracket_fail;
+  int32_t monotone;
+  int32_t n_tested;
+} bsg_capacity_result;
+bsg_status bsg_capacity_search(bsg_ctx* ctx, const bsg_workload* base, const bsg_instance_cfg* cfg,
+                               const bsg_replay_spec* spec, uint64_t seed, int32_t qps_min,
+                               int32_t qps_max, double slo_p99_ttft_s, bsg_capacity_result* out,
+                               double* tested_qps, int32_t* tested_pass, int32_t tested_cap);
 
 /* Synthetic trace + estimates + Poisson arrival ticks (no GPU needed). */
 bsg_status bsg_make_workload(const bsg_workload* w, int32_t* prompt, int32_t* output,

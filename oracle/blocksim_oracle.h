@@ -64,13 +64,21 @@ int ref_make_workload(const bsg_workload* w, int32_t* prompt, int32_t* output, i
 /* blocksim_ref::run_experiment (driver.cpp:316-319), static provisioning. */
 int ref_run_experiment(const bsg_workload* w, const bsg_instance_cfg* cfg,
                        const bsg_replay_spec* spec, bsg_request_outcome* out,
-                       int64_t* total_preemptions);
+                       bsg_replay_summary* summary);
+/* aggregate (metrics.cpp:21-124) of run_experiment. */
+int ref_run_report(const bsg_workload* w, const bsg_instance_cfg* c, const bsg_replay_spec* s,
+                   bsg_run_report* out);
+/* capacity_search (metrics.cpp:139-178) with run_capacity's runner (driver.cpp:398-418). */
+int ref_capacity_search(const bsg_workload* w, const bsg_instance_cfg* c, const bsg_replay_spec* s,
+                        uint64_t seed, int32_t qps_min, int32_t qps_max, double slo,
+                        bsg_capacity_result* out, double* tested_qps, int32_t* tested_pass,
+                        int32_t tested_cap);
 /* Hand replay of SimulationDriver (driver.cpp:134-289) over the reference's
  * public EventLoop / Instance / Dispatcher with a capturing PredictorClient;
  * returns an opaque capture (ref_capture_*). */
 typedef struct ref_capture ref_capture;
 int ref_replay(const bsg_workload* w, const bsg_instance_cfg* cfg, const bsg_replay_spec* spec,
-               bsg_request_outcome* out, int64_t* total_preemptions, ref_capture** capture);
+               bsg_request_outcome* out, bsg_replay_summary* summary, ref_capture** capture);
 void ref_capture_sizes(const ref_capture* c, int64_t* n_entries, int64_t* n_scenarios);
 void ref_capture_copy(const ref_capture* c, uint64_t* id, int32_t* prompt, int32_t* est,
                       int32_t* prefill, int32_t* decoded, bsg_scenario* scenarios);

@@ -96,15 +96,18 @@ class Reference:
         L.ref_make_workload.restype = C.c_int
         L.ref_make_workload.argtypes = [C.c_void_p] + [C.c_void_p] * 4
         L.ref_run_experiment.restype = C.c_int
-        L.ref_run_experiment.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                                         C.POINTER(C.c_int64)]
+        L.ref_run_experiment.argtypes = [C.c_void_p] * 5
         L.ref_replay.restype = C.c_int
-        L.ref_replay.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                                 C.POINTER(C.c_int64), C.POINTER(C.c_void_p)]
+        L.ref_replay.argtypes = [C.c_void_p] * 5 + [C.POINTER(C.c_void_p)]
         L.ref_capture_sizes.restype = None
         L.ref_capture_sizes.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.ref_capture_copy.restype = None
         L.ref_capture_copy.argtypes = [C.c_void_p] * 7
+        L.ref_run_report.restype = C.c_int
+        L.ref_run_report.argtypes = [C.c_void_p] * 4
+        L.ref_capacity_search.restype = C.c_int
+        L.ref_capacity_search.argtypes = [C.c_void_p] * 3 + [C.c_uint64, C.c_int32, C.c_int32,
+                                                              C.c_double] + [C.c_void_p] * 3 + [C.c_int32]
         L.ref_estimate_noisy.restype = C.c_int32
         L.ref_estimate_noisy.argtypes = [C.c_int32, C.c_uint64, C.c_uint64, C.c_double]
         L.ref_capture_free.restype = None
@@ -144,17 +147,31 @@ class Reference:
         n = int(w["count"][0]) if w["request_cap"][0] < 0 else min(int(w["count"][0]),
                                                                     int(w["request_cap"][0]))
         out = np.zeros(n, abi.outcome_dtype)
-        tp = C.c_int64(0)
-        self.lib.ref_run_experiment(_vp(w), _vp(cfg), _vp(spec), _vp(out), C.byref(tp))
-        return out, tp.value
+        summ = np.zeros(1, abi.summary_dtype)
+        self.lib.ref_run_experiment(_vp(w), _vp(cfg), _vp(spec), _vp(out), _vp(summ))
+        return out, summ[0]
+
+    def run_report(self, w, cfg, spec):
+        out = np.zeros(1, abi.report_dtype)
+        self.lib.ref_run_report(_vp(w), _vp(cfg), _vp(spec), _vp(out))
+        return out[0]
+
+    def capacity_search(self, w, cfg, spec, seed, qps_min, qps_max, slo):
+        out = np.zeros(1, abi.capacity_dtype)
+        tq = np.zeros(256, np.float64)
+        tp = np.zeros(256, np.int32)
+        st = self.lib.ref_capacity_search(_vp(w), _vp(cfg), _vp(spec), seed, qps_min, qps_max, slo,
+                                          _vp(out), _vp(tq), _vp(tp), 256)
+        n = int(out["n_tested"][0])
+        return st, out[0], list(zip(tq[:n].tolist(), tp[:n].astype(bool).tolist()))
 
     def replay(self, w, cfg, spec, capture: bool = True):
         n = int(w["count"][0]) if w["request_cap"][0] < 0 else min(int(w["count"][0]),
                                                                     int(w["request_cap"][0]))
         out = np.zeros(n, abi.outcome_dtype)
-        tp = C.c_int64(0)
+        summ = np.zeros(1, abi.summary_dtype)
         h = C.c_void_p(None)
-        self.lib.ref_replay(_vp(w), _vp(cfg), _vp(spec), _vp(out), C.byref(tp),
+        self.lib.ref_replay(_vp(w), _vp(cfg), _vp(spec), _vp(out), _vp(summ),
                             C.byref(h) if capture else None)
         ss = None
         if capture:
@@ -166,7 +183,7 @@ class Reference:
             self.lib.ref_capture_copy(h, _vp(ids), *[_vp(c) for c in cols], _vp(sc))
             self.lib.ref_capture_free(h)
             ss = abi.ScenarioSet(*cols, sc, ids=ids)
-        return out, tp.value, ss
+        return out, summ[0], ss
 
 
 def seconds_to_ticks_exact(sec: np.ndarray) -> np.ndarray:

@@ -28,6 +28,7 @@
 #include "blocksim/driver.h"
 #include "blocksim/error.h"
 #include "blocksim/event_loop.h"
+#include "blocksim/metrics.h"
 #include "blocksim/predictor.h"
 #include "blocksim/scheduler.h"
 #include "blocksim/workload.h"
@@ -541,9 +542,8 @@ int ref_make_workload(const bsg_workload* w, int32_t* prompt, int32_t* output, i
   return static_cast<int>(arrivals.size());
 }
 
-int ref_run_experiment(const bsg_workload* w, const bsg_instance_cfg* c,
-                       const bsg_replay_spec* s, bsg_request_outcome* out,
-                       int64_t* total_preemptions) {
+static ExperimentSpec make_experiment(const bsg_workload* w, const bsg_instance_cfg* c,
+                                     const bsg_replay_spec* s) {
   ExperimentSpec spec;
   spec.initial_instances = s->n_instances;
   spec.instance_template = to_ref_config(*c);
@@ -554,28 +554,100 @@ int ref_run_experiment(const bsg_workload* w, const bsg_instance_cfg* c,
   spec.workload.qps = w->qps;
   spec.workload.seed = w->arrival_seed;
   spec.workload.estimator = make_estimator(w);
-  spec.provision.kind = ProvisionKind::kStatic;
+  spec.provision.kind = s->provision_kind == 1 ? ProvisionKind::kPreempt
+                        : (s->provision_kind == 2 ? ProvisionKind::kRelief : ProvisionKind::kStatic);
   spec.provision.min_instances = s->n_instances;
-  spec.provision.max_instances = s->n_instances;
+  spec.provision.max_instances = std::max(s->n_instances, s->max_instances);
+  spec.provision.threshold_s = s->threshold_s;
+  spec.provision.cold_start_s = s->cold_start_s;
+  spec.provision.cooldown_s = s->cooldown_s;
   spec.cache_mode = to_ref_cache(c->cache_mode);
   spec.cache_bucket = c->context_bucket;
   spec.collect_events = false;
-  const RunLog log = run_experiment(spec);
+  return spec;
+}
+
+int ref_run_experiment(const bsg_workload* w, const bsg_instance_cfg* c,
+                       const bsg_replay_spec* s, bsg_request_outcome* out,
+                       bsg_replay_summary* summary) {
+  const RunLog log = run_experiment(make_experiment(w, c, s));
   std::vector<InstanceId> inst(log.requests.size(), -1);
   for (const auto& p : log.dispatch_points) inst[p.request_id] = p.instance_id;
   for (std::size_t i = 0; i < log.requests.size(); ++i)
     fill_outcome(log.requests[i], inst[i], log.preempt_counts[i], &out[i]);
-  if (total_preemptions) *total_preemptions = log.total_preemptions;
+  if (summary) {
+    summary->total_preemptions = log.total_preemptions;
+    summary->end_ticks = log.end_time.ticks();
+    summary->instances_provisioned = log.instances_provisioned;
+    summary->final_instance_count = log.final_instance_count;
+  }
   return static_cast<int>(log.requests.size());
 }
 
+// aggregate (metrics.cpp:21-124) of a reference run.
+int ref_run_report(const bsg_workload* w, const bsg_instance_cfg* c, const bsg_replay_spec* s,
+                   bsg_run_report* out) {
+  const RunLog log = run_experiment(make_experiment(w, c, s));
+  const RunReport r = aggregate(log);
+  std::memset(out, 0, sizeof(*out));
+  out->finished_requests = r.finished_requests;
+  out->censored_requests = r.censored_requests;
+  out->throughput_rps = r.throughput_rps;
+  out->mean_ttft_s = r.mean_ttft_s;
+  out->p50_ttft_s = r.p50_ttft_s;
+  out->p99_ttft_s = r.p99_ttft_s;
+  out->mean_e2e_s = r.mean_e2e_s;
+  out->p50_e2e_s = r.p50_e2e_s;
+  out->p99_e2e_s = r.p99_e2e_s;
+  out->total_preemptions = r.total_preemptions;
+  out->instances_provisioned = r.instances_provisioned;
+  out->final_instance_count = r.final_instance_count;
+  return 0;
+}
+
+// capacity_search (metrics.cpp:139-178) over run_experiment(spec_for_cell(...))
+// exactly as run_capacity builds its runner (driver.cpp:398-418). Returns 0,
+// or 12 (BSG_NO_CAPACITY) on NoCapacityError.
+int ref_capacity_search(const bsg_workload* w, const bsg_instance_cfg* c, const bsg_replay_spec* s,
+                        uint64_t seed, int32_t qps_min, int32_t qps_max, double slo,
+                        bsg_capacity_result* out, double* tested_qps, int32_t* tested_pass,
+                        int32_t tested_cap) {
+  const ExperimentSpec base = make_experiment(w, c, s);
+  const PolicyKind policy = base.policy.kind;
+  auto runner = [&](double qps) {
+    ExperimentSpec spec = spec_for_cell(base, policy, qps, seed);
+    spec.collect_events = false;
+    return aggregate(run_experiment(spec));
+  };
+  std::memset(out, 0, sizeof(*out));
+  try {
+    const CapacityResult r = capacity_search(runner, SloSpec{slo}, qps_min, qps_max);
+    out->capacity_qps = r.capacity_qps;
+    out->bracket_pass = r.bracket_pass;
+    out->bracket_fail = r.bracket_fail;
+    out->monotone = r.monotone ? 1 : 0;
+    out->n_tested = static_cast<int32_t>(r.tested.size());
+    for (std::size_t i = 0; i < r.tested.size() && static_cast<int32_t>(i) < tested_cap; ++i) {
+      tested_qps[i] = r.tested[i].first;
+      tested_pass[i] = r.tested[i].second ? 1 : 0;
+    }
+    return 0;
+  } catch (const NoCapacityError&) {
+    return BSG_NO_CAPACITY;
+  }
+}
+
 int ref_replay(const bsg_workload* w, const bsg_instance_cfg* cfg, const bsg_replay_spec* spec,
-               bsg_request_outcome* out, int64_t* total_preemptions, ref_capture** capture) {
+               bsg_request_outcome* out, bsg_replay_summary* summary, ref_capture** capture) {
   ref_capture* cap = capture ? new ref_capture() : nullptr;
   Replay replay(w, cfg, spec, cap);
   replay.run();
   if (out) replay.outcomes(out);
-  if (total_preemptions) *total_preemptions = replay.total_preemptions();
+  if (summary) {
+    std::memset(summary, 0, sizeof(*summary));
+    summary->total_preemptions = replay.total_preemptions();
+    summary->final_instance_count = spec->n_instances;
+  }
   if (capture) *capture = cap;
   return 0;
 }

@@ -69,8 +69,27 @@ workload_dtype = np.dtype([
 ])
 replay_spec_dtype = np.dtype([
     ("n_instances", "<i4"), ("policy", "<i4"), ("objective", "<i4"), ("capture", "<i4"),
-    ("policy_seed", "<u8"),
+    ("policy_seed", "<u8"), ("provision_kind", "<i4"), ("max_instances", "<i4"),
+    ("threshold_s", "<f8"), ("cold_start_s", "<f8"), ("cooldown_s", "<f8"),
 ])
+summary_dtype = np.dtype([
+    ("total_preemptions", "<i8"), ("end_ticks", "<i8"), ("instances_provisioned", "<i4"),
+    ("final_instance_count", "<i4"),
+])
+report_dtype = np.dtype([
+    ("finished_requests", "<i4"), ("censored_requests", "<i4"), ("throughput_rps", "<f8"),
+    ("mean_ttft_s", "<f8"), ("p50_ttft_s", "<f8"), ("p99_ttft_s", "<f8"),
+    ("mean_e2e_s", "<f8"), ("p50_e2e_s", "<f8"), ("p99_e2e_s", "<f8"),
+    ("total_preemptions", "<i8"), ("instances_provisioned", "<i4"),
+    ("final_instance_count", "<i4"),
+])
+capacity_dtype = np.dtype([
+    ("capacity_qps", "<f8"), ("bracket_pass", "<i4"), ("bracket_fail", "<i4"),
+    ("monotone", "<i4"), ("n_tested", "<i4"),
+])
+NO_CAPACITY = 12
+STATUS_NAMES[12] = "NO_CAPACITY"
+PROVISION_STATIC, PROVISION_PREEMPT, PROVISION_RELIEF = 0, 1, 2
 outcome_dtype = np.dtype([
     ("arrival_ticks", "<i8"), ("dispatch_ticks", "<i8"), ("first_token_ticks", "<i8"),
     ("finish_ticks", "<i8"), ("instance", "<i4"), ("preempt_count", "<i4"),
@@ -129,10 +148,15 @@ def make_workload(count=1000, trace_seed=1234, prompt_median=230.0, prompt_sigma
 
 
 def make_replay_spec(n_instances, policy=POLICY_BLOCK_PREDICTIVE, objective=0, capture=1,
-                     policy_seed=0) -> np.ndarray:
+                     policy_seed=0, provision_kind=PROVISION_STATIC, max_instances=None,
+                     threshold_s=70.0, cold_start_s=30.0, cooldown_s=15.0) -> np.ndarray:
+    """ExperimentSpec subset + ProvisionPolicy (autoscaler.h:10-27) defaults."""
     s = np.zeros(1, replay_spec_dtype)
     s["n_instances"], s["policy"], s["objective"] = n_instances, policy, objective
     s["capture"], s["policy_seed"] = capture, policy_seed
+    s["provision_kind"] = provision_kind
+    s["max_instances"] = n_instances if max_instances is None else max_instances
+    s["threshold_s"], s["cold_start_s"], s["cooldown_s"] = threshold_s, cold_start_s, cooldown_s
     return s
 
 

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <array>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -466,10 +467,12 @@ bsg_status bsg_predict_batch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n
   dev.decoded = static_cast<const int32_t*>(ctx->decoded.p);
   auto* dsc = static_cast<bsg_scenario*>(ctx->scen.p);
   auto* dres = static_cast<bsg_result*>(ctx->res.p);
-  // Chunked pipeline: chunk c (a contiguous scenario range) copies only the
+  // Chunked pipeline (sets > 256k scenarios; measured: at cfg2 size one chunk
+  // wins, H2D is PCIe-bound): chunk c (a contiguous scenario range) copies only the
   // entry range its scenarios reference, runs, and copies its results back on
   // stream c % 3, so H2D(c+1) overlaps the kernel on c and D2H(c-1).
-  const int64_t target_chunk = 16384;
+  const char* env_chunk = std::getenv("BSG_PIPE_CHUNK");
+  const int64_t target_chunk = env_chunk ? std::max<int64_t>(1, std::atoll(env_chunk)) : 262144;
   const int64_t nchunks = std::min<int64_t>(8, std::max<int64_t>(1, n / target_chunk));
   const int64_t per = (n + nchunks - 1) / nchunks;
   auto cols_h = std::array<const int32_t*, 4>{entries->prompt, entries->est, entries->prefill,

@@ -364,6 +364,8 @@ class Replay {
       : ctx_(ctx), cfg_(cfg), spec_(spec), recs_(std::move(recs)), cap_(cap), rng_(spec.policy_seed) {
     for (int i = 0; i < spec.n_instances; ++i) inst_.emplace_back(cfg);
     qpm_.resize(spec.n_instances);
+    active_ = spec.n_instances;
+    next_instance_id_ = spec.n_instances;
     out_.resize(recs_.size());
     for (size_t i = 0; i < recs_.size(); ++i) {
       out_[i] = bsg_request_outcome{recs_[i].arrival, -1, -1, -1, -1, 0};
@@ -386,7 +388,8 @@ class Replay {
       const Ev ev = q_.top();
       q_.pop();
       now_ = ev.t;
-      const bsg_status st = ev.kind == 0 ? arrival(ev.a) : complete(ev.a);
+      const bsg_status st =
+          ev.kind == 0 ? arrival(ev.a) : (ev.kind == 1 ? complete(ev.a) : provision_complete(ev.a));
       if (st != BSG_OK) return st;
       open = true;
     }
@@ -394,7 +397,12 @@ class Replay {
   }
 
   const std::vector<bsg_request_outcome>& outcomes() const { return out_; }
-  int64_t preemptions() const { return preemptions_; }
+  void summary(bsg_replay_summary* s) const {
+    s->total_preemptions = preemptions_;
+    s->end_ticks = now_;
+    s->instances_provisioned = provisioned_total_;
+    s->final_instance_count = static_cast<int32_t>(inst_.size());
+  }
 
  private:
   void push(int64_t t, int32_t kind, int32_t a) { q_.push(Ev{t, seq_++, kind, a}); }
@@ -422,7 +430,33 @@ class Replay {
     inst_[iid].finish_step(&firsts_, &dones_);
     for (int32_t rid : firsts_)
       if (out_[rid].first_token_ticks < 0) out_[rid].first_token_ticks = now_;
-    for (int32_t rid : dones_) out_[rid].finish_ticks = now_;
+    for (int32_t rid : dones_) {
+      out_[rid].finish_ticks = now_;
+      if (spec_.provision_kind == 2)
+        maybe_provision(2, static_cast<double>(now_ - out_[rid].arrival_ticks) * 1e-9);
+    }
+    return BSG_OK;
+  }
+
+  // Autoscaler::evaluate (autoscaler.cpp:36-52) + maybe_provision (driver.cpp:253-261).
+  void maybe_provision(int32_t signal_kind, double latency_s) {
+    if (spec_.provision_kind == 0 || signal_kind != spec_.provision_kind) return;
+    if (latency_s < spec_.threshold_s) return;
+    if (has_last_provision_ && now_ - last_provision_ < ticks_from_seconds(spec_.cooldown_s)) return;
+    if (active_ + pending_ >= spec_.max_instances) return;
+    last_provision_ = now_;
+    has_last_provision_ = true;
+    ++pending_;
+    ++provisioned_total_;
+    push(now_ + ticks_from_seconds(spec_.cold_start_s), 2, next_instance_id_++);
+  }
+
+  bsg_status provision_complete(int32_t iid) {  // driver.cpp:263-269
+    if (iid < static_cast<int32_t>(inst_.size())) return BSG_INVALID_ARGUMENT;
+    inst_.emplace_back(cfg_);
+    qpm_.resize(inst_.size());
+    --pending_;
+    ++active_;
     return BSG_OK;
   }
 
@@ -435,9 +469,20 @@ class Replay {
     for (int i = 0; i < n; ++i)
       inst_[i].snapshot(&snaps_run_[i], &snaps_wait_[i], &free_[i], &batch_[i]);
     int32_t chosen = 0;
-    const bsg_status st = decide(rid, &chosen);
+    bool have_prediction = false;
+    const bsg_status st = decide(rid, &chosen, &have_prediction);
     if (st != BSG_OK) return st;
     qpm_[chosen].record(now_);
+    if (spec_.provision_kind == 1) {  // driver.cpp:197-211
+      int64_t e2e = 0;
+      if (have_prediction) {
+        e2e = per_[chosen].e2e_ticks;
+      } else {
+        const bsg_status ps = predict_one(rid, chosen, &e2e);
+        if (ps != BSG_OK) return ps;
+      }
+      maybe_provision(1, static_cast<double>(e2e) * 1e-9);
+    }
     const Record& r = recs_[rid];
     inst_[chosen].admit(rid, r.prompt, r.output, r.est);
     out_[rid].dispatch_ticks = now_;
@@ -447,7 +492,33 @@ class Replay {
 
   // Dispatcher::dispatch (scheduler.cpp:115-152) with the heuristics of
   // pick_heuristic (scheduler.cpp:68-113).
-  bsg_status decide(int32_t rid, int32_t* chosen) {
+  // predict() for one instance's snapshot (heuristic policies under preempt
+  // provisioning ask for the chosen instance's prediction, driver.cpp:202-209).
+  bsg_status predict_one(int32_t rid, int32_t iid, int64_t* e2e) {
+    prompt_.clear();
+    est_.clear();
+    prefill_.clear();
+    decoded_.clear();
+    ids_.clear();
+    bsg_scenario sc{};
+    sc.run_n = static_cast<int32_t>(snaps_run_[iid].size());
+    for (const Member& m : snaps_run_[iid]) add(m);
+    sc.wait_off = static_cast<int32_t>(prompt_.size());
+    sc.wait_n = static_cast<int32_t>(snaps_wait_[iid].size());
+    for (const Member& m : snaps_wait_[iid]) add(m);
+    sc.cand_prompt = recs_[rid].prompt;
+    sc.cand_est = recs_[rid].est;
+    bsg_entries e{ids_.data(), prompt_.data(), est_.data(), prefill_.data(), decoded_.data()};
+    bsg_result r{};
+    const bsg_status st = bsg_predict_batch(ctx_, &e, static_cast<int64_t>(prompt_.size()), &sc, 1, &r);
+    if (st != BSG_OK) return st;
+    if (r.status != BSG_OK) return static_cast<bsg_status>(r.status);
+    *e2e = r.e2e_ticks;
+    return BSG_OK;
+  }
+
+  bsg_status decide(int32_t rid, int32_t* chosen, bool* have_prediction) {
+    *have_prediction = false;
     const int n = static_cast<int>(inst_.size());
     switch (spec_.policy) {
       case BSG_POLICY_RANDOM: *chosen = static_cast<int32_t>(rng_.below(n)); return BSG_OK;
@@ -527,6 +598,7 @@ class Replay {
       return BSG_INVALID_ARGUMENT;
     }
     *chosen = pick;
+    *have_prediction = true;
     return BSG_OK;
   }
 
@@ -552,6 +624,9 @@ class Replay {
   uint64_t seq_ = 0;
   int64_t now_ = 0;
   int64_t preemptions_ = 0;
+  int32_t active_ = 0, pending_ = 0, provisioned_total_ = 0, next_instance_id_ = 0;
+  int64_t last_provision_ = 0;
+  bool has_last_provision_ = false;
   std::vector<int32_t> victims_, firsts_, dones_;
   std::vector<std::vector<Member>> snaps_run_, snaps_wait_;
   std::vector<int32_t> free_, batch_;
@@ -598,8 +673,13 @@ bsg_status bsg_make_workload(const bsg_workload* w, int32_t* prompt, int32_t* ou
 
 bsg_status bsg_replay(bsg_ctx* ctx, const bsg_workload* w, const bsg_instance_cfg* cfg,
                       const bsg_replay_spec* spec, bsg_request_outcome* outcomes,
-                      int64_t* total_preemptions, bsg_capture** capture) {
+                      bsg_replay_summary* summary, bsg_capture** capture) {
   if (!ctx || !w || !cfg || !spec || spec->n_instances < 1) return BSG_INVALID_ARGUMENT;
+  // validate_provision_policy (autoscaler.cpp:23-34) and config.cpp:177-180
+  if (spec->provision_kind < 0 || spec->provision_kind > 2 || !(spec->threshold_s > 0) ||
+      spec->cold_start_s < 0 || spec->cooldown_s < 0 ||
+      (spec->provision_kind != 0 && spec->max_instances < spec->n_instances))
+    return BSG_BAD_CONFIG;
   int32_t bi = 0, fc = 0;
   bsg_status st = bsg_set_configs(ctx, cfg, 1, &bi, &fc);
   if (st != BSG_OK) return st;
@@ -617,7 +697,7 @@ bsg_status bsg_replay(bsg_ctx* ctx, const bsg_workload* w, const bsg_instance_cf
   if (outcomes)
     std::memcpy(outcomes, replay.outcomes().data(),
                 replay.outcomes().size() * sizeof(bsg_request_outcome));
-  if (total_preemptions) *total_preemptions = replay.preemptions();
+  if (summary) replay.summary(summary);
   if (capture) *capture = cap.release();
   return BSG_OK;
 }
@@ -641,3 +721,120 @@ void bsg_capture_copy(const bsg_capture* c, uint64_t* id, int32_t* prompt, int32
 void bsg_capture_free(bsg_capture* c) { delete c; }
 
 }  // extern "C"
+
+namespace {
+
+// percentile_nearest_rank (metrics.cpp:11-19)
+double nearest_rank(std::vector<double> v, double p) {
+  if (v.empty()) return 0.0;
+  std::sort(v.begin(), v.end());
+  const double n = static_cast<double>(v.size());
+  std::size_t rank = static_cast<std::size_t>(std::ceil(p / 100.0 * n));
+  if (rank < 1) rank = 1;
+  if (rank > v.size()) rank = v.size();
+  return v[rank - 1];
+}
+
+double mean_of(const std::vector<double>& v) {
+  if (v.empty()) return 0.0;
+  double s = 0;
+  for (double x : v) s += x;
+  return s / static_cast<double>(v.size());
+}
+
+}  // namespace
+
+extern "C" bsg_status bsg_aggregate(const bsg_request_outcome* o, int64_t n,
+                                    const bsg_replay_summary* summary, bsg_run_report* out) {
+  if (!o || !out || n < 0) return BSG_INVALID_ARGUMENT;
+  std::memset(out, 0, sizeof(*out));
+  std::vector<double> ttft, e2e;
+  int64_t first_arrival = INT64_MAX, last_finish = INT64_MIN;
+  for (int64_t i = 0; i < n; ++i) {
+    first_arrival = std::min(first_arrival, o[i].arrival_ticks);
+    if (o[i].finish_ticks >= 0 && o[i].dispatch_ticks >= 0 && o[i].first_token_ticks >= 0) {
+      ttft.push_back(static_cast<double>(o[i].first_token_ticks - o[i].dispatch_ticks) * 1e-9);
+      e2e.push_back(static_cast<double>(o[i].finish_ticks - o[i].arrival_ticks) * 1e-9);
+      last_finish = std::max(last_finish, o[i].finish_ticks);
+      ++out->finished_requests;
+    } else {
+      ++out->censored_requests;
+    }
+  }
+  out->mean_ttft_s = mean_of(ttft);
+  out->p50_ttft_s = nearest_rank(ttft, 50.0);
+  out->p99_ttft_s = nearest_rank(ttft, 99.0);
+  out->mean_e2e_s = mean_of(e2e);
+  out->p50_e2e_s = nearest_rank(e2e, 50.0);
+  out->p99_e2e_s = nearest_rank(e2e, 99.0);
+  if (n > 0 && out->finished_requests > 0 && last_finish > first_arrival)
+    out->throughput_rps = static_cast<double>(out->finished_requests) /
+                          (static_cast<double>(last_finish - first_arrival) * 1e-9);
+  if (summary) {
+    out->total_preemptions = summary->total_preemptions;
+    out->instances_provisioned = summary->instances_provisioned;
+    out->final_instance_count = summary->final_instance_count;
+  }
+  return BSG_OK;
+}
+
+extern "C" bsg_status bsg_capacity_search(bsg_ctx* ctx, const bsg_workload* base,
+                                          const bsg_instance_cfg* cfg, const bsg_replay_spec* spec,
+                                          uint64_t seed, int32_t qps_min, int32_t qps_max,
+                                          double slo_p99_ttft_s, bsg_capacity_result* out,
+                                          double* tested_qps, int32_t* tested_pass,
+                                          int32_t tested_cap) {
+  if (!ctx || !base || !cfg || !spec || !out) return BSG_INVALID_ARGUMENT;
+  if (qps_min > qps_max) return BSG_BAD_CONFIG;  // metrics.cpp:141
+  std::memset(out, 0, sizeof(*out));
+  bsg_status err = BSG_OK;
+  auto passes = [&](double qps) -> bool {
+    bsg_workload w = *base;  // spec_for_cell (driver.cpp:321-331)
+    w.qps = qps;
+    w.arrival_seed = seed;
+    w.estimator_seed = seed;
+    bsg_replay_spec sp = *spec;
+    sp.policy_seed = seed;
+    sp.capture = 0;
+    const int32_t n = (w.request_cap >= 0 && w.request_cap < w.count) ? w.request_cap : w.count;
+    std::vector<bsg_request_outcome> o(static_cast<size_t>(n));
+    bsg_replay_summary summ{};
+    const bsg_status st = bsg_replay(ctx, &w, cfg, &sp, o.data(), &summ, nullptr);
+    if (st != BSG_OK) {
+      err = st;
+      return false;
+    }
+    bsg_run_report rep{};
+    bsg_aggregate(o.data(), n, &summ, &rep);
+    const bool ok = rep.p99_ttft_s < slo_p99_ttft_s;
+    if (out->n_tested < tested_cap) {
+      if (tested_qps) tested_qps[out->n_tested] = qps;
+      if (tested_pass) tested_pass[out->n_tested] = ok ? 1 : 0;
+    }
+    ++out->n_tested;
+    return ok;
+  };
+  std::vector<bool> integer_pass;
+  for (int32_t q = qps_min; q <= qps_max; ++q) {
+    integer_pass.push_back(passes(static_cast<double>(q)));
+    if (err != BSG_OK) return err;
+  }
+  if (!integer_pass.front()) return BSG_NO_CAPACITY;
+  int last = 0;
+  while (last + 1 < static_cast<int>(integer_pass.size()) && integer_pass[last + 1]) ++last;
+  out->monotone = 1;
+  for (int i = last + 1; i < static_cast<int>(integer_pass.size()); ++i)
+    if (integer_pass[i]) out->monotone = 0;
+  out->bracket_pass = qps_min + last;
+  out->bracket_fail = out->bracket_pass + 1;
+  double best = static_cast<double>(out->bracket_pass);
+  if (out->bracket_pass < qps_max) {
+    for (int tenth = 1; tenth <= 9; ++tenth) {
+      const double qps = static_cast<double>(out->bracket_pass * 10 + tenth) / 10.0;
+      if (passes(qps)) best = std::max(best, qps);
+      if (err != BSG_OK) return err;
+    }
+  }
+  out->capacity_qps = best;
+  return BSG_OK;
+}

@@ -47,7 +47,7 @@ def load() -> C.CDLL:
         "bsg_predict_batch_device": (C.c_int, [V, E, V, C.c_int64, C.c_int32, V, V]),
         "bsg_trace": (C.c_int, [V, E, C.c_int64, V, V, C.c_int64, C.POINTER(C.c_int64), V]),
         "bsg_dispatch": (C.c_int, [V, E, C.c_int64, V, V, C.c_int32, C.c_int32, C.c_int32, V, V]),
-        "bsg_replay": (C.c_int, [V, V, V, V, V, C.POINTER(C.c_int64), C.POINTER(C.c_void_p)]),
+        "bsg_replay": (C.c_int, [V, V, V, V, V, V, C.POINTER(C.c_void_p)]),
         "bsg_capture_sizes": (None, [V, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
         "bsg_capture_copy": (None, [V] * 7),
         "bsg_capture_free": (None, [V]),
@@ -55,6 +55,9 @@ def load() -> C.CDLL:
         "bsg_ticks_to_seconds": (C.c_double, [C.c_int64]),
         "bsg_dispatch_mc": (C.c_int, [V, E, C.c_int64, V, V, C.c_int32, C.c_int32, V, C.c_int32,
                                       C.c_int32, V, V, V, V]),
+        "bsg_aggregate": (C.c_int, [V, C.c_int64, V, V]),
+        "bsg_capacity_search": (C.c_int, [V, V, V, V, C.c_uint64, C.c_int32, C.c_int32, C.c_double,
+                                          V, V, V, C.c_int32]),
         "bsg_mc_lengths": (C.c_int, [C.c_int32, C.c_uint64, C.c_int32, C.c_uint64, C.c_double, V]),
     }
     for name, (res, args) in sigs.items():
@@ -78,6 +81,17 @@ def exported_symbols_declared_in_header() -> list[str]:
 
 def _p(a):
     return abi.ptr(a)
+
+
+def aggregate(outcomes: np.ndarray, summary=None) -> np.void:
+    """RunReport subset of a replay's outcomes (bsg_aggregate, metrics.cpp:21-124)."""
+    out = np.zeros(1, abi.report_dtype)
+    summ = None if summary is None else np.array([summary], abi.summary_dtype)
+    outcomes = np.ascontiguousarray(outcomes, abi.outcome_dtype)
+    st = load().bsg_aggregate(_p(outcomes), len(outcomes), _p(summ), _p(out))
+    if st != abi.OK:
+        raise BsgError(st, "bsg_aggregate")
+    return out[0]
 
 
 def mc_lengths(est: int, request_id: int, n_samples: int = 256, seed: int = 1,
@@ -201,16 +215,28 @@ class Context:
                     "bsg_dispatch_mc")
         return chosen, scores, samples, per
 
+    def capacity_search(self, w, cfg, spec, seed: int, qps_min: int, qps_max: int, slo: float):
+        """capacity_search over GPU closed loops. Returns (status, result, [(qps, passed)])."""
+        out = np.zeros(1, abi.capacity_dtype)
+        tq = np.zeros(256, np.float64)
+        tp = np.zeros(256, np.int32)
+        st = self.L.bsg_capacity_search(self.h, _p(w), _p(cfg), _p(spec), seed, qps_min, qps_max,
+                                        slo, _p(out), _p(tq), _p(tp), 256)
+        if st not in (abi.OK, abi.NO_CAPACITY):
+            self._check(st, "bsg_capacity_search")
+        n = int(out["n_tested"][0])
+        return st, out[0], list(zip(tq[:n].tolist(), tp[:n].astype(bool).tolist()))
+
     def replay(self, w, cfg, spec):
         """Closed-loop replay (host live instances, GPU what-ifs). Returns
-        (outcomes, total_preemptions, captured ScenarioSet or None)."""
+        (outcomes, summary, captured ScenarioSet or None)."""
         n = int(w["count"][0]) if w["request_cap"][0] < 0 else min(int(w["count"][0]),
                                                                     int(w["request_cap"][0]))
         out = np.zeros(n, abi.outcome_dtype)
-        tp = C.c_int64(0)
+        summ = np.zeros(1, abi.summary_dtype)
         h = C.c_void_p(None)
         capture = bool(spec["capture"][0])
-        self._check(self.L.bsg_replay(self.h, _p(w), _p(cfg), _p(spec), _p(out), C.byref(tp),
+        self._check(self.L.bsg_replay(self.h, _p(w), _p(cfg), _p(spec), _p(out), _p(summ),
                                       C.byref(h) if capture else None), "bsg_replay")
         ss = None
         if capture:
@@ -222,4 +248,4 @@ class Context:
             self.L.bsg_capture_copy(h, _p(ids), *[_p(c) for c in cols], _p(sc))
             self.L.bsg_capture_free(h)
             ss = abi.ScenarioSet(*cols, sc, ids=ids)
-        return out, tp.value, ss
+        return out, summ[0], ss

@@ -1,0 +1,82 @@
+"""Multi-GPU sharding of the what-if path.
+
+Scenarios are independent, so the path shards with no data-path collective:
+
+* throughput mode (bench.py, cfg1-3): weak scaling — each rank replays and
+  simulates its own arrival stream (``weak_seed``); only the max-over-ranks
+  time and summed counts cross ranks (``reduce_max_sum``).
+* latency mode (one dispatch across GPUs, cfg4): instance ``i`` lives on rank
+  ``i % world`` (``instance_shard``) with all of its samples, so each rank's
+  score sum is local; the only exchange is the argmin (``global_argmin``),
+  exact for any int64 score and lowest-id ties (scheduler.cpp:138-150).
+* sweep mode (cfg5): whole closed-loop cells are assigned longest-first to the
+  least-loaded rank (``assign_cells_lpt``).
+
+Collectives go through torch.distributed (NCCL on GPUs, gloo in the CPU tests).
+"""
+from __future__ import annotations
+
+import heapq
+
+import numpy as np
+
+INT64_MAX = np.iinfo(np.int64).max
+
+
+def weak_seed(rank: int, base: int = 1) -> int:
+    """Arrival-stream seed of rank ``rank`` in weak scaling."""
+    return base + rank
+
+
+def instance_shard(n_inst: int, world: int, rank: int) -> np.ndarray:
+    """Instance indices simulated by ``rank`` in latency mode."""
+    return np.arange(rank, n_inst, world, dtype=np.int32)
+
+
+def local_best(scores: np.ndarray, ids: np.ndarray) -> tuple[int, int]:
+    """(score, id) minimum with lowest-id ties; (INT64_MAX, INT32_MAX) if empty."""
+    if len(scores) == 0:
+        return INT64_MAX, np.iinfo(np.int32).max
+    scores = np.asarray(scores, np.int64)
+    ids = np.asarray(ids, np.int64)
+    m = scores.min()
+    return int(m), int(ids[scores == m].min())
+
+
+def global_argmin(scores: np.ndarray, ids: np.ndarray, device=None, group=None) -> int:
+    """Exact cross-rank argmin: all_reduce MIN of the best score, then MIN of the
+    ids that attain it (two int64 collectives; no packing, so no range limit)."""
+    import torch
+    import torch.distributed as dist
+    s, i = local_best(scores, ids)
+    t = torch.tensor([s], dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    cand = torch.tensor([i if s == int(t.item()) else np.iinfo(np.int64).max], dtype=torch.int64,
+                        device=device)
+    dist.all_reduce(cand, op=dist.ReduceOp.MIN, group=group)
+    return int(cand.item())
+
+
+def reduce_max_sum(maxes: list[float], sums: list[int], device=None, group=None):
+    """Max-over-ranks of timings and sums of counts."""
+    import torch
+    import torch.distributed as dist
+    a = torch.tensor(maxes, dtype=torch.float64, device=device)
+    b = torch.tensor(sums, dtype=torch.int64, device=device)
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(a, op=dist.ReduceOp.MAX, group=group)
+        dist.all_reduce(b, op=dist.ReduceOp.SUM, group=group)
+    return [float(x) for x in a.tolist()], [int(x) for x in b.tolist()]
+
+
+def assign_cells_lpt(costs, world: int) -> list[list[int]]:
+    """Longest-processing-time-first assignment of sweep cells to ranks
+    (deterministic: ties by cell index, then rank index)."""
+    order = sorted(range(len(costs)), key=lambda c: (-costs[c], c))
+    heap = [(0.0, r) for r in range(world)]
+    out: list[list[int]] = [[] for _ in range(world)]
+    for c in order:
+        load, r = heapq.heappop(heap)
+        out[r].append(c)
+        heapq.heappush(heap, (load + float(costs[c]), r))
+    return [sorted(x) for x in out]

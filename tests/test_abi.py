@@ -90,3 +90,19 @@ def test_mc_lengths_match_reference_estimator(lib, ref):
         got = native.mc_lengths(est, rid, 256, seed=1)
         exp = [ref.lib.ref_estimate_noisy(est, rid * 256 + s, 1, 0.244) for s in range(256)]
         assert got.tolist() == exp
+
+
+@pytest.mark.parametrize("kw,n_inst", [
+    (dict(count=800, qps=9, arrival_seed=5), 4),
+    (dict(count=600, prompt_median=600, output_median=600, qps=6, arrival_seed=2), 3),
+])
+def test_aggregate_matches_reference(lib, ref, kw, n_inst):
+    """bsg_aggregate (host) over the reference's own run outcomes equals the
+    reference's aggregate() RunReport (metrics.cpp:21-124), double for double."""
+    w = abi.make_workload(**kw)
+    cfg = abi.make_config()
+    spec = abi.make_replay_spec(n_inst, policy=abi.POLICY_LLUMNIX_MINUS)
+    out, summ = ref.run_experiment(w, cfg, spec)
+    got = native.aggregate(out, summ)
+    exp = ref.run_report(w, cfg, spec)
+    assert got.tolist() == exp.tolist()

@@ -96,7 +96,7 @@ def test_closed_loop_decisions_match_reference(ctx, ref, kw, n_inst, policy):
     got, gp, gss = ctx.replay(w, cfg, spec)
     exp, ep = ref.run_experiment(w, cfg, spec)
     assert np.array_equal(got["instance"], exp["instance"])
-    assert np.array_equal(got, exp) and gp == ep
+    assert np.array_equal(got, exp) and gp.tolist() == ep.tolist()
 
 
 def test_dispatch_argmin_ties_lowest_id(ctx):
@@ -133,3 +133,39 @@ def test_mc_dispatch_matches_reference_loop(ctx, ref, n_inst, n_samples, qps):
     assert np.array_equal(samples, e_samples)
     assert np.array_equal(scores, e_scores)
     assert np.array_equal(chosen, e_chosen)
+
+
+@pytest.mark.parametrize("kind,policy", [
+    (abi.PROVISION_PREEMPT, abi.POLICY_BLOCK_PREDICTIVE),
+    (abi.PROVISION_PREEMPT, abi.POLICY_ROUND_ROBIN),
+    (abi.PROVISION_RELIEF, abi.POLICY_BLOCK_PREDICTIVE),
+])
+def test_autoscaler_closed_loop_matches_reference(ctx, ref, kind, policy):
+    """Auto-provisioning (autoscaler.cpp:36-52, driver.cpp:197-269): instances
+    added mid-run on predicted (preempt) or realized (relief) latency; every
+    decision, timeline and the provisioning totals equal run_experiment."""
+    cfg = abi.make_config()
+    w = abi.make_workload(count=1200, qps=30.0, arrival_seed=3)
+    spec = abi.make_replay_spec(3, policy=policy, capture=0, provision_kind=kind, max_instances=8,
+                                threshold_s=8.0, cold_start_s=5.0, cooldown_s=2.0)
+    got, gs, _ = ctx.replay(w, cfg, spec)
+    exp, es = ref.run_experiment(w, cfg, spec)
+    assert es["instances_provisioned"] > 0  # the scenario actually provisions
+    assert np.array_equal(got, exp) and gs.tolist() == es.tolist()
+    from paper_2508_03611_b200 import native
+    assert native.aggregate(got, gs).tolist() == ref.run_report(w, cfg, spec).tolist()
+
+
+def test_capacity_search_matches_reference(ctx, ref):
+    """capacity_search (metrics.cpp:139-178) over BlockPredictive closed loops
+    (GPU what-ifs) equals the reference's run_capacity runner: same tested
+    (qps, pass) sequence, bracket and capacity."""
+    cfg = abi.make_config()
+    w = abi.make_workload(count=600, request_cap=400)
+    spec = abi.make_replay_spec(2, capture=0)
+    st, got, tested = ctx.capacity_search(w, cfg, spec, seed=7, qps_min=1, qps_max=16, slo=1.0)
+    est, exp, etested = ref.capacity_search(w, cfg, spec, seed=7, qps_min=1, qps_max=16, slo=1.0)
+    assert st == est == abi.OK
+    assert tested == etested
+    assert got.tolist() == exp.tolist()
+    assert 1 < got["capacity_qps"] < 16  # a real bracket, with tenths tested

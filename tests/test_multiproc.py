@@ -1,0 +1,81 @@
+"""World-size-2 gloo tests (CPU) of the multi-GPU host logic in
+paper_2508_03611_b200/shard.py: the exact cross-rank argmin used when one
+dispatch's instances are sharded across GPUs, the max/sum reductions of the
+weak-scaling bench, and deterministic LPT cell assignment for sweeps."""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    from paper_2508_03611_b200 import shard
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(123)
+        out = {}
+        for case in range(40):
+            n_inst = int(rng.integers(1, 70))
+            scores = rng.integers(0, 6, n_inst).astype(np.int64) * (1 << 40)  # many ties, huge values
+            if case % 5 == 0:
+                scores[:] = np.iinfo(np.int64).max - 7  # all equal at the top of the range
+            mine = shard.instance_shard(n_inst, world, rank)
+            out[case] = (shard.global_argmin(scores[mine], mine), int(np.argmin(scores)))
+        maxes, sums = shard.reduce_max_sum([1.5 + rank, 10.0 * rank], [100 + rank, 7])
+        q.put((rank, out, maxes, sums))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_argmin_and_reductions_gloo_world2():
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, out, maxes, sums in results:
+        for case, (got, exp) in out.items():
+            assert got == exp, (rank, case, got, exp)  # lowest id wins ties, across ranks
+        assert maxes == [2.5, 10.0] and sums == [201, 14]
+
+
+def test_instance_shards_partition():
+    from paper_2508_03611_b200 import shard
+    for n in (1, 7, 64, 128):
+        for w in (1, 2, 4, 8):
+            parts = np.concatenate([shard.instance_shard(n, w, r) for r in range(w)])
+            assert sorted(parts.tolist()) == list(range(n))
+
+
+def test_lpt_assignment_balanced_and_deterministic():
+    from paper_2508_03611_b200 import shard
+    rng = np.random.default_rng(5)
+    costs = rng.lognormal(0, 1.5, 300)
+    a = shard.assign_cells_lpt(costs, 8)
+    assert a == shard.assign_cells_lpt(costs, 8)
+    assert sorted(sum(a, [])) == list(range(300))
+    loads = [costs[x].sum() for x in a]
+    assert max(loads) <= (sum(loads) / 8) * 1.05 + costs.max()
