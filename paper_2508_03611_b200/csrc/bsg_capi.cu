@@ -21,9 +21,15 @@
 namespace bsg {
 
 constexpr int kWarpsPerBlock = 4;
+// Resident-block target per SM for the 32-member kernels: 8 x 4 warps = 32
+// warps/SM needs <= 64 registers/thread (measured: see profiles/).
+#ifndef BSG_MINB_K1
+#define BSG_MINB_K1 8
+#endif
+constexpr int min_blocks(int k) { return k == 1 ? BSG_MINB_K1 : 1; }
 
-template <int K>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+template <int K, bool POW2>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, min_blocks(K))
     predict_kernel(const DevCfg* __restrict__ cfgs, int32_t ncfg,
                    const int32_t* __restrict__ prompt, const int32_t* __restrict__ est,
                    const int32_t* __restrict__ prefill, const int32_t* __restrict__ decoded,
@@ -54,11 +60,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     }
     return;
   }
-  simulate_scenario<K, false>(cfg, prompt, est, prefill, decoded, sc,
-                              smem + warp * (5 * 32 * K + 32), o, TraceSink{nullptr, 0});
+  simulate_scenario<K, false, false, POW2>(cfg, prompt, est, prefill, decoded, sc,
+                                          smem + warp * (5 * 32 * K + 32), o, TraceSink{nullptr, 0});
 }
 
-template <int K>
+template <int K, bool POW2>
 __global__ void __launch_bounds__(32)
     trace_kernel(const DevCfg* __restrict__ cfgs, const int32_t* __restrict__ prompt,
                  const int32_t* __restrict__ est, const int32_t* __restrict__ prefill,
@@ -67,8 +73,8 @@ __global__ void __launch_bounds__(32)
   __shared__ int32_t smem[5 * 32 * K + 32];
   const bsg_scenario sc = scen[0];
   const DevCfg cfg = cfgs[sc.cfg];
-  simulate_scenario<K, true>(cfg, prompt, est, prefill, decoded, sc, smem, out,
-                             TraceSink{rec, cap});
+  simulate_scenario<K, true, false, POW2>(cfg, prompt, est, prefill, decoded, sc, smem, out,
+                                         TraceSink{rec, cap});
 }
 
 // BlockPredictive argmin (scheduler.cpp:138-150): one warp per request, value
@@ -112,7 +118,7 @@ __global__ void argmin_kernel(const bsg_result* __restrict__ res,
 // last warp of each request to finish takes the argmin over the per-instance
 // scores (sum of per-sample e2e ticks), lowest instance id on ties
 // (scheduler.cpp:138-150).
-template <int K>
+template <int K, bool POW2>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     dispatch_mc_kernel(const DevCfg* __restrict__ cfgs, int32_t ncfg,
                        const int32_t* __restrict__ prompt, const int32_t* __restrict__ est,
@@ -152,7 +158,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         scores[w] = INT64_MAX;
       }
     } else {
-      simulate_scenario<K, false, true>(
+      simulate_scenario<K, false, true, POW2>(
           cfg, prompt, est, prefill, decoded, sc, smem, o, TraceSink{nullptr, 0},
           McArgs{len, S, sample_e2e ? sample_e2e + w * S : nullptr, scores + w, objective});
     }
@@ -231,6 +237,7 @@ struct bsg_ctx {
   size_t pinned_cap = 0;
   int32_t ncfg = 0;
   int32_t max_batch_all = 0;
+  bool all_pow2 = false;  // every config's block_size is a power of two
   std::mutex mu;
 };
 
@@ -288,9 +295,13 @@ template <int K>
 void launch_predict(bsg_ctx* ctx, int64_t n, const bsg_entries& e, const bsg_scenario* sc,
                     const int32_t* order, bsg_result* out, cudaStream_t s) {
   const int64_t blocks = (n + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  predict_kernel<K><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
-      static_cast<const DevCfg*>(ctx->cfgs.p), ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded,
-      sc, n, order, out);
+  auto* cf = static_cast<const DevCfg*>(ctx->cfgs.p);
+  if (ctx->all_pow2)
+    predict_kernel<K, true><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
+        cf, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, order, out);
+  else
+    predict_kernel<K, false><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
+        cf, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, order, out);
   ctx->launches += 1;
 }
 
@@ -443,6 +454,8 @@ bsg_status bsg_set_configs(bsg_ctx* ctx, const bsg_instance_cfg* cfgs, int32_t n
   ctx->dev_cfgs_host = dev;
   ctx->ncfg = n;
   ctx->max_batch_all = maxb;
+  ctx->all_pow2 = true;
+  for (int32_t i = 0; i < n; ++i) ctx->all_pow2 &= dev[i].div_magic == 0;
   return BSG_OK;
 }
 
@@ -556,10 +569,22 @@ bsg_status bsg_trace(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries
   auto* sc = static_cast<const bsg_scenario*>(ctx->scen.p);
   auto* cf = static_cast<const DevCfg*>(ctx->cfgs.p);
   switch (k) {
-    case 1: trace_kernel<1><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap); break;
-    case 2: trace_kernel<2><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap); break;
-    case 4: trace_kernel<4><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap); break;
-    case 8: trace_kernel<8><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap); break;
+    case 1:
+      if (ctx->all_pow2) trace_kernel<1, true><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap);
+      else trace_kernel<1, false><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap);
+      break;
+    case 2:
+      if (ctx->all_pow2) trace_kernel<2, true><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap);
+      else trace_kernel<2, false><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap);
+      break;
+    case 4:
+      if (ctx->all_pow2) trace_kernel<4, true><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap);
+      else trace_kernel<4, false><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap);
+      break;
+    case 8:
+      if (ctx->all_pow2) trace_kernel<8, true><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap);
+      else trace_kernel<8, false><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap);
+      break;
     default: ctx->last_error = "member capacity beyond 256"; return BSG_BAD_INPUT;
   }
   ctx->launches += 1;
@@ -694,15 +719,22 @@ bsg_status bsg_dispatch_mc(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_e
   auto* dcnt = static_cast<unsigned*>(ctx->counters.p);
   auto* dch = static_cast<int32_t*>(ctx->chosen.p);
   auto* dcf = static_cast<const DevCfg*>(ctx->cfgs.p);
-#define BSG_LAUNCH_MC(KK)                                                                       \
+#define BSG_LAUNCH_MC1(KK, P2)                                                                  \
   {                                                                                             \
     const size_t sm = static_cast<size_t>(kWarpsPerBlock) * (5 * 32 * KK + 32 + S) * 4;         \
     if (sm > 48 * 1024)                                                                         \
-      cudaFuncSetAttribute(dispatch_mc_kernel<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                           static_cast<int>(sm));                                               \
-    dispatch_mc_kernel<KK><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, sm, ctx->stream>>>( \
-        dcf, ctx->ncfg, dp, de, df, dd, ds, di, n_inst, n_requests, dl, n_samples, objective,   \
-        dsc, dse, dres, dcnt, dch);                                                             \
+      cudaFuncSetAttribute(dispatch_mc_kernel<KK, P2>,                                          \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));  \
+    dispatch_mc_kernel<KK, P2><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, sm,       \
+                                 ctx->stream>>>(dcf, ctx->ncfg, dp, de, df, dd, ds, di, n_inst,  \
+                                                n_requests, dl, n_samples, objective, dsc, dse,  \
+                                                dres, dcnt, dch);                                \
+  }
+#define BSG_LAUNCH_MC(KK)             \
+  if (ctx->all_pow2) {                \
+    BSG_LAUNCH_MC1(KK, true)          \
+  } else {                            \
+    BSG_LAUNCH_MC1(KK, false)         \
   }
   switch (k) {
     case 1: BSG_LAUNCH_MC(1); break;
@@ -711,6 +743,7 @@ bsg_status bsg_dispatch_mc(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_e
     default: BSG_LAUNCH_MC(8); break;
   }
 #undef BSG_LAUNCH_MC
+#undef BSG_LAUNCH_MC1
   ctx->launches += 1;
   BSG_CUDA(ctx, cudaGetLastError());
   BSG_CUDA(ctx, cudaMemcpyAsync(chosen, dch, n_requests * 4, cudaMemcpyDeviceToHost, ctx->stream));

@@ -56,6 +56,36 @@ __device__ __forceinline__ int32_t bn(int32_t t, const DevCfg& c) {
   return t <= 0 ? 0 : div_bs(t + c.block_size - 1, c);
 }
 
+// Compile-time specialisation for power-of-two block sizes (the common case):
+// division and modulo become a shift and a mask.
+template <bool POW2>
+__device__ __forceinline__ int32_t divt(int32_t n, const DevCfg& c) {
+  if constexpr (POW2) return n >> c.div_shift;
+  else return div_bs(n, c);
+}
+template <bool POW2>
+__device__ __forceinline__ int32_t modt(int32_t n, const DevCfg& c) {
+  if constexpr (POW2) return n & (c.block_size - 1);
+  else return n - div_bs(n, c) * c.block_size;
+}
+template <bool POW2>
+__device__ __forceinline__ int32_t bnt(int32_t t, const DevCfg& c) {
+  return t <= 0 ? 0 : divt<POW2>(t + c.block_size - 1, c);
+}
+
+// Sum of a per-lane non-negative int64 over the warp: two 32-bit redux.sync
+// on 16-bit-split halves when every value is < 2^42, shuffles otherwise.
+__device__ __forceinline__ int64_t warp_sum_i64(int64_t d) {
+  if (!__any_sync(kFull, d >= (int64_t{1} << 42))) {
+    const uint32_t lo = __reduce_add_sync(kFull, static_cast<uint32_t>(d & 0xffff));
+    const uint32_t hi = __reduce_add_sync(kFull, static_cast<uint32_t>(d >> 16));
+    return (static_cast<int64_t>(hi) << 16) + lo;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(kFull, d, o);
+  return d;
+}
+
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 __device__ __forceinline__ int32_t warp_incl_scan(int32_t x) {
@@ -167,7 +197,7 @@ struct McArgs {
 
 // Simulates one scenario with the calling warp. All lanes return the same
 // result; lane 0 writes it.
-template <int K, bool TRACE, bool MC = false>
+template <int K, bool TRACE, bool MC = false, bool POW2 = false>
 __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__ g_prompt,
                                   const int32_t* __restrict__ g_est,
                                   const int32_t* __restrict__ g_prefill,
@@ -209,7 +239,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
       org[k] = (p + 1) | kEverBit;
       bad |= prompt[k] < 1 || prompt[k] > (1 << 22) || prefill[k] < 0 || prefill[k] > prompt[k] ||
              decoded[k] < 0 || decoded[k] > (1 << 22) || est > (1 << 24);
-      held[k] = bn(prefill[k] + decoded[k], cfg);
+      held[k] = bnt<POW2>(prefill[k] + decoded[k], cfg);
     }
   }
   if (__any_sync(kFull, bad) || run_n > CAP) {
@@ -318,7 +348,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
         const int32_t np = prefill[k] + chunk[k];
         ns = np + decoded[k] + (np == prompt[k] ? 1 : 0);
       }
-      delta[k] = (decode_item[k] || chunk[k] > 0) ? bn(ns, cfg) - bn(stored[k], cfg) : 0;
+      delta[k] = (decode_item[k] || chunk[k] > 0) ? bnt<POW2>(ns, cfg) - bnt<POW2>(stored[k], cfg) : 0;
     }
     const int32_t run_delta = warp_sum<K>(delta);
 
@@ -355,7 +385,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
           decoded[k] = 0;
         }
         wprompt[k] = valid[k] ? prompt[k] : 0;
-        fdelta[k] = valid[k] ? bn(prompt[k] + 1, cfg) : 0;
+        fdelta[k] = valid[k] ? bnt<POW2>(prompt[k] + 1, cfg) : 0;
       }
       int32_t P[K], DX[K];
       excl_scan<K>(wprompt, P);
@@ -372,7 +402,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
           ok = ok && bj > 0;
           c = prompt[k] < bj ? prompt[k] : bj;
         }
-        const int32_t dj = bn(c + (c == prompt[k] ? 1 : 0), cfg);
+        const int32_t dj = bnt<POW2>(c + (c == prompt[k] ? 1 : 0), cfg);
         ok = ok && dj <= pf - DX[k];
         if (ok) chunk[k] = c;
         if (p >= L && valid[k])
@@ -403,7 +433,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
       for (int k = 0; k < K; ++k) {
         decode_item[k] = ready[k];
         const int32_t ns = stored[k] + 1;
-        delta[k] = ready[k] ? bn(ns, cfg) - bn(stored[k], cfg) : 0;
+        delta[k] = ready[k] ? bnt<POW2>(ns, cfg) - bnt<POW2>(stored[k], cfg) : 0;
       }
     }
     if (n == 0 && a == 0) {  // backend.cpp:245
@@ -439,13 +469,13 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
       for (int k = 0; k < K; ++k) {
         const int32_t p = lane * K + k;
         if (p < n) {
-          const int32_t m = stored[k] - div_bs(stored[k], cfg) * bs;
+          const int32_t m = modt<POW2>(stored[k], cfg);
           const int32_t r = m == 0 ? 0 : bs - m;
           if (r < 32) atomicAdd(&hist[r], 1);
         }
       }
       __syncwarp();
-      const int32_t dem = hist[bs <= 32 ? lane - div_bs(lane, cfg) * bs : lane];
+      const int32_t dem = hist[bs <= 32 ? modt<POW2>(lane, cfg) : lane];
       __syncwarp();
       const int32_t cum = warp_incl_scan(dem);
       const unsigned over = __ballot_sync(kFull, cum > free_blocks);
@@ -460,9 +490,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
         for (int k = 0; k < K; ++k) st_run[k] = (lane * K + k) < n ? stored[k] : 0;
         const int32_t c0 = warp_sum<K>(st_run);
         const int64_t d = lane < T ? step_ticks(cfg, 0, D, c0 + lane * D) : 0;
-        int64_t sum = d;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
+        const int64_t sum = warp_sum_i64(d);
         if constexpr (MC) {
           // inclusive prefix of step durations: elapsed at the end of window step `lane`
           int64_t pre = d;
@@ -518,7 +546,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
           first_tok[k] = false;  // only possible at window step 0; never the candidate
           if (p < n) decoded[k] += T;
           done[k] = p < n && decoded[k] >= target[k];
-          freed[k] = done[k] ? bn(prefill[k] + decoded[k], cfg) : 0;
+          freed[k] = done[k] ? bnt<POW2>(prefill[k] + decoded[k], cfg) : 0;
           if (org[k] == (kCandOrg | kEverBit)) cand_done |= done[k];
         }
       }
@@ -575,7 +603,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int32_t p = lane * K + k;
-        ho[k] = p < n ? bn(stored[k], cfg) : 0;
+        ho[k] = p < n ? bnt<POW2>(stored[k], cfg) : 0;
       }
       const int32_t htot = excl_scan<K>(ho, hinc);
       excl_scan<K>(delta, dinc);
@@ -693,7 +721,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
       const bool item = dec_s[k] || pre_s[k];
       first_tok[k] = item && prev == 0 && decoded[k] >= 1;
       done[k] = item && decoded[k] >= target[k];
-      freed[k] = done[k] ? bn(prefill[k] + decoded[k], cfg) : 0;
+      freed[k] = done[k] ? bnt<POW2>(prefill[k] + decoded[k], cfg) : 0;
       if (org[k] == (kCandOrg | kEverBit)) {
         cand_first |= first_tok[k];
         cand_done |= done[k];
