@@ -360,6 +360,31 @@ bsg_status bsg_capacity_search(bsg_ctx* ctx, const bsg_workload* base, const bsg
                                int32_t qps_max, double slo_p99_ttft_s, bsg_capacity_result* out,
                                double* tested_qps, int32_t* tested_pass, int32_t tested_cap);
 
+/* One capacity-sweep cell (BASELINE cfg5): a capacity_search over a closed
+ * loop with `spec.n_instances` instances of profile `cfg`. */
+typedef struct bsg_sweep_cell {
+  bsg_workload workload;     /* base workload (request_cap bounds each run) */
+  bsg_instance_cfg cfg;      /* latency profile + memory limits */
+  bsg_replay_spec spec;      /* instances, policy, provisioning */
+  uint64_t seed;             /* spec_for_cell seed */
+  int32_t qps_min, qps_max;
+  double slo_p99_ttft_s;
+} bsg_sweep_cell;
+typedef struct bsg_sweep_out {
+  int32_t status;                /* BSG_OK or BSG_NO_CAPACITY or an error */
+  int32_t reserved;
+  bsg_capacity_result result;
+  int64_t whatif_scenarios;      /* predict() scenarios simulated on the GPU for this cell */
+  int64_t kernel_launches;
+  double wall_s;
+} bsg_sweep_out;
+/* Runs cells (in the given order) on `threads` host threads, each with its own
+ * context on `device`, so independent closed loops overlap on the GPU. */
+bsg_status bsg_sweep_run(int device, const bsg_sweep_cell* cells, int32_t n_cells,
+                         int32_t threads, bsg_sweep_out* out);
+/* Scenarios simulated by this context so far (all entry points). */
+int64_t bsg_scenario_count(const bsg_ctx* ctx);
+
 /* Synthetic trace + estimates + Poisson arrival ticks (no GPU needed). */
 bsg_status bsg_make_workload(const bsg_workload* w, int32_t* prompt, int32_t* output,
                              int32_t* est, int64_t* arrival_ticks);

@@ -87,6 +87,14 @@ capacity_dtype = np.dtype([
     ("capacity_qps", "<f8"), ("bracket_pass", "<i4"), ("bracket_fail", "<i4"),
     ("monotone", "<i4"), ("n_tested", "<i4"),
 ])
+sweep_cell_dtype = np.dtype([
+    ("workload", workload_dtype), ("cfg", cfg_dtype), ("spec", replay_spec_dtype),
+    ("seed", "<u8"), ("qps_min", "<i4"), ("qps_max", "<i4"), ("slo_p99_ttft_s", "<f8"),
+])
+sweep_out_dtype = np.dtype([
+    ("status", "<i4"), ("reserved", "<i4"), ("result", capacity_dtype),
+    ("whatif_scenarios", "<i8"), ("kernel_launches", "<i8"), ("wall_s", "<f8"),
+])
 NO_CAPACITY = 12
 STATUS_NAMES[12] = "NO_CAPACITY"
 PROVISION_STATIC, PROVISION_PREEMPT, PROVISION_RELIEF = 0, 1, 2

@@ -229,6 +229,7 @@ struct bsg_ctx {
   cudaEvent_t pipe_done[3] = {nullptr, nullptr, nullptr};
   std::string last_error;
   int64_t launches = 0;
+  int64_t scenarios = 0;  // predict() scenarios simulated (MC: request x instance x sample)
   std::vector<bsg_instance_cfg> host_cfgs;
   std::vector<DevCfg> dev_cfgs_host;
   DevBuf cfgs, prompt, est, prefill, decoded, scen, res, rec, ids, chosen, order;
@@ -309,6 +310,7 @@ bsg_status launch_predict_k(bsg_ctx* ctx, int k, int64_t n, const bsg_entries& e
                             const bsg_scenario* sc, const int32_t* order, bsg_result* out,
                             cudaStream_t s) {
   if (n == 0) return BSG_OK;
+  ctx->scenarios += n;
   switch (k) {
     case 1: launch_predict<1>(ctx, n, e, sc, order, out, s); break;
     case 2: launch_predict<2>(ctx, n, e, sc, order, out, s); break;
@@ -410,6 +412,8 @@ void bsg_ctx_destroy(bsg_ctx* ctx) {
 const char* bsg_last_error(const bsg_ctx* ctx) { return ctx ? ctx->last_error.c_str() : ""; }
 
 int64_t bsg_launch_count(const bsg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int64_t bsg_scenario_count(const bsg_ctx* ctx) { return ctx ? ctx->scenarios : 0; }
 
 bsg_status bsg_set_configs(bsg_ctx* ctx, const bsg_instance_cfg* cfgs, int32_t n,
                            int32_t* bad_index, int32_t* field_code) {
@@ -745,6 +749,7 @@ bsg_status bsg_dispatch_mc(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_e
 #undef BSG_LAUNCH_MC
 #undef BSG_LAUNCH_MC1
   ctx->launches += 1;
+  ctx->scenarios += n * S;
   BSG_CUDA(ctx, cudaGetLastError());
   BSG_CUDA(ctx, cudaMemcpyAsync(chosen, dch, n_requests * 4, cudaMemcpyDeviceToHost, ctx->stream));
   if (scores)

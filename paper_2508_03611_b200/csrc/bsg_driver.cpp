@@ -14,7 +14,10 @@
 // members [0,n) in admission order, preemption victims [n,L) = the waiting
 // front, then never-scheduled arrivals in FIFO order.
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cmath>
+#include <thread>
 #include <cstring>
 #include <deque>
 #include <limits>
@@ -837,4 +840,39 @@ extern "C" bsg_status bsg_capacity_search(bsg_ctx* ctx, const bsg_workload* base
   }
   out->capacity_qps = best;
   return BSG_OK;
+}
+
+extern "C" bsg_status bsg_sweep_run(int device, const bsg_sweep_cell* cells, int32_t n_cells,
+                                    int32_t threads, bsg_sweep_out* out) {
+  if (!cells || !out || n_cells < 0) return BSG_INVALID_ARGUMENT;
+  const int nt = std::max(1, std::min<int32_t>(threads, std::max(n_cells, 1)));
+  std::atomic<int32_t> next{0};
+  std::atomic<int> failed{BSG_OK};
+  auto worker = [&]() {
+    bsg_ctx* ctx = nullptr;
+    const bsg_status cs = bsg_ctx_create(device, &ctx);
+    if (cs != BSG_OK) {
+      failed = cs;
+      return;
+    }
+    for (;;) {
+      const int32_t i = next.fetch_add(1);
+      if (i >= n_cells) break;
+      const bsg_sweep_cell& c = cells[i];
+      bsg_sweep_out& o = out[i];
+      std::memset(&o, 0, sizeof(o));
+      const int64_t s0 = bsg_scenario_count(ctx), l0 = bsg_launch_count(ctx);
+      const auto t0 = std::chrono::steady_clock::now();
+      o.status = bsg_capacity_search(ctx, &c.workload, &c.cfg, &c.spec, c.seed, c.qps_min, c.qps_max,
+                                     c.slo_p99_ttft_s, &o.result, nullptr, nullptr, 0);
+      o.wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      o.whatif_scenarios = bsg_scenario_count(ctx) - s0;
+      o.kernel_launches = bsg_launch_count(ctx) - l0;
+    }
+    bsg_ctx_destroy(ctx);
+  };
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nt; ++t) pool.emplace_back(worker);
+  for (auto& th : pool) th.join();
+  return static_cast<bsg_status>(failed.load());
 }

@@ -59,6 +59,8 @@ def load() -> C.CDLL:
         "bsg_aggregate": (C.c_int, [V, C.c_int64, V, V]),
         "bsg_capacity_search": (C.c_int, [V, V, V, V, C.c_uint64, C.c_int32, C.c_int32, C.c_double,
                                           V, V, V, C.c_int32]),
+        "bsg_sweep_run": (C.c_int, [C.c_int, V, C.c_int32, C.c_int32, V]),
+        "bsg_scenario_count": (C.c_int64, [V]),
         "bsg_mc_lengths": (C.c_int, [C.c_int32, C.c_uint64, C.c_int32, C.c_uint64, C.c_double, V]),
     }
     for name, (res, args) in sigs.items():
@@ -93,6 +95,16 @@ def aggregate(outcomes: np.ndarray, summary=None) -> np.void:
     if st != abi.OK:
         raise BsgError(st, "bsg_aggregate")
     return out[0]
+
+
+def sweep_run(device: int, cells: np.ndarray, threads: int = 8) -> np.ndarray:
+    """bsg_sweep_run: capacity searches for many cells, concurrent on one GPU."""
+    cells = np.ascontiguousarray(cells, abi.sweep_cell_dtype)
+    out = np.zeros(len(cells), abi.sweep_out_dtype)
+    st = load().bsg_sweep_run(device, _p(cells), len(cells), threads, _p(out))
+    if st != abi.OK:
+        raise BsgError(st, "bsg_sweep_run")
+    return out
 
 
 def mc_lengths(est: int, request_id: int, n_samples: int = 256, seed: int = 1,

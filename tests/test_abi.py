@@ -106,3 +106,32 @@ def test_aggregate_matches_reference(lib, ref, kw, n_inst):
     got = native.aggregate(out, summ)
     exp = ref.run_report(w, cfg, spec)
     assert got.tolist() == exp.tolist()
+
+
+def test_c_struct_layouts_match_numpy(tmp_path):
+    """Every struct crossing the C-ABI has the same size and field offsets in
+    C (gcc on include/blocksim_b200.h) and in paper_2508_03611_b200/abi.py."""
+    pairs = [("bsg_instance_cfg", abi.cfg_dtype), ("bsg_scenario", abi.scenario_dtype),
+             ("bsg_result", abi.result_dtype), ("bsg_step_record", abi.step_dtype),
+             ("bsg_workload", abi.workload_dtype), ("bsg_replay_spec", abi.replay_spec_dtype),
+             ("bsg_replay_summary", abi.summary_dtype), ("bsg_request_outcome", abi.outcome_dtype),
+             ("bsg_run_report", abi.report_dtype), ("bsg_capacity_result", abi.capacity_dtype),
+             ("bsg_sweep_cell", abi.sweep_cell_dtype), ("bsg_sweep_out", abi.sweep_out_dtype)]
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "blocksim_b200.h"',
+             'int main(void) {']
+    for cname, dt in pairs:
+        lines.append(f'  printf("%zu\\n", sizeof({cname}));')
+        for f in dt.names:
+            lines.append(f'  printf("%zu\\n", offsetof({cname}, {f}));')
+    lines.append("  return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    inc = os.path.join(os.path.dirname(native.HEADER))
+    subprocess.run(["gcc", "-I", inc, str(src), "-o", str(tmp_path / "layout")], check=True)
+    got = [int(x) for x in subprocess.run([str(tmp_path / "layout")], capture_output=True,
+                                          text=True, check=True).stdout.split()]
+    exp = []
+    for _, dt in pairs:
+        exp.append(dt.itemsize)
+        exp.extend(dt.fields[f][1] for f in dt.names)
+    assert got == exp

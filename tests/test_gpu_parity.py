@@ -169,3 +169,22 @@ def test_capacity_search_matches_reference(ctx, ref):
     assert tested == etested
     assert got.tolist() == exp.tolist()
     assert 1 < got["capacity_qps"] < 16  # a real bracket, with tenths tested
+
+
+def test_sweep_cells_match_reference_capacity_search(ref):
+    """bsg_sweep_run (concurrent capacity searches, one context per host
+    thread) gives, per cell, exactly the reference's capacity_search result
+    for that cell's profile and instance count."""
+    from paper_2508_03611_b200 import native, sweep
+    profiles = sweep.load_profiles()
+    cells, keys = sweep.make_cells([1, 2], profiles, request_cap=150, qps_max=12, slo=1.0)
+    out = native.sweep_run(0, cells, threads=4)
+    for c, o in zip(cells, out):
+        w = np.array([c["workload"]], abi.workload_dtype)
+        cfg = np.array([c["cfg"]], abi.cfg_dtype)
+        spec = np.array([c["spec"]], abi.replay_spec_dtype)
+        st, exp, _ = ref.capacity_search(w, cfg, spec, int(c["seed"]), int(c["qps_min"]),
+                                         int(c["qps_max"]), float(c["slo_p99_ttft_s"]))
+        assert int(o["status"]) == st
+        assert o["result"].tolist() == exp.tolist()
+        assert o["whatif_scenarios"] > 0
