@@ -781,6 +781,53 @@ extern "C" bsg_status bsg_aggregate(const bsg_request_outcome* o, int64_t n,
   return BSG_OK;
 }
 
+namespace {
+
+// One capacity-search point: run_experiment(spec_for_cell(base, policy, qps,
+// seed)) (driver.cpp:321-331, 409-414) + aggregate; pass iff p99 TTFT < slo
+// (metrics.cpp:145-150).
+bsg_status run_point(bsg_ctx* ctx, const bsg_workload* base, const bsg_instance_cfg* cfg,
+                     const bsg_replay_spec* spec, uint64_t seed, double qps, double slo,
+                     bool* passed) {
+  bsg_workload w = *base;
+  w.qps = qps;
+  w.arrival_seed = seed;
+  w.estimator_seed = seed;
+  bsg_replay_spec sp = *spec;
+  sp.policy_seed = seed;
+  sp.capture = 0;
+  const int32_t n = (w.request_cap >= 0 && w.request_cap < w.count) ? w.request_cap : w.count;
+  std::vector<bsg_request_outcome> o(static_cast<size_t>(n));
+  bsg_replay_summary summ{};
+  const bsg_status st = bsg_replay(ctx, &w, cfg, &sp, o.data(), &summ, nullptr);
+  if (st != BSG_OK) return st;
+  bsg_run_report rep{};
+  bsg_aggregate(o.data(), n, &summ, &rep);
+  *passed = rep.p99_ttft_s < slo;
+  return BSG_OK;
+}
+
+// capacity_search's decision logic (metrics.cpp:151-177) given the integer
+// results; returns the tenths to test (empty when bracket_pass == qps_max).
+std::vector<double> capacity_bracket(const std::vector<bool>& integer_pass, int32_t qps_min,
+                                     int32_t qps_max, bsg_capacity_result* out) {
+  int last = 0;
+  while (last + 1 < static_cast<int>(integer_pass.size()) && integer_pass[last + 1]) ++last;
+  out->monotone = 1;
+  for (int i = last + 1; i < static_cast<int>(integer_pass.size()); ++i)
+    if (integer_pass[i]) out->monotone = 0;
+  out->bracket_pass = qps_min + last;
+  out->bracket_fail = out->bracket_pass + 1;
+  out->capacity_qps = static_cast<double>(out->bracket_pass);
+  std::vector<double> tenths;
+  if (out->bracket_pass < qps_max)
+    for (int tenth = 1; tenth <= 9; ++tenth)
+      tenths.push_back(static_cast<double>(out->bracket_pass * 10 + tenth) / 10.0);
+  return tenths;
+}
+
+}  // namespace
+
 extern "C" bsg_status bsg_capacity_search(bsg_ctx* ctx, const bsg_workload* base,
                                           const bsg_instance_cfg* cfg, const bsg_replay_spec* spec,
                                           uint64_t seed, int32_t qps_min, int32_t qps_max,
@@ -790,89 +837,133 @@ extern "C" bsg_status bsg_capacity_search(bsg_ctx* ctx, const bsg_workload* base
   if (!ctx || !base || !cfg || !spec || !out) return BSG_INVALID_ARGUMENT;
   if (qps_min > qps_max) return BSG_BAD_CONFIG;  // metrics.cpp:141
   std::memset(out, 0, sizeof(*out));
-  bsg_status err = BSG_OK;
-  auto passes = [&](double qps) -> bool {
-    bsg_workload w = *base;  // spec_for_cell (driver.cpp:321-331)
-    w.qps = qps;
-    w.arrival_seed = seed;
-    w.estimator_seed = seed;
-    bsg_replay_spec sp = *spec;
-    sp.policy_seed = seed;
-    sp.capture = 0;
-    const int32_t n = (w.request_cap >= 0 && w.request_cap < w.count) ? w.request_cap : w.count;
-    std::vector<bsg_request_outcome> o(static_cast<size_t>(n));
-    bsg_replay_summary summ{};
-    const bsg_status st = bsg_replay(ctx, &w, cfg, &sp, o.data(), &summ, nullptr);
-    if (st != BSG_OK) {
-      err = st;
-      return false;
-    }
-    bsg_run_report rep{};
-    bsg_aggregate(o.data(), n, &summ, &rep);
-    const bool ok = rep.p99_ttft_s < slo_p99_ttft_s;
+  auto record = [&](double qps, bool ok) {
     if (out->n_tested < tested_cap) {
       if (tested_qps) tested_qps[out->n_tested] = qps;
       if (tested_pass) tested_pass[out->n_tested] = ok ? 1 : 0;
     }
     ++out->n_tested;
-    return ok;
   };
   std::vector<bool> integer_pass;
   for (int32_t q = qps_min; q <= qps_max; ++q) {
-    integer_pass.push_back(passes(static_cast<double>(q)));
-    if (err != BSG_OK) return err;
+    bool ok = false;
+    const bsg_status st = run_point(ctx, base, cfg, spec, seed, q, slo_p99_ttft_s, &ok);
+    if (st != BSG_OK) return st;
+    record(q, ok);
+    integer_pass.push_back(ok);
   }
-  if (!integer_pass.front()) return BSG_NO_CAPACITY;
-  int last = 0;
-  while (last + 1 < static_cast<int>(integer_pass.size()) && integer_pass[last + 1]) ++last;
-  out->monotone = 1;
-  for (int i = last + 1; i < static_cast<int>(integer_pass.size()); ++i)
-    if (integer_pass[i]) out->monotone = 0;
-  out->bracket_pass = qps_min + last;
-  out->bracket_fail = out->bracket_pass + 1;
-  double best = static_cast<double>(out->bracket_pass);
-  if (out->bracket_pass < qps_max) {
-    for (int tenth = 1; tenth <= 9; ++tenth) {
-      const double qps = static_cast<double>(out->bracket_pass * 10 + tenth) / 10.0;
-      if (passes(qps)) best = std::max(best, qps);
-      if (err != BSG_OK) return err;
-    }
+  if (!integer_pass.front()) return BSG_NO_CAPACITY;  // metrics.cpp:153-155
+  const std::vector<double> tenths = capacity_bracket(integer_pass, qps_min, qps_max, out);
+  for (double qps : tenths) {
+    bool ok = false;
+    const bsg_status st = run_point(ctx, base, cfg, spec, seed, qps, slo_p99_ttft_s, &ok);
+    if (st != BSG_OK) return st;
+    record(qps, ok);
+    if (ok) out->capacity_qps = std::max(out->capacity_qps, qps);
   }
-  out->capacity_qps = best;
   return BSG_OK;
 }
 
 extern "C" bsg_status bsg_sweep_run(int device, const bsg_sweep_cell* cells, int32_t n_cells,
                                     int32_t threads, bsg_sweep_out* out) {
   if (!cells || !out || n_cells < 0) return BSG_INVALID_ARGUMENT;
-  const int nt = std::max(1, std::min<int32_t>(threads, std::max(n_cells, 1)));
-  std::atomic<int32_t> next{0};
-  std::atomic<int> failed{BSG_OK};
-  auto worker = [&]() {
-    bsg_ctx* ctx = nullptr;
-    const bsg_status cs = bsg_ctx_create(device, &ctx);
-    if (cs != BSG_OK) {
-      failed = cs;
-      return;
-    }
-    for (;;) {
-      const int32_t i = next.fetch_add(1);
-      if (i >= n_cells) break;
-      const bsg_sweep_cell& c = cells[i];
-      bsg_sweep_out& o = out[i];
-      std::memset(&o, 0, sizeof(o));
-      const int64_t s0 = bsg_scenario_count(ctx), l0 = bsg_launch_count(ctx);
-      const auto t0 = std::chrono::steady_clock::now();
-      o.status = bsg_capacity_search(ctx, &c.workload, &c.cfg, &c.spec, c.seed, c.qps_min, c.qps_max,
-                                     c.slo_p99_ttft_s, &o.result, nullptr, nullptr, 0);
-      o.wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-      o.whatif_scenarios = bsg_scenario_count(ctx) - s0;
-      o.kernel_launches = bsg_launch_count(ctx) - l0;
-    }
-    bsg_ctx_destroy(ctx);
+  // Every closed loop of every cell is independent, so schedule at (cell, qps)
+  // granularity: phase 1 runs all integer points, phase 2 the tenths of each
+  // cell's bracket. The per-cell result is then assembled exactly as
+  // capacity_search would report it (same tested order and decisions).
+  struct Task {
+    int32_t cell;
+    double qps;
+    int32_t slot;  // index into the cell's result vector
   };
-  std::vector<std::thread> pool;
-  for (int t = 0; t < nt; ++t) pool.emplace_back(worker);
-  for (auto& th : pool) th.join();
-  return static_cast<bsg_status>(failed.load());
+  std::vector<std::vector<int8_t>> ipass(n_cells), tpass(n_cells);
+  std::vector<std::vector<double>> tenths(n_cells);
+  std::vector<std::atomic<int64_t>> scen(n_cells), launches(n_cells);
+  std::vector<std::atomic<int64_t>> nanos(n_cells);
+  std::vector<int> err(n_cells, BSG_OK);
+  for (int32_t c = 0; c < n_cells; ++c) {
+    std::memset(&out[c], 0, sizeof(out[c]));
+    if (cells[c].qps_min > cells[c].qps_max) err[c] = BSG_BAD_CONFIG;
+    ipass[c].assign(std::max(0, cells[c].qps_max - cells[c].qps_min + 1), -1);
+    scen[c] = 0;
+    launches[c] = 0;
+    nanos[c] = 0;
+  }
+  std::atomic<int> fatal{BSG_OK};
+  auto run_tasks = [&](std::vector<Task>& tasks, bool tenth_phase) {
+    // longest first: more instances and higher qps mean longer closed loops
+    std::stable_sort(tasks.begin(), tasks.end(), [&](const Task& a, const Task& b) {
+      const double ca = cells[a.cell].spec.n_instances * a.qps;
+      const double cb = cells[b.cell].spec.n_instances * b.qps;
+      return ca > cb;
+    });
+    std::atomic<size_t> next{0};
+    const int nt = std::max(1, std::min<int>(threads, static_cast<int>(tasks.size())));
+    auto worker = [&]() {
+      bsg_ctx* ctx = nullptr;
+      const bsg_status cs = bsg_ctx_create(device, &ctx);
+      if (cs != BSG_OK) {
+        fatal = cs;
+        return;
+      }
+      for (;;) {
+        const size_t i = next.fetch_add(1);
+        if (i >= tasks.size()) break;
+        const Task& t = tasks[i];
+        const bsg_sweep_cell& c = cells[t.cell];
+        const int64_t s0 = bsg_scenario_count(ctx), l0 = bsg_launch_count(ctx);
+        const auto t0 = std::chrono::steady_clock::now();
+        bool ok = false;
+        const bsg_status st =
+            run_point(ctx, &c.workload, &c.cfg, &c.spec, c.seed, t.qps, c.slo_p99_ttft_s, &ok);
+        nanos[t.cell] += std::chrono::duration_cast<std::chrono::nanoseconds>(
+                             std::chrono::steady_clock::now() - t0).count();
+        scen[t.cell] += bsg_scenario_count(ctx) - s0;
+        launches[t.cell] += bsg_launch_count(ctx) - l0;
+        if (st != BSG_OK) {
+          err[t.cell] = st;
+          continue;
+        }
+        (tenth_phase ? tpass : ipass)[t.cell][t.slot] = ok ? 1 : 0;
+      }
+      bsg_ctx_destroy(ctx);
+    };
+    std::vector<std::thread> pool;
+    for (int k = 0; k < nt; ++k) pool.emplace_back(worker);
+    for (auto& th : pool) th.join();
+  };
+  std::vector<Task> tasks;
+  for (int32_t c = 0; c < n_cells; ++c)
+    if (err[c] == BSG_OK)
+      for (int32_t q = cells[c].qps_min; q <= cells[c].qps_max; ++q)
+        tasks.push_back(Task{c, static_cast<double>(q), q - cells[c].qps_min});
+  run_tasks(tasks, false);
+  if (fatal != BSG_OK) return static_cast<bsg_status>(fatal.load());
+  tasks.clear();
+  for (int32_t c = 0; c < n_cells; ++c) {
+    if (err[c] != BSG_OK) continue;
+    std::vector<bool> ip(ipass[c].begin(), ipass[c].end());
+    if (!ip.front()) {
+      err[c] = BSG_NO_CAPACITY;
+      continue;
+    }
+    tenths[c] = capacity_bracket(ip, cells[c].qps_min, cells[c].qps_max, &out[c].result);
+    tpass[c].assign(tenths[c].size(), -1);
+    for (size_t j = 0; j < tenths[c].size(); ++j)
+      tasks.push_back(Task{c, tenths[c][j], static_cast<int32_t>(j)});
+  }
+  run_tasks(tasks, true);
+  if (fatal != BSG_OK) return static_cast<bsg_status>(fatal.load());
+  for (int32_t c = 0; c < n_cells; ++c) {
+    bsg_sweep_out& o = out[c];
+    o.whatif_scenarios = scen[c];
+    o.kernel_launches = launches[c];
+    o.wall_s = static_cast<double>(nanos[c]) * 1e-9;  // summed closed-loop time
+    o.result.n_tested = static_cast<int32_t>(ipass[c].size() + tpass[c].size());
+    o.status = err[c];
+    if (err[c] != BSG_OK) continue;
+    for (size_t j = 0; j < tenths[c].size(); ++j)
+      if (tpass[c][j] == 1) o.result.capacity_qps = std::max(o.result.capacity_qps, tenths[c][j]);
+  }
+  return BSG_OK;
 }
