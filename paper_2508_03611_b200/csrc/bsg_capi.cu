@@ -363,6 +363,14 @@ bsg_status upload(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries,
 
 }  // namespace
 
+namespace {
+bsg_status dispatch_fused(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries,
+                          const bsg_scenario* scenarios, const int32_t* instance_ids,
+                          int32_t n_inst, int32_t n_requests, const int32_t* lengths,
+                          int32_t n_samples, int32_t objective, int32_t* chosen, int64_t* scores,
+                          int64_t* sample_e2e, bsg_result* per_instance);
+}  // namespace
+
 extern "C" {
 
 int bsg_abi_version(void) { return BSG_ABI_VERSION; }
@@ -610,7 +618,23 @@ bsg_status bsg_dispatch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entr
   if (!ctx || !entries || !scenarios || !instance_ids || !chosen) return BSG_INVALID_ARGUMENT;
   if (n_inst <= 0) return BSG_NO_INSTANCES;  // scheduler.cpp:116
   if (n_requests <= 0) return BSG_OK;
+  if (ctx->ncfg == 0) return BSG_INVALID_ARGUMENT;
   std::lock_guard<std::mutex> lock(ctx->mu);
+  // A real fan-out evaluates ONE candidate on every instance: then the fused
+  // single-copy path applies (the candidate's estimate is its one "sample").
+  bool uniform = true;
+  std::vector<int32_t> est(static_cast<size_t>(n_requests));
+  for (int32_t r = 0; r < n_requests && uniform; ++r) {
+    const bsg_scenario& a = scenarios[static_cast<int64_t>(r) * n_inst];
+    est[r] = a.cand_est;
+    for (int32_t i = 1; i < n_inst; ++i) {
+      const bsg_scenario& b = scenarios[static_cast<int64_t>(r) * n_inst + i];
+      if (b.cand_est != a.cand_est || b.cand_prompt != a.cand_prompt) uniform = false;
+    }
+  }
+  if (uniform)
+    return dispatch_fused(ctx, entries, n_entries, scenarios, instance_ids, n_inst, n_requests,
+                          est.data(), 1, objective, chosen, nullptr, nullptr, per_instance);
   cudaSetDevice(ctx->device);
   const int64_t n = static_cast<int64_t>(n_inst) * n_requests;
   bsg_entries dev{};
@@ -641,18 +665,18 @@ bsg_status bsg_dispatch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entr
   return BSG_OK;
 }
 
-bsg_status bsg_dispatch_mc(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries,
-                           const bsg_scenario* scenarios, const int32_t* instance_ids,
-                           int32_t n_inst, int32_t n_requests, const int32_t* lengths,
-                           int32_t n_samples, int32_t objective, int32_t* chosen,
-                           int64_t* scores, int64_t* sample_e2e, bsg_result* per_instance) {
-  if (!ctx || !entries || !scenarios || !instance_ids || !lengths || !chosen)
-    return BSG_INVALID_ARGUMENT;
-  if (n_inst <= 0) return BSG_NO_INSTANCES;
-  if (n_samples < 1 || n_samples > 1024) return BSG_INVALID_ARGUMENT;
-  if (n_requests <= 0) return BSG_OK;
-  if (ctx->ncfg == 0) return BSG_INVALID_ARGUMENT;
-  std::lock_guard<std::mutex> lock(ctx->mu);
+}  // extern "C"
+
+namespace {
+
+// Fused what-if fan-out + argmin with one packed host->device copy: the
+// latency path of both bsg_dispatch (one "sample" = the candidate's estimate)
+// and bsg_dispatch_mc. Caller holds ctx->mu.
+bsg_status dispatch_fused(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries,
+                          const bsg_scenario* scenarios, const int32_t* instance_ids,
+                          int32_t n_inst, int32_t n_requests, const int32_t* lengths,
+                          int32_t n_samples, int32_t objective, int32_t* chosen, int64_t* scores,
+                          int64_t* sample_e2e, bsg_result* per_instance) {
   cudaSetDevice(ctx->device);
   const int64_t n = static_cast<int64_t>(n_inst) * n_requests;
   const int64_t S = n_samples;
@@ -770,6 +794,26 @@ bsg_status bsg_dispatch_mc(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_e
     }
   }
   return BSG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+bsg_status bsg_dispatch_mc(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries,
+                           const bsg_scenario* scenarios, const int32_t* instance_ids,
+                           int32_t n_inst, int32_t n_requests, const int32_t* lengths,
+                           int32_t n_samples, int32_t objective, int32_t* chosen,
+                           int64_t* scores, int64_t* sample_e2e, bsg_result* per_instance) {
+  if (!ctx || !entries || !scenarios || !instance_ids || !lengths || !chosen)
+    return BSG_INVALID_ARGUMENT;
+  if (n_inst <= 0) return BSG_NO_INSTANCES;
+  if (n_samples < 1 || n_samples > 1024) return BSG_INVALID_ARGUMENT;
+  if (n_requests <= 0) return BSG_OK;
+  if (ctx->ncfg == 0) return BSG_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  return dispatch_fused(ctx, entries, n_entries, scenarios, instance_ids, n_inst, n_requests,
+                        lengths, n_samples, objective, chosen, scores, sample_e2e, per_instance);
 }
 
 }  // extern "C"

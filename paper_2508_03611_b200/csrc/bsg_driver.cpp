@@ -15,6 +15,8 @@
 // front, then never-scheduled arrivals in FIFO order.
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <thread>
@@ -26,6 +28,8 @@
 #include <stdexcept>
 #include <string>
 #include <vector>
+
+#include <cuda_runtime.h>
 
 #include "bsg_internal.h"
 
@@ -890,6 +894,19 @@ extern "C" bsg_status bsg_sweep_run(int device, const bsg_sweep_cell* cells, int
     nanos[c] = 0;
   }
   std::atomic<int> fatal{BSG_OK};
+  // Closed loops are host-bound between GPU dispatches: oversubscribing the
+  // cores with spin-waiting threads stalls everything, so cap the pool at the
+  // hardware threads and let waiting threads yield (BSG_SCHED overrides).
+  threads = std::min<int32_t>(threads, std::max(1u, std::thread::hardware_concurrency()));
+  {
+    const char* sched = std::getenv("BSG_SCHED");
+    unsigned flags = cudaDeviceScheduleYield;
+    if (sched && std::string(sched) == "spin") flags = cudaDeviceScheduleSpin;
+    if (sched && std::string(sched) == "block") flags = cudaDeviceScheduleBlockingSync;
+    if (sched && std::string(sched) == "auto") flags = cudaDeviceScheduleAuto;
+    cudaSetDevice(device);
+    if (cudaSetDeviceFlags(flags) != cudaSuccess) cudaGetLastError();  // context already active
+  }
   auto run_tasks = [&](std::vector<Task>& tasks, bool tenth_phase) {
     // longest first: more instances and higher qps mean longer closed loops
     std::stable_sort(tasks.begin(), tasks.end(), [&](const Task& a, const Task& b) {
@@ -916,8 +933,13 @@ extern "C" bsg_status bsg_sweep_run(int device, const bsg_sweep_cell* cells, int
         bool ok = false;
         const bsg_status st =
             run_point(ctx, &c.workload, &c.cfg, &c.spec, c.seed, t.qps, c.slo_p99_ttft_s, &ok);
-        nanos[t.cell] += std::chrono::duration_cast<std::chrono::nanoseconds>(
-                             std::chrono::steady_clock::now() - t0).count();
+        const int64_t dt = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                               std::chrono::steady_clock::now() - t0).count();
+        nanos[t.cell] += dt;
+        if (std::getenv("BSG_SWEEP_TRACE"))
+          std::fprintf(stderr, "task cell=%d inst=%d qps=%.1f ms=%.1f scen=%lld\n", t.cell,
+                       c.spec.n_instances, t.qps, dt * 1e-6,
+                       static_cast<long long>(bsg_scenario_count(ctx) - s0));
         scen[t.cell] += bsg_scenario_count(ctx) - s0;
         launches[t.cell] += bsg_launch_count(ctx) - l0;
         if (st != BSG_OK) {
