@@ -246,6 +246,7 @@ namespace {
 
 bsg_status cuda_fail(bsg_ctx* ctx, cudaError_t e, const char* what) {
   if (ctx) ctx->last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  cudaGetLastError();  // a non-sticky error must not poison the context's next call
   return BSG_CUDA_ERROR;
 }
 
@@ -692,7 +693,9 @@ bsg_status dispatch_fused(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_en
   }
   // one packed host->device copy: 4 entry columns | scenarios | ids | sorted lengths
   const size_t ne = static_cast<size_t>(n_entries);
-  const size_t bytes = 4 * ne * 4 + n * sizeof(bsg_scenario) + n * 4 + sorted.size() * 4 + 64;
+  auto r16 = [](size_t b) { return (b + 15) & ~size_t(15); };
+  const size_t bytes = 4 * r16(ne * 4) + r16(n * sizeof(bsg_scenario)) + r16(n * 4) +
+                       r16(sorted.size() * 4);
   if (ctx->pinned_cap < bytes) {
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     ctx->pinned = nullptr;
@@ -715,7 +718,7 @@ bsg_status dispatch_fused(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_en
   auto put = [&](const void* src, size_t b) {
     std::memcpy(h + off, src, b);
     const size_t at = off;
-    off += (b + 15) & ~size_t(15);
+    off += r16(b);
     return at;
   };
   const size_t o_p = put(entries->prompt, ne * 4), o_e = put(entries->est, ne * 4),

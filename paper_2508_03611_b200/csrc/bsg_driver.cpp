@@ -943,6 +943,9 @@ extern "C" bsg_status bsg_sweep_run(int device, const bsg_sweep_cell* cells, int
         scen[t.cell] += bsg_scenario_count(ctx) - s0;
         launches[t.cell] += bsg_launch_count(ctx) - l0;
         if (st != BSG_OK) {
+          if (std::getenv("BSG_SWEEP_TRACE"))
+            std::fprintf(stderr, "task cell=%d qps=%.1f failed: status %d (%s)\n", t.cell, t.qps,
+                         static_cast<int>(st), bsg_last_error(ctx));
           err[t.cell] = st;
           continue;
         }
