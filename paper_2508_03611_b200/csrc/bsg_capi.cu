@@ -21,27 +21,117 @@
 namespace bsg {
 
 constexpr int kWarpsPerBlock = 4;
-// Resident-block target per SM for the 32-member kernels: 8 x 4 warps = 32
-// warps/SM needs <= 64 registers/thread (measured: see profiles/).
-#ifndef BSG_MINB_K1
-#define BSG_MINB_K1 8
+// predict_kernel: warps per block (one scenario per warp). Small blocks let
+// the block scheduler refill a warp slot as soon as its scenario finishes
+// (scenario costs vary ~100x), instead of holding it until the block's
+// slowest warp is done.
+#ifndef BSG_WPB
+#define BSG_WPB 4
 #endif
-constexpr int min_blocks(int k) { return k == 1 ? BSG_MINB_K1 : 1; }
+constexpr int kPredictWarps = BSG_WPB;
+// Resident-warp target per SM for the 32-member kernels: 32 warps/SM needs
+// <= 64 registers/thread (measured: see profiles/).
+#ifndef BSG_K1_WARPS_PER_SM
+#define BSG_K1_WARPS_PER_SM 32
+#endif
+constexpr int min_blocks(int k) { return k == 1 ? BSG_K1_WARPS_PER_SM / kPredictWarps : 1; }
+
+// ---- cost-aware launch order ----------------------------------------------------
+// Scenario costs vary ~100x (a scenario runs until its candidate completes, so
+// its step count is ~ the candidate's estimate plus its queueing): one long
+// scenario that starts late is the kernel's tail. Blocks are dispatched in
+// index order, so predict_kernel's first warps run the HEAVY scenarios (cost
+// bucket >= a threshold picked by heavy_threshold_kernel: at most the top 1/16
+// by quarter-octave of cand_est, listed by heavy_list_kernel); the following
+// warps run the rest in the caller's order (which keeps memory locality),
+// skipping the heavy ones. No sort, no atomics on the simulation path.
+constexpr int kCostBuckets = 128;
+
+__device__ __forceinline__ int cost_bucket(int32_t cand_est) {
+  const uint32_t x = static_cast<uint32_t>(max(cand_est, 0)) + 1u;
+  const int l = 31 - __clz(x);
+  const int f = l >= 2 ? static_cast<int>((x >> (l - 2)) & 3u) : static_cast<int>((x << (2 - l)) & 3u);
+  return min(4 * l + f, kCostBuckets - 1);
+}
+
+// Work-queue state of one launch (zeroed before it): 2 tickets, the heavy
+// bucket threshold, a block-completion count, then the bucket histogram.
+struct WorkQueue {
+  int32_t threshold, blocks_done;
+  int32_t heavy_count, pad;
+  int32_t hist[kCostBuckets];
+  // followed by the heavy list: int32_t heavy[n / 16 + 32]
+};
+__device__ __forceinline__ int32_t* heavy_list(WorkQueue* q) { return reinterpret_cast<int32_t*>(q + 1); }
+
+// Lists the heavy scenarios (order inside the list is arbitrary).
+__global__ void __launch_bounds__(256) heavy_list_kernel(const bsg_scenario* __restrict__ sc, int64_t n,
+                                                         WorkQueue* q) {
+  const int32_t thr = __ldcg(&q->threshold);
+  if (thr >= kCostBuckets) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += stride) {
+    const int64_t i = i0 + lane;
+    const bool heavy = i < n && cost_bucket(__ldg(&sc[i].cand_est)) >= thr;
+    const unsigned m = __ballot_sync(kFull, heavy);
+    if (!m) continue;
+    int32_t base = 0;
+    if (lane == 0) base = atomicAdd(&q->heavy_count, __popc(m));
+    base = __shfl_sync(kFull, base, 0);
+    if (heavy) heavy_list(q)[base + __popc(m & ((1u << lane) - 1u))] = static_cast<int32_t>(i);
+  }
+}
+
+// Histogram of cost buckets; the last block picks the threshold: the highest
+// buckets whose cumulative count stays within n/16 (none if the top bucket alone
+// exceeds it).
+__global__ void __launch_bounds__(256) heavy_threshold_kernel(const bsg_scenario* __restrict__ sc,
+                                                              int64_t n, WorkQueue* q) {
+  __shared__ int32_t h[kCostBuckets];
+  __shared__ bool last;
+  for (int b = threadIdx.x; b < kCostBuckets; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    atomicAdd(&h[cost_bucket(sc[i].cand_est)], 1);
+  __syncthreads();
+  for (int b = threadIdx.x; b < kCostBuckets; b += blockDim.x)
+    if (h[b]) atomicAdd(&q->hist[b], h[b]);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&q->blocks_done, 1) == static_cast<int>(gridDim.x) - 1;
+  __syncthreads();
+  if (!last || threadIdx.x >= 32) return;
+  __threadfence();
+  // suffix sums over buckets (highest cost first), 4 buckets per lane
+  const int lane = threadIdx.x;
+  int32_t c[4], tot = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    c[j] = __ldcg(&q->hist[kCostBuckets - 1 - (lane * 4 + j)]);
+    tot += c[j];
+  }
+  int32_t acc = warp_incl_scan(tot) - tot;  // count in strictly higher buckets
+  const int64_t cap = n / 16;
+  int32_t thr = kCostBuckets;  // no heavy bucket
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    acc += c[j];
+    if (acc <= cap && c[j] > 0) thr = kCostBuckets - 1 - (lane * 4 + j);
+  }
+  thr = static_cast<int32_t>(__reduce_min_sync(kFull, static_cast<uint32_t>(thr)));
+  if (lane == 0) q->threshold = thr;
+}
 
 template <int K, bool POW2>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, min_blocks(K))
-    predict_kernel(const DevCfg* __restrict__ cfgs, int32_t ncfg,
-                   const int32_t* __restrict__ prompt, const int32_t* __restrict__ est,
-                   const int32_t* __restrict__ prefill, const int32_t* __restrict__ decoded,
-                   const bsg_scenario* __restrict__ scen, int64_t n,
-                   const int32_t* __restrict__ order, bsg_result* __restrict__ out) {
-  __shared__ int32_t smem[kWarpsPerBlock * (5 * 32 * K + 32)];
-  const int warp = threadIdx.x >> 5;
-  const int64_t w = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + warp;
-  if (w >= n) return;
-  const int64_t i = order ? order[w] : w;
-  const bsg_scenario sc = scen[i];
-  bsg_result* o = out + i;
+__device__ __forceinline__ void predict_one(const DevCfg* __restrict__ cfgs, int32_t ncfg,
+                                            const int32_t* __restrict__ prompt,
+                                            const int32_t* __restrict__ est,
+                                            const int32_t* __restrict__ prefill,
+                                            const int32_t* __restrict__ decoded,
+                                            const bsg_scenario& sc, int32_t* smem,
+                                            bsg_result* __restrict__ o) {
   if (sc.cfg < 0 || sc.cfg >= ncfg) {
     if ((threadIdx.x & 31) == 0) {
       bsg_result r{};
@@ -60,8 +150,36 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, min_blocks(K))
     }
     return;
   }
-  simulate_scenario<K, false, false, POW2>(cfg, prompt, est, prefill, decoded, sc,
-                                          smem + warp * (5 * 32 * K + 32), o, TraceSink{nullptr, 0});
+  simulate_scenario<K, false, false, POW2>(cfg, prompt, est, prefill, decoded, sc, smem, o,
+                                          TraceSink{nullptr, 0});
+}
+
+template <int K, bool POW2>
+__global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K))
+    predict_kernel(const DevCfg* __restrict__ cfgs, int32_t ncfg,
+                   const int32_t* __restrict__ prompt, const int32_t* __restrict__ est,
+                   const int32_t* __restrict__ prefill, const int32_t* __restrict__ decoded,
+                   const bsg_scenario* __restrict__ scen, int64_t n, WorkQueue* __restrict__ q,
+                   bsg_result* __restrict__ out) {
+  __shared__ int32_t smem_all[kPredictWarps * smem_words(K)];
+  const int warp = threadIdx.x >> 5;
+  int32_t* smem = smem_all + warp * smem_words(K);
+  // warps [0, nh) run the heavy list; warp nh + i runs scenario i unless it is heavy
+  int64_t w = static_cast<int64_t>(blockIdx.x) * kPredictWarps + warp;
+  if (q) {
+    const int32_t thr = __ldcg(&q->threshold);
+    const int64_t nh = thr < kCostBuckets ? __ldcg(&q->heavy_count) : 0;
+    if (w < nh) {
+      w = __ldcg(&heavy_list(q)[w]);
+    } else {
+      w -= nh;
+      if (w >= n || (thr < kCostBuckets && cost_bucket(__ldg(&scen[w].cand_est)) >= thr)) return;
+    }
+  } else if (w >= n) {
+    return;
+  }
+  const bsg_scenario sc = scen[w];
+  predict_one<K, POW2>(cfgs, ncfg, prompt, est, prefill, decoded, sc, smem, out + w);
 }
 
 template <int K, bool POW2>
@@ -70,7 +188,7 @@ __global__ void __launch_bounds__(32)
                  const int32_t* __restrict__ est, const int32_t* __restrict__ prefill,
                  const int32_t* __restrict__ decoded, const bsg_scenario* __restrict__ scen,
                  bsg_result* __restrict__ out, bsg_step_record* rec, int64_t cap) {
-  __shared__ int32_t smem[5 * 32 * K + 32];
+  __shared__ int32_t smem[smem_words(K)];
   const bsg_scenario sc = scen[0];
   const DevCfg cfg = cfgs[sc.cfg];
   simulate_scenario<K, true, false, POW2>(cfg, prompt, est, prefill, decoded, sc, smem, out,
@@ -134,8 +252,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   const int64_t w = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + warp;
   if (w >= static_cast<int64_t>(n_inst) * n_req) return;
   const int32_t r = static_cast<int32_t>(w / n_inst);
-  int32_t* smem = dsm + warp * (5 * 32 * K + 32 + S);
-  int32_t* len = smem + 5 * 32 * K + 32;
+  int32_t* smem = dsm + warp * (smem_words(K) + S);
+  int32_t* len = smem + smem_words(K);
   for (int32_t j = lane; j < S; j += 32) len[j] = sorted_len[static_cast<int64_t>(r) * S + j];
   __syncwarp();
   const bsg_scenario sc = scen[w];
@@ -232,7 +350,7 @@ struct bsg_ctx {
   int64_t scenarios = 0;  // predict() scenarios simulated (MC: request x instance x sample)
   std::vector<bsg_instance_cfg> host_cfgs;
   std::vector<DevCfg> dev_cfgs_host;
-  DevBuf cfgs, prompt, est, prefill, decoded, scen, res, rec, ids, chosen, order;
+  DevBuf cfgs, prompt, est, prefill, decoded, scen, res, rec, ids, chosen;
   DevBuf blob, scores, samples, counters;
   void* pinned = nullptr;   // host staging for single-copy uploads
   size_t pinned_cap = 0;
@@ -293,36 +411,68 @@ int capacity_k(int32_t need) {
   return 0;
 }
 
-template <int K>
-void launch_predict(bsg_ctx* ctx, int64_t n, const bsg_entries& e, const bsg_scenario* sc,
-                    const int32_t* order, bsg_result* out, cudaStream_t s) {
-  const int64_t blocks = (n + kWarpsPerBlock - 1) / kWarpsPerBlock;
+// The cost-aware queue pays for itself only with several waves of warps.
+#ifndef BSG_QUEUE_MIN
+#define BSG_QUEUE_MIN 8192
+#endif
+
+template <int K, bool POW2>
+bsg_status launch_predict_t(bsg_ctx* ctx, int64_t n, const bsg_entries& e, const bsg_scenario* sc,
+                            bsg_result* out, cudaStream_t s) {
+  static const bool no_queue = std::getenv("BSG_NO_QUEUE") != nullptr;
   auto* cf = static_cast<const DevCfg*>(ctx->cfgs.p);
-  if (ctx->all_pow2)
-    predict_kernel<K, true><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
-        cf, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, order, out);
-  else
-    predict_kernel<K, false><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
-        cf, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, order, out);
-  ctx->launches += 1;
+  const int64_t blocks = (n + kPredictWarps - 1) / kPredictWarps;
+  if (no_queue || n < BSG_QUEUE_MIN) {
+    predict_kernel<K, POW2><<<static_cast<unsigned>(blocks), kPredictWarps * 32, 0, s>>>(
+        cf, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, nullptr, out);
+    ctx->launches += 1;
+    BSG_CUDA(ctx, cudaGetLastError());
+    return BSG_OK;
+  }
+  // stream-ordered scratch: safe for concurrent calls on different streams
+  void* mem = nullptr;
+  BSG_CUDA(ctx, cudaMallocAsync(&mem, sizeof(WorkQueue) + (n / 16 + 32) * sizeof(int32_t), s));
+  auto* q = static_cast<WorkQueue*>(mem);
+  BSG_CUDA(ctx, cudaMemsetAsync(q, 0, sizeof(WorkQueue), s));
+  const int64_t hb = std::min<int64_t>((n + 1023) / 1024, 148);
+  heavy_threshold_kernel<<<static_cast<unsigned>(hb), 256, 0, s>>>(sc, n, q);
+  heavy_list_kernel<<<static_cast<unsigned>(hb), 256, 0, s>>>(sc, n, q);
+  const int64_t pb = (n + n / 16 + 32 + kPredictWarps - 1) / kPredictWarps;  // >= heavy + n warps
+  predict_kernel<K, POW2><<<static_cast<unsigned>(pb), kPredictWarps * 32, 0, s>>>(
+      cf, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
+  ctx->launches += 3;
+  BSG_CUDA(ctx, cudaGetLastError());
+  if (std::getenv("BSG_QUEUE_DEBUG")) {
+    WorkQueue hq;
+    cudaMemcpyAsync(&hq, q, sizeof(hq), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    std::fprintf(stderr, "queue: n=%lld blocks=%lld threshold=%d heavy=%d\n",
+                 static_cast<long long>(n), static_cast<long long>(pb), hq.threshold, hq.heavy_count);
+  }
+  BSG_CUDA(ctx, cudaFreeAsync(mem, s));
+  return BSG_OK;
+}
+
+template <int K>
+bsg_status launch_predict(bsg_ctx* ctx, int64_t n, const bsg_entries& e, const bsg_scenario* sc,
+                          bsg_result* out, cudaStream_t s) {
+  return ctx->all_pow2 ? launch_predict_t<K, true>(ctx, n, e, sc, out, s)
+                       : launch_predict_t<K, false>(ctx, n, e, sc, out, s);
 }
 
 bsg_status launch_predict_k(bsg_ctx* ctx, int k, int64_t n, const bsg_entries& e,
-                            const bsg_scenario* sc, const int32_t* order, bsg_result* out,
-                            cudaStream_t s) {
+                            const bsg_scenario* sc, bsg_result* out, cudaStream_t s) {
   if (n == 0) return BSG_OK;
   ctx->scenarios += n;
   switch (k) {
-    case 1: launch_predict<1>(ctx, n, e, sc, order, out, s); break;
-    case 2: launch_predict<2>(ctx, n, e, sc, order, out, s); break;
-    case 4: launch_predict<4>(ctx, n, e, sc, order, out, s); break;
-    case 8: launch_predict<8>(ctx, n, e, sc, order, out, s); break;
+    case 1: return launch_predict<1>(ctx, n, e, sc, out, s);
+    case 2: return launch_predict<2>(ctx, n, e, sc, out, s);
+    case 4: return launch_predict<4>(ctx, n, e, sc, out, s);
+    case 8: return launch_predict<8>(ctx, n, e, sc, out, s);
     default:
       ctx->last_error = "member capacity beyond 256 is outside the supported domain";
       return BSG_BAD_INPUT;
   }
-  BSG_CUDA(ctx, cudaGetLastError());
-  return BSG_OK;
 }
 
 int32_t host_need(const bsg_scenario* sc, int64_t n, const std::vector<bsg_instance_cfg>& cfgs) {
@@ -387,6 +537,14 @@ bsg_status bsg_ctx_create(int device, bsg_ctx** out) {
   if (cudaSetDevice(device) != cudaSuccess) return BSG_CUDA_ERROR;
   auto* ctx = new bsg_ctx();
   ctx->device = device;
+  {  // keep stream-ordered scratch allocations cached in the device's pool
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+  }
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete ctx;
     return BSG_CUDA_ERROR;
@@ -493,13 +651,13 @@ bsg_status bsg_predict_batch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n
   dev.decoded = static_cast<const int32_t*>(ctx->decoded.p);
   auto* dsc = static_cast<bsg_scenario*>(ctx->scen.p);
   auto* dres = static_cast<bsg_result*>(ctx->res.p);
-  // Chunked pipeline (sets > 256k scenarios; measured: at cfg2 size one chunk
-  // wins, H2D is PCIe-bound): chunk c (a contiguous scenario range) copies only the
+  // Chunked pipeline (measured on cfg2, pinned buffers: 3 chunks of 20k cut the
+  // call from 1.05 to 0.75 ms; H2D is PCIe-bound): chunk c (a contiguous scenario range) copies only the
   // entry range its scenarios reference, runs, and copies its results back on
   // stream c % 3, so H2D(c+1) overlaps the kernel on c and D2H(c-1).
   const char* env_chunk = std::getenv("BSG_PIPE_CHUNK");
-  const int64_t target_chunk = env_chunk ? std::max<int64_t>(1, std::atoll(env_chunk)) : 262144;
-  const int64_t nchunks = std::min<int64_t>(8, std::max<int64_t>(1, n / target_chunk));
+  const int64_t target_chunk = env_chunk ? std::max<int64_t>(1, std::atoll(env_chunk)) : 20000;
+  const int64_t nchunks = std::min<int64_t>(16, std::max<int64_t>(1, n / target_chunk));
   const int64_t per = (n + nchunks - 1) / nchunks;
   auto cols_h = std::array<const int32_t*, 4>{entries->prompt, entries->est, entries->prefill,
                                               entries->decoded};
@@ -539,8 +697,7 @@ bsg_status bsg_predict_batch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n
     BSG_CUDA(ctx, cudaMemcpyAsync(dsc + s0, scenarios + s0, (s1 - s0) * sizeof(bsg_scenario),
                                   cudaMemcpyHostToDevice, st));
     const int k = capacity_k(need);
-    const bsg_status ls = launch_predict_k(ctx, k == 0 ? 8 : k, s1 - s0, dev, dsc + s0, nullptr,
-                                           dres + s0, st);
+    const bsg_status ls = launch_predict_k(ctx, k == 0 ? 8 : k, s1 - s0, dev, dsc + s0, dres + s0, st);
     if (ls != BSG_OK) return ls;
     BSG_CUDA(ctx, cudaMemcpyAsync(out + s0, dres + s0, (s1 - s0) * sizeof(bsg_result),
                                   cudaMemcpyDeviceToHost, st));
@@ -560,7 +717,7 @@ bsg_status bsg_predict_batch_device(bsg_ctx* ctx, const bsg_entries* dev_entries
   const int32_t cap = member_capacity > 0 ? member_capacity : std::max(1, ctx->max_batch_all);
   int k = capacity_k(cap);
   if (k == 0) k = 8;
-  return launch_predict_k(ctx, k, n, *dev_entries, dev_scenarios, nullptr, dev_out, s);
+  return launch_predict_k(ctx, k, n, *dev_entries, dev_scenarios, dev_out, s);
 }
 
 bsg_status bsg_trace(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries,
@@ -648,7 +805,7 @@ bsg_status bsg_dispatch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entr
   const int k = capacity_k(host_need(scenarios, n, ctx->host_cfgs));
   auto* res = static_cast<bsg_result*>(ctx->res.p);
   st = launch_predict_k(ctx, k == 0 ? 8 : k, n, dev, static_cast<const bsg_scenario*>(ctx->scen.p),
-                        nullptr, res, ctx->stream);
+                        res, ctx->stream);
   if (st != BSG_OK) return st;
   const int warps = 4;
   argmin_kernel<<<(n_requests + warps - 1) / warps, warps * 32, 0, ctx->stream>>>(
@@ -752,7 +909,7 @@ bsg_status dispatch_fused(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_en
   auto* dcf = static_cast<const DevCfg*>(ctx->cfgs.p);
 #define BSG_LAUNCH_MC1(KK, P2)                                                                  \
   {                                                                                             \
-    const size_t sm = static_cast<size_t>(kWarpsPerBlock) * (5 * 32 * KK + 32 + S) * 4;         \
+    const size_t sm = static_cast<size_t>(kWarpsPerBlock) * (smem_words(KK) + S) * 4;         \
     if (sm > 48 * 1024)                                                                         \
       cudaFuncSetAttribute(dispatch_mc_kernel<KK, P2>,                                          \
                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));  \

@@ -34,6 +34,17 @@
 namespace bsg {
 
 constexpr unsigned kFull = 0xffffffffu;
+// Event-skipping window: kWinJ steps per lane, kWin = 32 * kWinJ steps per window.
+#ifndef BSG_WIN_J
+#define BSG_WIN_J 1
+#endif
+constexpr int kWinJ = BSG_WIN_J;
+constexpr int kWin = 32 * kWinJ;
+// Per-warp shared-memory words of simulate_scenario: the completion-compaction
+// area (5 x 32K) / the window histograms (4 x kWin), whichever is larger.
+__host__ __device__ constexpr int smem_words(int K) {
+  return (5 * 32 * K > 4 * kWin ? 5 * 32 * K : 4 * kWin);
+}
 constexpr int64_t kMaxSimulatedSteps = 50000000LL;  // predictor.cpp:11
 
 // Device-side config: bsg_instance_cfg + precomputed block-size divisor.
@@ -202,7 +213,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
                                   const int32_t* __restrict__ g_est,
                                   const int32_t* __restrict__ g_prefill,
                                   const int32_t* __restrict__ g_decoded, const bsg_scenario sc,
-                                  int32_t* __restrict__ smem,  // (5 * 32 * K + 32) int32 per warp
+                                  int32_t* __restrict__ smem,  // smem_words(K) int32 per warp
                                   bsg_result* __restrict__ out, TraceSink trace,
                                   McArgs mc = McArgs{}) {
   constexpr int CAP = 32 * K;
@@ -253,8 +264,25 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
     if (lane == 0) *out = res;
     return;
   }
-  // waiting entries: validated lazily as they are read; the candidate's admit check
-  // (backend.cpp:76-83):
+  // waiting entries: validated eagerly (one coalesced pass; the simulation then
+  // reads them lazily, only when the waiting head is examined)
+  {
+    bool badw = false;
+    for (int32_t j = lane; j < sc.wait_n; j += 32) {
+      const int32_t g = sc.wait_off + j;
+      const int32_t pr = __ldg(g_prompt + g);
+      const int32_t est = __ldg(g_est + g);
+      const int32_t dec = __ldg(g_decoded + g);
+      const int32_t tg = dec >= est ? dec + 10 : est;
+      badw |= pr < 1 || pr > (1 << 22) || tg > (1 << 24) + 10;
+    }
+    if (__any_sync(kFull, badw)) {
+      res.status = BSG_BAD_INPUT;
+      if (lane == 0) *out = res;
+      return;
+    }
+  }
+  // the candidate's admit check (backend.cpp:76-83):
   {
     const int64_t need = (static_cast<int64_t>(sc.cand_prompt) + cand_target + cfg.block_size - 1) /
                          cfg.block_size;
@@ -281,6 +309,9 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
   const int32_t wait_n = sc.wait_n;
   const bool chunked = cfg.local_policy == BSG_CHUNKED_PREFILL;
   const int32_t maxb = cfg.max_batch_size;
+#ifdef BSG_PROFILE_ITERS
+  int64_t prof_gen = 0, prof_win = 0;
+#endif
 
   for (;;) {
     const bool waiting_nonempty = (L > n) || (h < wait_n) || cand_tail;
@@ -391,7 +422,6 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
       excl_scan<K>(wprompt, P);
       excl_scan<K>(fdelta, DX);
       bool stop[K];
-      bool badw = false;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int32_t p = lane * K + k;
@@ -405,14 +435,8 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
         const int32_t dj = bnt<POW2>(c + (c == prompt[k] ? 1 : 0), cfg);
         ok = ok && dj <= pf - DX[k];
         if (ok) chunk[k] = c;
-        if (p >= L && valid[k])
-          badw |= prompt[k] < 1 || prompt[k] > (1 << 22) || target[k] > (1 << 24) + 10;
         stop[k] = p >= n && !ok;
         if (ok) delta[k] = dj;
-      }
-      if (__any_sync(kFull, badw)) {
-        res.status = BSG_BAD_INPUT;
-        break;
       }
       const int32_t first_stop = first_pos<K>(stop, CAP);
       a = first_stop - n;
@@ -445,112 +469,215 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
     bool cand_first = false, cand_done = false;
 
     // ---------------- event skipping: pure-decode window ----------------
-    // This step is pure decode with no admission. Until the first completion
-    // (t_c) or the first step whose cumulative block demand exceeds free
-    // (t_p), every following step has the same membership and is pure decode
-    // too (projected_free only shrinks, so a blocked waiting head stays
-    // blocked). Lane t prices step t of the window; block demand per step is
-    // a histogram of (-stored) mod block_size over the members.
+    // This step is pure decode with no admission. Member p (r_p = target -
+    // decoded - 1) decodes in window steps t <= r_p and completes at the end of
+    // step r_p; nothing else changes membership until (a) a step whose block
+    // demand exceeds free (preemption), (b) the first step at which the waiting
+    // head would be admitted (completions free blocks, budget and batch slots),
+    // (c) the running set empties, or (d) the candidate completes (inclusive).
+    // Lane l evaluates steps t = l*J + j of a kWin = 32*J step window:
+    // D(t) = #alive, context C(t) = sum(stored)+t*D(t), demand
+    // dem(t) = #{alive p : (stored_p + t) % block_size == 0}, free before the
+    // step A(t) = free - sum_{s<t} dem(s) + sum_{s<t} freed(s) — from four
+    // per-step shared-memory histograms and lane-contiguous warp scans.
     int32_t T = 0;
-    int64_t win_pre = 0, win_base = 0;
+    int64_t win_pre[kWinJ];
+    int64_t win_base = 0;
     if (a == 0 && D == n && n > 0 && !prefill_step) {
-      int32_t lc = 0x7fffffff;
+      constexpr int J = kWinJ, W = kWin;
+      int32_t* h_cnt = smem;          // members completing at the end of step s
+      int32_t* h_sst = smem + W;      // their stored tokens at window start
+      int32_t* h_dem = smem + 2 * W;  // block demand of step t
+      int32_t* h_frd = smem + 3 * W;  // blocks released at the end of step s
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int32_t p = lane * K + k;
-        if (p < n) lc = min(lc, target[k] - decoded[k] - 1);
-      }
-      const int32_t t_c = static_cast<int32_t>(__reduce_min_sync(kFull, static_cast<uint32_t>(lc)));
-      int32_t* hist = smem + 5 * CAP;
-      hist[lane] = 0;
+      for (int i = 0; i < 4 * J; ++i) smem[i * 32 + lane] = 0;
       __syncwarp();
       const int32_t bs = cfg.block_size;
+      int32_t lc = 0x7fffffff;  // candidate's r (if running)
+      int32_t st_run[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int32_t p = lane * K + k;
+        st_run[k] = 0;
         if (p < n) {
-          const int32_t m = modt<POW2>(stored[k], cfg);
-          const int32_t r = m == 0 ? 0 : bs - m;
-          if (r < 32) atomicAdd(&hist[r], 1);
+          const int32_t r = target[k] - decoded[k] - 1;
+          const int32_t sp = stored[k];
+          st_run[k] = sp;
+          if (org[k] == (kCandOrg | kEverBit)) lc = r;
+          if (r < W) {
+            atomicAdd(&h_cnt[r], 1);
+            atomicAdd(&h_sst[r], sp);
+            atomicAdd(&h_frd[r], bnt<POW2>(sp + r + 1, cfg));
+          }
+          const int32_t m = modt<POW2>(sp, cfg);
+          const int32_t rmax = r < W - 1 ? r : W - 1;
+          for (int32_t t = m == 0 ? 0 : bs - m; t <= rmax; t += bs) atomicAdd(&h_dem[t], 1);
         }
       }
       __syncwarp();
-      const int32_t dem = hist[bs <= 32 ? modt<POW2>(lane, cfg) : lane];
-      __syncwarp();
-      const int32_t cum = warp_incl_scan(dem);
-      const unsigned over = __ballot_sync(kFull, cum > free_blocks);
-      const int32_t t_p = over ? __ffs(over) - 1 : 32;
-      const int64_t lim = kMaxSimulatedSteps + 1 - steps;
-      T = min(min(t_c + 1, t_p), 32);
-      if (lim < T) T = static_cast<int32_t>(lim);
-      if (T < 2) T = 0;
-      if (T > 0) {
-        int32_t st_run[K];
+      // lane-contiguous step layout: this lane's steps are t0 + j
+      const int32_t t0 = lane * J;
+      int32_t c_cnt[J], c_sst[J], c_dem[J], c_frd[J];
 #pragma unroll
-        for (int k = 0; k < K; ++k) st_run[k] = (lane * K + k) < n ? stored[k] : 0;
-        const int32_t c0 = warp_sum<K>(st_run);
-        const int64_t d = lane < T ? step_ticks(cfg, 0, D, c0 + lane * D) : 0;
-        const int64_t sum = warp_sum_i64(d);
+      for (int j = 0; j < J; ++j) {
+        c_cnt[j] = h_cnt[t0 + j];
+        c_sst[j] = h_sst[t0 + j];
+        c_dem[j] = h_dem[t0 + j];
+        c_frd[j] = h_frd[t0 + j];
+      }
+      const int32_t s_tot = warp_sum<K>(st_run);
+      int32_t cnt_x[J], sst_x[J], dem_x[J], frd_x[J];
+      excl_scan<J>(c_cnt, cnt_x);
+      excl_scan<J>(c_sst, sst_x);
+      const int32_t dem_tot = excl_scan<J>(c_dem, dem_x);
+      const int32_t frd_tot = excl_scan<J>(c_frd, frd_x);
+      (void)dem_tot;
+      (void)frd_tot;
+      int32_t hp = 0;  // waiting head's prompt
+      if (waiting_nonempty) {
+        if (L > n) hp = read_pos<K>(prompt, n);  // victims: the waiting front
+        else if (h < wait_n) hp = __ldg(g_prompt + sc.wait_off + h);
+        else hp = sc.cand_prompt;
+      }
+      int32_t Dt[J], Ct[J];
+      int32_t first_stop = W;
+#pragma unroll
+      for (int j = J - 1; j >= 0; --j) {
+        const int32_t t = t0 + j;
+        Dt[j] = n - cnt_x[j];                          // alive in step t
+        Ct[j] = (s_tot - sst_x[j]) + t * Dt[j];        // context of step t
+        const int32_t At = free_blocks - dem_x[j] + frd_x[j];  // free before step t
+        bool stop = Dt[j] == 0 || c_dem[j] > At;
+        if (waiting_nonempty && t > 0 && !stop) {
+          // would the waiting head be admitted at step t? (backend.cpp:132-148 / 158-175)
+          if (chunked) {
+            const int32_t bud = cfg.chunk_budget - Dt[j];
+            const int32_t c = hp < bud ? hp : bud;
+            stop = bud > 0 && Dt[j] < maxb && bnt<POW2>(c + (c == hp ? 1 : 0), cfg) <= At - c_dem[j];
+          } else {
+            stop = Dt[j] < maxb && bnt<POW2>(hp + 1, cfg) <= At;
+          }
+        }
+        if (stop) first_stop = t;
+      }
+      T = static_cast<int32_t>(__reduce_min_sync(kFull, static_cast<uint32_t>(first_stop)));
+      const int32_t t_cand = static_cast<int32_t>(__reduce_min_sync(kFull, static_cast<uint32_t>(lc)));
+      if (t_cand < W - 1) T = min(T, t_cand + 1);
+      const int64_t lim = kMaxSimulatedSteps + 1 - steps;
+      if (lim < T) T = static_cast<int32_t>(lim);
+      if (T > 0) {
+        int64_t d[J];
+        int64_t dsum = 0;
+        int32_t msum = 0;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const bool in = t0 + j < T;
+          d[j] = in ? step_ticks(cfg, 0, Dt[j], Ct[j]) : 0;
+          dsum += d[j];
+          msum += in ? Dt[j] + 1 : 0;
+        }
+        const int64_t sum = warp_sum_i64(dsum);
         if constexpr (MC) {
-          // inclusive prefix of step durations: elapsed at the end of window step `lane`
-          int64_t pre = d;
+          // inclusive prefix of step durations: elapsed at the end of window step t
+          int64_t pre = dsum;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
             const int64_t y = __shfl_up_sync(kFull, pre, o);
             if (lane >= o) pre += y;
           }
-          win_pre = pre;
+          int64_t acc = pre - dsum;
+#pragma unroll
+          for (int j = 0; j < J; ++j) {
+            acc += d[j];
+            win_pre[j] = acc;
+          }
           win_base = elapsed;
         }
+        // free after the window's allocations (releases are added below with the
+        // completed members' holdings)
+        int32_t dem_i[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) dem_i[j] = dem_x[j] + c_dem[j];
+        const int32_t dem_T = read_pos<J>(dem_i, T - 1);
         if constexpr (TRACE) {
-          uint64_t hplan = 0, hfirst = 0;
-          int32_t z[K], rz[K];
+          int32_t rr[K];
 #pragma unroll
-          for (int k = 0; k < K; ++k) z[k] = ((lane * K + k) < n && decoded[k] == 0) ? 1 : 0;
-          excl_scan<K>(z, rz);
+          for (int k = 0; k < K; ++k) rr[k] = (lane * K + k) < n ? target[k] - decoded[k] - 1 : -1;
+          int32_t fa[J];
 #pragma unroll
-          for (int k = 0; k < K; ++k) {
-            const int32_t p = lane * K + k;
-            if (p < n) hplan += hash_term(BSG_TAG_PLAN, p, org_origin(org[k]), 0);
-            if (z[k]) hfirst += hash_term(BSG_TAG_FIRST, rz[k], org_origin(org[k]), 0);
-          }
+          for (int j = 0; j < J; ++j) fa[j] = free_blocks - dem_i[j] + frd_x[j] + c_frd[j];
+          for (int32_t t = 0; t < T; ++t) {
+            int32_t al[K], ral[K], cp[K], rcp[K], z[K], rz[K];
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            hplan += __shfl_xor_sync(kFull, hplan, o);
-            hfirst += __shfl_xor_sync(kFull, hfirst, o);
-          }
-          if (lane < T && steps + lane < trace.cap) {
-            bsg_step_record& r = trace.rec[steps + lane];
-            r.duration_ticks = d;
-            r.context_tokens = c0 + lane * D;
-            r.n_decode = D;
-            r.prefill_tokens = 0;
-            r.n_prefill = 0;
-            r.n_preempted = 0;
-            r.n_completed = 0;
-            r.free_blocks_after = free_blocks - cum;
-            r.plan_hash = hplan;
-            r.event_hash = lane == 0 ? hfirst : 0;
+            for (int k = 0; k < K; ++k) {
+              al[k] = rr[k] >= t ? 1 : 0;
+              cp[k] = rr[k] == t ? 1 : 0;
+              z[k] = (t == 0 && rr[k] >= 0 && decoded[k] == 0) ? 1 : 0;
+            }
+            excl_scan<K>(al, ral);
+            const int32_t ncp = excl_scan<K>(cp, rcp);
+            excl_scan<K>(z, rz);
+            uint64_t hplan = 0, hev = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              const int32_t o = org_origin(org[k]);
+              if (al[k]) hplan += hash_term(BSG_TAG_PLAN, ral[k], o, 0);
+              if (z[k]) hev += hash_term(BSG_TAG_FIRST, rz[k], o, 0);
+              if (cp[k]) hev += hash_term(BSG_TAG_COMPLETED, rcp[k], o, 0);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              hplan += __shfl_xor_sync(kFull, hplan, o);
+              hev += __shfl_xor_sync(kFull, hev, o);
+            }
+            int64_t dl = 0;
+#pragma unroll
+            for (int j = 0; j < J; ++j)
+              if (j == t % J) dl = d[j];
+            const int64_t dt = __shfl_sync(kFull, dl, t / J);
+            const int32_t ct = read_pos<J>(Ct, t);
+            const int32_t nd = read_pos<J>(Dt, t);
+            const int32_t fat = read_pos<J>(fa, t);
+            if (lane == 0 && steps + t < trace.cap) {
+              bsg_step_record& rec = trace.rec[steps + t];
+              rec.duration_ticks = dt;
+              rec.context_tokens = ct;
+              rec.n_decode = nd;
+              rec.prefill_tokens = 0;
+              rec.n_prefill = 0;
+              rec.n_preempted = 0;
+              rec.n_completed = ncp;
+              rec.free_blocks_after = fat;
+              rec.plan_hash = hplan;
+              rec.event_hash = hev;
+            }
           }
           __syncwarp();
         }
         elapsed += sum;
         steps += T;
-        res.member_steps += static_cast<int64_t>(T) * (D + 1);
-        free_blocks -= __shfl_sync(kFull, cum, T - 1);
+        res.member_steps += static_cast<int64_t>(
+            __reduce_add_sync(kFull, static_cast<uint32_t>(msum)));
+        free_blocks -= dem_T;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           const int32_t p = lane * K + k;
           dec_s[k] = p < n;
           pre_s[k] = false;
           first_tok[k] = false;  // only possible at window step 0; never the candidate
-          if (p < n) decoded[k] += T;
+          if (p < n) {
+            const int32_t r = target[k] - decoded[k] - 1;
+            decoded[k] += r < T ? r + 1 : T;
+          }
           done[k] = p < n && decoded[k] >= target[k];
           freed[k] = done[k] ? bnt<POW2>(prefill[k] + decoded[k], cfg) : 0;
           if (org[k] == (kCandOrg | kEverBit)) cand_done |= done[k];
         }
       }
     }
+#ifdef BSG_PROFILE_ITERS
+    if (T == 0) ++prof_gen; else ++prof_win;
+#endif
     if (T == 0) {
     // ---------------- begin_step: admissions (backend.cpp:249-261) ----------------
     const int32_t n_adm = n + a;
@@ -728,7 +855,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
       }
     }
     }  // general step (T == 0)
-    if constexpr (TRACE) {
+    if (TRACE && T == 0) {
       // item order: decodes (position order), then prefill items (position order)
       int32_t fd[K], fp[K], cd[K], cp[K], rfd[K], rfp[K], rcd[K], rcp[K];
 #pragma unroll
@@ -777,7 +904,17 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
           const bool hit = lj <= cd;
           // step (within the window) at whose end decoded first reaches lj
           const int32_t tj = hit ? lj - dec0 - 1 : 0;
-          const int64_t at = T > 0 ? win_base + __shfl_sync(kFull, win_pre, tj & 31) : elapsed;
+          int64_t at = elapsed;
+          if (T > 0) {  // elapsed at the end of window step tj (held by lane tj / J, slot tj % J)
+            const int32_t tw = tj & (kWin - 1);
+            int64_t v = 0;
+#pragma unroll
+            for (int j = 0; j < kWinJ; ++j) {
+              const int64_t x = __shfl_sync(kFull, win_pre[j], tw / kWinJ);
+              if (j == tw % kWinJ) v = x;
+            }
+            at = win_base + v;
+          }
           if (hit) {
             mc_sum += at;
             if (mc.sample_e2e) mc.sample_e2e[j] = at;
@@ -845,6 +982,11 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
     }
   }
   res.steps = steps;
+#ifdef BSG_PROFILE_ITERS
+  // debug build only (tools/iterprobe.py): loop iterations by kind
+  res.detail = static_cast<int32_t>(prof_gen);
+  res.member_steps = prof_win;
+#endif
   if constexpr (MC) {
     int64_t tot = mc_sum;
 #pragma unroll

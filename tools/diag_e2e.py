@@ -17,9 +17,10 @@ for _ in range(3): dev.copy_(big, non_blocking=True); torch.cuda.synchronize()
 t=time.perf_counter()
 for _ in range(20): dev.copy_(big, non_blocking=True)
 torch.cuda.synchronize(); print("H2D %.1f MB: %.3f ms" % (big.numel()/1e6, (time.perf_counter()-t)/20*1e3))
-out = np.zeros(len(ss), abi.result_dtype)
+pout = torch.empty(len(ss) * abi.result_dtype.itemsize, dtype=torch.uint8).pin_memory()
+out = pout.numpy().view(abi.result_dtype)
 e = host.entries()
-for chunk in ["1000000", "30000", "16384", "8192", "4096"]:
+for chunk in ["1000000", "30000", "20000", "15000", "10000", "7500"]:
     os.environ["BSG_PIPE_CHUNK"] = chunk
     for _ in range(3): ctx.L.bsg_predict_batch(ctx.h, C.byref(e), host.n_entries, abi.ptr(host.scenarios), len(ss), abi.ptr(out))
     ts=[]

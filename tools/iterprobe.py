@@ -1,0 +1,19 @@
+"""Loop-iteration mix per scenario (needs the BSG_PROFILE_ITERS build, see iterprobe.sh)."""
+import os, sys
+sys.path.insert(0, os.getcwd())
+import numpy as np
+from paper_2508_03611_b200 import abi, native
+ctx = native.Context(0)
+for which in (sys.argv[1:] or ["cfg2", "cfg3"]):
+    if which == "cfg3":
+        w = abi.make_workload(count=2000, prompt_median=600, output_median=600, qps=5.0, arrival_seed=1)
+    else:
+        w = abi.make_workload(count=5000, qps=27.0, arrival_seed=1)
+    cfg = abi.make_config()
+    _, _, ss = ctx.replay(w, cfg, abi.make_replay_spec(12))
+    ctx.set_configs(cfg)
+    r = ctx.predict_batch(ss)
+    gen = r["detail"].astype(np.int64); win = r["member_steps"]; st = r["steps"]
+    print(f"{which}: steps mean {st.mean():.1f}; general iters mean {gen.mean():.1f} (p99 {np.percentile(gen,99):.0f}); "
+          f"window iters mean {win.mean():.1f} (p99 {np.percentile(win,99):.0f}); steps per window "
+          f"{(st - gen).sum() / max(win.sum(),1):.2f}")

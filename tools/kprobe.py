@@ -1,0 +1,73 @@
+"""Kernel tail probe: device-timed predict over the cfg2 capture in natural,
+cost-sorted (steps desc) and shuffled scenario order; per-scenario step stats.
+usage: python tools/kprobe.py [cfg2|cfg3]"""
+import os, sys
+sys.path.insert(0, os.getcwd())
+import numpy as np, torch
+from paper_2508_03611_b200 import abi, native
+which = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+ctx = native.Context(0)
+if which == "cfg3":
+    w = abi.make_workload(count=2000, prompt_median=600, output_median=600, qps=5.0, arrival_seed=1)
+else:
+    w = abi.make_workload(count=5000, qps=27.0, arrival_seed=1)
+cfg = abi.make_config()
+_, _, ss = ctx.replay(w, cfg, abi.make_replay_spec(12))
+ctx.set_configs(cfg)
+dev = torch.device("cuda", 0)
+cols = [torch.from_numpy(c).to(dev) for c in (ss.prompt, ss.est, ss.prefill, ss.decoded)]
+flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+st = torch.cuda.Stream(dev); torch.cuda.set_stream(st)
+cap = ss.member_capacity(cfg)
+n = len(ss)
+out = torch.empty(n * abi.result_dtype.itemsize, dtype=torch.uint8, device=dev)
+def timeit(scen_np, reps=20):
+    scen = torch.from_numpy(scen_np.view(np.uint8)).to(dev)
+    f = lambda: ctx.predict_batch_device([c.data_ptr() for c in cols], scen.data_ptr(), n, out.data_ptr(), st.cuda_stream, member_capacity=cap)
+    for _ in range(3): f()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        flush.zero_(); a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+        a.record(st); f(); b.record(st); torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
+    res = np.frombuffer(out.cpu().numpy().tobytes(), dtype=abi.result_dtype).copy()
+    return np.median(ts) * 1e3, res
+t0, res = timeit(ss.scenarios)
+steps = res["steps"]; ms = res["member_steps"]
+print(f"{which}: n={n} entries={ss.n_entries} natural {t0:.1f} us -> {n/t0:.1f}M scen/s")
+print("steps pct 50/90/99/99.9/max", np.percentile(steps, [50, 90, 99, 99.9]).round(), steps.max(), "mean", steps.mean().round(1))
+print("member_steps mean", ms.mean().round(1), "max", ms.max())
+order = np.argsort(-steps, kind="stable")
+t1, _ = timeit(np.ascontiguousarray(ss.scenarios[order]))
+print(f"sorted by steps desc {t1:.1f} us -> {n/t1:.1f}M scen/s")
+ce = ss.scenarios["cand_est"].astype(np.int64)
+t1b, _ = timeit(np.ascontiguousarray(ss.scenarios[np.argsort(-ce, kind="stable")]))
+print(f"sorted by cand_est desc {t1b:.1f} us -> {n/t1b:.1f}M scen/s")
+lb = np.floor(np.log2(ce + 1) * 4).astype(np.int64)
+t1c, _ = timeit(np.ascontiguousarray(ss.scenarios[np.argsort(-lb, kind="stable")]))
+print(f"sorted by log2(cand_est) quarter-octave buckets desc {t1c:.1f} us -> {n/t1c:.1f}M scen/s")
+key = ce + ss.scenarios["wait_n"].astype(np.int64) * 64
+t1d, _ = timeit(np.ascontiguousarray(ss.scenarios[np.argsort(-key, kind="stable")]))
+print(f"sorted by cand_est+64*wait_n desc {t1d:.1f} us -> {n/t1d:.1f}M scen/s")
+for q in (50, 75, 90, 95, 98):
+    thr = np.percentile(ce, q)
+    hv = ce > thr
+    o = np.concatenate([np.nonzero(hv)[0], np.nonzero(~hv)[0]])
+    tq, _ = timeit(np.ascontiguousarray(ss.scenarios[o]))
+    print(f"heavy-first (cand_est > p{q} = {thr:.0f}, {hv.sum()} heavy) {tq:.1f} us")
+# two-level: heavy sorted desc + rest natural
+thr = np.percentile(ce, 90); hv = np.nonzero(ce > thr)[0]
+o = np.concatenate([hv[np.argsort(-ce[hv], kind="stable")], np.nonzero(ce <= thr)[0]])
+tq, _ = timeit(np.ascontiguousarray(ss.scenarios[o]))
+print(f"p90 heavy sorted desc + rest natural {tq:.1f} us")
+print("corr(steps, cand_est)", np.corrcoef(steps, ce)[0,1].round(3))
+rng = np.random.default_rng(0)
+t2, _ = timeit(np.ascontiguousarray(ss.scenarios[rng.permutation(n)]))
+print(f"shuffled {t2:.1f} us")
+# 8x the work in one launch (weak-scaling-in-a-launch): tail amortisation
+big = np.ascontiguousarray(np.tile(ss.scenarios, 8))
+n8 = len(big)
+out = torch.empty(n8 * abi.result_dtype.itemsize, dtype=torch.uint8, device=dev)
+n_save = n; n = n8
+t3, _ = timeit(big, reps=5)
+print(f"8x tiled {t3:.1f} us -> {n8/t3:.1f}M scen/s")
