@@ -72,7 +72,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "10"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -216,6 +216,8 @@ def run_gpu(args):
     line = None
     if rank == 0:
         peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {}
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
         hbm_peak = peaks.get("hbm_gbs", 6650.0)
         props = torch.cuda.get_device_properties(dev)
         sms = props.multi_processor_count
@@ -242,10 +244,13 @@ def run_gpu(args):
             "gpu_launches": launches_all,
             "roofline": {
                 "bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved_gbs / hbm_peak, "traffic": None,
-                "kernel": f"bsg::predict_kernel<{1 if cap <= 32 else 2 if cap <= 64 else 4}>",
+                "frac": achieved_gbs / hbm_peak, "traffic": traffic.get("dram_bytes_per_launch"),
+                "kernel": f"bsg::predict_kernel<{1 if cap <= 32 else 2 if cap <= 64 else 4}, true>",
                 "note": "neither HBM nor tensor cores bind: dependent integer state machine; "
-                        "see issue roof",
+                        "the binding resource is SM issue (ncu issue-active "
+                        f"{traffic.get('issue_active_pct', 'n/a')}%, {traffic.get('source', 'no capture')}); "
+                        "the timed step also holds the two small launch-order kernels "
+                        "(heavy_threshold/heavy_list, ~4% of the step in the ncu launch list)",
                 "issue": {"achieved_int_ops_per_s": achieved_int, "peak_int_ops_per_s": issue_peak,
                           "frac": achieved_int / issue_peak,
                           "member_steps_per_step": member_steps, "ops_per_member_step": 24,

@@ -99,12 +99,33 @@ __device__ __forceinline__ int64_t warp_sum_i64(int64_t d) {
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// Inclusive warp scan: 5 x (shfl.up with its in-range predicate + predicated
+// add) — no lane-index compares on the dependent chain.
 __device__ __forceinline__ int32_t warp_incl_scan(int32_t x) {
-  const int lane = lane_id();
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
-    const int32_t y = __shfl_up_sync(kFull, x, d);
-    if (lane >= d) x += y;
+    asm("{\n\t.reg .s32 r;\n\t.reg .pred p;\n\t"
+        "shfl.sync.up.b32 r|p, %0, %1, 0, -1;\n\t"
+        "@p add.s32 %0, %0, r;\n\t}"
+        : "+r"(x)
+        : "r"(d));
+  }
+  return x;
+}
+
+// Inclusive warp scan of a 64-bit value (e.g. two packed 32-bit counters whose
+// low-half sums never carry).
+__device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t x) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    asm("{\n\t.reg .b32 lo, hi;\n\t.reg .b64 y;\n\t.reg .pred p;\n\t"
+        "mov.b64 {lo, hi}, %0;\n\t"
+        "shfl.sync.up.b32 lo|p, lo, %1, 0, -1;\n\t"
+        "shfl.sync.up.b32 hi, hi, %1, 0, -1;\n\t"
+        "mov.b64 y, {lo, hi};\n\t"
+        "@p add.u64 %0, %0, y;\n\t}"
+        : "+l"(x)
+        : "r"(d));
   }
   return x;
 }
@@ -122,7 +143,8 @@ __device__ __forceinline__ int32_t excl_scan(const int32_t (&in)[K], int32_t (&o
   const int32_t base = incl - s;
 #pragma unroll
   for (int k = 0; k < K; ++k) out[k] += base;
-  return __shfl_sync(kFull, incl, 31);
+  // the total off the scan's dependent chain
+  return static_cast<int32_t>(__reduce_add_sync(kFull, static_cast<uint32_t>(s)));
 }
 
 template <int K>
@@ -526,13 +548,31 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
         c_frd[j] = h_frd[t0 + j];
       }
       const int32_t s_tot = warp_sum<K>(st_run);
+      // two scans instead of four: (cnt | dem << 16) — both <= 256 per step and
+      // <= 256 * kWin in total — and (sst | frd << 32) — sums of held tokens and
+      // blocks, < 2^31 by the integer domain, so the low half never carries.
       int32_t cnt_x[J], sst_x[J], dem_x[J], frd_x[J];
-      excl_scan<J>(c_cnt, cnt_x);
-      excl_scan<J>(c_sst, sst_x);
-      const int32_t dem_tot = excl_scan<J>(c_dem, dem_x);
-      const int32_t frd_tot = excl_scan<J>(c_frd, frd_x);
-      (void)dem_tot;
-      (void)frd_tot;
+      {
+        int32_t cd_in[J], cd_x[J];
+        uint64_t sf_lane = 0;
+        uint64_t sf_x[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          cd_in[j] = c_cnt[j] | (c_dem[j] << 16);
+          sf_x[j] = sf_lane;
+          sf_lane += static_cast<uint32_t>(c_sst[j]) | (static_cast<uint64_t>(c_frd[j]) << 32);
+        }
+        excl_scan<J>(cd_in, cd_x);
+        const uint64_t sf_base = warp_incl_scan_u64(sf_lane) - sf_lane;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          cnt_x[j] = cd_x[j] & 0xffff;
+          dem_x[j] = static_cast<int32_t>(static_cast<uint32_t>(cd_x[j]) >> 16);
+          const uint64_t v = sf_x[j] + sf_base;
+          sst_x[j] = static_cast<int32_t>(static_cast<uint32_t>(v));
+          frd_x[j] = static_cast<int32_t>(v >> 32);
+        }
+      }
       int32_t hp = 0;  // waiting head's prompt
       if (waiting_nonempty) {
         if (L > n) hp = read_pos<K>(prompt, n);  // victims: the waiting front
