@@ -385,6 +385,28 @@ bsg_status bsg_sweep_run(int device, const bsg_sweep_cell* cells, int32_t n_cell
 /* Scenarios simulated by this context so far (all entry points). */
 int64_t bsg_scenario_count(const bsg_ctx* ctx);
 
+/* Device-resident closed loops: each run is one
+ * run_experiment (driver.cpp:134-289) with static provisioning, zero dispatch
+ * overhead and BlockPredictive dispatch, executed entirely on the GPU — one
+ * thread block per run: live instances in HBM, every arrival's per-instance
+ * what-ifs + argmin on the block's warps, the event loop on the device.
+ * Requests of run r are rows [req_off, req_off + n_requests) of the request
+ * columns (arrival ticks non-decreasing; request id = row - req_off);
+ * outcomes has the same rows. run_status[r] is BSG_OK or the error that ended
+ * run r (BSG_DEADLOCK / BSG_EMPTY_PLAN / a what-if failure). HOST buffers. */
+typedef struct bsg_closed_loop_run {
+  int32_t n_instances;  /* 1..256 */
+  int32_t objective;    /* 0 e2e, 1 ttft */
+  int32_t cfg;          /* index into the configs set by bsg_set_configs */
+  int32_t n_requests;
+  int64_t req_off;
+} bsg_closed_loop_run;
+bsg_status bsg_replay_device(bsg_ctx* ctx, const bsg_closed_loop_run* runs, int32_t n_runs,
+                             const int32_t* prompt, const int32_t* output, const int32_t* est,
+                             const int64_t* arrival_ticks, int64_t n_requests_total,
+                             bsg_request_outcome* outcomes, bsg_replay_summary* summaries,
+                             int32_t* run_status);
+
 /* Synthetic trace + estimates + Poisson arrival ticks (no GPU needed). */
 bsg_status bsg_make_workload(const bsg_workload* w, int32_t* prompt, int32_t* output,
                              int32_t* est, int64_t* arrival_ticks);

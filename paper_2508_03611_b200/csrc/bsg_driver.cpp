@@ -274,10 +274,8 @@ class LiveInstance {
         pt += chunk_[p];
       }
     }
-    if (c_.cache_mode == BSG_CACHE_BUCKETED) {
-      const int64_t b = std::max(1, c_.context_bucket);
-      ctx = (ctx + b / 2) / b * b;
-    }
+    // batch_latency itself (driver.cpp:274: begin_step() without a latency
+    // function); the predictor's cache mode does not apply to live instances
     const double x = c_.c0_s + c_.prefill_s_per_token * static_cast<double>(pt) +
                      c_.decode_s_per_seq * static_cast<double>(nd) +
                      c_.context_s_per_token * static_cast<double>(ctx);

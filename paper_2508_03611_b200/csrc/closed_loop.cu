@@ -1,0 +1,685 @@
+// closed_loop.cu — K5: device-resident closed-loop replay.
+//
+// One thread block runs one whole closed loop — SimulationDriver
+// (core/src/driver.cpp:134-289) with static provisioning, zero dispatch
+// overhead and BlockPredictive dispatch — without returning to the host:
+//
+//   * live serving instances (Instance, core/src/backend.cpp:238-331) are kept
+//     in HBM as SoA columns; instance i owns a running region R (max_batch
+//     slots, admission order) and a waiting region A (victims are pushed at its
+//     front, arrivals at its back), so every instance's status snapshot
+//     (backend.cpp:351-373) is directly a (running, waiting) slice pair — the
+//     what-if kernel reads it in place, no snapshot copy;
+//   * every arrival's per-instance what-ifs (predict(), predictor.cpp:76-137)
+//     run on the block's warps with the same simulate_scenario as K1, followed
+//     by the BlockPredictive argmin (scheduler.cpp:138-150, lowest id on ties);
+//   * the event loop (event_loop.cpp:28-57) exploits that instances only
+//     interact through dispatch: between two arrival instants each warp
+//     advances its own instances' steps independently (completions strictly
+//     before the next arrival; at an arrival instant the arrivals go first —
+//     their sequence numbers are lower — then that instant's completions, then
+//     end_of_instant's begin_step for every idle instance with work,
+//     driver.cpp:271-289).
+//
+// Outcomes (arrival/dispatch/first-token/finish ticks, instance, preemptions)
+// are bit-identical to the host driver and to the reference's run_experiment.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "bsg_ctx.cuh"
+#include "bsg_internal.h"
+
+namespace bsg {
+
+constexpr int kClWarps = 8;
+constexpr int kClMaxInst = 256;
+constexpr int64_t kNever = INT64_MAX;
+
+struct ClRun {
+  int32_t n_inst, objective, cfg, n_req;
+  int64_t req_off;    // first request row
+  int64_t arena_off;  // first arena entry
+};
+
+// Live-state SoA columns.
+struct Arena {
+  int32_t *prompt, *est, *prefill, *decoded, *target, *rid, *chunk;
+};
+
+struct ClInst {
+  int32_t n;           // running members R[0, n)
+  int32_t whead;       // waiting = A[whead, wtail)
+  int32_t wtail;
+  int32_t free_blocks;
+  int64_t t_done;      // completion time of the current step
+  int32_t mid;         // mid-step
+  int32_t pad;
+};
+
+// Instance i of a run: R at base, A at base + maxb (A's first maxb slots are
+// the room for victims pushed in front of the first arrival).
+__device__ __forceinline__ int64_t inst_stride(int32_t maxb, int32_t n_req) {
+  return 2 * static_cast<int64_t>(maxb) + n_req;
+}
+
+// begin_step (backend.cpp:238-296) of a live instance; warp-wide. Returns a
+// bsg_status (EMPTY_PLAN / DEADLOCK propagate like the reference's throws).
+template <int K, bool POW2>
+__device__ int32_t live_begin(const DevCfg& cfg, const Arena& ar, int64_t Rb, int64_t Ab,
+                              ClInst& st, int64_t now, bsg_request_outcome* outs,
+                              unsigned long long* preempts) {
+  constexpr int CAP = 32 * K;
+  const int lane = lane_id();
+  const int32_t n = st.n, whead = st.whead, wtail = st.wtail;
+  int32_t free_blocks = st.free_blocks;
+  const int32_t maxb = cfg.max_batch_size;
+  const bool chunked = cfg.local_policy == BSG_CHUNKED_PREFILL;
+  const bool waiting_nonempty = whead < wtail;
+  int32_t prompt[K], prefill[K], decoded[K], est[K], target[K], rid[K];
+  bool ready[K], nonready[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int32_t p = lane * K + k;
+    prompt[k] = 1;
+    prefill[k] = decoded[k] = est[k] = target[k] = rid[k] = 0;
+    if (p < n) {
+      const int64_t g = Rb + p;
+      prompt[k] = ar.prompt[g];
+      prefill[k] = ar.prefill[g];
+      decoded[k] = ar.decoded[g];
+      est[k] = ar.est[g];
+      target[k] = ar.target[g];
+      rid[k] = ar.rid[g];
+    }
+    ready[k] = p < n && prefill[k] == prompt[k];
+    nonready[k] = p < n && prefill[k] != prompt[k];
+  }
+  const int32_t D = count<K>(ready);
+  bool any_local = false;
+#pragma unroll
+  for (int k = 0; k < K; ++k) any_local |= nonready[k];
+  const bool any_nonready = __any_sync(kFull, any_local);
+  int32_t chunk[K];
+  bool dec[K];
+  int32_t budget = 0;
+  bool prefill_step = false;
+  if (chunked) {  // plan_chunked_prefill (backend.cpp:113-149)
+    int32_t b0 = cfg.chunk_budget - D;
+    if (b0 < 0) b0 = 0;
+    budget = b0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      chunk[k] = 0;
+      dec[k] = ready[k];
+    }
+    if (any_nonready) {
+      int32_t rem[K], S[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) rem[k] = nonready[k] ? prompt[k] - prefill[k] : 0;
+      const int32_t tot = excl_scan<K>(rem, S);
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        int32_t c = b0 - S[k];
+        c = c < 0 ? 0 : c;
+        chunk[k] = nonready[k] ? (c < rem[k] ? c : rem[k]) : 0;
+      }
+      budget = b0 - tot;
+      if (budget < 0) budget = 0;
+    }
+  } else {  // plan_prefill_priority (backend.cpp:151-182)
+    prefill_step = waiting_nonempty || any_nonready;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      chunk[k] = (prefill_step && nonready[k]) ? prompt[k] - prefill[k] : 0;
+      dec[k] = !prefill_step && ready[k];
+    }
+  }
+  int32_t delta[K], stored[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {  // make_item (backend.cpp:94-111)
+    stored[k] = prefill[k] + decoded[k];
+    int32_t ns = stored[k];
+    if (dec[k]) {
+      ns = stored[k] + 1;
+    } else if (chunk[k] > 0) {
+      const int32_t np = prefill[k] + chunk[k];
+      ns = np + decoded[k] + (np == prompt[k] ? 1 : 0);
+    }
+    delta[k] = (dec[k] || chunk[k] > 0) ? bnt<POW2>(ns, cfg) - bnt<POW2>(stored[k], cfg) : 0;
+  }
+  const int32_t run_delta = warp_sum<K>(delta);
+  // waiting admissions: FCFS prefix of A (backend.cpp:132-148 / 158-175)
+  int32_t a = 0;
+  if (waiting_nonempty && n < maxb && (chunked ? budget > 0 : true)) {
+    const int32_t pf = free_blocks - run_delta;
+    bool valid[K];
+    int32_t wprompt[K], fdelta[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int32_t p = lane * K + k;
+      valid[k] = p >= n && p < maxb && (p - n) < (wtail - whead);
+      if (p >= n) {
+        if (valid[k]) {
+          const int64_t g = Ab + whead + (p - n);
+          prompt[k] = ar.prompt[g];
+          est[k] = ar.est[g];
+          target[k] = ar.target[g];
+          rid[k] = ar.rid[g];
+        }
+        prefill[k] = 0;
+        decoded[k] = 0;
+        stored[k] = 0;
+      }
+      wprompt[k] = valid[k] ? prompt[k] : 0;
+      fdelta[k] = valid[k] ? bnt<POW2>(prompt[k] + 1, cfg) : 0;
+    }
+    int32_t P[K], DX[K];
+    excl_scan<K>(wprompt, P);
+    excl_scan<K>(fdelta, DX);
+    bool stop[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int32_t p = lane * K + k;
+      bool ok = valid[k];
+      int32_t c = prompt[k];
+      if (chunked) {
+        const int32_t bj = budget - P[k];
+        ok = ok && bj > 0;
+        c = prompt[k] < bj ? prompt[k] : bj;
+      }
+      const int32_t dj = bnt<POW2>(c + (c == prompt[k] ? 1 : 0), cfg);
+      ok = ok && dj <= pf - DX[k];
+      if (ok && p >= n) {
+        chunk[k] = c;
+        delta[k] = dj;
+      }
+      stop[k] = p >= n && !ok;
+    }
+    a = first_pos<K>(stop, CAP) - n;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int32_t p = lane * K + k;
+      if (p >= n + a) {
+        chunk[k] = 0;
+        delta[k] = 0;
+      }
+    }
+  }
+  if (!chunked && prefill_step && !any_nonready && a == 0) {  // backend.cpp:176-181
+    prefill_step = false;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      dec[k] = ready[k];
+      delta[k] = ready[k] ? bnt<POW2>(stored[k] + 1, cfg) - bnt<POW2>(stored[k], cfg) : 0;
+    }
+  }
+  if (n == 0 && a == 0) return BSG_EMPTY_PLAN;  // backend.cpp:245
+  const int32_t n_adm = n + a;
+  // allocation with newest-member preemption: e* = max{e : F(e) >= 0}
+  // (backend.cpp:263-288; derivation in scenario_sim.cuh / DESIGN.md)
+  const int32_t tot_delta = warp_sum<K>(delta);
+  int32_t e_star = n_adm;
+  if (tot_delta > free_blocks) {
+    int32_t ho[K], hinc[K], dinc[K], fe[K];
+    bool badp[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) ho[k] = (lane * K + k) < n ? bnt<POW2>(stored[k], cfg) : 0;
+    const int32_t htot = excl_scan<K>(ho, hinc);
+    excl_scan<K>(delta, dinc);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int32_t p = lane * K + k;
+      fe[k] = free_blocks + (htot - hinc[k] - ho[k]) - (dinc[k] + delta[k]);
+      badp[k] = p < n_adm && fe[k] < 0;
+    }
+    e_star = first_pos<K>(badp, n_adm);
+    if (e_star == 0) return BSG_DEADLOCK;  // backend.cpp:274-277
+    free_blocks = read_pos<K>(fe, e_star - 1);
+  } else {
+    free_blocks -= tot_delta;
+  }
+  const int32_t v = n_adm - e_star;  // victims, oldest first
+  const int32_t new_whead = whead + a - v;
+  __syncwarp();  // every lane has read its A entries before victims overwrite A's front
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int32_t p = lane * K + k;
+    if (p >= n && p < e_star) {  // admitted and kept: into R
+      const int64_t g = Rb + p;
+      ar.prompt[g] = prompt[k];
+      ar.est[g] = est[k];
+      ar.prefill[g] = 0;
+      ar.decoded[g] = 0;
+      ar.target[g] = target[k];
+      ar.rid[g] = rid[k];
+    }
+    if (p >= e_star && p < n_adm) {  // victim: recompute, to the waiting front (preempt, 221-232)
+      const int64_t g = Ab + new_whead + (p - e_star);
+      ar.prompt[g] = prompt[k];
+      ar.est[g] = est[k];
+      ar.prefill[g] = 0;
+      ar.decoded[g] = 0;
+      ar.target[g] = target[k];
+      ar.rid[g] = rid[k];
+      outs[rid[k]].preempt_count += 1;
+    }
+  }
+  if (v > 0 && lane == 0) atomicAdd(preempts, static_cast<unsigned long long>(v));
+  // price the surviving plan (to_batch_plan 194-209, batch_latency 10-14)
+  bool ds[K], ps[K];
+  int32_t ctx[K], pt[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int32_t p = lane * K + k;
+    ds[k] = p < e_star && dec[k];
+    ps[k] = p < e_star && chunk[k] > 0;
+    ctx[k] = ds[k] ? stored[k] : 0;
+    pt[k] = ps[k] ? chunk[k] : 0;
+    if (p < e_star) ar.chunk[Rb + p] = ds[k] ? -1 : (ps[k] ? chunk[k] : 0);
+  }
+  const int32_t n_dec = count<K>(ds);
+  const int64_t dur = step_ticks(cfg, warp_sum<K>(pt), n_dec, warp_sum<K>(ctx));
+  __syncwarp();
+  if (lane == 0) {
+    st.n = e_star;
+    st.whead = new_whead;
+    st.free_blocks = free_blocks;
+    st.mid = 1;
+    st.t_done = now + dur;
+  }
+  __syncwarp();
+  return BSG_OK;
+}
+
+// finish_step (backend.cpp:298-331) + the driver's outcome bookkeeping
+// (handle_batch_complete, driver.cpp:233-251); warp-wide.
+template <int K, bool POW2>
+__device__ void live_finish(const DevCfg& cfg, const Arena& ar, int64_t Rb, ClInst& st,
+                            int64_t now, bsg_request_outcome* outs) {
+  const int lane = lane_id();
+  const int32_t n = st.n;
+  int32_t prompt[K], prefill[K], decoded[K], est[K], target[K], rid[K], keep[K], dst[K], freed[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int32_t p = lane * K + k;
+    keep[k] = 0;
+    freed[k] = 0;
+    if (p < n) {
+      const int64_t g = Rb + p;
+      prompt[k] = ar.prompt[g];
+      prefill[k] = ar.prefill[g];
+      decoded[k] = ar.decoded[g];
+      est[k] = ar.est[g];
+      target[k] = ar.target[g];
+      rid[k] = ar.rid[g];
+      const int32_t c = ar.chunk[g];
+      const int32_t prev = decoded[k];
+      if (c < 0) {
+        decoded[k] += 1;
+      } else if (c > 0) {
+        prefill[k] += c;
+        if (prefill[k] == prompt[k]) decoded[k] += 1;
+      }
+      const bool item = c != 0;
+      if (item && prev == 0 && decoded[k] >= 1 && outs[rid[k]].first_token_ticks < 0)
+        outs[rid[k]].first_token_ticks = now;
+      const bool done = item && decoded[k] >= target[k];
+      if (done) {
+        outs[rid[k]].finish_ticks = now;
+        freed[k] = bnt<POW2>(prefill[k] + decoded[k], cfg);
+      }
+      keep[k] = done ? 0 : 1;
+    }
+  }
+  const int32_t kept = excl_scan<K>(keep, dst);
+  const int32_t rel = warp_sum<K>(freed);
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < K; ++k) {  // stable erase of completed members (backend.cpp:319-322)
+    if (keep[k]) {
+      const int64_t g = Rb + dst[k];
+      ar.prompt[g] = prompt[k];
+      ar.prefill[g] = prefill[k];
+      ar.decoded[g] = decoded[k];
+      ar.est[g] = est[k];
+      ar.target[g] = target[k];
+      ar.rid[g] = rid[k];
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    st.n = kept;
+    st.free_blocks += rel;
+    st.mid = 0;
+  }
+  __syncwarp();
+}
+
+template <int K>
+struct ClShared {
+  ClInst inst[kClMaxInst];
+  bsg_result res[kClMaxInst];
+  int32_t scratch[kClWarps][smem_words(K)];
+  unsigned long long preempts;
+  unsigned long long end_ticks;
+  int32_t next;
+  int32_t err;
+};
+
+template <int K, bool POW2>
+__global__ void __launch_bounds__(kClWarps * 32, 2)
+    closed_loop_kernel(const DevCfg* __restrict__ cfgs, const ClRun* __restrict__ runs,
+                       const int32_t* __restrict__ rq_prompt, const int32_t* __restrict__ rq_output,
+                       const int32_t* __restrict__ rq_est, const int64_t* __restrict__ rq_arrival,
+                       Arena ar, bsg_request_outcome* __restrict__ outcomes,
+                       bsg_replay_summary* __restrict__ summaries, int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) unsigned char cl_smem[];
+  ClShared<K>& S = *reinterpret_cast<ClShared<K>*>(cl_smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const ClRun run = runs[blockIdx.x];
+  const DevCfg cfg = cfgs[run.cfg];
+  // live instances price steps with batch_latency itself (driver.cpp:274 calls
+  // begin_step() without a latency function); only predict() uses the cache
+  DevCfg live_cfg = cfg;
+  live_cfg.cache_mode = BSG_CACHE_OFF;
+  const int32_t I = run.n_inst, N = run.n_req, maxb = cfg.max_batch_size;
+  const int64_t stride = inst_stride(maxb, N);
+  bsg_request_outcome* outs = outcomes + run.req_off;
+  const int64_t* arrival = rq_arrival + run.req_off;
+  if (I > kClMaxInst || maxb > 32 * K) {  // the host validates; never reached
+    if (threadIdx.x == 0) status[blockIdx.x] = BSG_BAD_INPUT;
+    return;
+  }
+  for (int i = threadIdx.x; i < I; i += blockDim.x) {
+    ClInst& s = S.inst[i];
+    s.n = 0;
+    s.whead = maxb;
+    s.wtail = maxb;
+    s.free_blocks = cfg.total_blocks;
+    s.t_done = 0;
+    s.mid = 0;
+  }
+  if (threadIdx.x == 0) {
+    S.preempts = 0;
+    S.end_ticks = 0;
+    S.err = BSG_OK;
+  }
+  __syncthreads();
+  int64_t last_done = 0;  // this warp's latest processed completion
+  // close the instant tc (its completions, then end_of_instant's begin_step) and
+  // advance through every completion strictly before t
+  auto advance = [&](int32_t i, int64_t tc, int64_t t) -> int32_t {
+    ClInst& s = S.inst[i];
+    const int64_t Rb = run.arena_off + i * stride;
+    const int64_t Ab = Rb + maxb;
+    if (tc >= 0) {
+      if (s.mid && s.t_done == tc) {
+        live_finish<K, POW2>(cfg, ar, Rb, s, tc, outs);
+        last_done = max(last_done, tc);
+      }
+      if (!s.mid && (s.n > 0 || s.whead < s.wtail)) {
+        const int32_t e = live_begin<K, POW2>(live_cfg, ar, Rb, Ab, s, tc, outs, &S.preempts);
+        if (e != BSG_OK) return e;
+      }
+    }
+    while (s.mid && s.t_done < t) {
+      const int64_t now = s.t_done;
+      live_finish<K, POW2>(cfg, ar, Rb, s, now, outs);
+      last_done = max(last_done, now);
+      if (s.n > 0 || s.whead < s.wtail) {
+        const int32_t e = live_begin<K, POW2>(live_cfg, ar, Rb, Ab, s, now, outs, &S.preempts);
+        if (e != BSG_OK) return e;
+      }
+    }
+    return BSG_OK;
+  };
+  auto fail = [&](int32_t e) {
+    if (lane == 0) atomicCAS(&S.err, BSG_OK, e);
+  };
+  int64_t t_prev = -1;
+  for (int32_t k = 0; k < N; ++k) {
+    const int64_t t = arrival[k];
+    if (t != t_prev) {
+      for (int32_t i = warp; i < I; i += kClWarps) {
+        const int32_t e = advance(i, t_prev, t);
+        if (e != BSG_OK) {
+          fail(e);
+          break;
+        }
+      }
+      __syncthreads();
+      if (S.err != BSG_OK) break;
+    }
+    // ---- dispatch: per-instance what-ifs (predict_across) + argmin ----
+    if (threadIdx.x == 0) S.next = 0;
+    __syncthreads();
+    const int32_t cp = rq_prompt[run.req_off + k], ce = rq_est[run.req_off + k];
+    for (;;) {
+      int32_t i = 0;
+      if (lane == 0) i = atomicAdd(&S.next, 1);
+      i = __shfl_sync(kFull, i, 0);
+      if (i >= I) break;
+      const ClInst& s = S.inst[i];
+      bsg_scenario sc;
+      sc.run_off = static_cast<int32_t>(run.arena_off + i * stride);
+      sc.run_n = s.n;
+      sc.wait_off = static_cast<int32_t>(run.arena_off + i * stride + maxb + s.whead);
+      sc.wait_n = s.wtail - s.whead;
+      sc.cand_prompt = cp;
+      sc.cand_est = ce;
+      sc.cfg = run.cfg;
+      sc.reserved = 0;
+      simulate_scenario<K, false, false, POW2, false>(cfg, ar.prompt, ar.est, ar.prefill, ar.decoded, sc,
+                                              S.scratch[warp], &S.res[i], TraceSink{nullptr, 0});
+    }
+    __syncthreads();
+    if (warp == 0) {  // BlockPredictive argmin (scheduler.cpp:138-150)
+      int64_t best_v = INT64_MAX;
+      int32_t best_i = INT32_MAX, bad = BSG_OK;
+      for (int32_t i = lane; i < I; i += 32) {
+        const bsg_result& r = S.res[i];
+        if (r.status != BSG_OK && bad == BSG_OK) bad = r.status;
+        const int64_t v = run.objective == 1 ? r.ttft_ticks : r.e2e_ticks;
+        if (v < best_v || (v == best_v && i < best_i)) {
+          best_v = v;
+          best_i = i;
+        }
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) {
+        const int64_t ov = __shfl_xor_sync(kFull, best_v, d);
+        const int32_t oi = __shfl_xor_sync(kFull, best_i, d);
+        if (ov < best_v || (ov == best_v && oi < best_i)) {
+          best_v = ov;
+          best_i = oi;
+        }
+      }
+      bad = static_cast<int32_t>(__reduce_max_sync(kFull, static_cast<uint32_t>(bad)));
+      if (bad != BSG_OK) {
+        fail(bad);  // PredictionError propagates out of the run (predictor.cpp:132-136)
+      } else if (lane == 0) {  // admit the arrival at the chosen instance's waiting tail
+        ClInst& s = S.inst[best_i];
+        const int64_t g = run.arena_off + best_i * stride + maxb + s.wtail;
+        ar.prompt[g] = cp;
+        ar.est[g] = ce;
+        ar.prefill[g] = 0;
+        ar.decoded[g] = 0;
+        ar.target[g] = rq_output[run.req_off + k];
+        ar.rid[g] = k;
+        s.wtail += 1;
+        outs[k].dispatch_ticks = t;
+        outs[k].instance = best_i;
+      }
+    }
+    __syncthreads();
+    if (S.err != BSG_OK) break;
+    t_prev = t;
+  }
+  if (S.err == BSG_OK) {  // drain
+    for (int32_t i = warp; i < I; i += kClWarps) {
+      const int32_t e = advance(i, t_prev, kNever);
+      if (e != BSG_OK) {
+        fail(e);
+        break;
+      }
+    }
+  }
+  if (lane == 0) atomicMax(&S.end_ticks, static_cast<unsigned long long>(max(last_done, t_prev)));
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    status[blockIdx.x] = S.err;
+    bsg_replay_summary sm{};
+    sm.total_preemptions = static_cast<int64_t>(S.preempts);
+    sm.end_ticks = static_cast<int64_t>(S.end_ticks);
+    sm.instances_provisioned = 0;
+    sm.final_instance_count = I;
+    summaries[blockIdx.x] = sm;
+  }
+}
+
+}  // namespace bsg
+
+using namespace bsg;
+
+namespace {
+
+template <int K, bool POW2>
+bsg_status launch_closed_loop(bsg_ctx* ctx, int32_t n_runs, const ClRun* runs,
+                              const int32_t* p, const int32_t* o, const int32_t* e,
+                              const int64_t* arr, const Arena& ar, bsg_request_outcome* outs,
+                              bsg_replay_summary* sums, int32_t* st) {
+  const size_t sm = sizeof(ClShared<K>);
+  cudaFuncSetAttribute(closed_loop_kernel<K, POW2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(sm));
+  closed_loop_kernel<K, POW2><<<n_runs, kClWarps * 32, sm, ctx->stream>>>(
+      static_cast<const DevCfg*>(ctx->cfgs.p), runs, p, o, e, arr, ar, outs, sums, st);
+  ctx->launches += 1;
+  const cudaError_t err = cudaGetLastError();
+  return err == cudaSuccess ? BSG_OK : bsg_cuda_fail(ctx, err, "closed_loop_kernel launch");
+}
+
+}  // namespace
+
+extern "C" bsg_status bsg_replay_device(bsg_ctx* ctx, const bsg_closed_loop_run* runs,
+                                        int32_t n_runs, const int32_t* prompt,
+                                        const int32_t* output, const int32_t* est,
+                                        const int64_t* arrival_ticks, int64_t n_requests_total,
+                                        bsg_request_outcome* outcomes,
+                                        bsg_replay_summary* summaries, int32_t* run_status) {
+  if (!ctx || !runs || n_runs < 0 || !prompt || !output || !est || !arrival_ticks || !outcomes ||
+      !run_status)
+    return BSG_INVALID_ARGUMENT;
+  if (n_runs == 0) return BSG_OK;
+  if (ctx->ncfg == 0) return BSG_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaSetDevice(ctx->device);
+  // host-side layout: arena offsets, validation (driver.cpp config checks)
+  std::vector<ClRun> dr(static_cast<size_t>(n_runs));
+  int64_t arena = 0;
+  int32_t maxb_all = 1;
+  bool pow2 = true;
+  for (int32_t r = 0; r < n_runs; ++r) {
+    const bsg_closed_loop_run& x = runs[r];
+    if (x.cfg < 0 || x.cfg >= ctx->ncfg || x.n_instances < 1 || x.n_instances > kClMaxInst ||
+        x.n_requests < 0 || x.req_off < 0 || x.req_off + x.n_requests > n_requests_total ||
+        x.objective < 0 || x.objective > 1) {
+      ctx->last_error = "bad closed-loop run descriptor";
+      return BSG_INVALID_ARGUMENT;
+    }
+    const bsg_instance_cfg& c = ctx->host_cfgs[x.cfg];
+    maxb_all = std::max(maxb_all, c.max_batch_size);
+    pow2 &= ctx->dev_cfgs_host[x.cfg].div_magic == 0;
+    for (int64_t q = x.req_off; q < x.req_off + x.n_requests; ++q) {
+      // the workload must be servable (config.cpp:197-205)
+      const int64_t need = (static_cast<int64_t>(prompt[q]) + output[q] + c.block_size - 1) / c.block_size;
+      if (need > c.total_blocks) return BSG_TOO_LARGE_CANDIDATE;
+      if (prompt[q] < 1 || prompt[q] > (1 << 22) || output[q] < 1 || output[q] > (1 << 24) ||
+          est[q] < 0 || est[q] > (1 << 24) || (q > x.req_off && arrival_ticks[q] < arrival_ticks[q - 1])) {
+        ctx->last_error = "closed-loop request outside the supported domain";
+        return BSG_BAD_INPUT;
+      }
+    }
+    dr[r] = ClRun{x.n_instances, x.objective, x.cfg, x.n_requests, x.req_off, arena};
+    arena += static_cast<int64_t>(x.n_instances) * (2 * static_cast<int64_t>(c.max_batch_size) + x.n_requests);
+  }
+  if (arena >= (int64_t{1} << 31)) {
+    ctx->last_error = "closed-loop arena exceeds 2^31 entries; split the batch";
+    return BSG_BAD_INPUT;
+  }
+  int k = 1;
+  while (32 * k < maxb_all) k *= 2;
+  if (k > 8) return BSG_BAD_INPUT;
+  // device buffers (one allocation, freed at the end of the call)
+  const int64_t nq = n_requests_total;
+  const size_t b_runs = n_runs * sizeof(ClRun), b_req = nq * 4, b_arr = nq * 8,
+               b_out = nq * sizeof(bsg_request_outcome), b_sum = n_runs * sizeof(bsg_replay_summary),
+               b_st = n_runs * 4, b_col = static_cast<size_t>(std::max<int64_t>(arena, 1)) * 4;
+  auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t total = up(b_runs) + 3 * up(b_req) + up(b_arr) + up(b_out) + up(b_sum) + up(b_st) + 7 * up(b_col);
+  char* base = nullptr;
+  cudaError_t ce = cudaMallocAsync(reinterpret_cast<void**>(&base), total, ctx->stream);
+  if (ce != cudaSuccess) return bsg_cuda_fail(ctx, ce, "cudaMallocAsync(closed-loop)");
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    char* p = base + off;
+    off += up(b);
+    return p;
+  };
+  auto* d_runs = reinterpret_cast<ClRun*>(take(b_runs));
+  auto* d_p = reinterpret_cast<int32_t*>(take(b_req));
+  auto* d_o = reinterpret_cast<int32_t*>(take(b_req));
+  auto* d_e = reinterpret_cast<int32_t*>(take(b_req));
+  auto* d_a = reinterpret_cast<int64_t*>(take(b_arr));
+  auto* d_out = reinterpret_cast<bsg_request_outcome*>(take(b_out));
+  auto* d_sum = reinterpret_cast<bsg_replay_summary*>(take(b_sum));
+  auto* d_st = reinterpret_cast<int32_t*>(take(b_st));
+  Arena ar{};
+  int32_t** cols[7] = {&ar.prompt, &ar.est, &ar.prefill, &ar.decoded, &ar.target, &ar.rid, &ar.chunk};
+  for (auto* c : cols) *c = reinterpret_cast<int32_t*>(take(b_col));
+  // outcomes start as the driver's Request records: arrival set, the rest unset
+  std::vector<bsg_request_outcome> init(static_cast<size_t>(nq));
+  for (int64_t q = 0; q < nq; ++q) init[q] = bsg_request_outcome{arrival_ticks[q], -1, -1, -1, -1, 0};
+  cudaStream_t s = ctx->stream;
+  bsg_status st = BSG_OK;
+#define BSG_CL_CHECK(call)                                  \
+  do {                                                      \
+    cudaError_t _e = (call);                                \
+    if (_e != cudaSuccess && st == BSG_OK) st = bsg_cuda_fail(ctx, _e, #call); \
+  } while (0)
+  BSG_CL_CHECK(cudaMemcpyAsync(d_runs, dr.data(), b_runs, cudaMemcpyHostToDevice, s));
+  BSG_CL_CHECK(cudaMemcpyAsync(d_p, prompt, b_req, cudaMemcpyHostToDevice, s));
+  BSG_CL_CHECK(cudaMemcpyAsync(d_o, output, b_req, cudaMemcpyHostToDevice, s));
+  BSG_CL_CHECK(cudaMemcpyAsync(d_e, est, b_req, cudaMemcpyHostToDevice, s));
+  BSG_CL_CHECK(cudaMemcpyAsync(d_a, arrival_ticks, b_arr, cudaMemcpyHostToDevice, s));
+  BSG_CL_CHECK(cudaMemcpyAsync(d_out, init.data(), b_out, cudaMemcpyHostToDevice, s));
+  if (st == BSG_OK) {
+    switch (k * 2 + (pow2 ? 1 : 0)) {
+      case 2: st = launch_closed_loop<1, false>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st); break;
+      case 3: st = launch_closed_loop<1, true>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st); break;
+      case 4: st = launch_closed_loop<2, false>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st); break;
+      case 5: st = launch_closed_loop<2, true>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st); break;
+      case 8: st = launch_closed_loop<4, false>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st); break;
+      case 9: st = launch_closed_loop<4, true>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st); break;
+      case 16: st = launch_closed_loop<8, false>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st); break;
+      default: st = launch_closed_loop<8, true>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st); break;
+    }
+  }
+  if (st == BSG_OK) {
+    BSG_CL_CHECK(cudaMemcpyAsync(outcomes, d_out, b_out, cudaMemcpyDeviceToHost, s));
+    if (summaries) BSG_CL_CHECK(cudaMemcpyAsync(summaries, d_sum, b_sum, cudaMemcpyDeviceToHost, s));
+    BSG_CL_CHECK(cudaMemcpyAsync(run_status, d_st, b_st, cudaMemcpyDeviceToHost, s));
+  }
+  BSG_CL_CHECK(cudaFreeAsync(base, s));
+  BSG_CL_CHECK(cudaStreamSynchronize(s));
+#undef BSG_CL_CHECK
+  if (st == BSG_OK) {
+    int64_t whatifs = 0;
+    for (int32_t r = 0; r < n_runs; ++r) whatifs += static_cast<int64_t>(runs[r].n_instances) * runs[r].n_requests;
+    ctx->scenarios += whatifs;
+  }
+  return st;
+}

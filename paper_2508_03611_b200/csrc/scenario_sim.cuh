@@ -230,7 +230,17 @@ struct McArgs {
 
 // Simulates one scenario with the calling warp. All lanes return the same
 // result; lane 0 writes it.
-template <int K, bool TRACE, bool MC = false, bool POW2 = false>
+// Snapshot loads: read-only-cache loads (__ldg) when the entries are immutable
+// for the kernel's lifetime (K1 and the dispatch kernels); coherent L2 loads
+// when other warps of the same kernel write them (the device-resident closed
+// loop, closed_loop.cu).
+template <bool LDG>
+__device__ __forceinline__ int32_t ld_entry(const int32_t* p) {
+  if constexpr (LDG) return __ldg(p);
+  else return __ldcg(p);
+}
+
+template <int K, bool TRACE, bool MC = false, bool POW2 = false, bool LDG = true>
 __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__ g_prompt,
                                   const int32_t* __restrict__ g_est,
                                   const int32_t* __restrict__ g_prefill,
@@ -264,10 +274,10 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
     held[k] = 0;
     if (p < run_n) {
       const int32_t g = sc.run_off + p;
-      prompt[k] = __ldg(g_prompt + g);
-      const int32_t est = __ldg(g_est + g);
-      prefill[k] = __ldg(g_prefill + g);
-      decoded[k] = __ldg(g_decoded + g);
+      prompt[k] = ld_entry<LDG>(g_prompt + g);
+      const int32_t est = ld_entry<LDG>(g_est + g);
+      prefill[k] = ld_entry<LDG>(g_prefill + g);
+      decoded[k] = ld_entry<LDG>(g_decoded + g);
       target[k] = decoded[k] >= est ? decoded[k] + 10 : est;
       org[k] = (p + 1) | kEverBit;
       bad |= prompt[k] < 1 || prompt[k] > (1 << 22) || prefill[k] < 0 || prefill[k] > prompt[k] ||
@@ -292,9 +302,9 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
     bool badw = false;
     for (int32_t j = lane; j < sc.wait_n; j += 32) {
       const int32_t g = sc.wait_off + j;
-      const int32_t pr = __ldg(g_prompt + g);
-      const int32_t est = __ldg(g_est + g);
-      const int32_t dec = __ldg(g_decoded + g);
+      const int32_t pr = ld_entry<LDG>(g_prompt + g);
+      const int32_t est = ld_entry<LDG>(g_est + g);
+      const int32_t dec = ld_entry<LDG>(g_decoded + g);
       const int32_t tg = dec >= est ? dec + 10 : est;
       badw |= pr < 1 || pr > (1 << 22) || tg > (1 << 24) + 10;
     }
@@ -422,9 +432,9 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
           const int32_t j = h + (p - L);
           if (j < wait_n) {
             const int32_t g = sc.wait_off + j;
-            prompt[k] = __ldg(g_prompt + g);
-            const int32_t est = __ldg(g_est + g);
-            const int32_t dec = __ldg(g_decoded + g);
+            prompt[k] = ld_entry<LDG>(g_prompt + g);
+            const int32_t est = ld_entry<LDG>(g_est + g);
+            const int32_t dec = ld_entry<LDG>(g_decoded + g);
             target[k] = dec >= est ? dec + 10 : est;  // correct_lengths on waiting too
             org[k] = run_n + j + 1;
           } else if (j == wait_n && cand_tail) {
@@ -576,7 +586,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
       int32_t hp = 0;  // waiting head's prompt
       if (waiting_nonempty) {
         if (L > n) hp = read_pos<K>(prompt, n);  // victims: the waiting front
-        else if (h < wait_n) hp = __ldg(g_prompt + sc.wait_off + h);
+        else if (h < wait_n) hp = ld_entry<LDG>(g_prompt + sc.wait_off + h);
         else hp = sc.cand_prompt;
       }
       int32_t Dt[J], Ct[J];

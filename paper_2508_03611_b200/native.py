@@ -62,6 +62,7 @@ def load() -> C.CDLL:
         "bsg_sweep_run": (C.c_int, [C.c_int, V, C.c_int32, C.c_int32, V]),
         "bsg_scenario_count": (C.c_int64, [V]),
         "bsg_mc_lengths": (C.c_int, [C.c_int32, C.c_uint64, C.c_int32, C.c_uint64, C.c_double, V]),
+        "bsg_replay_device": (C.c_int, [V, V, C.c_int32, V, V, V, V, C.c_int64, V, V, V]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -239,6 +240,28 @@ class Context:
             self._check(st, "bsg_capacity_search")
         n = int(out["n_tested"][0])
         return st, out[0], list(zip(tq[:n].tolist(), tp[:n].astype(bool).tolist()))
+
+    def replay_device(self, runs):
+        """Device-resident closed loops (bsg_replay_device). runs: list of
+        (workload, n_instances, objective, cfg_index) with the configs already
+        set. Returns [(status, outcomes, summary)] per run."""
+        cols = [make_workload_host(w) for w, *_ in runs]
+        desc = np.zeros(len(runs), abi.closed_loop_run_dtype)
+        off = 0
+        for r, ((w, ni, obj, cf), c) in enumerate(zip(runs, cols)):
+            desc[r] = (ni, obj, cf, len(c[0]), off)
+            off += len(c[0])
+        p, o, e, t = (np.ascontiguousarray(np.concatenate([c[j] for c in cols])) for j in range(4))
+        out = np.zeros(off, abi.outcome_dtype)
+        summ = np.zeros(len(runs), abi.summary_dtype)
+        st = np.zeros(len(runs), np.int32)
+        self._check(self.L.bsg_replay_device(self.h, _p(desc), len(runs), _p(p), _p(o), _p(e), _p(t),
+                                             off, _p(out), _p(summ), _p(st)), "bsg_replay_device")
+        res = []
+        for r in range(len(runs)):
+            a, n = int(desc[r]["req_off"]), int(desc[r]["n_requests"])
+            res.append((int(st[r]), out[a:a + n], summ[r]))
+        return res
 
     def replay(self, w, cfg, spec):
         """Closed-loop replay (host live instances, GPU what-ifs). Returns

@@ -188,3 +188,33 @@ def test_sweep_cells_match_reference_capacity_search(ref):
         assert int(o["status"]) == st
         assert o["result"].tolist() == exp.tolist()
         assert o["whatif_scenarios"] > 0
+
+
+@pytest.mark.parametrize("policy_cfg", [
+    dict(),                                                      # chunked prefill, P1
+    dict(local_policy=1),                                        # prefill priority
+    dict(total_blocks=300, max_batch_size=24),                   # KV pressure: preemptions
+    dict(block_size=10, total_blocks=1500, chunk_budget=256),    # non-power-of-two blocks
+    dict(cache_mode=2, context_bucket=256, max_batch_size=64),   # bucketed latency cache, K=2
+])
+def test_device_closed_loop_matches_reference(ctx, ref, policy_cfg):
+    """bsg_replay_device (whole closed loop on the GPU) == the reference's own
+    run_experiment replay: every request's dispatch instance and tick-exact
+    dispatch / first-token / finish times and preemption counts."""
+    cfg = abi.make_config(**policy_cfg)
+    ctx.set_configs(cfg)
+    cases = [(abi.make_workload(count=300, qps=q, arrival_seed=s, estimator_kind=2, estimator_seed=s),
+              ni, obj) for q, s, ni, obj in [(6.0, 1, 4, 0), (14.0, 2, 12, 0), (30.0, 3, 7, 1),
+                                              (3.0, 4, 1, 0)]]
+    got = ctx.replay_device([(w, ni, obj, 0) for w, ni, obj in cases])
+    for (w, ni, obj), (st, out, summ) in zip(cases, got):
+        spec = abi.make_replay_spec(ni, objective=obj, capture=0)
+        exp, esum, _ = ref.replay(w, cfg, spec, capture=False)
+        host, hsum, _ = ctx.replay(w, cfg, spec)  # the host-driven closed loop, same contract
+        ctx.set_configs(cfg)
+        assert st == abi.OK
+        for f in ("instance", "dispatch_ticks", "first_token_ticks", "finish_ticks", "preempt_count"):
+            assert np.array_equal(out[f], exp[f]), (policy_cfg, ni, f, np.nonzero(out[f] != exp[f])[0][:5])
+            assert np.array_equal(host[f], exp[f]), ("host", policy_cfg, ni, f)
+        assert int(summ["total_preemptions"]) == int(esum["total_preemptions"])
+        assert int(hsum["total_preemptions"]) == int(esum["total_preemptions"])
