@@ -376,10 +376,16 @@ typedef struct bsg_sweep_out {
   bsg_capacity_result result;
   int64_t whatif_scenarios;      /* predict() scenarios simulated on the GPU for this cell */
   int64_t kernel_launches;
-  double wall_s;
+  double wall_s;                 /* host path: summed closed-loop time; device path: the
+                                    wall time of the batched launches holding its points */
 } bsg_sweep_out;
-/* Runs cells (in the given order) on `threads` host threads, each with its own
- * context on `device`, so independent closed loops overlap on the GPU. */
+/* Runs the cells' capacity searches. When every cell is a statically
+ * provisioned BlockPredictive cluster of <= 256 instances, every (cell, qps)
+ * point is a device-resident closed loop (bsg_replay_device): all integer
+ * points in one batched launch, then all tenths in a second one (records
+ * generated on `threads` host threads). Otherwise the closed loops run on
+ * `threads` host threads, each with its own context on `device` (GPU what-ifs
+ * per arrival). BSG_SWEEP_HOST=1 forces the host path. */
 bsg_status bsg_sweep_run(int device, const bsg_sweep_cell* cells, int32_t n_cells,
                          int32_t threads, bsg_sweep_out* out);
 /* Scenarios simulated by this context so far (all entry points). */

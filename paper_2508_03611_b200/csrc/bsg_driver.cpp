@@ -866,9 +866,176 @@ extern "C" bsg_status bsg_capacity_search(bsg_ctx* ctx, const bsg_workload* base
   return BSG_OK;
 }
 
+namespace {
+
+// Runs closed-loop points (cell, qps) as device-resident closed loops
+// (bsg_replay_device, one thread block per point) and reports pass/fail per
+// point: p99 TTFT < slo (metrics.cpp:145-150). Records are generated on
+// `threads` host threads; points are launched longest-first.
+struct Point {
+  int32_t cell;
+  double qps;
+};
+bsg_status run_points_device(bsg_ctx* ctx, const bsg_sweep_cell* cells, const std::vector<Point>& pts,
+                             int32_t threads, std::vector<int8_t>* passed, std::vector<int32_t>* status,
+                             std::vector<int64_t>* whatifs) {
+  const size_t np = pts.size();
+  passed->assign(np, 0);
+  status->assign(np, BSG_OK);
+  whatifs->assign(np, 0);
+  if (np == 0) return BSG_OK;
+  std::vector<std::vector<Record>> recs(np);
+  std::vector<int32_t> gen_err(np, BSG_OK);
+  {
+    std::atomic<size_t> next{0};
+    auto work = [&]() {
+      for (size_t i; (i = next.fetch_add(1)) < np;) {
+        bsg_workload w = cells[pts[i].cell].workload;
+        w.qps = pts[i].qps;  // spec_for_cell (driver.cpp:321-331)
+        w.arrival_seed = cells[pts[i].cell].seed;
+        w.estimator_seed = cells[pts[i].cell].seed;
+        gen_err[i] = make_records(w, &recs[i]);
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < std::max(1, threads); ++t) pool.emplace_back(work);
+    for (auto& th : pool) th.join();
+  }
+  // longest first: blocks are dispatched in index order
+  std::vector<size_t> order(np);
+  for (size_t i = 0; i < np; ++i) order[i] = i;
+  auto cost = [&](size_t i) {
+    const double ni = cells[pts[i].cell].spec.n_instances;
+    return static_cast<double>(recs[i].size()) * ni * (1.0 + pts[i].qps / ni);
+  };
+  std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return cost(a) > cost(b); });
+  std::vector<bsg_closed_loop_run> runs;
+  std::vector<size_t> run_pt;
+  std::vector<int32_t> p, o, e;
+  std::vector<int64_t> t;
+  for (size_t i : order) {
+    if (gen_err[i] != BSG_OK) {
+      (*status)[i] = gen_err[i];
+      continue;
+    }
+    const bsg_sweep_cell& c = cells[pts[i].cell];
+    runs.push_back(bsg_closed_loop_run{c.spec.n_instances, c.spec.objective, pts[i].cell,
+                                       static_cast<int32_t>(recs[i].size()), static_cast<int64_t>(p.size())});
+    run_pt.push_back(i);
+    for (const Record& r : recs[i]) {
+      p.push_back(r.prompt);
+      o.push_back(r.output);
+      e.push_back(r.est);
+      t.push_back(r.arrival);
+    }
+  }
+  std::vector<bsg_request_outcome> outs(p.size());
+  std::vector<bsg_replay_summary> sums(runs.size());
+  std::vector<int32_t> rst(runs.size(), BSG_OK);
+  const bsg_status st = bsg_replay_device(ctx, runs.data(), static_cast<int32_t>(runs.size()), p.data(),
+                                          o.data(), e.data(), t.data(), static_cast<int64_t>(p.size()),
+                                          outs.data(), sums.data(), rst.data());
+  if (st != BSG_OK) return st;
+  for (size_t r = 0; r < runs.size(); ++r) {
+    const size_t i = run_pt[r];
+    (*status)[i] = rst[r];
+    (*whatifs)[i] = static_cast<int64_t>(runs[r].n_instances) * runs[r].n_requests;
+    if (rst[r] != BSG_OK) continue;
+    bsg_run_report rep{};
+    bsg_aggregate(outs.data() + runs[r].req_off, runs[r].n_requests, &sums[r], &rep);
+    (*passed)[i] = rep.p99_ttft_s < cells[pts[i].cell].slo_p99_ttft_s ? 1 : 0;
+  }
+  return BSG_OK;
+}
+
+// bsg_sweep_run on device-resident closed loops: every cell must be a
+// BlockPredictive, statically provisioned cluster of <= 256 instances.
+bsg_status sweep_device(int device, const bsg_sweep_cell* cells, int32_t n_cells, int32_t threads,
+                        bsg_sweep_out* out) {
+  bsg_ctx* ctx = nullptr;
+  bsg_status st = bsg_ctx_create(device, &ctx);
+  if (st != BSG_OK) return st;
+  std::unique_ptr<bsg_ctx, void (*)(bsg_ctx*)> guard(ctx, bsg_ctx_destroy);
+  std::vector<bsg_instance_cfg> cfgs(static_cast<size_t>(n_cells));
+  for (int32_t c = 0; c < n_cells; ++c) cfgs[c] = cells[c].cfg;
+  int32_t bi = 0, fc = 0;
+  st = bsg_set_configs(ctx, cfgs.data(), n_cells, &bi, &fc);
+  if (st != BSG_OK) return st;
+  std::vector<int> err(n_cells, BSG_OK);
+  std::vector<std::vector<int8_t>> ipass(n_cells);
+  std::vector<double> wall(n_cells, 0.0);
+  std::vector<int64_t> scen(n_cells, 0);
+  auto phase = [&](const std::vector<Point>& pts, std::vector<int8_t>* passed) -> bsg_status {
+    std::vector<int32_t> pst;
+    std::vector<int64_t> wi;
+    const auto t0 = std::chrono::steady_clock::now();
+    const bsg_status s = run_points_device(ctx, cells, pts, threads, passed, &pst, &wi);
+    const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (s != BSG_OK) return s;
+    for (size_t i = 0; i < pts.size(); ++i) {
+      if (pst[i] != BSG_OK) err[pts[i].cell] = pst[i];
+      scen[pts[i].cell] += wi[i];
+    }
+    for (int32_t c = 0; c < n_cells; ++c) wall[c] += dt;  // cells share the batched launch
+    return BSG_OK;
+  };
+  std::vector<Point> pts;
+  for (int32_t c = 0; c < n_cells; ++c) {
+    std::memset(&out[c], 0, sizeof(out[c]));
+    if (cells[c].qps_min > cells[c].qps_max) {
+      err[c] = BSG_BAD_CONFIG;
+      continue;
+    }
+    for (int32_t q = cells[c].qps_min; q <= cells[c].qps_max; ++q) pts.push_back(Point{c, static_cast<double>(q)});
+  }
+  std::vector<int8_t> passed;
+  st = phase(pts, &passed);
+  if (st != BSG_OK) return st;
+  for (size_t i = 0; i < pts.size(); ++i) ipass[pts[i].cell].push_back(passed[i]);
+  std::vector<Point> tpts;
+  std::vector<std::vector<double>> tenths(n_cells);
+  for (int32_t c = 0; c < n_cells; ++c) {
+    if (err[c] != BSG_OK) continue;
+    std::vector<bool> ip(ipass[c].begin(), ipass[c].end());
+    if (!ip.front()) {
+      err[c] = BSG_NO_CAPACITY;
+      continue;
+    }
+    tenths[c] = capacity_bracket(ip, cells[c].qps_min, cells[c].qps_max, &out[c].result);
+    for (double q : tenths[c]) tpts.push_back(Point{c, q});
+  }
+  std::vector<int8_t> tpassed;
+  st = phase(tpts, &tpassed);
+  if (st != BSG_OK) return st;
+  std::vector<int32_t> n_tenths(n_cells, 0);
+  for (size_t i = 0; i < tpts.size(); ++i) {
+    const int32_t c = tpts[i].cell;
+    ++n_tenths[c];
+    if (tpassed[i]) out[c].result.capacity_qps = std::max(out[c].result.capacity_qps, tpts[i].qps);
+  }
+  for (int32_t c = 0; c < n_cells; ++c) {
+    out[c].status = err[c];
+    out[c].whatif_scenarios = scen[c];
+    out[c].kernel_launches = 2;
+    out[c].wall_s = wall[c];
+    out[c].result.n_tested = static_cast<int32_t>(ipass[c].size()) + n_tenths[c];
+  }
+  return BSG_OK;
+}
+
+}  // namespace
+
 extern "C" bsg_status bsg_sweep_run(int device, const bsg_sweep_cell* cells, int32_t n_cells,
                                     int32_t threads, bsg_sweep_out* out) {
   if (!cells || !out || n_cells < 0) return BSG_INVALID_ARGUMENT;
+  {
+    bool device_ok = n_cells > 0 && std::getenv("BSG_SWEEP_HOST") == nullptr;
+    for (int32_t c = 0; c < n_cells && device_ok; ++c)
+      device_ok = cells[c].spec.policy == BSG_POLICY_BLOCK_PREDICTIVE &&
+                  cells[c].spec.provision_kind == 0 && cells[c].spec.n_instances >= 1 &&
+                  cells[c].spec.n_instances <= 256;
+    if (device_ok) return sweep_device(device, cells, n_cells, threads, out);
+  }
   // Every closed loop of every cell is independent, so schedule at (cell, qps)
   // granularity: phase 1 runs all integer points, phase 2 the tenths of each
   // cell's bracket. The per-cell result is then assembled exactly as
