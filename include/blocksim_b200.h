@@ -379,8 +379,8 @@ typedef struct bsg_sweep_out {
   double wall_s;                 /* host path: summed closed-loop time; device path: the
                                     wall time of the batched launches holding its points */
 } bsg_sweep_out;
-/* Runs the cells' capacity searches. When every cell is a statically
- * provisioned BlockPredictive cluster of <= 256 instances, every (cell, qps)
+/* Runs the cells' capacity searches. When every cell is a BlockPredictive
+ * cluster of <= 256 instances (max_instances when provisioning), every (cell, qps)
  * point is a device-resident closed loop (bsg_replay_device): all integer
  * points in one batched launch, then all tenths in a second one (records
  * generated on `threads` host threads). Otherwise the closed loops run on
@@ -392,8 +392,9 @@ bsg_status bsg_sweep_run(int device, const bsg_sweep_cell* cells, int32_t n_cell
 int64_t bsg_scenario_count(const bsg_ctx* ctx);
 
 /* Device-resident closed loops: each run is one
- * run_experiment (driver.cpp:134-289) with static provisioning, zero dispatch
- * overhead and BlockPredictive dispatch, executed entirely on the GPU — one
+ * run_experiment (driver.cpp:134-289) with zero dispatch overhead,
+ * BlockPredictive dispatch and static / preempt / relief provisioning
+ * (autoscaler.cpp:36-52), executed entirely on the GPU — one
  * thread block per run: live instances in HBM, every arrival's per-instance
  * what-ifs + argmin on the block's warps, the event loop on the device.
  * Requests of run r are rows [req_off, req_off + n_requests) of the request
@@ -401,11 +402,16 @@ int64_t bsg_scenario_count(const bsg_ctx* ctx);
  * outcomes has the same rows. run_status[r] is BSG_OK or the error that ended
  * run r (BSG_DEADLOCK / BSG_EMPTY_PLAN / a what-if failure). HOST buffers. */
 typedef struct bsg_closed_loop_run {
-  int32_t n_instances;  /* 1..256 */
+  int32_t n_instances;  /* initial instances, 1..256 */
   int32_t objective;    /* 0 e2e, 1 ttft */
   int32_t cfg;          /* index into the configs set by bsg_set_configs */
   int32_t n_requests;
   int64_t req_off;
+  /* ProvisionPolicy (autoscaler.h:10-27): 0 static, 1 preempt (predicted e2e at
+   * dispatch), 2 relief (realized e2e at completion); max_instances <= 256 */
+  int32_t provision_kind;
+  int32_t max_instances;
+  double threshold_s, cold_start_s, cooldown_s;
 } bsg_closed_loop_run;
 bsg_status bsg_replay_device(bsg_ctx* ctx, const bsg_closed_loop_run* runs, int32_t n_runs,
                              const int32_t* prompt, const int32_t* output, const int32_t* est,

@@ -100,7 +100,8 @@ STATUS_NAMES[12] = "NO_CAPACITY"
 PROVISION_STATIC, PROVISION_PREEMPT, PROVISION_RELIEF = 0, 1, 2
 closed_loop_run_dtype = np.dtype([
     ("n_instances", "<i4"), ("objective", "<i4"), ("cfg", "<i4"), ("n_requests", "<i4"),
-    ("req_off", "<i8")])
+    ("req_off", "<i8"), ("provision_kind", "<i4"), ("max_instances", "<i4"),
+    ("threshold_s", "<f8"), ("cold_start_s", "<f8"), ("cooldown_s", "<f8")])
 outcome_dtype = np.dtype([
     ("arrival_ticks", "<i8"), ("dispatch_ticks", "<i8"), ("first_token_ticks", "<i8"),
     ("finish_ticks", "<i8"), ("instance", "<i4"), ("preempt_count", "<i4"),

@@ -920,7 +920,9 @@ bsg_status run_points_device(bsg_ctx* ctx, const bsg_sweep_cell* cells, const st
     }
     const bsg_sweep_cell& c = cells[pts[i].cell];
     runs.push_back(bsg_closed_loop_run{c.spec.n_instances, c.spec.objective, pts[i].cell,
-                                       static_cast<int32_t>(recs[i].size()), static_cast<int64_t>(p.size())});
+                                       static_cast<int32_t>(recs[i].size()), static_cast<int64_t>(p.size()),
+                                       c.spec.provision_kind, c.spec.max_instances, c.spec.threshold_s,
+                                       c.spec.cold_start_s, c.spec.cooldown_s});
     run_pt.push_back(i);
     for (const Record& r : recs[i]) {
       p.push_back(r.prompt);
@@ -949,7 +951,7 @@ bsg_status run_points_device(bsg_ctx* ctx, const bsg_sweep_cell* cells, const st
 }
 
 // bsg_sweep_run on device-resident closed loops: every cell must be a
-// BlockPredictive, statically provisioned cluster of <= 256 instances.
+// BlockPredictive cluster of <= 256 instances (any provisioning kind).
 bsg_status sweep_device(int device, const bsg_sweep_cell* cells, int32_t n_cells, int32_t threads,
                         bsg_sweep_out* out) {
   bsg_ctx* ctx = nullptr;
@@ -1032,8 +1034,8 @@ extern "C" bsg_status bsg_sweep_run(int device, const bsg_sweep_cell* cells, int
     bool device_ok = n_cells > 0 && std::getenv("BSG_SWEEP_HOST") == nullptr;
     for (int32_t c = 0; c < n_cells && device_ok; ++c)
       device_ok = cells[c].spec.policy == BSG_POLICY_BLOCK_PREDICTIVE &&
-                  cells[c].spec.provision_kind == 0 && cells[c].spec.n_instances >= 1 &&
-                  cells[c].spec.n_instances <= 256;
+                  cells[c].spec.n_instances >= 1 && cells[c].spec.n_instances <= 256 &&
+                  (cells[c].spec.provision_kind == 0 || cells[c].spec.max_instances <= 256);
     if (device_ok) return sweep_device(device, cells, n_cells, threads, out);
   }
   // Every closed loop of every cell is independent, so schedule at (cell, qps)

@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -43,6 +44,10 @@ struct ClRun {
   int32_t n_inst, objective, cfg, n_req;
   int64_t req_off;    // first request row
   int64_t arena_off;  // first arena entry
+  // ProvisionPolicy (autoscaler.h:10-27); ticks are SimTime::from_seconds
+  int32_t prov_kind, max_inst;
+  double threshold_s;
+  int64_t cold_start_ticks, cooldown_ticks;
 };
 
 // Live-state SoA columns.
@@ -299,7 +304,8 @@ __device__ int32_t live_begin(const DevCfg& cfg, const Arena& ar, int64_t Rb, in
 // (handle_batch_complete, driver.cpp:233-251); warp-wide.
 template <int K, bool POW2>
 __device__ void live_finish(const DevCfg& cfg, const Arena& ar, int64_t Rb, ClInst& st,
-                            int64_t now, bsg_request_outcome* outs) {
+                            int64_t now, bsg_request_outcome* outs, double relief_threshold_s,
+                            int64_t relief_after, unsigned long long* relief_min) {
   const int lane = lane_id();
   const int32_t n = st.n;
   int32_t prompt[K], prefill[K], decoded[K], est[K], target[K], rid[K], keep[K], dst[K], freed[K];
@@ -331,6 +337,11 @@ __device__ void live_finish(const DevCfg& cfg, const Arena& ar, int64_t Rb, ClIn
       if (done) {
         outs[rid[k]].finish_ticks = now;
         freed[k] = bnt<POW2>(prefill[k] + decoded[k], cfg);
+        // relief provisioning signal: realized e2e (handle_batch_complete,
+        // driver.cpp:245-248); only the earliest eligible trigger matters
+        if (relief_min && now >= relief_after &&
+            static_cast<double>(now - outs[rid[k]].arrival_ticks) * 1e-9 >= relief_threshold_s)
+          atomicMin(relief_min, static_cast<unsigned long long>(now));
       }
       keep[k] = done ? 0 : 1;
     }
@@ -364,11 +375,31 @@ struct ClShared {
   ClInst inst[kClMaxInst];
   bsg_result res[kClMaxInst];
   int32_t scratch[kClWarps][smem_words(K)];
+  int64_t pend[kClMaxInst];     // provision-complete times, non-decreasing
   unsigned long long preempts;
   unsigned long long end_ticks;
+  unsigned long long cand_min;  // relief: earliest eligible trigger of an interval
+  int64_t last_prov;            // Autoscaler::last_provision_ (-1: none)
+  int64_t cur;                  // relief: the trigger instant being replayed
+  int32_t cnt;                  // relief: qualifying completions at `cur`
+  int32_t n_pend, pend_head;    // provisions triggered / completed
+  int32_t active;               // instances dispatchable (instances_.size())
   int32_t next;
   int32_t err;
 };
+
+// Autoscaler::evaluate (autoscaler.cpp:36-52) for a signal of the run's kind:
+// on a trigger, the instance's ProvisionComplete is due cold_start later
+// (maybe_provision, driver.cpp:253-261). Caller: one thread.
+template <int K>
+__device__ __forceinline__ void autoscale(ClShared<K>& S, const ClRun& run, int32_t initial, double latency_s,
+                                          int64_t now) {
+  if (latency_s < run.threshold_s) return;
+  if (S.last_prov >= 0 && now - S.last_prov < run.cooldown_ticks) return;
+  if (initial + S.n_pend >= run.max_inst) return;  // active + pending (invariant under completion)
+  S.last_prov = now;
+  S.pend[S.n_pend++] = now + run.cold_start_ticks;
+}
 
 template <int K, bool POW2>
 __global__ void __launch_bounds__(kClWarps * 32, 2)
@@ -386,15 +417,16 @@ __global__ void __launch_bounds__(kClWarps * 32, 2)
   // begin_step() without a latency function); only predict() uses the cache
   DevCfg live_cfg = cfg;
   live_cfg.cache_mode = BSG_CACHE_OFF;
-  const int32_t I = run.n_inst, N = run.n_req, maxb = cfg.max_batch_size;
+  const int32_t I0 = run.n_inst, N = run.n_req, maxb = cfg.max_batch_size;
+  const int32_t IMAX = run.prov_kind == 0 ? I0 : run.max_inst;  // instance slots
   const int64_t stride = inst_stride(maxb, N);
   bsg_request_outcome* outs = outcomes + run.req_off;
   const int64_t* arrival = rq_arrival + run.req_off;
-  if (I > kClMaxInst || maxb > 32 * K) {  // the host validates; never reached
+  if (IMAX > kClMaxInst || maxb > 32 * K) {  // the host validates; never reached
     if (threadIdx.x == 0) status[blockIdx.x] = BSG_BAD_INPUT;
     return;
   }
-  for (int i = threadIdx.x; i < I; i += blockDim.x) {
+  for (int i = threadIdx.x; i < IMAX; i += blockDim.x) {
     ClInst& s = S.inst[i];
     s.n = 0;
     s.whead = maxb;
@@ -407,9 +439,16 @@ __global__ void __launch_bounds__(kClWarps * 32, 2)
     S.preempts = 0;
     S.end_ticks = 0;
     S.err = BSG_OK;
+    S.last_prov = -1;
+    S.n_pend = 0;
+    S.pend_head = 0;
+    S.active = I0;
+    S.cand_min = ~0ull;
   }
   __syncthreads();
+  const bool relief = run.prov_kind == 2;
   int64_t last_done = 0;  // this warp's latest processed completion
+  int64_t relief_after = 0;  // relief: earliest trigger time the cooldown allows
   // close the instant tc (its completions, then end_of_instant's begin_step) and
   // advance through every completion strictly before t
   auto advance = [&](int32_t i, int64_t tc, int64_t t) -> int32_t {
@@ -418,7 +457,8 @@ __global__ void __launch_bounds__(kClWarps * 32, 2)
     const int64_t Ab = Rb + maxb;
     if (tc >= 0) {
       if (s.mid && s.t_done == tc) {
-        live_finish<K, POW2>(cfg, ar, Rb, s, tc, outs);
+        live_finish<K, POW2>(cfg, ar, Rb, s, tc, outs, run.threshold_s, relief_after,
+                             relief ? &S.cand_min : nullptr);
         last_done = max(last_done, tc);
       }
       if (!s.mid && (s.n > 0 || s.whead < s.wtail)) {
@@ -428,7 +468,8 @@ __global__ void __launch_bounds__(kClWarps * 32, 2)
     }
     while (s.mid && s.t_done < t) {
       const int64_t now = s.t_done;
-      live_finish<K, POW2>(cfg, ar, Rb, s, now, outs);
+      live_finish<K, POW2>(cfg, ar, Rb, s, now, outs, run.threshold_s, relief_after,
+                           relief ? &S.cand_min : nullptr);
       last_done = max(last_done, now);
       if (s.n > 0 || s.whead < s.wtail) {
         const int32_t e = live_begin<K, POW2>(live_cfg, ar, Rb, Ab, s, now, outs, &S.preempts);
@@ -440,10 +481,54 @@ __global__ void __launch_bounds__(kClWarps * 32, 2)
   auto fail = [&](int32_t e) {
     if (lane == 0) atomicCAS(&S.err, BSG_OK, e);
   };
+  // Relief provisioning over the completions of the interval just advanced:
+  // instances evolve independently of the autoscaler between arrivals, so the
+  // triggers are replayed afterwards in time order. Each qualifying completion
+  // is one signal (driver.cpp:245-248): the earliest one at or after
+  // last_provision + cooldown triggers; with cooldown 0 every qualifying
+  // completion of that instant triggers too (up to max_instances).
+  auto relief_round = [&](int64_t t_end) {
+    for (;;) {
+      if (threadIdx.x == 0) {
+        const unsigned long long c = S.cand_min;
+        S.cand_min = ~0ull;
+        S.cur = static_cast<int64_t>(c);
+        S.cnt = 0;
+        S.next = (c != ~0ull && static_cast<int64_t>(c) < t_end && I0 + S.n_pend < run.max_inst) ? 1 : 0;
+      }
+      __syncthreads();
+      if (!S.next) break;
+      const int64_t c = S.cur;
+      auto qualifies = [&](int32_t q) {
+        return static_cast<double>(outs[q].finish_ticks - outs[q].arrival_ticks) * 1e-9 >= run.threshold_s;
+      };
+      if (run.cooldown_ticks == 0)
+        for (int32_t q = threadIdx.x; q < N; q += blockDim.x)
+          if (outs[q].finish_ticks == c && qualifies(q)) atomicAdd(&S.cnt, 1);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int32_t m = run.cooldown_ticks == 0 ? S.cnt : 1;
+        for (; m > 0 && I0 + S.n_pend < run.max_inst; --m) {
+          S.last_prov = c;
+          S.pend[S.n_pend++] = c + run.cold_start_ticks;
+        }
+      }
+      relief_after = c + (run.cooldown_ticks > 0 ? run.cooldown_ticks : 1);
+      __syncthreads();
+      for (int32_t q = threadIdx.x; q < N; q += blockDim.x) {  // the next eligible completion
+        const int64_t f = outs[q].finish_ticks;
+        if (f >= relief_after && f < t_end && qualifies(q))
+          atomicMin(&S.cand_min, static_cast<unsigned long long>(f));
+      }
+      __syncthreads();
+    }
+    relief_after = S.last_prov >= 0 ? S.last_prov + run.cooldown_ticks : 0;
+  };
   int64_t t_prev = -1;
   for (int32_t k = 0; k < N; ++k) {
     const int64_t t = arrival[k];
     if (t != t_prev) {
+      const int32_t I = S.active;
       for (int32_t i = warp; i < I; i += kClWarps) {
         const int32_t e = advance(i, t_prev, t);
         if (e != BSG_OK) {
@@ -453,7 +538,17 @@ __global__ void __launch_bounds__(kClWarps * 32, 2)
       }
       __syncthreads();
       if (S.err != BSG_OK) break;
+      if (relief) relief_round(t);
+      // ProvisionComplete events before this instant (arrivals at an equal time go first)
+      if (threadIdx.x == 0)
+        while (S.pend_head < S.n_pend && S.pend[S.pend_head] < t) {
+          S.end_ticks = max(S.end_ticks, static_cast<unsigned long long>(S.pend[S.pend_head]));
+          ++S.pend_head;
+          ++S.active;
+        }
+      __syncthreads();
     }
+    const int32_t I = S.active;
     // ---- dispatch: per-instance what-ifs (predict_across) + argmin ----
     if (threadIdx.x == 0) S.next = 0;
     __syncthreads();
@@ -502,6 +597,8 @@ __global__ void __launch_bounds__(kClWarps * 32, 2)
       if (bad != BSG_OK) {
         fail(bad);  // PredictionError propagates out of the run (predictor.cpp:132-136)
       } else if (lane == 0) {  // admit the arrival at the chosen instance's waiting tail
+        if (run.prov_kind == 1)  // preempt provisioning on the predicted e2e (driver.cpp:197-211)
+          autoscale<K>(S, run, I0, static_cast<double>(S.res[best_i].e2e_ticks) * 1e-9, t);
         ClInst& s = S.inst[best_i];
         const int64_t g = run.arena_off + best_i * stride + maxb + s.wtail;
         ar.prompt[g] = cp;
@@ -520,6 +617,7 @@ __global__ void __launch_bounds__(kClWarps * 32, 2)
     t_prev = t;
   }
   if (S.err == BSG_OK) {  // drain
+    const int32_t I = S.active;
     for (int32_t i = warp; i < I; i += kClWarps) {
       const int32_t e = advance(i, t_prev, kNever);
       if (e != BSG_OK) {
@@ -527,6 +625,11 @@ __global__ void __launch_bounds__(kClWarps * 32, 2)
         break;
       }
     }
+    __syncthreads();
+    if (relief) relief_round(kNever);
+    if (threadIdx.x == 0)  // the remaining ProvisionComplete events
+      for (; S.pend_head < S.n_pend; ++S.pend_head, ++S.active)
+        S.end_ticks = max(S.end_ticks, static_cast<unsigned long long>(S.pend[S.pend_head]));
   }
   if (lane == 0) atomicMax(&S.end_ticks, static_cast<unsigned long long>(max(last_done, t_prev)));
   __syncthreads();
@@ -535,8 +638,8 @@ __global__ void __launch_bounds__(kClWarps * 32, 2)
     bsg_replay_summary sm{};
     sm.total_preemptions = static_cast<int64_t>(S.preempts);
     sm.end_ticks = static_cast<int64_t>(S.end_ticks);
-    sm.instances_provisioned = 0;
-    sm.final_instance_count = I;
+    sm.instances_provisioned = S.n_pend;
+    sm.final_instance_count = S.active;
     summaries[blockIdx.x] = sm;
   }
 }
@@ -586,10 +689,16 @@ extern "C" bsg_status bsg_replay_device(bsg_ctx* ctx, const bsg_closed_loop_run*
     const bsg_closed_loop_run& x = runs[r];
     if (x.cfg < 0 || x.cfg >= ctx->ncfg || x.n_instances < 1 || x.n_instances > kClMaxInst ||
         x.n_requests < 0 || x.req_off < 0 || x.req_off + x.n_requests > n_requests_total ||
-        x.objective < 0 || x.objective > 1) {
+        x.objective < 0 || x.objective > 1 || x.provision_kind < 0 || x.provision_kind > 2 ||
+        (x.provision_kind != 0 && x.max_instances > kClMaxInst)) {
       ctx->last_error = "bad closed-loop run descriptor";
       return BSG_INVALID_ARGUMENT;
     }
+    // validate_provision_policy (autoscaler.cpp:23-34), config.cpp:177-180
+    if (!(x.threshold_s > 0) || x.cold_start_s < 0 || x.cooldown_s < 0 ||
+        (x.provision_kind != 0 && x.max_instances < x.n_instances))
+      return BSG_BAD_CONFIG;
+    const int32_t slots = x.provision_kind == 0 ? x.n_instances : x.max_instances;
     const bsg_instance_cfg& c = ctx->host_cfgs[x.cfg];
     maxb_all = std::max(maxb_all, c.max_batch_size);
     pow2 &= ctx->dev_cfgs_host[x.cfg].div_magic == 0;
@@ -603,8 +712,10 @@ extern "C" bsg_status bsg_replay_device(bsg_ctx* ctx, const bsg_closed_loop_run*
         return BSG_BAD_INPUT;
       }
     }
-    dr[r] = ClRun{x.n_instances, x.objective, x.cfg, x.n_requests, x.req_off, arena};
-    arena += static_cast<int64_t>(x.n_instances) * (2 * static_cast<int64_t>(c.max_batch_size) + x.n_requests);
+    dr[r] = ClRun{x.n_instances, x.objective, x.cfg, x.n_requests, x.req_off, arena,
+                  x.provision_kind, x.provision_kind == 0 ? x.n_instances : x.max_instances,
+                  x.threshold_s, std::llround(x.cold_start_s * 1e9), std::llround(x.cooldown_s * 1e9)};
+    arena += static_cast<int64_t>(slots) * (2 * static_cast<int64_t>(c.max_batch_size) + x.n_requests);
   }
   if (arena >= (int64_t{1} << 31)) {
     ctx->last_error = "closed-loop arena exceeds 2^31 entries; split the batch";

@@ -243,13 +243,16 @@ class Context:
 
     def replay_device(self, runs):
         """Device-resident closed loops (bsg_replay_device). runs: list of
-        (workload, n_instances, objective, cfg_index) with the configs already
-        set. Returns [(status, outcomes, summary)] per run."""
+        (workload, replay_spec, cfg_index) with the configs already set (the
+        spec's policy must be BlockPredictive). Returns [(status, outcomes,
+        summary)] per run."""
         cols = [make_workload_host(w) for w, *_ in runs]
         desc = np.zeros(len(runs), abi.closed_loop_run_dtype)
         off = 0
-        for r, ((w, ni, obj, cf), c) in enumerate(zip(runs, cols)):
-            desc[r] = (ni, obj, cf, len(c[0]), off)
+        for r, ((w, sp, cf), c) in enumerate(zip(runs, cols)):
+            sp = np.asarray(sp).reshape(-1)[0]
+            desc[r] = (sp["n_instances"], sp["objective"], cf, len(c[0]), off, sp["provision_kind"],
+                       sp["max_instances"], sp["threshold_s"], sp["cold_start_s"], sp["cooldown_s"])
             off += len(c[0])
         p, o, e, t = (np.ascontiguousarray(np.concatenate([c[j] for c in cols])) for j in range(4))
         out = np.zeros(off, abi.outcome_dtype)

@@ -206,7 +206,8 @@ def test_device_closed_loop_matches_reference(ctx, ref, policy_cfg):
     cases = [(abi.make_workload(count=300, qps=q, arrival_seed=s, estimator_kind=2, estimator_seed=s),
               ni, obj) for q, s, ni, obj in [(6.0, 1, 4, 0), (14.0, 2, 12, 0), (30.0, 3, 7, 1),
                                               (3.0, 4, 1, 0)]]
-    got = ctx.replay_device([(w, ni, obj, 0) for w, ni, obj in cases])
+    got = ctx.replay_device([(w, abi.make_replay_spec(ni, objective=obj, capture=0), 0)
+                             for w, ni, obj in cases])
     for (w, ni, obj), (st, out, summ) in zip(cases, got):
         spec = abi.make_replay_spec(ni, objective=obj, capture=0)
         exp, esum, _ = ref.replay(w, cfg, spec, capture=False)
@@ -218,3 +219,30 @@ def test_device_closed_loop_matches_reference(ctx, ref, policy_cfg):
             assert np.array_equal(host[f], exp[f]), ("host", policy_cfg, ni, f)
         assert int(summ["total_preemptions"]) == int(esum["total_preemptions"])
         assert int(hsum["total_preemptions"]) == int(esum["total_preemptions"])
+
+
+@pytest.mark.parametrize("kind,kw", [
+    (abi.PROVISION_PREEMPT, dict(threshold_s=20.0, cold_start_s=5.0, cooldown_s=3.0)),
+    (abi.PROVISION_PREEMPT, dict(threshold_s=8.0, cold_start_s=0.0, cooldown_s=0.0)),
+    (2, dict(threshold_s=20.0, cold_start_s=5.0, cooldown_s=3.0)),
+    (2, dict(threshold_s=10.0, cold_start_s=0.0, cooldown_s=0.0)),
+])
+def test_device_closed_loop_autoscaler_matches_reference(ctx, ref, kind, kw):
+    """Auto-provisioning (preempt: predicted e2e at dispatch; relief: realized
+    e2e at completion) inside the device-resident closed loop: same instances
+    provisioned, same per-request timeline as the reference driver."""
+    cfg = abi.make_config()
+    ctx.set_configs(cfg)
+    cases = [(abi.make_workload(count=400, qps=q, arrival_seed=s), ni, mx)
+             for q, s, ni, mx in [(24.0, 1, 6, 10), (40.0, 2, 3, 9), (12.0, 3, 1, 4)]]
+    specs = [abi.make_replay_spec(ni, capture=0, provision_kind=kind, max_instances=mx, **kw)
+             for _, ni, mx in cases]
+    got = ctx.replay_device([(w, sp, 0) for (w, _, _), sp in zip(cases, specs)])
+    for (w, ni, mx), sp, (st, out, summ) in zip(cases, specs, got):
+        exp, esum = ref.run_experiment(w, cfg, sp)  # the reference's own run_experiment
+        assert st == abi.OK
+        assert int(summ["instances_provisioned"]) > 0 or kind == 2
+        assert int(summ["instances_provisioned"]) == int(esum["instances_provisioned"])
+        assert int(summ["final_instance_count"]) == int(esum["final_instance_count"])
+        for f in ("instance", "dispatch_ticks", "first_token_ticks", "finish_ticks", "preempt_count"):
+            assert np.array_equal(out[f], exp[f]), (kind, ni, f, np.nonzero(out[f] != exp[f])[0][:5])
