@@ -34,7 +34,13 @@ def load_profiles(path: str = PROFILES_JSON) -> dict[str, np.ndarray]:
 
 def make_cells(instances, profiles: dict, request_cap: int, qps_min: int = 1, qps_max: int = 64,
                slo: float = 3.0, seed: int = 1, count: int | None = None,
-               policy: int = abi.POLICY_BLOCK_PREDICTIVE) -> tuple[np.ndarray, list]:
+               policy: int = abi.POLICY_BLOCK_PREDICTIVE, provision: dict | None = None
+               ) -> tuple[np.ndarray, list]:
+    """Cells of the grid. provision: ProvisionPolicy overrides for auto-provisioned
+    cells, e.g. dict(provision_kind=abi.PROVISION_PREEMPT, extra_instances=4,
+    threshold_s=70, cold_start_s=30, cooldown_s=15) (max_instances = n + extra)."""
+    provision = dict(provision or {})
+    extra = provision.pop("extra_instances", 0)
     cells = np.zeros(len(instances) * len(profiles), abi.sweep_cell_dtype)
     keys = []
     i = 0
@@ -43,7 +49,9 @@ def make_cells(instances, profiles: dict, request_cap: int, qps_min: int = 1, qp
             c = cells[i]
             c["workload"] = abi.make_workload(count=count or request_cap, request_cap=request_cap)[0]
             c["cfg"] = cfg[0]
-            c["spec"] = abi.make_replay_spec(n, policy=policy, capture=0)[0]
+            c["spec"] = abi.make_replay_spec(n, policy=policy, capture=0,
+                                             max_instances=(n + extra) if provision else None,
+                                             **provision)[0]
             c["seed"], c["qps_min"], c["qps_max"], c["slo_p99_ttft_s"] = seed, qps_min, qps_max, slo
             keys.append((pname, int(n)))
             i += 1
@@ -62,6 +70,10 @@ def main(argv=None):
     ap.add_argument("--qps-max", type=int, default=64)
     ap.add_argument("--threads", type=int, default=16)
     ap.add_argument("--slo", type=float, default=3.0)
+    ap.add_argument("--provision", choices=["static", "preempt", "relief"], default="static",
+                    help="auto-provisioning policy of every cell (autoscaler.cpp:36-52)")
+    ap.add_argument("--extra-instances", type=int, default=4,
+                    help="max_instances = instances + this, when provisioning")
     args = ap.parse_args(argv)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -71,8 +83,12 @@ def main(argv=None):
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    prov = None if args.provision == "static" else dict(
+        provision_kind={"preempt": abi.PROVISION_PREEMPT, "relief": abi.PROVISION_RELIEF}[args.provision],
+        extra_instances=args.extra_instances)
     cells, keys = make_cells([int(x) for x in args.instances.split(",")], load_profiles(),
-                             args.request_cap, qps_max=args.qps_max, slo=args.slo)
+                             args.request_cap, qps_max=args.qps_max, slo=args.slo, provision=prov)
+    native.sweep_run(local, cells[:1], threads=args.threads)  # warm-up: context + module load
     assign = shard.assign_cells_lpt([cell_cost(c) for c in cells], world)
     mine = sorted(assign[rank], key=lambda c: -cell_cost(cells[c]))
     t0 = time.perf_counter()
@@ -98,6 +114,7 @@ def main(argv=None):
             "config": {"instances": args.instances, "profiles": list(load_profiles()),
                        "qps": f"1..{args.qps_max} + tenths", "request_cap": args.request_cap,
                        "slo_p99_ttft_s": args.slo, "policy": "block_predictive",
+                       "provision": args.provision,
                        "threads_per_gpu": args.threads},
             "capacity_qps": table}
     print(json.dumps(line), flush=True)

@@ -171,13 +171,25 @@ def test_capacity_search_matches_reference(ctx, ref):
     assert 1 < got["capacity_qps"] < 16  # a real bracket, with tenths tested
 
 
-def test_sweep_cells_match_reference_capacity_search(ref):
-    """bsg_sweep_run (concurrent capacity searches, one context per host
-    thread) gives, per cell, exactly the reference's capacity_search result
-    for that cell's profile and instance count."""
+@pytest.mark.parametrize("path,provision", [
+    ("device", None),
+    ("device", dict(provision_kind=abi.PROVISION_PREEMPT, extra_instances=2, threshold_s=4.0,
+                    cold_start_s=2.0, cooldown_s=1.0)),
+    ("device", dict(provision_kind=abi.PROVISION_RELIEF, extra_instances=2, threshold_s=6.0,
+                    cold_start_s=2.0, cooldown_s=1.0)),
+    ("host", None),
+])
+def test_sweep_cells_match_reference_capacity_search(ref, monkeypatch, path, provision):
+    """bsg_sweep_run — device-resident closed loops (batched launches), or the
+    host-driven loops (BSG_SWEEP_HOST) — gives, per cell, exactly the
+    reference's capacity_search result for that cell's profile, instance count
+    and auto-provisioning policy."""
     from paper_2508_03611_b200 import native, sweep
+    if path == "host":
+        monkeypatch.setenv("BSG_SWEEP_HOST", "1")
     profiles = sweep.load_profiles()
-    cells, keys = sweep.make_cells([1, 2], profiles, request_cap=150, qps_max=12, slo=1.0)
+    cells, keys = sweep.make_cells([1, 2], profiles, request_cap=150, qps_max=12, slo=1.0,
+                                   provision=provision)
     out = native.sweep_run(0, cells, threads=4)
     for c, o in zip(cells, out):
         w = np.array([c["workload"]], abi.workload_dtype)
