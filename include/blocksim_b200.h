@@ -419,6 +419,38 @@ bsg_status bsg_replay_device(bsg_ctx* ctx, const bsg_closed_loop_run* runs, int3
                              bsg_request_outcome* outcomes, bsg_replay_summary* summaries,
                              int32_t* run_status);
 
+/* Fleet: a persistent device mirror of n_instances live serving instances
+ * (incremental snapshot mirrors). Every instance's running
+ * and waiting lists stay resident in HBM (K5's arena); bsg_fleet_dispatch is
+ * one launch, one warp per instance: the warp advances its instance to
+ * now_ticks (completions strictly before it, after closing the previous
+ * dispatch instant — driver.cpp:233-289 semantics), runs predict() on the
+ * updated state in place, and the last warp takes the BlockPredictive argmin
+ * (scheduler.cpp:138-150) and admits the request; `output` is the request's
+ * true length, which drives the simulated instance. lengths/n_samples: the
+ * request's Monte-Carlo lengths (bsg_mc_lengths; score = sum of per-sample
+ * e2e ticks) or NULL (score = the estimate's e2e / ttft ticks). Arrivals must
+ * be non-decreasing in time. Driving a fleet with a workload's arrivals gives
+ * exactly bsg_replay_device's outcomes. */
+typedef struct bsg_fleet bsg_fleet;
+bsg_status bsg_fleet_create(bsg_ctx* ctx, int32_t cfg, int32_t n_instances, int32_t max_requests,
+                            bsg_fleet** out);
+void bsg_fleet_destroy(bsg_fleet* f);
+bsg_status bsg_fleet_dispatch(bsg_fleet* f, int64_t now_ticks, int32_t prompt, int32_t est,
+                              int32_t output, const int32_t* lengths, int32_t n_samples,
+                              int32_t objective, int32_t* chosen, int64_t* scores);
+/* The mirror's Status API (Instance::snapshot, backend.cpp:351-373) as of the
+ * last dispatch: run_n running entries (admission order) then wait_n waiting
+ * entries (head first) into the caller's columns (any may be NULL); when
+ * run_n + wait_n > cap only the sizes are written. */
+bsg_status bsg_fleet_snapshot(bsg_fleet* f, int32_t instance, int32_t* run_n, int32_t* wait_n,
+                              int32_t* prompt, int32_t* est, int32_t* prefill, int32_t* decoded,
+                              int32_t cap);
+/* Runs every remaining step; copies the outcomes of the admitted requests (in
+ * admission order) and the run summary. */
+bsg_status bsg_fleet_finish(bsg_fleet* f, bsg_request_outcome* outcomes, int32_t* n_requests,
+                            bsg_replay_summary* summary);
+
 /* Synthetic trace + estimates + Poisson arrival ticks (no GPU needed). */
 bsg_status bsg_make_workload(const bsg_workload* w, int32_t* prompt, int32_t* output,
                              int32_t* est, int64_t* arrival_ticks);

@@ -273,7 +273,7 @@ __device__ int32_t live_begin(const DevCfg& cfg, const Arena& ar, int64_t Rb, in
       outs[rid[k]].preempt_count += 1;
     }
   }
-  if (v > 0 && lane == 0) atomicAdd(preempts, static_cast<unsigned long long>(v));
+  if (v > 0 && lane == 0 && preempts) atomicAdd(preempts, static_cast<unsigned long long>(v));
   // price the surviving plan (to_batch_plan 194-209, batch_latency 10-14)
   bool ds[K], ps[K];
   int32_t ctx[K], pt[K];
@@ -288,14 +288,14 @@ __device__ int32_t live_begin(const DevCfg& cfg, const Arena& ar, int64_t Rb, in
   }
   const int32_t n_dec = count<K>(ds);
   const int64_t dur = step_ticks(cfg, warp_sum<K>(pt), n_dec, warp_sum<K>(ctx));
+  // every lane writes the (warp-uniform) new state: no lane ever reads a value
+  // another lane stored, so the state may live in registers, shared or global
   __syncwarp();
-  if (lane == 0) {
-    st.n = e_star;
-    st.whead = new_whead;
-    st.free_blocks = free_blocks;
-    st.mid = 1;
-    st.t_done = now + dur;
-  }
+  st.n = e_star;
+  st.whead = new_whead;
+  st.free_blocks = free_blocks;
+  st.mid = 1;
+  st.t_done = now + dur;
   __syncwarp();
   return BSG_OK;
 }
@@ -362,11 +362,11 @@ __device__ void live_finish(const DevCfg& cfg, const Arena& ar, int64_t Rb, ClIn
     }
   }
   __syncwarp();
-  if (lane == 0) {
-    st.n = kept;
-    st.free_blocks += rel;
-    st.mid = 0;
-  }
+  const int32_t nf = st.free_blocks + rel;  // warp-uniform state update, every lane
+  __syncwarp();
+  st.n = kept;
+  st.free_blocks = nf;
+  st.mid = 0;
   __syncwarp();
 }
 
@@ -644,6 +644,161 @@ __global__ void __launch_bounds__(kClWarps * 32, 2)
   }
 }
 
+// ---- fleet: the live instances as a persistent device mirror ----------------
+// SURVEY §8(f) row 2. A fleet keeps K5's arena (every instance's running and
+// waiting lists) resident in HBM across calls; each bsg_fleet_dispatch is ONE
+// launch with one warp per instance: the warp advances its instance to the
+// arrival instant (the snapshot is updated in place — nothing is packed or
+// copied), runs the what-if on it, and the last warp to finish takes the
+// argmin and admits the request. The host sends only the candidate (and its
+// Monte-Carlo lengths) and reads back the decision.
+struct FleetDev {
+  int64_t t_prev;        // last dispatch instant (-1: none)
+  int32_t n_req;         // requests admitted so far
+  int32_t done;          // warps finished in the current call
+  int32_t chosen;
+  int32_t status;
+  int64_t end_ticks;
+};
+
+constexpr int kFleetWarps = 4;
+
+template <int K, bool POW2, bool MC>
+__global__ void __launch_bounds__(kFleetWarps * 32)
+    fleet_dispatch_kernel(const DevCfg* __restrict__ cfgs, int32_t cfg_index, int32_t n_inst, int32_t n_cap,
+                          Arena ar, ClInst* __restrict__ inst, FleetDev* __restrict__ fd,
+                          bsg_request_outcome* __restrict__ outs, int64_t now, int32_t prompt,
+                          int32_t est, int32_t output, const int32_t* __restrict__ sorted_len,
+                          int32_t S, int32_t objective, bsg_result* __restrict__ res,
+                          int64_t* __restrict__ scores, int32_t drain) {
+  extern __shared__ __align__(16) int32_t fsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t i = blockIdx.x * kFleetWarps + warp;
+  if (i >= n_inst) return;
+  int32_t* smem = fsm + warp * (smem_words(K) + S);
+  int32_t* len = smem + smem_words(K);
+  const DevCfg cfg = cfgs[cfg_index];
+  DevCfg live_cfg = cfg;
+  live_cfg.cache_mode = BSG_CACHE_OFF;  // live steps use batch_latency itself
+  const int32_t maxb = cfg.max_batch_size;
+  const int64_t stride = inst_stride(maxb, n_cap);
+  const int64_t Rb = static_cast<int64_t>(i) * stride, Ab = Rb + maxb;
+  ClInst s = inst[i];  // warp-uniform working copy; written back before the hand-off
+  const int64_t tc = __ldcg(&fd->t_prev);
+  int32_t err = BSG_OK;
+  int64_t last_done = 0;
+  // close the previous instant, then every completion strictly before `now`
+  if (tc >= 0 && tc != now) {
+    if (s.mid && s.t_done == tc) {
+      live_finish<K, POW2>(cfg, ar, Rb, s, tc, outs, 0.0, 0, nullptr);
+      last_done = tc;
+    }
+    if (!s.mid && (s.n > 0 || s.whead < s.wtail))
+      err = live_begin<K, POW2>(live_cfg, ar, Rb, Ab, s, tc, outs, nullptr);
+  }
+  while (err == BSG_OK && s.mid && s.t_done < now) {
+    const int64_t t = s.t_done;
+    live_finish<K, POW2>(cfg, ar, Rb, s, t, outs, 0.0, 0, nullptr);
+    last_done = t;
+    if (s.n > 0 || s.whead < s.wtail) err = live_begin<K, POW2>(live_cfg, ar, Rb, Ab, s, t, outs, nullptr);
+  }
+  if (last_done > 0 && lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(&fd->end_ticks),
+                                            static_cast<unsigned long long>(last_done));
+  if (!drain && err == BSG_OK) {
+    // the what-if on the live state, in place (predict(), predictor.cpp:76-137)
+    bsg_scenario sc;
+    sc.run_off = static_cast<int32_t>(Rb);
+    sc.run_n = s.n;
+    sc.wait_off = static_cast<int32_t>(Ab + s.whead);
+    sc.wait_n = s.wtail - s.whead;
+    sc.cand_prompt = prompt;
+    sc.cand_est = est;
+    sc.cfg = cfg_index;
+    sc.reserved = 0;
+    if constexpr (MC) {
+      for (int32_t j = lane; j < S; j += 32) len[j] = sorted_len[j];
+      __syncwarp();
+      simulate_scenario<K, false, true, POW2, false>(cfg, ar.prompt, ar.est, ar.prefill, ar.decoded, sc,
+                                                    smem, &res[i], TraceSink{nullptr, 0},
+                                                    McArgs{len, S, nullptr, &scores[i], objective});
+    } else {
+      simulate_scenario<K, false, false, POW2, false>(cfg, ar.prompt, ar.est, ar.prefill, ar.decoded, sc,
+                                                     smem, &res[i], TraceSink{nullptr, 0});
+      __syncwarp();
+      if (lane == 0) {
+        const bsg_result r = res[i];
+        scores[i] = r.status != BSG_OK ? INT64_MAX : (objective == 1 ? r.ttft_ticks : r.e2e_ticks);
+      }
+    }
+  } else if (lane == 0) {
+    bsg_result r{};
+    r.status = err;
+    res[i] = r;
+    scores[i] = INT64_MAX;
+  }
+  if (lane == 0) inst[i] = s;
+  // the last warp to finish takes the argmin (scheduler.cpp:138-150) and admits
+  __threadfence();
+  int32_t prev = 0;
+  if (lane == 0) prev = atomicAdd(&fd->done, 1);
+  prev = __shfl_sync(kFull, prev, 0);
+  if (prev != n_inst - 1) return;
+  __threadfence();
+  int64_t best_v = INT64_MAX;
+  int32_t best_i = INT32_MAX, bad = BSG_OK;
+  for (int32_t q = lane; q < n_inst; q += 32) {
+    const int32_t stq = __ldcg(&res[q].status);
+    if (stq != BSG_OK && bad == BSG_OK) bad = stq;
+    const int64_t v = __ldcg(&scores[q]);
+    if (v < best_v || (v == best_v && q < best_i)) {
+      best_v = v;
+      best_i = q;
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const int64_t ov = __shfl_xor_sync(kFull, best_v, d);
+    const int32_t oi = __shfl_xor_sync(kFull, best_i, d);
+    if (ov < best_v || (ov == best_v && oi < best_i)) {
+      best_v = ov;
+      best_i = oi;
+    }
+  }
+  bad = static_cast<int32_t>(__reduce_max_sync(kFull, static_cast<uint32_t>(bad)));
+  if (lane != 0) return;
+  fd->done = 0;
+  if (drain) {
+    fd->status = bad;
+    return;
+  }
+  fd->t_prev = now;
+  if (bad != BSG_OK || fd->n_req >= n_cap) {
+    fd->status = bad != BSG_OK ? bad : BSG_INVALID_ARGUMENT;
+    fd->chosen = -1;
+    return;
+  }
+  ClInst& c = inst[best_i];
+  const int32_t k = fd->n_req++;
+  const int64_t g = static_cast<int64_t>(best_i) * stride + maxb + c.wtail;
+  ar.prompt[g] = prompt;
+  ar.est[g] = est;
+  ar.prefill[g] = 0;
+  ar.decoded[g] = 0;
+  ar.target[g] = output;
+  ar.rid[g] = k;
+  c.wtail += 1;
+  bsg_request_outcome o;
+  o.arrival_ticks = now;
+  o.dispatch_ticks = now;
+  o.first_token_ticks = -1;
+  o.finish_ticks = -1;
+  o.instance = best_i;
+  o.preempt_count = 0;
+  outs[k] = o;
+  fd->chosen = best_i;
+  fd->status = BSG_OK;
+}
+
 }  // namespace bsg
 
 using namespace bsg;
@@ -793,4 +948,233 @@ extern "C" bsg_status bsg_replay_device(bsg_ctx* ctx, const bsg_closed_loop_run*
     ctx->scenarios += whatifs;
   }
   return st;
+}
+
+// ---- fleet host side ------------------------------------------------------------
+struct bsg_fleet {
+  bsg_ctx* ctx;
+  int32_t cfg, n_inst, n_cap, k;
+  bool pow2;
+  char* base = nullptr;  // device allocation
+  Arena ar{};
+  ClInst* inst = nullptr;
+  FleetDev* fd = nullptr;
+  bsg_request_outcome* outs = nullptr;
+  bsg_result* res = nullptr;
+  int64_t* scores = nullptr;
+  int32_t* lens = nullptr;  // sorted MC lengths (device)
+  void* pinned = nullptr;   // host staging: lengths in, (chosen, status) + scores out
+  int64_t last_now = -1;
+};
+
+namespace {
+
+template <int K, bool POW2, bool MC>
+cudaError_t launch_fleet(bsg_fleet* f, int64_t now, int32_t prompt, int32_t est, int32_t output,
+                         int32_t S, int32_t objective, int32_t drain) {
+  const size_t sm = static_cast<size_t>(kFleetWarps) * (smem_words(K) + S) * 4;
+  if (sm > 48 * 1024)
+    cudaFuncSetAttribute(fleet_dispatch_kernel<K, POW2, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sm));
+  const int blocks = (f->n_inst + kFleetWarps - 1) / kFleetWarps;
+  fleet_dispatch_kernel<K, POW2, MC><<<blocks, kFleetWarps * 32, sm, f->ctx->stream>>>(
+      static_cast<const DevCfg*>(f->ctx->cfgs.p), f->cfg, f->n_inst, f->n_cap, f->ar, f->inst, f->fd,
+      f->outs, now, prompt, est, output, f->lens, S, objective, f->res, f->scores, drain);
+  f->ctx->launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fleet_any(bsg_fleet* f, int64_t now, int32_t prompt, int32_t est, int32_t output,
+                             int32_t S, int32_t objective, int32_t drain, bool mc) {
+#define BSG_FLEET_CASE(KK)                                                                           \
+  case KK:                                                                                           \
+    if (mc) return f->pow2 ? launch_fleet<KK, true, true>(f, now, prompt, est, output, S, objective, drain)  \
+                           : launch_fleet<KK, false, true>(f, now, prompt, est, output, S, objective, drain); \
+    return f->pow2 ? launch_fleet<KK, true, false>(f, now, prompt, est, output, S, objective, drain)          \
+                   : launch_fleet<KK, false, false>(f, now, prompt, est, output, S, objective, drain);
+  switch (f->k) {
+    BSG_FLEET_CASE(1)
+    BSG_FLEET_CASE(2)
+    BSG_FLEET_CASE(4)
+    default:
+      BSG_FLEET_CASE(8)
+  }
+#undef BSG_FLEET_CASE
+}
+
+}  // namespace
+
+extern "C" bsg_status bsg_fleet_create(bsg_ctx* ctx, int32_t cfg, int32_t n_instances,
+                                       int32_t max_requests, bsg_fleet** out) {
+  if (!ctx || !out || n_instances < 1 || max_requests < 1) return BSG_INVALID_ARGUMENT;
+  *out = nullptr;
+  if (cfg < 0 || cfg >= ctx->ncfg) return BSG_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaSetDevice(ctx->device);
+  const bsg_instance_cfg& c = ctx->host_cfgs[cfg];
+  int k = 1;
+  while (32 * k < c.max_batch_size) k *= 2;
+  if (k > 8) return BSG_BAD_INPUT;
+  const int64_t entries = static_cast<int64_t>(n_instances) * (2 * static_cast<int64_t>(c.max_batch_size) + max_requests);
+  if (entries >= (int64_t{1} << 31)) return BSG_BAD_INPUT;
+  auto* f = new bsg_fleet();
+  f->ctx = ctx;
+  f->cfg = cfg;
+  f->n_inst = n_instances;
+  f->n_cap = max_requests;
+  f->k = k;
+  f->pow2 = ctx->dev_cfgs_host[cfg].div_magic == 0;
+  auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t b_col = up(static_cast<size_t>(entries) * 4), b_inst = up(n_instances * sizeof(ClInst)),
+               b_fd = up(sizeof(FleetDev)), b_out = up(static_cast<size_t>(max_requests) * sizeof(bsg_request_outcome)),
+               b_res = up(n_instances * sizeof(bsg_result)), b_sc = up(n_instances * 8), b_len = up(1024 * 4);
+  const size_t total = 7 * b_col + b_inst + b_fd + b_out + b_res + b_sc + b_len;
+  if (cudaMalloc(&f->base, total) != cudaSuccess) {
+    cudaGetLastError();
+    delete f;
+    ctx->last_error = "fleet allocation failed";
+    return BSG_CUDA_ERROR;
+  }
+  char* p = f->base;
+  int32_t** cols[7] = {&f->ar.prompt, &f->ar.est, &f->ar.prefill, &f->ar.decoded, &f->ar.target, &f->ar.rid, &f->ar.chunk};
+  for (auto* col : cols) {
+    *col = reinterpret_cast<int32_t*>(p);
+    p += b_col;
+  }
+  f->inst = reinterpret_cast<ClInst*>(p);
+  p += b_inst;
+  f->fd = reinterpret_cast<FleetDev*>(p);
+  p += b_fd;
+  f->outs = reinterpret_cast<bsg_request_outcome*>(p);
+  p += b_out;
+  f->res = reinterpret_cast<bsg_result*>(p);
+  p += b_res;
+  f->scores = reinterpret_cast<int64_t*>(p);
+  p += b_sc;
+  f->lens = reinterpret_cast<int32_t*>(p);
+  std::vector<ClInst> init(static_cast<size_t>(n_instances));
+  for (auto& x : init) x = ClInst{0, c.max_batch_size, c.max_batch_size, c.total_blocks, 0, 0, 0};
+  FleetDev fd0{-1, 0, 0, -1, BSG_OK, 0};
+  bool ok = cudaHostAlloc(&f->pinned, 1024 * 4 + 64 + static_cast<size_t>(n_instances) * 8, cudaHostAllocDefault) == cudaSuccess;
+  ok = ok && cudaMemcpyAsync(f->inst, init.data(), n_instances * sizeof(ClInst), cudaMemcpyHostToDevice, ctx->stream) == cudaSuccess;
+  ok = ok && cudaMemcpyAsync(f->fd, &fd0, sizeof(fd0), cudaMemcpyHostToDevice, ctx->stream) == cudaSuccess;
+  ok = ok && cudaStreamSynchronize(ctx->stream) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    if (f->pinned) cudaFreeHost(f->pinned);
+    cudaFree(f->base);
+    delete f;
+    ctx->last_error = "fleet initialisation failed";
+    return BSG_CUDA_ERROR;
+  }
+  *out = f;
+  return BSG_OK;
+}
+
+extern "C" void bsg_fleet_destroy(bsg_fleet* f) {
+  if (!f) return;
+  cudaSetDevice(f->ctx->device);
+  cudaStreamSynchronize(f->ctx->stream);
+  if (f->pinned) cudaFreeHost(f->pinned);
+  cudaFree(f->base);
+  delete f;
+}
+
+extern "C" bsg_status bsg_fleet_dispatch(bsg_fleet* f, int64_t now_ticks, int32_t prompt, int32_t est,
+                                         int32_t output, const int32_t* lengths, int32_t n_samples,
+                                         int32_t objective, int32_t* chosen, int64_t* scores) {
+  if (!f || !chosen || now_ticks < 0 || objective < 0 || objective > 1) return BSG_INVALID_ARGUMENT;
+  if (now_ticks < f->last_now) return BSG_INVALID_ARGUMENT;  // arrivals in time order
+  if (prompt < 1 || prompt > (1 << 22) || est < 0 || est > (1 << 24) || output < 1 || output > (1 << 24))
+    return BSG_BAD_INPUT;
+  const bool mc = lengths != nullptr;
+  if (mc && (n_samples < 1 || n_samples > 1024)) return BSG_INVALID_ARGUMENT;
+  bsg_ctx* ctx = f->ctx;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaSetDevice(ctx->device);
+  // the workload must be servable (config.cpp:197-205)
+  const bsg_instance_cfg& c = ctx->host_cfgs[f->cfg];
+  if ((static_cast<int64_t>(prompt) + output + c.block_size - 1) / c.block_size > c.total_blocks)
+    return BSG_TOO_LARGE_CANDIDATE;
+  auto* hl = static_cast<int32_t*>(f->pinned);
+  auto* hout = reinterpret_cast<int32_t*>(static_cast<char*>(f->pinned) + 1024 * 4);
+  auto* hsc = reinterpret_cast<int64_t*>(static_cast<char*>(f->pinned) + 1024 * 4 + 64);
+  cudaStream_t s = ctx->stream;
+  int32_t S = 0;
+  if (mc) {
+    S = n_samples;
+    std::memcpy(hl, lengths, S * 4);
+    std::sort(hl, hl + S);  // the kernel walks the samples in ascending order
+    cudaError_t e = cudaMemcpyAsync(f->lens, hl, S * 4, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return bsg_cuda_fail(ctx, e, "fleet lengths");
+  }
+  cudaError_t e = launch_fleet_any(f, now_ticks, prompt, est, output, S, objective, 0, mc);
+  if (e != cudaSuccess) return bsg_cuda_fail(ctx, e, "fleet_dispatch_kernel");
+  e = cudaMemcpyAsync(hout, &f->fd->chosen, 8, cudaMemcpyDeviceToHost, s);  // chosen, status
+  if (e == cudaSuccess && scores) e = cudaMemcpyAsync(hsc, f->scores, f->n_inst * 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return bsg_cuda_fail(ctx, e, "fleet dispatch");
+  f->last_now = now_ticks;
+  ctx->scenarios += static_cast<int64_t>(f->n_inst) * (mc ? S : 1);
+  *chosen = hout[0];
+  if (scores) std::memcpy(scores, hsc, f->n_inst * 8);
+  if (hout[1] != BSG_OK) {
+    ctx->last_error = "fleet dispatch failed (see status)";
+    return static_cast<bsg_status>(hout[1]);
+  }
+  return BSG_OK;
+}
+
+extern "C" bsg_status bsg_fleet_finish(bsg_fleet* f, bsg_request_outcome* outcomes, int32_t* n_requests,
+                                       bsg_replay_summary* summary) {
+  if (!f || !outcomes || !n_requests) return BSG_INVALID_ARGUMENT;
+  bsg_ctx* ctx = f->ctx;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = ctx->stream;
+  cudaError_t e = launch_fleet_any(f, INT64_MAX, 1, 1, 1, 0, 0, 1, false);  // drain: run every step
+  FleetDev fd{};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&fd, f->fd, sizeof(fd), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess && fd.n_req > 0)
+    e = cudaMemcpy(outcomes, f->outs, static_cast<size_t>(fd.n_req) * sizeof(bsg_request_outcome),
+                   cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return bsg_cuda_fail(ctx, e, "fleet finish");
+  *n_requests = fd.n_req;
+  if (summary) {
+    std::memset(summary, 0, sizeof(*summary));
+    int64_t pre = 0;
+    for (int32_t q = 0; q < fd.n_req; ++q) pre += outcomes[q].preempt_count;
+    summary->total_preemptions = pre;
+    summary->end_ticks = std::max(fd.end_ticks, fd.t_prev);
+    summary->final_instance_count = f->n_inst;
+  }
+  return fd.status == BSG_OK ? BSG_OK : static_cast<bsg_status>(fd.status);
+}
+
+extern "C" bsg_status bsg_fleet_snapshot(bsg_fleet* f, int32_t instance, int32_t* run_n, int32_t* wait_n,
+                                         int32_t* prompt, int32_t* est, int32_t* prefill,
+                                         int32_t* decoded, int32_t cap) {
+  if (!f || !run_n || !wait_n || instance < 0 || instance >= f->n_inst) return BSG_INVALID_ARGUMENT;
+  bsg_ctx* ctx = f->ctx;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaSetDevice(ctx->device);
+  ClInst st{};
+  cudaError_t e = cudaMemcpy(&st, f->inst + instance, sizeof(st), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return bsg_cuda_fail(ctx, e, "fleet snapshot");
+  *run_n = st.n;
+  *wait_n = st.wtail - st.whead;
+  if (st.n + *wait_n > cap) return BSG_OK;  // sizes only
+  const int32_t maxb = ctx->host_cfgs[f->cfg].max_batch_size;
+  const int64_t Rb = static_cast<int64_t>(instance) * (2 * static_cast<int64_t>(maxb) + f->n_cap);
+  const int64_t Ab = Rb + maxb + st.whead;
+  int32_t* dst[4] = {prompt, est, prefill, decoded};
+  int32_t* src[4] = {f->ar.prompt, f->ar.est, f->ar.prefill, f->ar.decoded};
+  for (int c = 0; c < 4 && e == cudaSuccess; ++c) {
+    if (!dst[c]) continue;
+    if (st.n > 0) e = cudaMemcpy(dst[c], src[c] + Rb, st.n * 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && *wait_n > 0) e = cudaMemcpy(dst[c] + st.n, src[c] + Ab, *wait_n * 4, cudaMemcpyDeviceToHost);
+  }
+  if (e != cudaSuccess) return bsg_cuda_fail(ctx, e, "fleet snapshot");
+  return BSG_OK;
 }

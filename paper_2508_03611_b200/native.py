@@ -63,6 +63,13 @@ def load() -> C.CDLL:
         "bsg_scenario_count": (C.c_int64, [V]),
         "bsg_mc_lengths": (C.c_int, [C.c_int32, C.c_uint64, C.c_int32, C.c_uint64, C.c_double, V]),
         "bsg_replay_device": (C.c_int, [V, V, C.c_int32, V, V, V, V, C.c_int64, V, V, V]),
+        "bsg_fleet_create": (C.c_int, [V, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+        "bsg_fleet_destroy": (None, [V]),
+        "bsg_fleet_dispatch": (C.c_int, [V, C.c_int64, C.c_int32, C.c_int32, C.c_int32, V, C.c_int32,
+                                         C.c_int32, V, V]),
+        "bsg_fleet_finish": (C.c_int, [V, V, V, V]),
+        "bsg_fleet_snapshot": (C.c_int, [V, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                         V, V, V, V, C.c_int32]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -130,6 +137,59 @@ def make_workload_host(w: np.ndarray):
     if st != abi.OK:
         raise BsgError(st, "bsg_make_workload")
     return p, o, e, t
+
+
+class Fleet:
+    """A device-resident mirror of live instances (bsg_fleet_*): one launch per
+    dispatch, the snapshots never leave HBM."""
+
+    def __init__(self, ctx: "Context", n_instances: int, max_requests: int, cfg: int = 0):
+        self.ctx, self.n = ctx, n_instances
+        h = C.c_void_p()
+        ctx._check(ctx.L.bsg_fleet_create(ctx.h, cfg, n_instances, max_requests, C.byref(h)),
+                   "bsg_fleet_create")
+        self.h = h
+        self._chosen = C.c_int32(-1)
+
+    def dispatch(self, now_ticks: int, prompt: int, est: int, output: int, lengths=None,
+                 objective: int = 0, scores: np.ndarray | None = None) -> int:
+        lp, ns = (None, 0) if lengths is None else (_p(lengths), len(lengths))
+        st = self.ctx.L.bsg_fleet_dispatch(self.h, int(now_ticks), int(prompt), int(est), int(output),
+                                           lp, ns, objective, C.byref(self._chosen),
+                                           None if scores is None else _p(scores))
+        self.ctx._check(st, "bsg_fleet_dispatch")
+        return self._chosen.value
+
+    def snapshot(self, instance: int):
+        """(running, waiting) columns (prompt, est, prefill, decoded) of one instance."""
+        rn, wn = C.c_int32(0), C.c_int32(0)
+        L = self.ctx.L
+        self.ctx._check(L.bsg_fleet_snapshot(self.h, instance, C.byref(rn), C.byref(wn), None, None,
+                                             None, None, 0), "bsg_fleet_snapshot")
+        n = rn.value + wn.value
+        cols = [np.zeros(max(n, 1), np.int32) for _ in range(4)]
+        self.ctx._check(L.bsg_fleet_snapshot(self.h, instance, C.byref(rn), C.byref(wn),
+                                             *[_p(c) for c in cols], max(n, 1)), "bsg_fleet_snapshot")
+        return rn.value, wn.value, [c[:n] for c in cols]
+
+    def finish(self, max_requests: int):
+        out = np.zeros(max_requests, abi.outcome_dtype)
+        n = C.c_int32(0)
+        summ = np.zeros(1, abi.summary_dtype)
+        self.ctx._check(self.ctx.L.bsg_fleet_finish(self.h, _p(out), C.byref(n), _p(summ)),
+                        "bsg_fleet_finish")
+        return out[:n.value], summ[0]
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.L.bsg_fleet_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Context:

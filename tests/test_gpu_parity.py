@@ -258,3 +258,60 @@ def test_device_closed_loop_autoscaler_matches_reference(ctx, ref, kind, kw):
         assert int(summ["final_instance_count"]) == int(esum["final_instance_count"])
         for f in ("instance", "dispatch_ticks", "first_token_ticks", "finish_ticks", "preempt_count"):
             assert np.array_equal(out[f], exp[f]), (kind, ni, f, np.nonzero(out[f] != exp[f])[0][:5])
+
+
+@pytest.mark.parametrize("policy_cfg,n_inst,obj", [
+    (dict(), 12, 0), (dict(local_policy=1), 5, 1), (dict(total_blocks=300, max_batch_size=24), 7, 0),
+])
+def test_fleet_matches_reference(ctx, ref, policy_cfg, n_inst, obj):
+    """A fleet (device-resident instance mirror, one launch per dispatch) driven
+    by a workload's arrivals reproduces the reference's replay exactly."""
+    from paper_2508_03611_b200 import native
+    cfg = abi.make_config(**policy_cfg)
+    ctx.set_configs(cfg)
+    w = abi.make_workload(count=300, qps=14.0, arrival_seed=5, estimator_kind=2, estimator_seed=5)
+    p, o, e, t = native.make_workload_host(w)
+    fl = native.Fleet(ctx, n_inst, len(p))
+    picks = [fl.dispatch(t[k], p[k], e[k], o[k], objective=obj) for k in range(len(p))]
+    out, summ = fl.finish(len(p))
+    exp, esum, _ = ref.replay(w, cfg, abi.make_replay_spec(n_inst, objective=obj, capture=0),
+                              capture=False)
+    assert picks == exp["instance"].tolist()
+    for f in ("instance", "dispatch_ticks", "first_token_ticks", "finish_ticks", "preempt_count"):
+        assert np.array_equal(out[f], exp[f]), (f, np.nonzero(out[f] != exp[f])[0][:5])
+    assert int(summ["total_preemptions"]) == int(esum["total_preemptions"])
+
+
+def test_fleet_mc_dispatch_matches_dispatch_mc(ctx):
+    """Monte-Carlo fleet dispatches (prefix-shared samples on the mirror, in
+    place): per-instance scores and decisions == bsg_dispatch_mc on the same
+    snapshots, exported through the mirror's Status API after each dispatch
+    (pre-dispatch snapshot = post-dispatch minus the admitted tail entry)."""
+    from paper_2508_03611_b200 import native
+    cfg = abi.make_config()
+    ctx.set_configs(cfg)
+    n_inst, S = 8, 64
+    w = abi.make_workload(count=150, qps=12.0, arrival_seed=3)
+    p, o, e, t = native.make_workload_host(w)
+    fl = native.Fleet(ctx, n_inst, len(p))
+    ids = np.arange(n_inst, dtype=np.int32)
+    for k in range(len(p)):
+        lens = native.mc_lengths(int(e[k]), k, S, seed=7)
+        sc = np.zeros(n_inst, np.int64)
+        pick = fl.dispatch(t[k], p[k], e[k], o[k], lengths=lens, scores=sc)
+        if k % 5:
+            continue
+        cols, scen, off = [[] for _ in range(4)], np.zeros(n_inst, abi.scenario_dtype), 0
+        for i in range(n_inst):
+            rn, wn, c = fl.snapshot(i)
+            if i == pick:
+                wn -= 1
+            for j in range(4):
+                cols[j].append(c[j][:rn + wn])
+            scen[i] = (off, rn, off + rn, wn, p[k], e[k], 0, 0)
+            off += rn + wn
+        ss = abi.ScenarioSet(*[np.concatenate(c).astype(np.int32) for c in cols], scen)
+        exp_pick, exp_scores, _, _ = ctx.dispatch_mc(ss, ids, n_inst, lens)
+        assert pick == int(exp_pick[0]) and np.array_equal(sc, exp_scores), (k, sc, exp_scores)
+    out, _ = fl.finish(len(p))
+    assert (out["finish_ticks"] > 0).all()
