@@ -266,6 +266,7 @@ def run_gpu(args):
         lat = mc_latency(ctx, world, rank, dev)
         if rank == 0:
             line["dispatch_latency"] = lat
+            line["dispatch_latency_mirror"] = fleet_latency(ctx)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -321,6 +322,37 @@ def mc_latency(ctx, world: int = 1, rank: int = 0, device=None, n_calls: int = 4
                       "snapshots from a 3000-request 130 QPS closed loop; host buffers, "
                       "wall clock per call" + (f"; instances sharded i % {world}, NCCL argmin"
                                                 if world > 1 else "")}
+
+
+def fleet_latency(ctx, n_inst: int = 64, n_samples: int = 256, count: int = 3000,
+                  qps: float = 130.0):
+    """cfg4 on the device mirror (bsg_fleet_dispatch): the 64-instance cluster's
+    live state stays in HBM; every arrival of a 3000-request 130 QPS stream is
+    ONE call — advance the instances in place, 256-sample Monte-Carlo what-ifs
+    on all 64, argmin, admit — timed per call (wall clock, host API; only the
+    candidate's lengths go in and the decision comes out)."""
+    from paper_2508_03611_b200 import abi, native
+    cfg = abi.make_config()
+    ctx.set_configs(cfg)
+    w = abi.make_workload(count=count, qps=qps, arrival_seed=1)
+    p, o, e, t = native.make_workload_host(w)
+    lens = [native.mc_lengths(int(e[k]), k, n_samples, seed=1) for k in range(count)]
+    lat = []
+    for rep in range(2):  # first pass warms up (module load, allocations)
+        fl = native.Fleet(ctx, n_inst, count)
+        for k in range(count):
+            t0 = time.perf_counter()
+            fl.dispatch(t[k], p[k], e[k], o[k], lengths=lens[k])
+            if rep:
+                lat.append((time.perf_counter() - t0) * 1e6)
+        fl.finish(count)
+        fl.close()
+    lat = np.array(lat)
+    return {"p50_us": float(np.percentile(lat, 50)), "p99_us": float(np.percentile(lat, 99)),
+            "max_us": float(lat.max()), "calls": len(lat),
+            "config": f"cfg4 on the device mirror: {n_inst} instances x {n_samples} MC samples, "
+                      f"{count} arrivals @ {qps:g} QPS, one bsg_fleet_dispatch per arrival "
+                      "(advance + what-ifs + argmin + admit), wall clock per call"}
 
 
 def cpu_baseline(ss, cfg):

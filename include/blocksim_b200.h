@@ -339,6 +339,11 @@ typedef struct bsg_run_report {
   double mean_e2e_s, p50_e2e_s, p99_e2e_s;
   int64_t total_preemptions;
   int32_t instances_provisioned, final_instance_count;
+  /* means over dispatch points of the per-dispatch mean / variance of the
+   * instances' snapshot free blocks (driver.cpp:142-157, metrics.cpp:79-85);
+   * produced by bsg_replay_device's device reports (bsg_aggregate, which has
+   * no dispatch points, leaves them 0) */
+  double free_blocks_mean_avg, free_blocks_var_avg;
 } bsg_run_report;
 bsg_status bsg_aggregate(const bsg_request_outcome* outcomes, int64_t n,
                          const bsg_replay_summary* summary, bsg_run_report* out);
@@ -413,11 +418,15 @@ typedef struct bsg_closed_loop_run {
   int32_t max_instances;
   double threshold_s, cold_start_s, cooldown_s;
 } bsg_closed_loop_run;
+/* outcomes may be NULL (not copied back); reports (optional, one per run) is
+ * aggregate (metrics.cpp:21-124) computed on the device:
+ * nearest-rank percentiles by radix select over tick keys, means summed in
+ * request order as the reference does, so every field is bit-identical. */
 bsg_status bsg_replay_device(bsg_ctx* ctx, const bsg_closed_loop_run* runs, int32_t n_runs,
                              const int32_t* prompt, const int32_t* output, const int32_t* est,
                              const int64_t* arrival_ticks, int64_t n_requests_total,
                              bsg_request_outcome* outcomes, bsg_replay_summary* summaries,
-                             int32_t* run_status);
+                             int32_t* run_status, bsg_run_report* reports);
 
 /* Fleet: a persistent device mirror of n_instances live serving instances
  * (incremental snapshot mirrors). Every instance's running

@@ -602,6 +602,8 @@ int ref_run_report(const bsg_workload* w, const bsg_instance_cfg* c, const bsg_r
   out->total_preemptions = r.total_preemptions;
   out->instances_provisioned = r.instances_provisioned;
   out->final_instance_count = r.final_instance_count;
+  out->free_blocks_mean_avg = r.free_blocks_mean_avg;
+  out->free_blocks_var_avg = r.free_blocks_var_avg;
   return 0;
 }
 

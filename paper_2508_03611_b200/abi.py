@@ -81,7 +81,7 @@ report_dtype = np.dtype([
     ("mean_ttft_s", "<f8"), ("p50_ttft_s", "<f8"), ("p99_ttft_s", "<f8"),
     ("mean_e2e_s", "<f8"), ("p50_e2e_s", "<f8"), ("p99_e2e_s", "<f8"),
     ("total_preemptions", "<i8"), ("instances_provisioned", "<i4"),
-    ("final_instance_count", "<i4"),
+    ("final_instance_count", "<i4"), ("free_blocks_mean_avg", "<f8"), ("free_blocks_var_avg", "<f8"),
 ])
 capacity_dtype = np.dtype([
     ("capacity_qps", "<f8"), ("bracket_pass", "<i4"), ("bracket_fail", "<i4"),

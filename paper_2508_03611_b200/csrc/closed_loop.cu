@@ -386,7 +386,135 @@ struct ClShared {
   int32_t active;               // instances dispatchable (instances_.size())
   int32_t next;
   int32_t err;
+  // metric pipeline (aggregate, metrics.cpp:21-124, and the per-dispatch
+  // free-block balance, driver.cpp:142-157)
+  int32_t snap_free[kClMaxInst];
+  double fm_sum, fv_sum;
+  int32_t n_points;
+  int32_t hist[256];
+  unsigned long long sel_prefix;
+  long long sel_k;
+  long long cnt_fin;
+  unsigned long long min_arr, max_fin;
 };
+
+__device__ __forceinline__ bool finished(const bsg_request_outcome& o) {
+  return o.finish_ticks >= 0 && o.dispatch_ticks >= 0 && o.first_token_ticks >= 0;
+}
+__device__ __forceinline__ int64_t ttft_ticks(const bsg_request_outcome& o) {
+  return o.first_token_ticks - o.dispatch_ticks;
+}
+__device__ __forceinline__ int64_t e2e_ticks(const bsg_request_outcome& o) {
+  return o.finish_ticks - o.arrival_ticks;
+}
+
+// k-th smallest (0-based) TTFT (which = 0) or e2e (which = 1) tick count over
+// the finished requests: block-wide radix select, 8 passes of 8-bit digits.
+// SimTime::seconds is monotone in ticks, so this is the nearest-rank
+// percentile of the reference's sorted doubles (metrics.cpp:11-19).
+template <int K>
+__device__ int64_t block_select(ClShared<K>& S, const bsg_request_outcome* outs, int32_t N, int which,
+                                long long k) {
+  if (threadIdx.x == 0) {
+    S.sel_prefix = 0;
+    S.sel_k = k;
+  }
+  unsigned long long mask = 0;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) S.hist[b] = 0;
+    __syncthreads();
+    const unsigned long long prefix = S.sel_prefix;
+    for (int32_t q = threadIdx.x; q < N; q += blockDim.x) {
+      const bsg_request_outcome o = outs[q];
+      if (!finished(o)) continue;
+      const unsigned long long key = static_cast<unsigned long long>(which ? e2e_ticks(o) : ttft_ticks(o));
+      if ((key & mask) == prefix) atomicAdd(&S.hist[(key >> shift) & 255], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long kk = S.sel_k;
+      int d = 0;
+      for (; d < 255 && kk >= S.hist[d]; ++d) kk -= S.hist[d];
+      S.sel_k = kk;
+      S.sel_prefix = prefix | (static_cast<unsigned long long>(d) << shift);
+    }
+    mask |= 0xffull << shift;
+    __syncthreads();
+  }
+  return static_cast<int64_t>(S.sel_prefix);
+}
+
+// percentile_nearest_rank's rank (metrics.cpp:14-17), 0-based
+__device__ __forceinline__ long long nearest_rank0(double p, long long n) {
+  long long rank = static_cast<long long>(ceil(__dmul_rn(p / 100.0, static_cast<double>(n))));
+  if (rank < 1) rank = 1;
+  if (rank > n) rank = n;
+  return rank - 1;
+}
+
+// aggregate (metrics.cpp:21-124) of one finished run, on its block.
+template <int K>
+__device__ void block_report(ClShared<K>& S, const bsg_request_outcome* outs, int32_t N,
+                             const bsg_replay_summary& sm, bsg_run_report* rep) {
+  if (threadIdx.x == 0) {
+    S.cnt_fin = 0;
+    S.min_arr = ~0ull;
+    S.max_fin = 0;
+  }
+  __syncthreads();
+  long long fin = 0;
+  unsigned long long mn = ~0ull, mx = 0;
+  for (int32_t q = threadIdx.x; q < N; q += blockDim.x) {
+    const bsg_request_outcome o = outs[q];
+    mn = min(mn, static_cast<unsigned long long>(o.arrival_ticks));
+    if (finished(o)) {
+      ++fin;
+      mx = max(mx, static_cast<unsigned long long>(o.finish_ticks));
+    }
+  }
+  atomicAdd(reinterpret_cast<unsigned long long*>(&S.cnt_fin), static_cast<unsigned long long>(fin));
+  atomicMin(&S.min_arr, mn);
+  atomicMax(&S.max_fin, mx);
+  __syncthreads();
+  const long long n_fin = S.cnt_fin;
+  bsg_run_report r{};
+  if (n_fin > 0) {
+    const int64_t t50 = block_select(S, outs, N, 0, nearest_rank0(50.0, n_fin));
+    const int64_t t99 = block_select(S, outs, N, 0, nearest_rank0(99.0, n_fin));
+    const int64_t e50 = block_select(S, outs, N, 1, nearest_rank0(50.0, n_fin));
+    const int64_t e99 = block_select(S, outs, N, 1, nearest_rank0(99.0, n_fin));
+    r.p50_ttft_s = static_cast<double>(t50) * 1e-9;
+    r.p99_ttft_s = static_cast<double>(t99) * 1e-9;
+    r.p50_e2e_s = static_cast<double>(e50) * 1e-9;
+    r.p99_e2e_s = static_cast<double>(e99) * 1e-9;
+  }
+  if (threadIdx.x != 0) return;
+  // means: summed in request order, as the reference does
+  double st = 0, se = 0;
+  for (int32_t q = 0; q < N; ++q) {
+    const bsg_request_outcome o = outs[q];
+    if (!finished(o)) continue;
+    st = __dadd_rn(st, static_cast<double>(ttft_ticks(o)) * 1e-9);
+    se = __dadd_rn(se, static_cast<double>(e2e_ticks(o)) * 1e-9);
+  }
+  r.finished_requests = static_cast<int32_t>(n_fin);
+  r.censored_requests = N - static_cast<int32_t>(n_fin);
+  if (n_fin > 0) {
+    r.mean_ttft_s = st / static_cast<double>(n_fin);
+    r.mean_e2e_s = se / static_cast<double>(n_fin);
+    const int64_t first = static_cast<int64_t>(S.min_arr), last = static_cast<int64_t>(S.max_fin);
+    if (N > 0 && last > first)
+      r.throughput_rps = static_cast<double>(n_fin) / (static_cast<double>(last - first) * 1e-9);
+  }
+  r.total_preemptions = sm.total_preemptions;
+  r.instances_provisioned = sm.instances_provisioned;
+  r.final_instance_count = sm.final_instance_count;
+  if (S.n_points > 0) {
+    r.free_blocks_mean_avg = S.fm_sum / static_cast<double>(S.n_points);
+    r.free_blocks_var_avg = S.fv_sum / static_cast<double>(S.n_points);
+  }
+  *rep = r;
+}
 
 // Autoscaler::evaluate (autoscaler.cpp:36-52) for a signal of the run's kind:
 // on a trigger, the instance's ProvisionComplete is due cold_start later
@@ -407,7 +535,8 @@ __global__ void __launch_bounds__(kClWarps * 32, 2)
                        const int32_t* __restrict__ rq_prompt, const int32_t* __restrict__ rq_output,
                        const int32_t* __restrict__ rq_est, const int64_t* __restrict__ rq_arrival,
                        Arena ar, bsg_request_outcome* __restrict__ outcomes,
-                       bsg_replay_summary* __restrict__ summaries, int32_t* __restrict__ status) {
+                       bsg_replay_summary* __restrict__ summaries, int32_t* __restrict__ status,
+                       bsg_run_report* __restrict__ reports) {
   extern __shared__ __align__(16) unsigned char cl_smem[];
   ClShared<K>& S = *reinterpret_cast<ClShared<K>*>(cl_smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -444,6 +573,9 @@ __global__ void __launch_bounds__(kClWarps * 32, 2)
     S.pend_head = 0;
     S.active = I0;
     S.cand_min = ~0ull;
+    S.fm_sum = 0;
+    S.fv_sum = 0;
+    S.n_points = 0;
   }
   __syncthreads();
   const bool relief = run.prov_kind == 2;
@@ -559,6 +691,15 @@ __global__ void __launch_bounds__(kClWarps * 32, 2)
       i = __shfl_sync(kFull, i, 0);
       if (i >= I) break;
       const ClInst& s = S.inst[i];
+      if (reports) {  // the snapshot's free blocks (backend.cpp:357-365): total - sum held(stored)
+        int32_t held = 0;
+        for (int32_t p = lane; p < s.n; p += 32) {
+          const int64_t g = run.arena_off + i * stride + p;
+          held += bnt<POW2>(__ldcg(&ar.prefill[g]) + __ldcg(&ar.decoded[g]), cfg);
+        }
+        held = static_cast<int32_t>(__reduce_add_sync(kFull, static_cast<uint32_t>(held)));
+        if (lane == 0) S.snap_free[i] = cfg.total_blocks - held;
+      }
       bsg_scenario sc;
       sc.run_off = static_cast<int32_t>(run.arena_off + i * stride);
       sc.run_n = s.n;
@@ -597,6 +738,20 @@ __global__ void __launch_bounds__(kClWarps * 32, 2)
       if (bad != BSG_OK) {
         fail(bad);  // PredictionError propagates out of the run (predictor.cpp:132-136)
       } else if (lane == 0) {  // admit the arrival at the chosen instance's waiting tail
+        if (reports) {  // memory-balance sample of this dispatch (driver.cpp:142-157)
+          double mean = 0;
+          for (int32_t q = 0; q < I; ++q) mean = __dadd_rn(mean, static_cast<double>(S.snap_free[q]));
+          mean /= static_cast<double>(I);
+          double var = 0;
+          for (int32_t q = 0; q < I; ++q) {
+            const double d = __dsub_rn(static_cast<double>(S.snap_free[q]), mean);
+            var = __dadd_rn(var, __dmul_rn(d, d));
+          }
+          var /= static_cast<double>(I);
+          S.fm_sum = __dadd_rn(S.fm_sum, mean);
+          S.fv_sum = __dadd_rn(S.fv_sum, var);
+          S.n_points += 1;
+        }
         if (run.prov_kind == 1)  // preempt provisioning on the predicted e2e (driver.cpp:197-211)
           autoscale<K>(S, run, I0, static_cast<double>(S.res[best_i].e2e_ticks) * 1e-9, t);
         ClInst& s = S.inst[best_i];
@@ -641,6 +796,14 @@ __global__ void __launch_bounds__(kClWarps * 32, 2)
     sm.instances_provisioned = S.n_pend;
     sm.final_instance_count = S.active;
     summaries[blockIdx.x] = sm;
+  }
+  if (reports && S.err == BSG_OK) {
+    __syncthreads();
+    bsg_replay_summary sm{};
+    sm.total_preemptions = static_cast<int64_t>(S.preempts);
+    sm.instances_provisioned = S.n_pend;
+    sm.final_instance_count = S.active;
+    block_report<K>(S, outs, N, sm, &reports[blockIdx.x]);
   }
 }
 
@@ -809,12 +972,12 @@ template <int K, bool POW2>
 bsg_status launch_closed_loop(bsg_ctx* ctx, int32_t n_runs, const ClRun* runs,
                               const int32_t* p, const int32_t* o, const int32_t* e,
                               const int64_t* arr, const Arena& ar, bsg_request_outcome* outs,
-                              bsg_replay_summary* sums, int32_t* st) {
+                              bsg_replay_summary* sums, int32_t* st, bsg_run_report* rep) {
   const size_t sm = sizeof(ClShared<K>);
   cudaFuncSetAttribute(closed_loop_kernel<K, POW2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(sm));
   closed_loop_kernel<K, POW2><<<n_runs, kClWarps * 32, sm, ctx->stream>>>(
-      static_cast<const DevCfg*>(ctx->cfgs.p), runs, p, o, e, arr, ar, outs, sums, st);
+      static_cast<const DevCfg*>(ctx->cfgs.p), runs, p, o, e, arr, ar, outs, sums, st, rep);
   ctx->launches += 1;
   const cudaError_t err = cudaGetLastError();
   return err == cudaSuccess ? BSG_OK : bsg_cuda_fail(ctx, err, "closed_loop_kernel launch");
@@ -827,9 +990,9 @@ extern "C" bsg_status bsg_replay_device(bsg_ctx* ctx, const bsg_closed_loop_run*
                                         const int32_t* output, const int32_t* est,
                                         const int64_t* arrival_ticks, int64_t n_requests_total,
                                         bsg_request_outcome* outcomes,
-                                        bsg_replay_summary* summaries, int32_t* run_status) {
-  if (!ctx || !runs || n_runs < 0 || !prompt || !output || !est || !arrival_ticks || !outcomes ||
-      !run_status)
+                                        bsg_replay_summary* summaries, int32_t* run_status,
+                                        bsg_run_report* reports) {
+  if (!ctx || !runs || n_runs < 0 || !prompt || !output || !est || !arrival_ticks || !run_status)
     return BSG_INVALID_ARGUMENT;
   if (n_runs == 0) return BSG_OK;
   if (ctx->ncfg == 0) return BSG_INVALID_ARGUMENT;
@@ -883,9 +1046,11 @@ extern "C" bsg_status bsg_replay_device(bsg_ctx* ctx, const bsg_closed_loop_run*
   const int64_t nq = n_requests_total;
   const size_t b_runs = n_runs * sizeof(ClRun), b_req = nq * 4, b_arr = nq * 8,
                b_out = nq * sizeof(bsg_request_outcome), b_sum = n_runs * sizeof(bsg_replay_summary),
-               b_st = n_runs * 4, b_col = static_cast<size_t>(std::max<int64_t>(arena, 1)) * 4;
+               b_st = n_runs * 4, b_col = static_cast<size_t>(std::max<int64_t>(arena, 1)) * 4,
+               b_rep = reports ? n_runs * sizeof(bsg_run_report) : 0;
   auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
-  const size_t total = up(b_runs) + 3 * up(b_req) + up(b_arr) + up(b_out) + up(b_sum) + up(b_st) + 7 * up(b_col);
+  const size_t total = up(b_runs) + 3 * up(b_req) + up(b_arr) + up(b_out) + up(b_sum) + up(b_st) +
+                       7 * up(b_col) + up(b_rep);
   char* base = nullptr;
   cudaError_t ce = cudaMallocAsync(reinterpret_cast<void**>(&base), total, ctx->stream);
   if (ce != cudaSuccess) return bsg_cuda_fail(ctx, ce, "cudaMallocAsync(closed-loop)");
@@ -903,6 +1068,7 @@ extern "C" bsg_status bsg_replay_device(bsg_ctx* ctx, const bsg_closed_loop_run*
   auto* d_out = reinterpret_cast<bsg_request_outcome*>(take(b_out));
   auto* d_sum = reinterpret_cast<bsg_replay_summary*>(take(b_sum));
   auto* d_st = reinterpret_cast<int32_t*>(take(b_st));
+  auto* d_rep = reports ? reinterpret_cast<bsg_run_report*>(take(b_rep)) : nullptr;
   Arena ar{};
   int32_t** cols[7] = {&ar.prompt, &ar.est, &ar.prefill, &ar.decoded, &ar.target, &ar.rid, &ar.chunk};
   for (auto* c : cols) *c = reinterpret_cast<int32_t*>(take(b_col));
@@ -924,18 +1090,19 @@ extern "C" bsg_status bsg_replay_device(bsg_ctx* ctx, const bsg_closed_loop_run*
   BSG_CL_CHECK(cudaMemcpyAsync(d_out, init.data(), b_out, cudaMemcpyHostToDevice, s));
   if (st == BSG_OK) {
     switch (k * 2 + (pow2 ? 1 : 0)) {
-      case 2: st = launch_closed_loop<1, false>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st); break;
-      case 3: st = launch_closed_loop<1, true>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st); break;
-      case 4: st = launch_closed_loop<2, false>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st); break;
-      case 5: st = launch_closed_loop<2, true>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st); break;
-      case 8: st = launch_closed_loop<4, false>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st); break;
-      case 9: st = launch_closed_loop<4, true>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st); break;
-      case 16: st = launch_closed_loop<8, false>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st); break;
-      default: st = launch_closed_loop<8, true>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st); break;
+      case 2: st = launch_closed_loop<1, false>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
+      case 3: st = launch_closed_loop<1, true>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
+      case 4: st = launch_closed_loop<2, false>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
+      case 5: st = launch_closed_loop<2, true>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
+      case 8: st = launch_closed_loop<4, false>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
+      case 9: st = launch_closed_loop<4, true>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
+      case 16: st = launch_closed_loop<8, false>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
+      default: st = launch_closed_loop<8, true>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
     }
   }
   if (st == BSG_OK) {
-    BSG_CL_CHECK(cudaMemcpyAsync(outcomes, d_out, b_out, cudaMemcpyDeviceToHost, s));
+    if (outcomes) BSG_CL_CHECK(cudaMemcpyAsync(outcomes, d_out, b_out, cudaMemcpyDeviceToHost, s));
+    if (reports) BSG_CL_CHECK(cudaMemcpyAsync(reports, d_rep, b_rep, cudaMemcpyDeviceToHost, s));
     if (summaries) BSG_CL_CHECK(cudaMemcpyAsync(summaries, d_sum, b_sum, cudaMemcpyDeviceToHost, s));
     BSG_CL_CHECK(cudaMemcpyAsync(run_status, d_st, b_st, cudaMemcpyDeviceToHost, s));
   }

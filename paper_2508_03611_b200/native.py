@@ -62,7 +62,7 @@ def load() -> C.CDLL:
         "bsg_sweep_run": (C.c_int, [C.c_int, V, C.c_int32, C.c_int32, V]),
         "bsg_scenario_count": (C.c_int64, [V]),
         "bsg_mc_lengths": (C.c_int, [C.c_int32, C.c_uint64, C.c_int32, C.c_uint64, C.c_double, V]),
-        "bsg_replay_device": (C.c_int, [V, V, C.c_int32, V, V, V, V, C.c_int64, V, V, V]),
+        "bsg_replay_device": (C.c_int, [V, V, C.c_int32, V, V, V, V, C.c_int64, V, V, V, V]),
         "bsg_fleet_create": (C.c_int, [V, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
         "bsg_fleet_destroy": (None, [V]),
         "bsg_fleet_dispatch": (C.c_int, [V, C.c_int64, C.c_int32, C.c_int32, C.c_int32, V, C.c_int32,
@@ -318,8 +318,11 @@ class Context:
         out = np.zeros(off, abi.outcome_dtype)
         summ = np.zeros(len(runs), abi.summary_dtype)
         st = np.zeros(len(runs), np.int32)
+        rep = np.zeros(len(runs), abi.report_dtype)
         self._check(self.L.bsg_replay_device(self.h, _p(desc), len(runs), _p(p), _p(o), _p(e), _p(t),
-                                             off, _p(out), _p(summ), _p(st)), "bsg_replay_device")
+                                             off, _p(out), _p(summ), _p(st), _p(rep)),
+                    "bsg_replay_device")
+        self.last_reports = rep
         res = []
         for r in range(len(runs)):
             a, n = int(desc[r]["req_off"]), int(desc[r]["n_requests"])

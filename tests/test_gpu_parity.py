@@ -153,7 +153,9 @@ def test_autoscaler_closed_loop_matches_reference(ctx, ref, kind, policy):
     assert es["instances_provisioned"] > 0  # the scenario actually provisions
     assert np.array_equal(got, exp) and gs.tolist() == es.tolist()
     from paper_2508_03611_b200 import native
-    assert native.aggregate(got, gs).tolist() == ref.run_report(w, cfg, spec).tolist()
+    host_fields = [f for f in abi.report_dtype.names if not f.startswith("free_blocks")]
+    rep, exp_rep = native.aggregate(got, gs), ref.run_report(w, cfg, spec)
+    assert [rep[f] for f in host_fields] == [exp_rep[f] for f in host_fields]
 
 
 def test_capacity_search_matches_reference(ctx, ref):
@@ -231,6 +233,10 @@ def test_device_closed_loop_matches_reference(ctx, ref, policy_cfg):
             assert np.array_equal(host[f], exp[f]), ("host", policy_cfg, ni, f)
         assert int(summ["total_preemptions"]) == int(esum["total_preemptions"])
         assert int(hsum["total_preemptions"]) == int(esum["total_preemptions"])
+    # the device metric pipeline: aggregate() of every run, bit-identical
+    for (w, ni, obj), rep in zip(cases, ctx.last_reports):
+        exp = ref.run_report(w, cfg, abi.make_replay_spec(ni, objective=obj, capture=0))
+        assert rep.tobytes() == exp.tobytes(), (policy_cfg, ni, rep, exp)
 
 
 @pytest.mark.parametrize("kind,kw", [
