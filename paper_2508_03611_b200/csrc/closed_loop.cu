@@ -441,7 +441,9 @@ __device__ int64_t block_select(ClShared<K>& S, const bsg_request_outcome* outs,
     mask |= 0xffull << shift;
     __syncthreads();
   }
-  return static_cast<int64_t>(S.sel_prefix);
+  const int64_t v = static_cast<int64_t>(S.sel_prefix);
+  __syncthreads();  // every thread has read the result before the next selection resets it
+  return v;
 }
 
 // percentile_nearest_rank's rank (metrics.cpp:14-17), 0-based
