@@ -43,12 +43,36 @@ def local_best(scores: np.ndarray, ids: np.ndarray) -> tuple[int, int]:
     return int(m), int(ids[scores == m].min())
 
 
+PACK_BITS = 16                            # instance id field of the packed key
+PACK_SAT = (1 << (63 - PACK_BITS)) - 1    # largest score the packed key holds exactly
+
+
 def global_argmin(scores: np.ndarray, ids: np.ndarray, device=None, group=None) -> int:
-    """Exact cross-rank argmin: all_reduce MIN of the best score, then MIN of the
-    ids that attain it (two int64 collectives; no packing, so no range limit)."""
+    """Exact cross-rank argmin with lowest-id ties (scheduler.cpp:138-150).
+
+    One collective in the common case: all_reduce MIN of the packed
+    key (min(score, 2^47 - 1) << 16 | id) — the minimum is exact whenever the
+    winning score is below the saturation point, since every other rank's key
+    is then larger. Only when the winner saturated (scores >= 2^47 ticks, i.e.
+    sums of ~39 hours of e2e) does it fall back to the two-pass reduce (MIN of
+    the score, then MIN of the ids attaining it)."""
     import torch
     import torch.distributed as dist
+    if len(ids) and int(np.max(ids)) >= (1 << PACK_BITS) - 1:
+        raise ValueError("instance ids must be < 65535")  # every rank decides the same way
     s, i = local_best(scores, ids)
+    key = (min(s, PACK_SAT) << PACK_BITS) | (i if s != INT64_MAX else (1 << PACK_BITS) - 1)
+    t = torch.tensor([key], dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    k = int(t.item())
+    if (k >> PACK_BITS) < PACK_SAT:  # the same reduced value on every rank: a uniform branch
+        return k & ((1 << PACK_BITS) - 1)
+    return _global_argmin_two_pass(s, i, device, group)
+
+
+def _global_argmin_two_pass(s: int, i: int, device=None, group=None) -> int:
+    import torch
+    import torch.distributed as dist
     t = torch.tensor([s], dtype=torch.int64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
     cand = torch.tensor([i if s == int(t.item()) else np.iinfo(np.int64).max], dtype=torch.int64,

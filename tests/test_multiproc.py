@@ -33,9 +33,14 @@ def _worker(rank, world, port, q):
         out = {}
         for case in range(40):
             n_inst = int(rng.integers(1, 70))
-            scores = rng.integers(0, 6, n_inst).astype(np.int64) * (1 << 40)  # many ties, huge values
+            scores = rng.integers(0, 6, n_inst).astype(np.int64) * (1 << 40)  # many ties, packed path
             if case % 5 == 0:
-                scores[:] = np.iinfo(np.int64).max - 7  # all equal at the top of the range
+                scores[:] = np.iinfo(np.int64).max - 7  # all equal at the top: two-pass fallback
+            if case % 5 == 1:
+                scores = rng.integers(1 << 47, 1 << 50, n_inst).astype(np.int64)  # saturated keys
+                scores[rng.integers(0, n_inst)] = 5  # ...except one winner below saturation
+            if case % 5 == 2:
+                scores = rng.integers(1 << 47, 1 << 48, n_inst).astype(np.int64) // 3 * 3  # ties, all saturated
             mine = shard.instance_shard(n_inst, world, rank)
             out[case] = (shard.global_argmin(scores[mine], mine), int(np.argmin(scores)))
         maxes, sums = shard.reduce_max_sum([1.5 + rank, 10.0 * rank], [100 + rank, 7])
