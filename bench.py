@@ -267,6 +267,9 @@ def run_gpu(args):
         if rank == 0:
             line["dispatch_latency"] = lat
             line["dispatch_latency_mirror"] = fleet_latency(ctx)
+    if args.extra and rank == 0 and world == 1:
+        line["other_configs"] = other_configs(ctx, dev)
+        line["capacity_sweep"] = capacity_sweep(local)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -355,6 +358,111 @@ def fleet_latency(ctx, n_inst: int = 64, n_samples: int = 256, count: int = 3000
                       "(advance + what-ifs + argmin + admit), wall clock per call"}
 
 
+def device_time(ctx, ss, cfg, dev, reps: int = 5):
+    """Device-timed predict over a resident scenario set (L2 flushed between
+    launches); returns (scenarios/s, member_steps, all-OK)."""
+    import torch
+    from paper_2508_03611_b200 import abi
+    ctx.set_configs(cfg)
+    n = len(ss)
+    cols = [torch.from_numpy(c).to(dev) for c in (ss.prompt, ss.est, ss.prefill, ss.decoded)]
+    scen = torch.from_numpy(ss.scenarios.view(np.uint8)).to(dev)
+    out = torch.empty(n * abi.result_dtype.itemsize, dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    cap = ss.member_capacity(cfg)
+    f = lambda: ctx.predict_batch_device([c.data_ptr() for c in cols], scen.data_ptr(), n,
+                                         out.data_ptr(), stream.cuda_stream, member_capacity=cap)
+    for _ in range(3):
+        f()
+    ms = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        f()
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        ms.append(a.elapsed_time(b))
+    res = np.frombuffer(out.cpu().numpy().tobytes(), dtype=abi.result_dtype)
+    return n / (statistics.median(ms) / 1e3), int(res["member_steps"].sum()), bool(
+        (res["status"] == abi.OK).all())
+
+
+def other_configs(ctx, dev):
+    """BASELINE configs[0] and [2] (parity cases, reported beside the headline):
+    device-timed throughput on their captured what-if sets and the reference's
+    predict() on this host's cores over a bounded sample of the same set."""
+    from oracle.oracle import Reference
+    from paper_2508_03611_b200 import abi
+    ref = Reference()
+    threads = os.cpu_count() or 1
+    out = {}
+    for name, kw, n_inst, sample, desc in [
+        ("cfg1", dict(count=1000, estimator_kind=2, estimator_seed=1, qps=10.0, arrival_seed=1), 4,
+         4000, "4 instances, 1000 requests @ 10 QPS, Noisy(0.244) predicted lengths"),
+        ("cfg3", dict(count=2000, prompt_median=600, output_median=600, qps=5.0, arrival_seed=1), 12,
+         2400, "12 instances, long-response shape (prompt/output medians 600), 2000 requests @ 5 QPS, "
+               "KV-pressure preemption + chunked prefill"),
+    ]:
+        cfg = abi.make_config()
+        _, _, ss = ctx.replay(abi.make_workload(**kw), cfg, abi.make_replay_spec(n_inst))
+        value, msteps, ok = device_time(ctx, ss, cfg, dev)
+        sub = ss.compact(np.unique(np.linspace(0, len(ss) - 1, min(sample, len(ss))).astype(np.int64)))
+        secs = ref.time_predict(cfg, sub, threads=threads, reps=1)
+        out[name] = {"workload": desc, "scenarios": len(ss), "value": value, "unit": "scenarios/s",
+                     "all_ok": ok, "member_steps": msteps,
+                     "cpu_baseline": {"value": len(sub) / secs, "unit": "scenarios/s", "cores": threads,
+                                      "kind": "reference",
+                                      "sample": f"{len(sub)} scenarios evenly spaced over the same set"}}
+    return out
+
+
+def capacity_sweep(local: int):
+    """BASELINE configs[4]: the auto-provisioning capacity sweep on device-resident
+    closed loops (bsg_sweep_run) — the full grid on this GPU, and a 9-cell subset
+    timed against the reference's capacity_search on all host cores."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle.oracle import Reference
+    from paper_2508_03611_b200 import abi, native, sweep
+    threads = os.cpu_count() or 1
+    prof = sweep.load_profiles()
+    native.sweep_run(local, sweep.make_cells([4], prof, request_cap=50, qps_max=2)[0][:1], threads=threads)
+    full, _ = sweep.make_cells([4, 8, 16, 32, 64, 128], prof, request_cap=400, qps_max=64)
+    t0 = time.perf_counter()
+    fo = native.sweep_run(local, full, threads=threads)
+    full_s = time.perf_counter() - t0
+    sub, _ = sweep.make_cells([4, 16, 64], prof, request_cap=300, qps_max=24)
+    t0 = time.perf_counter()
+    so = native.sweep_run(local, sub, threads=threads)
+    sub_s = time.perf_counter() - t0
+    ref = Reference()
+
+    def one(c):
+        w = np.array([c["workload"]], abi.workload_dtype)
+        return ref.capacity_search(w, np.array([c["cfg"]], abi.cfg_dtype),
+                                   np.array([c["spec"]], abi.replay_spec_dtype), int(c["seed"]),
+                                   int(c["qps_min"]), int(c["qps_max"]), float(c["slo_p99_ttft_s"]))
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        rr = list(ex.map(one, sub))
+    ref_s = time.perf_counter() - t0
+    same = all(int(o["status"]) == st and (st != 0 or float(o["result"]["capacity_qps"]) ==
+                                           float(np.asarray(e["capacity_qps"]).ravel()[0]))
+               for o, (st, e, _) in zip(so, rr))
+    scen_sub = int(so["whatif_scenarios"].sum())
+    return {"metric": "capacity-sweep what-if scenarios/s (device-resident closed loops)",
+            "full_grid": {"value": int(fo["whatif_scenarios"].sum()) / full_s, "wall_s": full_s,
+                          "closed_loops": int(fo["result"]["n_tested"].sum()),
+                          "cells": "instances 4-128 x 3 profiles x QPS 1-64 (+tenths), 400 requests"},
+            "subset": {"value": scen_sub / sub_s, "wall_s": sub_s,
+                       "cells": "instances 4,16,64 x 3 profiles x QPS 1-24 (+tenths), 300 requests",
+                       "capacities_identical_to_reference": same},
+            "cpu_baseline": {"value": scen_sub / ref_s, "unit": "scenarios/s", "wall_s": ref_s,
+                             "cores": threads, "kind": "reference",
+                             "sample": "the subset's capacity_search, one cell per host thread"}}
+
+
 def cpu_baseline(ss, cfg):
     """The reference predict() (oracle/_ref, built from /root/reference) timed on
     this host's cores over the same captured scenario set (bounded sample:
@@ -410,6 +518,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-latency", dest="latency", action="store_false")
+    ap.add_argument("--no-extra", dest="extra", action="store_false",
+                    help="skip the cfg1/cfg3/cfg5 side measurements")
     args = ap.parse_args()
     line = run_reference(args) if args.impl == "reference" else run_gpu(args)
     if line is not None:

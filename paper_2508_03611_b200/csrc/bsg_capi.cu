@@ -34,7 +34,13 @@ constexpr int kPredictWarps = BSG_WPB;
 #ifndef BSG_K1_WARPS_PER_SM
 #define BSG_K1_WARPS_PER_SM 32
 #endif
-constexpr int min_blocks(int k) { return k == 1 ? BSG_K1_WARPS_PER_SM / kPredictWarps : 1; }
+// ... and for the 64-member kernels (KV-pressure sets with deep waiting queues)
+#ifndef BSG_K2_WARPS_PER_SM
+#define BSG_K2_WARPS_PER_SM 24
+#endif
+constexpr int min_blocks(int k) {
+  return k == 1 ? BSG_K1_WARPS_PER_SM / kPredictWarps : (k == 2 ? BSG_K2_WARPS_PER_SM / kPredictWarps : 1);
+}
 
 // ---- cost-aware launch order ----------------------------------------------------
 // Scenario costs vary ~100x (a scenario runs until its candidate completes, so
@@ -58,11 +64,13 @@ __device__ __forceinline__ int cost_bucket(int32_t cand_est) {
 // bucket threshold, a block-completion count, then the bucket histogram.
 struct WorkQueue {
   int32_t threshold, blocks_done;
-  int32_t heavy_count, pad;
+  int32_t heavy_count, retry_count;
   int32_t hist[kCostBuckets];
-  // followed by the heavy list: int32_t heavy[n / 16 + 32]
+  // followed by the heavy list: int32_t heavy[n / 16 + 32], then the retry
+  // list of the optimistic narrow pass: int32_t retry[n]
 };
 __device__ __forceinline__ int32_t* heavy_list(WorkQueue* q) { return reinterpret_cast<int32_t*>(q + 1); }
+__device__ __forceinline__ int32_t* retry_list(WorkQueue* q, int64_t n) { return heavy_list(q) + n / 16 + 32; }
 
 // Lists the heavy scenarios (order inside the list is arbitrary).
 __global__ void __launch_bounds__(256) heavy_list_kernel(const bsg_scenario* __restrict__ sc, int64_t n,
@@ -124,7 +132,7 @@ __global__ void __launch_bounds__(256) heavy_threshold_kernel(const bsg_scenario
   if (lane == 0) q->threshold = thr;
 }
 
-template <int K, bool POW2>
+template <int K, bool POW2, bool OPT = false>
 __device__ __forceinline__ void predict_one(const DevCfg* __restrict__ cfgs, int32_t ncfg,
                                             const int32_t* __restrict__ prompt,
                                             const int32_t* __restrict__ est,
@@ -142,7 +150,7 @@ __device__ __forceinline__ void predict_one(const DevCfg* __restrict__ cfgs, int
   }
   const DevCfg cfg = cfgs[sc.cfg];
   const int32_t need = max(sc.run_n, min(cfg.max_batch_size, sc.run_n + sc.wait_n + 1));
-  if (need > 32 * K || sc.run_n < 0 || sc.wait_n < 0) {
+  if ((!OPT && need > 32 * K) || sc.run_n < 0 || sc.wait_n < 0) {
     if ((threadIdx.x & 31) == 0) {
       bsg_result r{};
       r.status = BSG_BAD_INPUT;
@@ -150,11 +158,11 @@ __device__ __forceinline__ void predict_one(const DevCfg* __restrict__ cfgs, int
     }
     return;
   }
-  simulate_scenario<K, false, false, POW2>(cfg, prompt, est, prefill, decoded, sc, smem, o,
-                                          TraceSink{nullptr, 0});
+  simulate_scenario<K, false, false, POW2, true, OPT>(cfg, prompt, est, prefill, decoded, sc, smem, o,
+                                                     TraceSink{nullptr, 0});
 }
 
-template <int K, bool POW2>
+template <int K, bool POW2, bool OPT = false>
 __global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K))
     predict_kernel(const DevCfg* __restrict__ cfgs, int32_t ncfg,
                    const int32_t* __restrict__ prompt, const int32_t* __restrict__ est,
@@ -179,7 +187,33 @@ __global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K))
     return;
   }
   const bsg_scenario sc = scen[w];
-  predict_one<K, POW2>(cfgs, ncfg, prompt, est, prefill, decoded, sc, smem, out + w);
+  predict_one<K, POW2, OPT>(cfgs, ncfg, prompt, est, prefill, decoded, sc, smem, out + w);
+  if constexpr (OPT) {  // too wide for this pass: list it for the wide kernel
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0 && out[w].status == kStatusRetryWider)
+      retry_list(q, n)[atomicAdd(&q->retry_count, 1)] = static_cast<int32_t>(w);
+  }
+}
+
+// The wide pass over the scenarios the optimistic narrow pass handed back.
+template <int K, bool POW2>
+__global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K))
+    predict_retry_kernel(const DevCfg* __restrict__ cfgs, int32_t ncfg,
+                         const int32_t* __restrict__ prompt, const int32_t* __restrict__ est,
+                         const int32_t* __restrict__ prefill, const int32_t* __restrict__ decoded,
+                         const bsg_scenario* __restrict__ scen, int64_t n, WorkQueue* __restrict__ q,
+                         bsg_result* __restrict__ out) {
+  __shared__ int32_t smem_all[kPredictWarps * smem_words(K)];
+  const int warp = threadIdx.x >> 5;
+  int32_t* smem = smem_all + warp * smem_words(K);
+  const int32_t cnt = __ldcg(&q->retry_count);
+  const int32_t* rl = retry_list(q, n);
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * kPredictWarps + warp; j < cnt;
+       j += static_cast<int64_t>(gridDim.x) * kPredictWarps) {
+    const int64_t w = __ldcg(&rl[j]);
+    const bsg_scenario sc = scen[w];
+    predict_one<K, POW2>(cfgs, ncfg, prompt, est, prefill, decoded, sc, smem, out + w);
+  }
 }
 
 template <int K, bool POW2>
@@ -401,13 +435,31 @@ bsg_status launch_predict_t(bsg_ctx* ctx, int64_t n, const bsg_entries& e, const
   }
   // stream-ordered scratch: safe for concurrent calls on different streams
   void* mem = nullptr;
-  BSG_CUDA(ctx, cudaMallocAsync(&mem, sizeof(WorkQueue) + (n / 16 + 32) * sizeof(int32_t), s));
+  BSG_CUDA(ctx, cudaMallocAsync(&mem, sizeof(WorkQueue) + (n / 16 + 32 + n) * sizeof(int32_t), s));
   auto* q = static_cast<WorkQueue*>(mem);
   BSG_CUDA(ctx, cudaMemsetAsync(q, 0, sizeof(WorkQueue), s));
   const int64_t hb = std::min<int64_t>((n + 1023) / 1024, 148);
   heavy_threshold_kernel<<<static_cast<unsigned>(hb), 256, 0, s>>>(sc, n, q);
   heavy_list_kernel<<<static_cast<unsigned>(hb), 256, 0, s>>>(sc, n, q);
   const int64_t pb = (n + n / 16 + 32 + kPredictWarps - 1) / kPredictWarps;  // >= heavy + n warps
+  static const bool no_opt = std::getenv("BSG_NO_OPT") != nullptr;
+  if constexpr (K > 1) {
+    if (!no_opt) {
+      // Optimistic narrow pass: most scenarios' resident lists fit 32 slots even when
+      // the batch cap admits more (KV pressure keeps running sets small); the
+      // 32-slot kernel runs at 32 warps/SM with half the per-member work, and hands
+      // the rest to the wide kernel.
+      predict_kernel<1, POW2, true><<<static_cast<unsigned>(pb), kPredictWarps * 32, 0, s>>>(
+          cf, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
+      const int64_t rb = std::min<int64_t>(pb, 148 * 8);
+      predict_retry_kernel<K, POW2><<<static_cast<unsigned>(rb), kPredictWarps * 32, 0, s>>>(
+          cf, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
+      ctx->launches += 4;
+      BSG_CUDA(ctx, cudaGetLastError());
+      BSG_CUDA(ctx, cudaFreeAsync(mem, s));
+      return BSG_OK;
+    }
+  }
   predict_kernel<K, POW2><<<static_cast<unsigned>(pb), kPredictWarps * 32, 0, s>>>(
       cf, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
   ctx->launches += 3;

@@ -240,7 +240,11 @@ __device__ __forceinline__ int32_t ld_entry(const int32_t* p) {
   else return __ldcg(p);
 }
 
-template <int K, bool TRACE, bool MC = false, bool POW2 = false, bool LDG = true>
+// Internal status of an optimistic (OPT) narrow simulation whose resident list
+// would outgrow its 32K member slots: the caller re-runs it with a wider K.
+constexpr int32_t kStatusRetryWider = 100;
+
+template <int K, bool TRACE, bool MC = false, bool POW2 = false, bool LDG = true, bool OPT = false>
 __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__ g_prompt,
                                   const int32_t* __restrict__ g_est,
                                   const int32_t* __restrict__ g_prefill,
@@ -286,7 +290,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
     }
   }
   if (__any_sync(kFull, bad) || run_n > CAP) {
-    res.status = BSG_BAD_INPUT;
+    res.status = (OPT && run_n > CAP) ? kStatusRetryWider : BSG_BAD_INPUT;
     if (lane == 0) *out = res;
     return;
   }
@@ -342,7 +346,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
   const bool chunked = cfg.local_policy == BSG_CHUNKED_PREFILL;
   const int32_t maxb = cfg.max_batch_size;
 #ifdef BSG_PROFILE_ITERS
-  int64_t prof_gen = 0, prof_win = 0;
+  int64_t prof_gen = 0, prof_win = 0, prof_adm = 0, prof_pre = 0, prof_prf = 0;
 #endif
 
   for (;;) {
@@ -417,8 +421,19 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
 
     // ---------------- waiting admissions ----------------
     int32_t a = 0;  // admitted waiting heads
-    const bool try_admit =
-        waiting_nonempty && n < maxb && (chunked ? budget > 0 : true);
+    bool try_admit = waiting_nonempty && n < maxb && (chunked ? budget > 0 : true);
+    if (try_admit) {
+      // Fast reject: admission is a prefix of the waiting queue, so when the
+      // head's first chunk does not fit projected_free (backend.cpp:141-142)
+      // nothing is admitted — decided from one entry instead of materialising
+      // the queue (KV-pressure sets spend most steps here).
+      int32_t hp;
+      if (L > n) hp = read_pos<K>(prompt, n);  // victims: the waiting front
+      else if (h < wait_n) hp = ld_entry<LDG>(g_prompt + sc.wait_off + h);
+      else hp = sc.cand_prompt;
+      const int32_t hc = chunked ? (hp < budget ? hp : budget) : hp;
+      if (bnt<POW2>(hc + (hc == hp ? 1 : 0), cfg) > free_blocks - run_delta) try_admit = false;
+    }
     if (try_admit) {
       const int32_t pf = free_blocks - run_delta;  // projected_free (backend.cpp:131-133 / 158-164)
       // Materialise waiting heads at positions [L, CAP): snapshot.waiting[h..], then candidate.
@@ -472,6 +487,15 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
       }
       const int32_t first_stop = first_pos<K>(stop, CAP);
       a = first_stop - n;
+      if constexpr (OPT) {
+        // every slot admitted while the batch cap allows more and more waiting
+        // entries exist: the wider kernel must decide (resident list > 32K)
+        if (first_stop == CAP && CAP < maxb &&
+            (L - n) + (wait_n - h) + (cand_tail ? 1 : 0) > a) {
+          res.status = kStatusRetryWider;
+          break;
+        }
+      }
       // entries that were not admitted keep chunk 0 / delta 0
 #pragma unroll
       for (int k = 0; k < K; ++k) {
@@ -727,6 +751,8 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
     }
 #ifdef BSG_PROFILE_ITERS
     if (T == 0) ++prof_gen; else ++prof_win;
+    if (T == 0 && a > 0) ++prof_adm;
+    if (T == 0 && any_nonready) ++prof_prf;
 #endif
     if (T == 0) {
     // ---------------- begin_step: admissions (backend.cpp:249-261) ----------------
@@ -838,6 +864,9 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
         if (lane == 0 && steps < trace.cap) trace.rec[steps].n_preempted = 0;
       }
     }
+#ifdef BSG_PROFILE_ITERS
+    if (e_star < n_adm) ++prof_pre;
+#endif
     n = e_star;
 
     // ---------------- price the surviving plan (to_batch_plan 194-209) ----------------
@@ -1036,6 +1065,9 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
   // debug build only (tools/iterprobe.py): loop iterations by kind
   res.detail = static_cast<int32_t>(prof_gen);
   res.member_steps = prof_win;
+  res.ttft_ticks = prof_adm;    // general steps that admit
+  res.qdelay_ticks = prof_prf;  // general steps with a running partial prefill
+  res.e2e_ticks = prof_pre;     // general steps that preempt
 #endif
   if constexpr (MC) {
     int64_t tot = mc_sum;

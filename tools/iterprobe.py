@@ -16,4 +16,5 @@ for which in (sys.argv[1:] or ["cfg2", "cfg3"]):
     gen = r["detail"].astype(np.int64); win = r["member_steps"]; st = r["steps"]
     print(f"{which}: steps mean {st.mean():.1f}; general iters mean {gen.mean():.1f} (p99 {np.percentile(gen,99):.0f}); "
           f"window iters mean {win.mean():.1f} (p99 {np.percentile(win,99):.0f}); steps per window "
-          f"{(st - gen).sum() / max(win.sum(),1):.2f}")
+          f"{(st - gen).sum() / max(win.sum(),1):.2f}; general steps that admit {r['ttft_ticks'].mean():.1f}, "
+          f"with running partial prefill {r['qdelay_ticks'].mean():.1f}, that preempt {r['e2e_ticks'].mean():.1f}")

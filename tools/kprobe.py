@@ -1,7 +1,8 @@
 """Kernel tail probe: device-timed predict over the cfg2 capture in natural,
 cost-sorted (steps desc) and shuffled scenario order; per-scenario step stats.
 usage: python tools/kprobe.py [cfg2|cfg3]"""
-import os, sys
+import os, sys, signal
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
 from paper_2508_03611_b200 import abi, native

@@ -14,4 +14,4 @@ g++ -std=c++20 -O3 -fPIC -ffp-contract=off -I/usr/local/cuda/include -c -o $d/dr
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $d/lib.so $d/bsg_capi.o $d/closed_loop.o $d/drv.o -lcudart
 cp $d/lib.so gpurun_out/lib_$tag.so
 BSG_LIB_PATH=$d/lib.so timeout 600 ncu --set full --import-source on --clock-control none \
-  -k regex:predict_kernel -c 1 -o gpurun_out/prof_$tag python tools/ncu_one.py cfg2 > gpurun_out/ncu_$tag.log 2>&1
+  -k regex:predict_kernel -c 1 -o gpurun_out/prof_$tag python tools/ncu_one.py ${3:-cfg2} > gpurun_out/ncu_$tag.log 2>&1
