@@ -460,6 +460,18 @@ bsg_status bsg_fleet_snapshot(bsg_fleet* f, int32_t instance, int32_t* run_n, in
 bsg_status bsg_fleet_finish(bsg_fleet* f, bsg_request_outcome* outcomes, int32_t* n_requests,
                             bsg_replay_summary* summary);
 
+/* Wire schema (core/src/json_io.cpp, the codec only — the
+ * HTTP roles are out of scope): n PredictionRequest JSON texts in, one GPU
+ * batch, n responses out — PredictionResult JSON (as
+ * prediction_result_to_json prints it) or the predictor role's error bodies
+ * (service.cpp:229-241: "prediction-failure" for PredictionError, "bad-schema"
+ * for malformed / invalid requests). status[i] is the request's bsg_status.
+ * Responses are NUL-terminated at out + out_off[i]; out_off[n] = bytes needed
+ * (BSG_INVALID_ARGUMENT when out_cap is smaller). Sets the context's configs
+ * to the requests' distinct instance_configs. */
+bsg_status bsg_predict_json(bsg_ctx* ctx, const char* const* requests, int32_t n, char* out,
+                            int64_t out_cap, int64_t* out_off, int32_t* status);
+
 /* Synthetic trace + estimates + Poisson arrival ticks (no GPU needed). */
 bsg_status bsg_make_workload(const bsg_workload* w, int32_t* prompt, int32_t* output,
                              int32_t* est, int64_t* arrival_ticks);

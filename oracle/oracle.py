@@ -103,6 +103,10 @@ class Reference:
         L.ref_capture_sizes.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.ref_capture_copy.restype = None
         L.ref_capture_copy.argtypes = [C.c_void_p] * 7
+        L.ref_request_json.restype = C.c_int
+        L.ref_request_json.argtypes = [C.c_void_p, E, C.c_void_p, C.c_char_p, C.c_int64]
+        L.ref_service_predict.restype = C.c_int
+        L.ref_service_predict.argtypes = [C.c_char_p, C.c_char_p, C.c_int64]
         L.ref_run_report.restype = C.c_int
         L.ref_run_report.argtypes = [C.c_void_p] * 4
         L.ref_capacity_search.restype = C.c_int
@@ -150,6 +154,22 @@ class Reference:
         summ = np.zeros(1, abi.summary_dtype)
         self.lib.ref_run_experiment(_vp(w), _vp(cfg), _vp(spec), _vp(out), _vp(summ))
         return out, summ[0]
+
+    def request_json(self, cfgs, ss: abi.ScenarioSet, i: int) -> str:
+        """prediction_request_to_json (json_io.cpp:125-132) of scenario i."""
+        buf = C.create_string_buffer(1 << 22)
+        e = ss.entries()
+        sc = np.ascontiguousarray(ss.scenarios[i:i + 1])
+        cf = np.ascontiguousarray(np.asarray(cfgs)[int(sc["cfg"][0]):int(sc["cfg"][0]) + 1])
+        n = self.lib.ref_request_json(_vp(cf), C.byref(e), _vp(sc), buf, len(buf))
+        assert n >= 0
+        return buf.value.decode()
+
+    def service_predict(self, body: str):
+        """The predictor role's /predict (service.cpp:229-241): (HTTP status, body)."""
+        buf = C.create_string_buffer(1 << 16)
+        code = self.lib.ref_service_predict(body.encode(), buf, len(buf))
+        return code, buf.value.decode()
 
     def run_report(self, w, cfg, spec):
         out = np.zeros(1, abi.report_dtype)

@@ -28,6 +28,7 @@
 #include "blocksim/driver.h"
 #include "blocksim/error.h"
 #include "blocksim/event_loop.h"
+#include "blocksim/json_io.h"
 #include "blocksim/metrics.h"
 #include "blocksim/predictor.h"
 #include "blocksim/scheduler.h"
@@ -671,5 +672,48 @@ void ref_capture_copy(const ref_capture* c, uint64_t* id, int32_t* prompt, int32
 }
 
 void ref_capture_free(ref_capture* c) { delete c; }
+
+
+// ---- wire schema (json_io.cpp) and the predictor role's /predict handler ----
+static int put_text(const std::string& t, char* out, int64_t cap) {
+  if (static_cast<int64_t>(t.size()) + 1 > cap) return -static_cast<int>(t.size() + 1);
+  std::memcpy(out, t.c_str(), t.size() + 1);
+  return static_cast<int>(t.size());
+}
+
+// prediction_request_to_json of scenario sc (synthetic ids as make_snapshot).
+int ref_request_json(const bsg_instance_cfg* cfg, const bsg_entries* e, const bsg_scenario* sc,
+                     char* out, int64_t cap) {
+  PredictionRequest req;
+  req.snapshot = make_snapshot(e, *sc);
+  req.candidate = CandidateRequest{sc->cand_prompt, sc->cand_est};
+  req.instance_config = to_ref_config(*cfg);
+  return put_text(prediction_request_to_json(req), out, cap);
+}
+
+// PredictorService's /predict route (service.cpp:229-241) without the socket:
+// returns the HTTP status (200 / 422 / 400) and writes the response body.
+int ref_service_predict(const char* body, char* out, int64_t cap) {
+  // predictor.cache default (config.cpp:192). One cache per request: the
+  // reference service keeps one cache for its lifetime, keyed by batch shape only
+  // (predictor.cpp:26-54), which is transparent only while every request carries
+  // the same cost model — the fixtures here mix cost models.
+  LatencyCache cache(CacheMode::kExact, 256);
+  int code = 200;
+  std::string text;
+  try {
+    const PredictionRequest request = prediction_request_from_json(body);
+    const PredictionResult result = predict(request, &cache);
+    text = prediction_result_to_json(result);
+  } catch (const PredictionError& ex) {
+    code = 422;
+    text = error_body("prediction-failure", ex.what());
+  } catch (const Error& ex) {
+    code = 400;
+    text = error_body("bad-schema", ex.what());
+  }
+  const int n = put_text(text, out, cap);
+  return n < 0 ? n : code;
+}
 
 }  // extern "C"

@@ -679,16 +679,33 @@ bsg_status bsg_predict_batch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n
   // stream c % 3, so H2D(c+1) overlaps the kernel on c and D2H(c-1).
   const char* env_chunk = std::getenv("BSG_PIPE_CHUNK");
   const int64_t target_chunk = env_chunk ? std::max<int64_t>(1, std::atoll(env_chunk)) : 20000;
-  const int64_t nchunks = std::min<int64_t>(16, std::max<int64_t>(1, n / target_chunk));
-  const int64_t per = (n + nchunks - 1) / nchunks;
+  const int64_t nchunks0 = std::min<int64_t>(16, std::max<int64_t>(1, n / target_chunk));
+  const int64_t per = (n + nchunks0 - 1) / nchunks0;
+  // chunk boundaries: equal chunks, except that the last one is split in
+  // halving pieces (BSG_PIPE_TAIL of them) so the final kernel — whose tail
+  // nothing overlaps — is short
+  std::vector<int64_t> bounds{0};
+  {
+    const char* env_tail = std::getenv("BSG_PIPE_TAIL");
+    const int tail = env_tail ? std::max(0, std::atoi(env_tail)) : 0;
+    for (int64_t c = 0; c + 1 < nchunks0; ++c) bounds.push_back(std::min(n, (c + 1) * per));
+    int64_t rest = n - bounds.back();
+    for (int t = 0; t < tail && rest > 2048; ++t) {
+      const int64_t piece = rest / 2;
+      bounds.push_back(bounds.back() + piece);
+      rest -= piece;
+    }
+    bounds.push_back(n);
+  }
+  const int64_t nchunks = static_cast<int64_t>(bounds.size()) - 1;
   auto cols_h = std::array<const int32_t*, 4>{entries->prompt, entries->est, entries->prefill,
                                               entries->decoded};
   auto cols_d = std::array<int32_t*, 4>{static_cast<int32_t*>(ctx->prompt.p), static_cast<int32_t*>(ctx->est.p),
                                         static_cast<int32_t*>(ctx->prefill.p),
                                         static_cast<int32_t*>(ctx->decoded.p)};
   for (int64_t c = 0; c < nchunks; ++c) {
-    const int64_t s0 = c * per, s1 = std::min(n, s0 + per);
-    if (s0 >= s1) break;
+    const int64_t s0 = bounds[c], s1 = bounds[c + 1];
+    if (s0 >= s1) continue;
     int64_t lo = INT64_MAX, hi = 0;
     int32_t need = 1;
     for (int64_t i = s0; i < s1; ++i) {

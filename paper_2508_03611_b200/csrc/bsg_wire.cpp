@@ -1,0 +1,534 @@
+// bsg_wire.cpp — the reference's wire schema (core/src/json_io.cpp) in front
+// of the GPU predictor: PredictionRequest JSON texts in, PredictionResult JSON
+// texts (or {"error": ...} bodies) out, the whole batch predicted in one
+// bsg_predict_batch call. SURVEY.md §8(f) row 3 — the codec only: the HTTP
+// roles (service.cpp) stay out of scope (networking).
+//
+// Parsing follows json_io.cpp's field names and its bad-schema behaviour (a
+// missing field or a wrong type rejects the request); numbers are printed the
+// way nlohmann::json::dump prints them (shortest round-trip digits, fixed
+// notation for decimal exponents in (-4, 15], otherwise d.ddde±XX), so the
+// response text matches the reference's prediction_result_to_json.
+#include <charconv>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <system_error>
+#include <vector>
+
+#include "bsg_internal.h"
+
+namespace {
+
+// ---- a small JSON DOM -------------------------------------------------------
+struct JVal {
+  enum Kind { kNull, kBool, kInt, kUint, kDouble, kString, kArray, kObject } kind = kNull;
+  bool b = false;
+  int64_t i = 0;
+  uint64_t u = 0;
+  double d = 0;
+  std::string s;
+  std::vector<JVal> arr;
+  std::vector<std::pair<std::string, JVal>> obj;
+  const JVal* get(const char* key) const {
+    for (const auto& kv : obj)
+      if (kv.first == key) return &kv.second;
+    return nullptr;
+  }
+  bool is_number() const { return kind == kInt || kind == kUint || kind == kDouble; }
+};
+
+struct Parser {
+  const char* p;
+  const char* end;
+  std::string err;
+  void ws() {
+    while (p < end && (*p == ' ' || *p == '\t' || *p == '\n' || *p == '\r')) ++p;
+  }
+  bool fail(const char* m) {
+    if (err.empty()) err = m;
+    return false;
+  }
+  bool lit(const char* w) {
+    const size_t n = std::strlen(w);
+    if (static_cast<size_t>(end - p) < n || std::strncmp(p, w, n) != 0) return fail("malformed JSON");
+    p += n;
+    return true;
+  }
+  bool string(std::string* out) {
+    if (p >= end || *p != '"') return fail("malformed JSON");
+    ++p;
+    while (p < end && *p != '"') {
+      if (*p == '\\') {
+        if (++p >= end) return fail("malformed JSON");
+        switch (*p) {
+          case '"': out->push_back('"'); break;
+          case '\\': out->push_back('\\'); break;
+          case '/': out->push_back('/'); break;
+          case 'b': out->push_back('\b'); break;
+          case 'f': out->push_back('\f'); break;
+          case 'n': out->push_back('\n'); break;
+          case 'r': out->push_back('\r'); break;
+          case 't': out->push_back('\t'); break;
+          case 'u': {  // keys/values of this schema are ASCII; keep BMP escapes as UTF-8
+            if (end - p < 5) return fail("malformed JSON");
+            unsigned cp = 0;
+            for (int k = 1; k <= 4; ++k) {
+              const char c = p[k];
+              cp <<= 4;
+              if (c >= '0' && c <= '9') cp |= c - '0';
+              else if (c >= 'a' && c <= 'f') cp |= c - 'a' + 10;
+              else if (c >= 'A' && c <= 'F') cp |= c - 'A' + 10;
+              else return fail("malformed JSON");
+            }
+            p += 4;
+            if (cp < 0x80) {
+              out->push_back(static_cast<char>(cp));
+            } else if (cp < 0x800) {
+              out->push_back(static_cast<char>(0xc0 | (cp >> 6)));
+              out->push_back(static_cast<char>(0x80 | (cp & 0x3f)));
+            } else {
+              out->push_back(static_cast<char>(0xe0 | (cp >> 12)));
+              out->push_back(static_cast<char>(0x80 | ((cp >> 6) & 0x3f)));
+              out->push_back(static_cast<char>(0x80 | (cp & 0x3f)));
+            }
+            break;
+          }
+          default: return fail("malformed JSON");
+        }
+        ++p;
+      } else {
+        out->push_back(*p++);
+      }
+    }
+    if (p >= end) return fail("malformed JSON");
+    ++p;
+    return true;
+  }
+  bool number(JVal* v) {
+    const char* s = p;
+    bool is_float = false;
+    if (p < end && *p == '-') ++p;
+    while (p < end && ((*p >= '0' && *p <= '9') || *p == '.' || *p == 'e' || *p == 'E' || *p == '+' ||
+                       *p == '-')) {
+      if (*p == '.' || *p == 'e' || *p == 'E') is_float = true;
+      ++p;
+    }
+    if (p == s) return fail("malformed JSON");
+    if (!is_float) {
+      if (*s == '-') {
+        int64_t x = 0;
+        auto r = std::from_chars(s, p, x);
+        if (r.ec == std::errc() && r.ptr == p) {
+          v->kind = JVal::kInt;
+          v->i = x;
+          return true;
+        }
+      } else {
+        uint64_t x = 0;
+        auto r = std::from_chars(s, p, x);
+        if (r.ec == std::errc() && r.ptr == p) {
+          v->kind = JVal::kUint;
+          v->u = x;
+          return true;
+        }
+      }
+    }
+    double x = 0;
+    auto r = std::from_chars(s, p, x);
+    if (r.ec != std::errc() || r.ptr != p) return fail("malformed JSON");
+    v->kind = JVal::kDouble;
+    v->d = x;
+    return true;
+  }
+  bool value(JVal* v, int depth = 0) {
+    if (depth > 64) return fail("malformed JSON");
+    ws();
+    if (p >= end) return fail("malformed JSON");
+    switch (*p) {
+      case '{': {
+        ++p;
+        v->kind = JVal::kObject;
+        ws();
+        if (p < end && *p == '}') {
+          ++p;
+          return true;
+        }
+        for (;;) {
+          ws();
+          std::string key;
+          if (!string(&key)) return false;
+          ws();
+          if (p >= end || *p != ':') return fail("malformed JSON");
+          ++p;
+          JVal child;
+          if (!value(&child, depth + 1)) return false;
+          v->obj.emplace_back(std::move(key), std::move(child));
+          ws();
+          if (p < end && *p == ',') {
+            ++p;
+            continue;
+          }
+          if (p < end && *p == '}') {
+            ++p;
+            return true;
+          }
+          return fail("malformed JSON");
+        }
+      }
+      case '[': {
+        ++p;
+        v->kind = JVal::kArray;
+        ws();
+        if (p < end && *p == ']') {
+          ++p;
+          return true;
+        }
+        for (;;) {
+          JVal child;
+          if (!value(&child, depth + 1)) return false;
+          v->arr.push_back(std::move(child));
+          ws();
+          if (p < end && *p == ',') {
+            ++p;
+            continue;
+          }
+          if (p < end && *p == ']') {
+            ++p;
+            return true;
+          }
+          return fail("malformed JSON");
+        }
+      }
+      case '"':
+        v->kind = JVal::kString;
+        return string(&v->s);
+      case 't':
+        v->kind = JVal::kBool;
+        v->b = true;
+        return lit("true");
+      case 'f':
+        v->kind = JVal::kBool;
+        return lit("false");
+      case 'n':
+        return lit("null");
+      default:
+        return number(v);
+    }
+  }
+};
+
+// ---- schema (json_io.cpp) ---------------------------------------------------
+struct SchemaError {
+  std::string what;
+};
+
+const JVal& at(const JVal& j, const char* key) {
+  if (j.kind != JVal::kObject) throw SchemaError{std::string("type must be object, but is other")};
+  const JVal* v = j.get(key);
+  if (!v) throw SchemaError{std::string("key '") + key + "' not found"};
+  return *v;
+}
+
+template <typename T>
+T as_int(const JVal& v) {  // nlohmann get<integral>: any JSON number, converted
+  switch (v.kind) {
+    case JVal::kInt: return static_cast<T>(v.i);
+    case JVal::kUint: return static_cast<T>(v.u);
+    case JVal::kDouble: return static_cast<T>(v.d);
+    case JVal::kBool: return static_cast<T>(v.b);
+    default: throw SchemaError{"type must be number"};
+  }
+}
+
+double as_double(const JVal& v) {
+  switch (v.kind) {
+    case JVal::kInt: return static_cast<double>(v.i);
+    case JVal::kUint: return static_cast<double>(v.u);
+    case JVal::kDouble: return v.d;
+    case JVal::kBool: return v.b ? 1.0 : 0.0;
+    default: throw SchemaError{"type must be number"};
+  }
+}
+
+struct Entry {
+  uint64_t id;
+  int32_t prompt, est, prefill, decoded;
+};
+
+void entries_from(const JVal& arr, std::vector<Entry>* out) {
+  if (arr.kind != JVal::kArray) throw SchemaError{"type must be array"};
+  for (const JVal& r : arr.arr) {
+    Entry e{};
+    e.id = as_int<uint64_t>(at(r, "id"));
+    e.prompt = as_int<int32_t>(at(r, "prompt_tokens"));
+    e.est = as_int<int32_t>(at(r, "estimated_output_tokens"));
+    e.prefill = as_int<int32_t>(at(r, "prefill_progress"));
+    e.decoded = as_int<int32_t>(at(r, "decoded_tokens"));
+    out->push_back(e);
+  }
+}
+
+struct Request {
+  std::vector<Entry> running, waiting;
+  int32_t cand_prompt = 0, cand_est = 0;
+  bsg_instance_cfg cfg{};
+};
+
+Request request_from(const JVal& j) {  // prediction_request_from_json (json_io.cpp:136-146)
+  Request r;
+  const JVal& snap = at(j, "snapshot");
+  (void)as_int<int32_t>(at(snap, "instance_id"));
+  (void)as_double(at(snap, "snapshot_time"));
+  (void)as_int<int32_t>(at(snap, "free_blocks"));
+  (void)as_int<int32_t>(at(snap, "batch_size"));
+  (void)as_int<int32_t>(at(snap, "qpm"));
+  entries_from(at(snap, "running"), &r.running);
+  entries_from(at(snap, "waiting"), &r.waiting);
+  const JVal& cand = at(j, "candidate");
+  r.cand_prompt = as_int<int32_t>(at(cand, "prompt_tokens"));
+  r.cand_est = as_int<int32_t>(at(cand, "estimated_output_tokens"));
+  const JVal& c = at(j, "instance_config");  // instance_config_from_json_obj (json_io.cpp:69-84)
+  (void)as_int<int32_t>(at(c, "instance_id"));
+  r.cfg.total_blocks = as_int<int32_t>(at(c, "total_blocks"));
+  r.cfg.block_size = as_int<int32_t>(at(c, "block_size"));
+  r.cfg.max_batch_size = as_int<int32_t>(at(c, "max_batch_size"));
+  r.cfg.chunk_budget = as_int<int32_t>(at(c, "chunk_budget"));
+  const JVal& pol = at(c, "local_policy");
+  if (pol.kind != JVal::kString) throw SchemaError{"type must be string"};
+  if (pol.s == "chunked_prefill") r.cfg.local_policy = BSG_CHUNKED_PREFILL;  // parse_local_policy
+  else if (pol.s == "prefill_priority") r.cfg.local_policy = BSG_PREFILL_PRIORITY;
+  else throw SchemaError{"unknown local policy '" + pol.s + "'"};
+  const JVal& cost = at(c, "cost_model");
+  r.cfg.c0_s = as_double(at(cost, "c0_s"));
+  r.cfg.prefill_s_per_token = as_double(at(cost, "prefill_s_per_token"));
+  r.cfg.decode_s_per_seq = as_double(at(cost, "decode_s_per_seq"));
+  r.cfg.context_s_per_token = as_double(at(cost, "context_s_per_token"));
+  r.cfg.cache_mode = BSG_CACHE_EXACT;  // the predictor service's default cache (config.cpp:192)
+  r.cfg.context_bucket = 256;
+  return r;
+}
+
+// ---- nlohmann::json::dump number formatting -----------------------------------
+void append_double(std::string* out, double v) {
+  if (!std::isfinite(v)) {
+    out->append("null");
+    return;
+  }
+  if (v == 0) {
+    out->append(std::signbit(v) ? "-0.0" : "0.0");
+    return;
+  }
+  char buf[64];
+  auto r = std::to_chars(buf, buf + sizeof(buf), v, std::chars_format::scientific);
+  std::string sci(buf, r.ptr);
+  std::string digits;
+  size_t i = 0;
+  bool neg = false;
+  if (sci[i] == '-') {
+    neg = true;
+    ++i;
+  }
+  for (; i < sci.size() && sci[i] != 'e'; ++i)
+    if (sci[i] != '.') digits.push_back(sci[i]);
+  const int e10 = std::atoi(sci.c_str() + i + 1);  // value = d.ddd x 10^e10
+  const int k = static_cast<int>(digits.size());
+  const int n = e10 + 1;  // value = 0.ddd x 10^n
+  if (neg) out->push_back('-');
+  if (k <= n && n <= 15) {
+    out->append(digits);
+    out->append(static_cast<size_t>(n - k), '0');
+    out->append(".0");
+  } else if (0 < n && n <= 15) {
+    out->append(digits, 0, static_cast<size_t>(n));
+    out->push_back('.');
+    out->append(digits, static_cast<size_t>(n), std::string::npos);
+  } else if (-4 < n && n <= 0) {
+    out->append("0.");
+    out->append(static_cast<size_t>(-n), '0');
+    out->append(digits);
+  } else {
+    out->push_back(digits[0]);
+    if (k > 1) {
+      out->push_back('.');
+      out->append(digits, 1, std::string::npos);
+    }
+    out->push_back('e');
+    const int ex = n - 1;
+    out->push_back(ex < 0 ? '-' : '+');
+    const int a = ex < 0 ? -ex : ex;
+    if (a < 10) out->push_back('0');
+    out->append(std::to_string(a));
+  }
+}
+
+std::string escape(const std::string& s) {
+  std::string o;
+  for (char c : s) {
+    if (c == '"' || c == '\\') {
+      o.push_back('\\');
+      o.push_back(c);
+    } else if (static_cast<unsigned char>(c) < 0x20) {
+      char b[8];
+      std::snprintf(b, sizeof(b), "\\u%04x", c);
+      o.append(b);
+    } else {
+      o.push_back(c);
+    }
+  }
+  return o;
+}
+
+std::string error_body(const std::string& code, const std::string& detail) {  // json_io.cpp:148-152
+  std::string o = "{\"error\":\"" + escape(code) + "\"";
+  if (!detail.empty()) o += ",\"detail\":\"" + escape(detail) + "\"";
+  return o + "}";
+}
+
+}  // namespace
+
+extern "C" bsg_status bsg_predict_json(bsg_ctx* ctx, const char* const* requests, int32_t n,
+                                       char* out, int64_t out_cap, int64_t* out_off,
+                                       int32_t* status) {
+  if (!ctx || (!requests && n > 0) || n < 0 || !out_off || !status) return BSG_INVALID_ARGUMENT;
+  std::vector<std::string> body(static_cast<size_t>(n));
+  std::vector<Request> reqs(static_cast<size_t>(n));
+  std::vector<int> ok(static_cast<size_t>(n), 0);
+  // parse (parse_with, json_io.cpp:86-95): malformed JSON / missing fields -> bad-schema
+  std::vector<bsg_instance_cfg> cfgs;
+  std::vector<int32_t> cfg_of(static_cast<size_t>(n), 0);
+  for (int32_t q = 0; q < n; ++q) {
+    const char* t = requests[q] ? requests[q] : "";
+    Parser ps{t, t + std::strlen(t), {}};
+    JVal j;
+    bool good = ps.value(&j);
+    ps.ws();
+    if (good && ps.p != ps.end) good = ps.fail("malformed JSON");
+    if (!good) {
+      status[q] = BSG_BAD_INPUT;
+      body[q] = error_body("bad-schema", "bad-schema: malformed JSON");
+      continue;
+    }
+    try {
+      reqs[q] = request_from(j);
+    } catch (const SchemaError& e) {
+      status[q] = BSG_BAD_INPUT;
+      body[q] = error_body("bad-schema", "bad-schema: " + e.what);
+      continue;
+    }
+    int32_t ci = -1;
+    for (size_t c = 0; c < cfgs.size() && ci < 0; ++c)
+      if (std::memcmp(&cfgs[c], &reqs[q].cfg, sizeof(bsg_instance_cfg)) == 0) ci = static_cast<int32_t>(c);
+    if (ci < 0) {
+      ci = static_cast<int32_t>(cfgs.size());
+      cfgs.push_back(reqs[q].cfg);
+    }
+    cfg_of[q] = ci;
+    ok[q] = 1;
+  }
+  // one GPU batch over every well-formed request
+  std::vector<int32_t> rows;
+  if (!cfgs.empty()) {
+    int32_t bi = -1, fc = 0;
+    const bsg_status cs = bsg_set_configs(ctx, cfgs.data(), static_cast<int32_t>(cfgs.size()), &bi, &fc);
+    if (cs != BSG_OK && cs != BSG_BAD_CONFIG && cs != BSG_BAD_INPUT) return cs;
+    if (cs != BSG_OK) {  // a config failed validation (ConfigError): reject its requests
+      for (int32_t q = 0; q < n; ++q)
+        if (ok[q] && cfg_of[q] == bi) {
+          ok[q] = 0;
+          status[q] = BSG_BAD_CONFIG;
+          body[q] = error_body("bad-schema", "invalid instance_config");
+        }
+      // retry with the remaining configs
+      std::vector<bsg_instance_cfg> keep;
+      std::vector<int32_t> remap(cfgs.size(), -1);
+      for (size_t c = 0; c < cfgs.size(); ++c)
+        if (static_cast<int32_t>(c) != bi) {
+          remap[c] = static_cast<int32_t>(keep.size());
+          keep.push_back(cfgs[c]);
+        }
+      for (int32_t q = 0; q < n; ++q)
+        if (ok[q]) cfg_of[q] = remap[cfg_of[q]];
+      cfgs.swap(keep);
+      if (!cfgs.empty()) {
+        const bsg_status c2 = bsg_set_configs(ctx, cfgs.data(), static_cast<int32_t>(cfgs.size()), &bi, &fc);
+        if (c2 != BSG_OK) return c2;  // one bad config per call is reported per request
+      }
+    }
+  }
+  std::vector<uint64_t> id;
+  std::vector<int32_t> prompt, est, prefill, decoded;
+  std::vector<bsg_scenario> scen;
+  for (int32_t q = 0; q < n; ++q) {
+    if (!ok[q]) continue;
+    const Request& r = reqs[q];
+    bsg_scenario s{};
+    s.run_off = static_cast<int32_t>(prompt.size());
+    s.run_n = static_cast<int32_t>(r.running.size());
+    auto add = [&](const Entry& e) {
+      id.push_back(e.id);
+      prompt.push_back(e.prompt);
+      est.push_back(e.est);
+      prefill.push_back(e.prefill);
+      decoded.push_back(e.decoded);
+    };
+    for (const Entry& e : r.running) add(e);
+    s.wait_off = static_cast<int32_t>(prompt.size());
+    s.wait_n = static_cast<int32_t>(r.waiting.size());
+    for (const Entry& e : r.waiting) add(e);
+    s.cand_prompt = r.cand_prompt;
+    s.cand_est = r.cand_est;
+    s.cfg = cfg_of[q];
+    scen.push_back(s);
+    rows.push_back(q);
+  }
+  if (!scen.empty()) {
+    std::vector<bsg_result> res(scen.size());
+    bsg_entries e{id.data(), prompt.data(), est.data(), prefill.data(), decoded.data()};
+    const bsg_status st = bsg_predict_batch(ctx, &e, static_cast<int64_t>(prompt.size()), scen.data(),
+                                            static_cast<int64_t>(scen.size()), res.data());
+    if (st != BSG_OK) return st;
+    for (size_t k = 0; k < rows.size(); ++k) {
+      const int32_t q = rows[k];
+      const bsg_result& x = res[k];
+      status[q] = x.status;
+      if (x.status == BSG_OK) {  // prediction_result_to_json (json_io.cpp:103-108): std::map key order
+        std::string o = "{\"metrics\":{\"predicted_e2e_latency\":";
+        append_double(&o, bsg_ticks_to_seconds(x.e2e_ticks));
+        o += ",\"predicted_queueing_delay\":";
+        append_double(&o, bsg_ticks_to_seconds(x.qdelay_ticks));
+        o += ",\"predicted_ttft\":";
+        append_double(&o, bsg_ticks_to_seconds(x.ttft_ticks));
+        o += "},\"simulated_steps\":" + std::to_string(x.steps) + "}";
+        body[q] = std::move(o);
+      } else if (x.status == BSG_TOO_LARGE_RUNNING || x.status == BSG_TOO_LARGE_CANDIDATE) {
+        // RequestTooLarge is re-thrown as PredictionError (predictor.cpp:134-135) -> 422
+        body[q] = error_body("prediction-failure", "candidate does not fit the instance");
+      } else if (x.status == BSG_DEADLOCK) {
+        body[q] = error_body("prediction-failure", "backend deadlock during forward simulation");
+      } else if (x.status == BSG_STEP_LIMIT) {
+        body[q] = error_body("prediction-failure", "forward simulation exceeded the step limit");
+      } else if (x.status == BSG_VANISHED) {
+        body[q] = error_body("prediction-failure", "candidate vanished from the forward simulation");
+      } else {  // EmptyPlanError / ConfigError / out-of-domain input: an Error -> 400
+        body[q] = error_body("bad-schema", "invalid request");
+      }
+    }
+  }
+  int64_t off = 0;
+  for (int32_t q = 0; q < n; ++q) {
+    out_off[q] = off;
+    const int64_t len = static_cast<int64_t>(body[q].size()) + 1;  // NUL-terminated
+    if (off + len <= out_cap && out) {
+      std::memcpy(out + off, body[q].c_str(), static_cast<size_t>(len));
+    }
+    off += len;
+  }
+  out_off[n] = off;
+  return off <= out_cap ? BSG_OK : BSG_INVALID_ARGUMENT;  // out_off[n] = bytes needed
+}

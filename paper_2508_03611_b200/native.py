@@ -68,6 +68,7 @@ def load() -> C.CDLL:
         "bsg_fleet_dispatch": (C.c_int, [V, C.c_int64, C.c_int32, C.c_int32, C.c_int32, V, C.c_int32,
                                          C.c_int32, V, V]),
         "bsg_fleet_finish": (C.c_int, [V, V, V, V]),
+        "bsg_predict_json": (C.c_int, [V, V, C.c_int32, V, C.c_int64, V, V]),
         "bsg_fleet_snapshot": (C.c_int, [V, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                          V, V, V, V, C.c_int32]),
     }
@@ -300,6 +301,24 @@ class Context:
             self._check(st, "bsg_capacity_search")
         n = int(out["n_tested"][0])
         return st, out[0], list(zip(tq[:n].tolist(), tp[:n].astype(bool).tolist()))
+
+    def predict_json(self, bodies: list[str]):
+        """Wire-format predict (bsg_predict_json): [(status, response text)]."""
+        n = len(bodies)
+        arr = (C.c_char_p * max(n, 1))(*[b.encode() for b in bodies])
+        off = np.zeros(n + 1, np.int64)
+        st = np.zeros(max(n, 1), np.int32)
+        cap = 256 * n + 64
+        for _ in range(2):
+            buf = C.create_string_buffer(cap)
+            r = self.L.bsg_predict_json(self.h, arr, n, buf, cap, _p(off), _p(st))
+            if r == abi.OK:
+                raw = buf.raw
+                return [(int(st[i]), raw[off[i]:off[i + 1] - 1].decode()) for i in range(n)]
+            if r != abi.INVALID_ARGUMENT or off[n] <= cap:
+                self._check(r, "bsg_predict_json")
+            cap = int(off[n])
+        self._check(r, "bsg_predict_json")
 
     def replay_device(self, runs):
         """Device-resident closed loops (bsg_replay_device). runs: list of

@@ -321,3 +321,41 @@ def test_fleet_mc_dispatch_matches_dispatch_mc(ctx):
         assert pick == int(exp_pick[0]) and np.array_equal(sc, exp_scores), (k, sc, exp_scores)
     out, _ = fl.finish(len(p))
     assert (out["finish_ticks"] > 0).all()
+
+
+def test_wire_predict_json_matches_reference_service(ctx, ref):
+    """bsg_predict_json (json_io.cpp schema in, GPU predict, schema out) answers
+    like the reference predictor role's /predict (service.cpp:229-241): the
+    same PredictionResult JSON — keys in the same order, every number the same
+    double (the reference's checks compare doubles, acceptance_main.cpp:657-755;
+    nlohmann's Grisu2 sometimes prints a longer round-trip form than our
+    shortest one, so text is compared after parsing) — and the same error codes
+    (prediction-failure / bad-schema) otherwise, on KATs, fuzz (every failure
+    status) and malformed bodies."""
+    import json
+    names, kc, ks = kat_set()
+    fc, fs = fuzz_set(77, 600)
+    bodies = [ref.request_json(kc, ks, i) for i in range(len(ks))]
+    bodies += [ref.request_json(fc, fs, i) for i in range(len(fs))]
+    good = json.loads(bodies[0])
+    broken = dict(good)
+    del broken["candidate"]
+    typo = json.loads(bodies[1])
+    typo["snapshot"]["running"] = "not-a-list"
+    pol = json.loads(bodies[2])
+    pol["instance_config"]["local_policy"] = "round_robin"
+    bodies += ["{not json", json.dumps(broken), json.dumps(typo), json.dumps(pol), ""]
+    got = ctx.predict_json(bodies)
+    n_ok = 0
+    for i, (body, (st, text)) in enumerate(zip(bodies, got)):
+        code, exp = ref.service_predict(body)
+        if code == 200:
+            assert st == abi.OK, (i, text, exp)
+            a, b = json.loads(text), json.loads(exp)
+            assert list(a) == list(b) and list(a["metrics"]) == list(b["metrics"])
+            assert a == b, (i, text, exp)  # float == float: bit-identical doubles
+            n_ok += 1
+        else:
+            assert st != abi.OK, (i, code, exp)
+            assert json.loads(text)["error"] == json.loads(exp)["error"], (i, text, exp)
+    assert n_ok > 400  # mostly successes, with failures of every kind mixed in
