@@ -403,25 +403,36 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
         decode_item[k] = !prefill_step && ready[k];
       }
     }
-    // deltas of running items (make_item, backend.cpp:94-111)
+    // deltas of running items (make_item, backend.cpp:94-111) — computed only
+    // when a waiting head is examined or a general step runs: a pure-decode
+    // window derives its block demand itself
     int32_t delta[K], stored[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      stored[k] = prefill[k] + decoded[k];
-      int32_t ns = stored[k];
-      if (decode_item[k]) {
-        ns = stored[k] + 1;
-      } else if (chunk[k] > 0) {
-        const int32_t np = prefill[k] + chunk[k];
-        ns = np + decoded[k] + (np == prompt[k] ? 1 : 0);
+    for (int k = 0; k < K; ++k) stored[k] = prefill[k] + decoded[k];
+    bool delta_ready = false;
+    auto running_deltas = [&]() {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        int32_t ns = stored[k];
+        if (decode_item[k]) {
+          ns = stored[k] + 1;
+        } else if (chunk[k] > 0) {
+          const int32_t np = prefill[k] + chunk[k];
+          ns = np + decoded[k] + (np == prompt[k] ? 1 : 0);
+        }
+        delta[k] = (decode_item[k] || chunk[k] > 0) ? bnt<POW2>(ns, cfg) - bnt<POW2>(stored[k], cfg) : 0;
       }
-      delta[k] = (decode_item[k] || chunk[k] > 0) ? bnt<POW2>(ns, cfg) - bnt<POW2>(stored[k], cfg) : 0;
-    }
-    const int32_t run_delta = warp_sum<K>(delta);
+      delta_ready = true;
+    };
 
     // ---------------- waiting admissions ----------------
     int32_t a = 0;  // admitted waiting heads
+    int32_t run_delta = 0;
     bool try_admit = waiting_nonempty && n < maxb && (chunked ? budget > 0 : true);
+    if (try_admit) {
+      running_deltas();
+      run_delta = warp_sum<K>(delta);
+    }
     if (try_admit) {
       // Fast reject: admission is a prefix of the waiting queue, so when the
       // head's first chunk does not fit projected_free (backend.cpp:141-142)
@@ -515,6 +526,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
         const int32_t ns = stored[k] + 1;
         delta[k] = ready[k] ? bnt<POW2>(ns, cfg) - bnt<POW2>(stored[k], cfg) : 0;
       }
+      delta_ready = true;
     }
     if (n == 0 && a == 0) {  // backend.cpp:245
       res.status = BSG_EMPTY_PLAN;
@@ -540,6 +552,9 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
     int64_t win_pre[kWinJ];
     int64_t win_base = 0;
     if (a == 0 && D == n && n > 0 && !prefill_step) {
+#ifdef BSG_PROFILE_WENTRY
+      ++prof_pre;  // debug: window entries (reported in the preempt counter's slot)
+#endif
       constexpr int J = kWinJ, W = kWin;
       int32_t* h_cnt = smem;          // members completing at the end of step s
       int32_t* h_sst = smem + W;      // their stored tokens at window start
@@ -754,6 +769,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
     if (T == 0 && a > 0) ++prof_adm;
     if (T == 0 && any_nonready) ++prof_prf;
 #endif
+    if (T == 0 && !delta_ready) running_deltas();
     if (T == 0) {
     // ---------------- begin_step: admissions (backend.cpp:249-261) ----------------
     const int32_t n_adm = n + a;
@@ -864,7 +880,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
         if (lane == 0 && steps < trace.cap) trace.rec[steps].n_preempted = 0;
       }
     }
-#ifdef BSG_PROFILE_ITERS
+#if defined(BSG_PROFILE_ITERS) && !defined(BSG_PROFILE_WENTRY)
     if (e_star < n_adm) ++prof_pre;
 #endif
     n = e_star;
