@@ -688,6 +688,11 @@ bsg_status bsg_predict_batch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n
   {
     const char* env_tail = std::getenv("BSG_PIPE_TAIL");
     const int tail = env_tail ? std::max(0, std::atoi(env_tail)) : 0;
+    // an optional small first chunk: its host-side range scan and copy start the
+    // pipeline sooner (BSG_PIPE_HEAD scenarios)
+    const char* env_head = std::getenv("BSG_PIPE_HEAD");
+    const int64_t head = env_head ? std::max<int64_t>(0, std::atoll(env_head)) : 0;
+    if (head > 0 && head < per) bounds.push_back(head);
     for (int64_t c = 0; c + 1 < nchunks0; ++c) bounds.push_back(std::min(n, (c + 1) * per));
     int64_t rest = n - bounds.back();
     for (int t = 0; t < tail && rest > 2048; ++t) {

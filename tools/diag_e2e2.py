@@ -19,10 +19,10 @@ for _ in range(3): dev.copy_(big, non_blocking=True)
 torch.cuda.synchronize(); t=time.perf_counter()
 for _ in range(20): dev.copy_(big, non_blocking=True)
 torch.cuda.synchronize(); print("H2D %.1f MB: %.3f ms" % (big.numel()/1e6, (time.perf_counter()-t)/20*1e3))
-for chunk, tail in [("20000", "0"), ("20000", "2"), ("20000", "3"), ("15000", "2"), ("30000", "3"), ("12000", "0")]:
-    os.environ["BSG_PIPE_CHUNK"] = chunk; os.environ["BSG_PIPE_TAIL"] = tail
+for chunk, tail, head in [("20000", "0", "0"), ("20000", "0", "4096"), ("20000", "0", "8192"), ("20000", "0", "2048"), ("30000", "0", "8192"), ("20000", "1", "8192")]:
+    os.environ["BSG_PIPE_CHUNK"] = chunk; os.environ["BSG_PIPE_TAIL"] = tail; os.environ["BSG_PIPE_HEAD"] = head
     for _ in range(3): ctx.L.bsg_predict_batch(ctx.h, C.byref(e), host.n_entries, abi.ptr(host.scenarios), len(ss), abi.ptr(out))
     ts=[]
     for _ in range(15):
         t=time.perf_counter(); ctx.L.bsg_predict_batch(ctx.h, C.byref(e), host.n_entries, abi.ptr(host.scenarios), len(ss), abi.ptr(out)); ts.append(time.perf_counter()-t)
-    print("chunk", chunk, "tail", tail, "e2e ms median %.3f min %.3f" % (np.median(ts)*1e3, min(ts)*1e3))
+    print("chunk", chunk, "tail", tail, "head", head, "e2e ms median %.3f min %.3f" % (np.median(ts)*1e3, min(ts)*1e3))

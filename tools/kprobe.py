@@ -8,12 +8,14 @@ import numpy as np, torch
 from paper_2508_03611_b200 import abi, native
 which = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 ctx = native.Context(0)
-if which == "cfg3":
+if which == "cfg1":
+    w = abi.make_workload(count=1000, estimator_kind=2, estimator_seed=1, qps=10.0, arrival_seed=1)
+elif which == "cfg3":
     w = abi.make_workload(count=2000, prompt_median=600, output_median=600, qps=5.0, arrival_seed=1)
 else:
     w = abi.make_workload(count=5000, qps=27.0, arrival_seed=1)
 cfg = abi.make_config()
-_, _, ss = ctx.replay(w, cfg, abi.make_replay_spec(12))
+_, _, ss = ctx.replay(w, cfg, abi.make_replay_spec(4 if which == "cfg1" else 12))
 ctx.set_configs(cfg)
 dev = torch.device("cuda", 0)
 cols = [torch.from_numpy(c).to(dev) for c in (ss.prompt, ss.est, ss.prefill, ss.decoded)]
