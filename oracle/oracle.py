@@ -152,7 +152,8 @@ class Reference:
                                                                     int(w["request_cap"][0]))
         out = np.zeros(n, abi.outcome_dtype)
         summ = np.zeros(1, abi.summary_dtype)
-        self.lib.ref_run_experiment(_vp(w), _vp(cfg), _vp(spec), _vp(out), _vp(summ))
+        if self.lib.ref_run_experiment(_vp(w), _vp(cfg), _vp(spec), _vp(out), _vp(summ)) < 0:
+            raise RuntimeError("reference run_experiment threw (e.g. an unservable workload)")
         return out, summ[0]
 
     def request_json(self, cfgs, ss: abi.ScenarioSet, i: int) -> str:
@@ -191,8 +192,9 @@ class Reference:
         out = np.zeros(n, abi.outcome_dtype)
         summ = np.zeros(1, abi.summary_dtype)
         h = C.c_void_p(None)
-        self.lib.ref_replay(_vp(w), _vp(cfg), _vp(spec), _vp(out), _vp(summ),
-                            C.byref(h) if capture else None)
+        if self.lib.ref_replay(_vp(w), _vp(cfg), _vp(spec), _vp(out), _vp(summ),
+                               C.byref(h) if capture else None) < 0:
+            raise RuntimeError("reference replay threw (e.g. an unservable workload)")
         ss = None
         if capture:
             ne, ns = C.c_int64(0), C.c_int64(0)

@@ -571,7 +571,12 @@ static ExperimentSpec make_experiment(const bsg_workload* w, const bsg_instance_
 int ref_run_experiment(const bsg_workload* w, const bsg_instance_cfg* c,
                        const bsg_replay_spec* s, bsg_request_outcome* out,
                        bsg_replay_summary* summary) {
-  const RunLog log = run_experiment(make_experiment(w, c, s));
+  RunLog log;
+  try {
+    log = run_experiment(make_experiment(w, c, s));
+  } catch (const std::exception&) {
+    return -1;
+  }
   std::vector<InstanceId> inst(log.requests.size(), -1);
   for (const auto& p : log.dispatch_points) inst[p.request_id] = p.instance_id;
   for (std::size_t i = 0; i < log.requests.size(); ++i)
@@ -644,7 +649,13 @@ int ref_replay(const bsg_workload* w, const bsg_instance_cfg* cfg, const bsg_rep
                bsg_request_outcome* out, bsg_replay_summary* summary, ref_capture** capture) {
   ref_capture* cap = capture ? new ref_capture() : nullptr;
   Replay replay(w, cfg, spec, cap);
-  replay.run();
+  try {
+    replay.run();
+  } catch (const std::exception&) {  // e.g. an unservable workload: report, don't abort the host
+    delete cap;
+    if (capture) *capture = nullptr;
+    return -1;
+  }
   if (out) replay.outcomes(out);
   if (summary) {
     std::memset(summary, 0, sizeof(*summary));

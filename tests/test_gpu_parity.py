@@ -210,14 +210,19 @@ def test_sweep_cells_match_reference_capacity_search(ref, monkeypatch, path, pro
     dict(total_blocks=300, max_batch_size=24),                   # KV pressure: preemptions
     dict(block_size=10, total_blocks=1500, chunk_budget=256),    # non-power-of-two blocks
     dict(cache_mode=2, context_bucket=256, max_batch_size=64),   # bucketed latency cache, K=2
+    dict(max_batch_size=160, total_blocks=2000, chunk_budget=1024),  # K=8 member slots
+    dict(local_policy=1, total_blocks=260, max_batch_size=40, block_size=8,  # prefill priority
+         _wl=dict(max_prompt_tokens=1024, max_output_tokens=1024)),          # under KV pressure
 ])
 def test_device_closed_loop_matches_reference(ctx, ref, policy_cfg):
     """bsg_replay_device (whole closed loop on the GPU) == the reference's own
     run_experiment replay: every request's dispatch instance and tick-exact
     dispatch / first-token / finish times and preemption counts."""
+    policy_cfg = dict(policy_cfg)
+    wl = policy_cfg.pop("_wl", {})  # keep the workload servable (config.cpp:197-205)
     cfg = abi.make_config(**policy_cfg)
     ctx.set_configs(cfg)
-    cases = [(abi.make_workload(count=300, qps=q, arrival_seed=s, estimator_kind=2, estimator_seed=s),
+    cases = [(abi.make_workload(count=300, qps=q, arrival_seed=s, estimator_kind=2, estimator_seed=s, **wl),
               ni, obj) for q, s, ni, obj in [(6.0, 1, 4, 0), (14.0, 2, 12, 0), (30.0, 3, 7, 1),
                                               (3.0, 4, 1, 0)]]
     got = ctx.replay_device([(w, abi.make_replay_spec(ni, objective=obj, capture=0), 0)
@@ -268,6 +273,8 @@ def test_device_closed_loop_autoscaler_matches_reference(ctx, ref, kind, kw):
 
 @pytest.mark.parametrize("policy_cfg,n_inst,obj", [
     (dict(), 12, 0), (dict(local_policy=1), 5, 1), (dict(total_blocks=300, max_batch_size=24), 7, 0),
+    (dict(block_size=12, total_blocks=1500, max_batch_size=100, chunk_budget=600), 3, 0),  # K=4, non-pow2
+    (dict(cache_mode=2, context_bucket=128), 6, 1),                                       # bucketed what-ifs
 ])
 def test_fleet_matches_reference(ctx, ref, policy_cfg, n_inst, obj):
     """A fleet (device-resident instance mirror, one launch per dispatch) driven
