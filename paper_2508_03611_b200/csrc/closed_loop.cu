@@ -36,7 +36,16 @@
 
 namespace bsg {
 
-constexpr int kClWarps = 8;
+#ifndef BSG_CL_WARPS
+#define BSG_CL_WARPS 8
+#endif
+#ifndef BSG_CL_MINB
+#define BSG_CL_MINB 2
+#endif
+// warps per closed-loop block / resident blocks per SM (measured on the cfg5 grid:
+// 8 x 2 beats 16 x 1, 4 x 4, 4 x 6 and 8 x 3; optimistic 32-slot what-ifs, which
+// pay off in K1, double the cost here: live running lists reach max_batch)
+constexpr int kClWarps = BSG_CL_WARPS;
 constexpr int kClMaxInst = 256;
 constexpr int64_t kNever = INT64_MAX;
 
@@ -532,7 +541,7 @@ __device__ __forceinline__ void autoscale(ClShared<K>& S, const ClRun& run, int3
 }
 
 template <int K, bool POW2>
-__global__ void __launch_bounds__(kClWarps * 32, 2)
+__global__ void __launch_bounds__(kClWarps * 32, BSG_CL_MINB)
     closed_loop_kernel(const DevCfg* __restrict__ cfgs, const ClRun* __restrict__ runs,
                        const int32_t* __restrict__ rq_prompt, const int32_t* __restrict__ rq_output,
                        const int32_t* __restrict__ rq_est, const int64_t* __restrict__ rq_arrival,
