@@ -158,7 +158,8 @@ __device__ __forceinline__ void predict_one(const DevCfg* __restrict__ cfgs, int
     }
     return;
   }
-  simulate_scenario<K, false, false, POW2, true, OPT>(cfg, prompt, est, prefill, decoded, sc, smem, o,
+  constexpr int WJ = (K == 1 && !OPT) ? BSG_WIN_J_PREDICT : BSG_WIN_J_WIDE;
+  simulate_scenario<K, false, false, POW2, true, OPT, WJ>(cfg, prompt, est, prefill, decoded, sc, smem, o,
                                                      TraceSink{nullptr, 0});
 }
 
@@ -216,7 +217,7 @@ __global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K))
   }
 }
 
-template <int K, bool POW2>
+template <int K, bool POW2, int WJ>
 __global__ void __launch_bounds__(32)
     trace_kernel(const DevCfg* __restrict__ cfgs, const int32_t* __restrict__ prompt,
                  const int32_t* __restrict__ est, const int32_t* __restrict__ prefill,
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(32)
   __shared__ int32_t smem[smem_words(K)];
   const bsg_scenario sc = scen[0];
   const DevCfg cfg = cfgs[sc.cfg];
-  simulate_scenario<K, true, false, POW2>(cfg, prompt, est, prefill, decoded, sc, smem, out,
+  simulate_scenario<K, true, false, POW2, true, false, WJ>(cfg, prompt, est, prefill, decoded, sc, smem, out,
                                          TraceSink{rec, cap});
 }
 
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         scores[w] = INT64_MAX;
       }
     } else {
-      simulate_scenario<K, false, true, POW2>(
+      simulate_scenario<K, false, true, POW2, true, false, BSG_WIN_J_LATENCY>(
           cfg, prompt, est, prefill, decoded, sc, smem, o, TraceSink{nullptr, 0},
           McArgs{len, S, sample_e2e ? sample_e2e + w * S : nullptr, scores + w, objective});
     }
@@ -782,25 +783,28 @@ bsg_status bsg_trace(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries
   auto* res = static_cast<bsg_result*>(ctx->res.p);
   auto* sc = static_cast<const bsg_scenario*>(ctx->scen.p);
   auto* cf = static_cast<const DevCfg*>(ctx->cfgs.p);
+  // the window width under test: the kernels use 1 (wide / KV-pressure sets) and
+  // 4 (32-member sets, latency path); BSG_TRACE_J picks which per-step trace to emit
+  const char* tj = std::getenv("BSG_TRACE_J");
+  const int wj = tj ? std::atoi(tj) : 1;
+#define BSG_TRACE_LAUNCH(KK)                                                                     \
+  {                                                                                              \
+    if (wj == 4) {                                                                               \
+      if (ctx->all_pow2) trace_kernel<KK, true, 4><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap); \
+      else trace_kernel<KK, false, 4><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap); \
+    } else {                                                                                     \
+      if (ctx->all_pow2) trace_kernel<KK, true, 1><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap); \
+      else trace_kernel<KK, false, 1><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap); \
+    }                                                                                            \
+  }
   switch (k) {
-    case 1:
-      if (ctx->all_pow2) trace_kernel<1, true><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap);
-      else trace_kernel<1, false><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap);
-      break;
-    case 2:
-      if (ctx->all_pow2) trace_kernel<2, true><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap);
-      else trace_kernel<2, false><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap);
-      break;
-    case 4:
-      if (ctx->all_pow2) trace_kernel<4, true><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap);
-      else trace_kernel<4, false><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap);
-      break;
-    case 8:
-      if (ctx->all_pow2) trace_kernel<8, true><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap);
-      else trace_kernel<8, false><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap);
-      break;
+    case 1: BSG_TRACE_LAUNCH(1); break;
+    case 2: BSG_TRACE_LAUNCH(2); break;
+    case 4: BSG_TRACE_LAUNCH(4); break;
+    case 8: BSG_TRACE_LAUNCH(8); break;
     default: ctx->last_error = "member capacity beyond 256"; return BSG_BAD_INPUT;
   }
+#undef BSG_TRACE_LAUNCH
   ctx->launches += 1;
   BSG_CUDA(ctx, cudaGetLastError());
   BSG_CUDA(ctx, cudaMemcpyAsync(out, res, sizeof(bsg_result), cudaMemcpyDeviceToHost, ctx->stream));

@@ -34,16 +34,27 @@
 namespace bsg {
 
 constexpr unsigned kFull = 0xffffffffu;
-// Event-skipping window: kWinJ steps per lane, kWin = 32 * kWinJ steps per window.
-#ifndef BSG_WIN_J
-#define BSG_WIN_J 1
+// Event-skipping window: WJ steps per lane, 32 * WJ steps per window — a
+// template parameter of simulate_scenario, chosen per kernel (measured, see
+// DESIGN.md): wide windows for decode-dominated throughput sets and for the
+// latency path, narrow ones where events keep windows short.
+constexpr int kMaxWinJ = 4;
+#ifndef BSG_WIN_J_PREDICT
+#define BSG_WIN_J_PREDICT 4   // K1, 32-member sets (cfg1/cfg2 shape)
 #endif
-constexpr int kWinJ = BSG_WIN_J;
-constexpr int kWin = 32 * kWinJ;
+#ifndef BSG_WIN_J_WIDE
+#define BSG_WIN_J_WIDE 1      // K1 for wide / KV-pressure sets (and their optimistic pass)
+#endif
+#ifndef BSG_WIN_J_LATENCY
+#define BSG_WIN_J_LATENCY 4   // per-request dispatch (dispatch_mc, fleet)
+#endif
+#ifndef BSG_WIN_J_CLOSED
+#define BSG_WIN_J_CLOSED 1    // K5 closed-loop what-ifs
+#endif
 // Per-warp shared-memory words of simulate_scenario: the completion-compaction
-// area (5 x 32K) / the window histograms (4 x kWin), whichever is larger.
+// area (5 x 32K) / the window histograms (4 x 32 x kMaxWinJ), whichever is larger.
 __host__ __device__ constexpr int smem_words(int K) {
-  return (5 * 32 * K > 4 * kWin ? 5 * 32 * K : 4 * kWin);
+  return (5 * 32 * K > 4 * 32 * kMaxWinJ ? 5 * 32 * K : 4 * 32 * kMaxWinJ);
 }
 constexpr int64_t kMaxSimulatedSteps = 50000000LL;  // predictor.cpp:11
 
@@ -244,7 +255,8 @@ __device__ __forceinline__ int32_t ld_entry(const int32_t* p) {
 // would outgrow its 32K member slots: the caller re-runs it with a wider K.
 constexpr int32_t kStatusRetryWider = 100;
 
-template <int K, bool TRACE, bool MC = false, bool POW2 = false, bool LDG = true, bool OPT = false>
+template <int K, bool TRACE, bool MC = false, bool POW2 = false, bool LDG = true, bool OPT = false,
+          int WJ = 1>
 __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__ g_prompt,
                                   const int32_t* __restrict__ g_est,
                                   const int32_t* __restrict__ g_prefill,
@@ -549,13 +561,14 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
     // step A(t) = free - sum_{s<t} dem(s) + sum_{s<t} freed(s) — from four
     // per-step shared-memory histograms and lane-contiguous warp scans.
     int32_t T = 0;
-    int64_t win_pre[kWinJ];
+    static_assert(WJ >= 1 && WJ <= kMaxWinJ, "window width");
+    int64_t win_pre[WJ];
     int64_t win_base = 0;
     if (a == 0 && D == n && n > 0 && !prefill_step) {
 #ifdef BSG_PROFILE_WENTRY
       ++prof_pre;  // debug: window entries (reported in the preempt counter's slot)
 #endif
-      constexpr int J = kWinJ, W = kWin;
+      constexpr int J = WJ, W = 32 * WJ;
       int32_t* h_cnt = smem;          // members completing at the end of step s
       int32_t* h_sst = smem + W;      // their stored tokens at window start
       int32_t* h_dem = smem + 2 * W;  // block demand of step t
@@ -565,24 +578,42 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
       __syncwarp();
       const int32_t bs = cfg.block_size;
       int32_t lc = 0x7fffffff;  // candidate's r (if running)
-      int32_t st_run[K];
+      int32_t st_run[K], rr[K], fd[K];
+      const unsigned lanes_lt = (1u << lane) - 1u;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int32_t p = lane * K + k;
         st_run[k] = 0;
+        rr[k] = -1;
+        fd[k] = W;
         if (p < n) {
           const int32_t r = target[k] - decoded[k] - 1;
           const int32_t sp = stored[k];
           st_run[k] = sp;
+          rr[k] = r;
           if (org[k] == (kCandOrg | kEverBit)) lc = r;
-          if (r < W) {
+          if (r < W) {  // completes inside the window (few members): histogram by step
             atomicAdd(&h_cnt[r], 1);
             atomicAdd(&h_sst[r], sp);
             atomicAdd(&h_frd[r], bnt<POW2>(sp + r + 1, cfg));
           }
           const int32_t m = modt<POW2>(sp, cfg);
-          const int32_t rmax = r < W - 1 ? r : W - 1;
-          for (int32_t t = m == 0 ? 0 : bs - m; t <= rmax; t += bs) atomicAdd(&h_dem[t], 1);
+          fd[k] = m == 0 ? 0 : bs - m;  // first step whose decode opens a new block
+          if constexpr (J == 1) {  // 32-step window: at most ceil(32 / bs) demand steps
+            const int32_t rmax = r < W - 1 ? r : W - 1;
+            for (int32_t t = fd[k]; t <= rmax; t += bs) atomicAdd(&h_dem[t], 1);
+          }
+        }
+        if constexpr (J > 1) {
+          // Block demand: member p demands at steps fd, fd + bs, ... while alive.
+          // Histogram the first demand step with match_any (one writer per
+          // distinct key, no shared atomics — per-step atomics over a 64-128
+          // step window cost more than the window saves), so
+          // dem(t) = R[t mod bs] minus the members that completed before t.
+          const bool v = fd[k] < W;
+          const unsigned peers = __match_any_sync(kFull, v ? fd[k] : -1 - lane);
+          if (v && (peers & lanes_lt) == 0) h_dem[fd[k]] += __popc(peers);
+          __syncwarp();
         }
       }
       __syncwarp();
@@ -591,10 +622,26 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
       int32_t c_cnt[J], c_sst[J], c_dem[J], c_frd[J];
 #pragma unroll
       for (int j = 0; j < J; ++j) {
-        c_cnt[j] = h_cnt[t0 + j];
-        c_sst[j] = h_sst[t0 + j];
-        c_dem[j] = h_dem[t0 + j];
-        c_frd[j] = h_frd[t0 + j];
+        const int32_t t = t0 + j;
+        c_cnt[j] = h_cnt[t];
+        c_sst[j] = h_sst[t];
+        c_dem[j] = h_dem[(J > 1 && bs < W) ? modt<POW2>(t, cfg) : t];
+        c_frd[j] = h_frd[t];
+      }
+      // members completing before the window's last step stop demanding after r
+#pragma unroll
+      for (int k = 0; k < (J > 1 ? K : 0); ++k) {
+        for (unsigned cm = __ballot_sync(kFull, rr[k] >= 0 && rr[k] < W - 1 && fd[k] < W); cm;
+             cm &= cm - 1) {
+          const int src = __ffs(cm) - 1;
+          const int32_t rp = __shfl_sync(kFull, rr[k], src);
+          const int32_t fp = __shfl_sync(kFull, fd[k], src);
+#pragma unroll
+          for (int j = 0; j < J; ++j) {
+            const int32_t t = t0 + j;
+            if (t > rp && t >= fp && modt<POW2>(t - fp, cfg) == 0) c_dem[j] -= 1;
+          }
+        }
       }
       const int32_t s_tot = warp_sum<K>(st_run);
       // two scans instead of four: (cnt | dem << 16) — both <= 256 per step and
@@ -661,7 +708,14 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
 #pragma unroll
         for (int j = 0; j < J; ++j) {
           const bool in = t0 + j < T;
+#ifdef BSG_ABL_TICKS
+          {  // ablation (timing experiments only): branch-free pricing
+            const int64_t tk = step_ticks(cfg, 0, Dt[j], Ct[j]);
+            d[j] = in ? tk : 0;
+          }
+#else
           d[j] = in ? step_ticks(cfg, 0, Dt[j], Ct[j]) : 0;
+#endif
           dsum += d[j];
           msum += in ? Dt[j] + 1 : 0;
         }
@@ -1001,12 +1055,12 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
           const int32_t tj = hit ? lj - dec0 - 1 : 0;
           int64_t at = elapsed;
           if (T > 0) {  // elapsed at the end of window step tj (held by lane tj / J, slot tj % J)
-            const int32_t tw = tj & (kWin - 1);
+            const int32_t tw = tj & (32 * WJ - 1);
             int64_t v = 0;
 #pragma unroll
-            for (int j = 0; j < kWinJ; ++j) {
-              const int64_t x = __shfl_sync(kFull, win_pre[j], tw / kWinJ);
-              if (j == tw % kWinJ) v = x;
+            for (int j = 0; j < WJ; ++j) {
+              const int64_t x = __shfl_sync(kFull, win_pre[j], tw / WJ);
+              if (j == tw % WJ) v = x;
             }
             at = win_base + v;
           }

@@ -36,9 +36,13 @@ def test_gpu_matches_reference_fuzz(ctx, ref, seed):
     assert bad.sum() == 0, [(i, got[i], exp[i]) for i in np.nonzero(bad)[0][:5]]
 
 
-def test_gpu_trace_matches_reference(ctx, ref):
+@pytest.mark.parametrize("win_j", ["1", "4"])
+def test_gpu_trace_matches_reference(ctx, ref, monkeypatch, win_j):
     """Per-step batch composition, allocations, preemption victims, first
-    tokens, completions and durations (bsg_step_record) for every step."""
+    tokens, completions and durations (bsg_step_record) for every step — with
+    the event-skipping window at both widths the kernels use (32 and 128 steps
+    per iteration), so every window-retired step is checked too."""
+    monkeypatch.setenv("BSG_TRACE_J", win_j)
     cfgs, ss = fuzz_set(12, 400)
     ctx.set_configs(cfgs)
     names, kc, ks = kat_set()
