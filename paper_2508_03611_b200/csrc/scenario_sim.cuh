@@ -580,6 +580,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
       int32_t lc = 0x7fffffff;  // candidate's r (if running)
       int32_t st_run[K], rr[K], fd[K];
       const unsigned lanes_lt = (1u << lane) - 1u;
+      const bool strided = J > 1 && (bs >= W || bs % J == 0);
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int32_t p = lane * K + k;
@@ -605,14 +606,25 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
           }
         }
         if constexpr (J > 1) {
-          // Block demand: member p demands at steps fd, fd + bs, ... while alive.
-          // Histogram the first demand step with match_any (one writer per
-          // distinct key, no shared atomics — per-step atomics over a 64-128
-          // step window cost more than the window saves), so
-          // dem(t) = R[t mod bs] minus the members that completed before t.
-          const bool v = fd[k] < W;
-          const unsigned peers = __match_any_sync(kFull, v ? fd[k] : -1 - lane);
-          if (v && (peers & lanes_lt) == 0) h_dem[fd[k]] += __popc(peers);
+          // Block demand: member p demands at steps fd, fd + bs, ... <= r_p.
+          // Histograms with match_any (one writer per distinct key — per-step
+          // shared atomics over a 64-128 step window cost more than the window
+          // saves). Strided layout (bs a multiple of J): histogram the LAST
+          // demand step in the window; dem(t) is then the suffix sum along
+          // t, t+bs, t+2bs, ... (shuffles below) and completions need no
+          // correction. Otherwise: histogram the first demand step,
+          // dem(t) = R[t mod bs], minus completed members (loop below).
+          int32_t key = -1;
+          if (rr[k] >= 0 && fd[k] < W) {
+            if (strided) {
+              const int32_t rmax = rr[k] < W - 1 ? rr[k] : W - 1;
+              if (fd[k] <= rmax) key = fd[k] + divt<POW2>(rmax - fd[k], cfg) * bs;
+            } else {
+              key = fd[k];
+            }
+          }
+          const unsigned peers = __match_any_sync(kFull, key >= 0 ? key : -1 - lane);
+          if (key >= 0 && (peers & lanes_lt) == 0) h_dem[key] += __popc(peers);
           __syncwarp();
         }
       }
@@ -625,12 +637,23 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
         const int32_t t = t0 + j;
         c_cnt[j] = h_cnt[t];
         c_sst[j] = h_sst[t];
-        c_dem[j] = h_dem[(J > 1 && bs < W) ? modt<POW2>(t, cfg) : t];
+        c_dem[j] = h_dem[(J > 1 && !strided) ? modt<POW2>(t, cfg) : t];
         c_frd[j] = h_frd[t];
+      }
+      if (strided) {  // suffix sums along each residue class: strides bs, 2bs, 4bs, ...
+        for (int32_t st = bs; st < W; st <<= 1) {
+          const int32_t dl = st / J;  // lanes per stride (bs is a multiple of J)
+#pragma unroll
+          for (int j = 0; j < J; ++j) {
+            const int32_t v = __shfl_down_sync(kFull, c_dem[j], dl);
+            if (t0 + j + st < W) c_dem[j] += v;
+          }
+        }
       }
       // members completing before the window's last step stop demanding after r
 #pragma unroll
       for (int k = 0; k < (J > 1 ? K : 0); ++k) {
+        if (strided) break;
         for (unsigned cm = __ballot_sync(kFull, rr[k] >= 0 && rr[k] < W - 1 && fd[k] < W); cm;
              cm &= cm - 1) {
           const int src = __ffs(cm) - 1;
