@@ -38,7 +38,10 @@ constexpr unsigned kFull = 0xffffffffu;
 // template parameter of simulate_scenario, chosen per kernel (measured, see
 // DESIGN.md): wide windows for decode-dominated throughput sets and for the
 // latency path, narrow ones where events keep windows short.
-constexpr int kMaxWinJ = 4;
+#ifndef BSG_MAX_WIN_J
+#define BSG_MAX_WIN_J 4
+#endif
+constexpr int kMaxWinJ = BSG_MAX_WIN_J;
 #ifndef BSG_WIN_J_PREDICT
 #define BSG_WIN_J_PREDICT 4   // K1, 32-member sets (cfg1/cfg2 shape)
 #endif
