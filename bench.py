@@ -37,6 +37,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 N_INST, N_REQ, QPS = 12, 5000, 27.0
+E2E_WARMUP_CALLS = 50
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 
@@ -190,7 +191,11 @@ def run_gpu(args):
         e2e_times = []
         import ctypes as C
         ent = host.entries()
-        for i in range(args.warmup + args.steps):
+        # The host-buffer path needs ~40 calls to reach steady state (pinned-page
+        # DMA mappings, the stream-ordered scratch pool, clocks): measured 0.99 ms
+        # per call over the first 40, 0.72 ms after (tools/e2e_sampler_probe.py).
+        e2e_warm = max(args.warmup, E2E_WARMUP_CALLS)
+        for i in range(e2e_warm + args.steps):
             flush.zero_()
             torch.cuda.synchronize(dev)
             ta = time.perf_counter()
@@ -198,7 +203,7 @@ def run_gpu(args):
                                          abi.ptr(host.scenarios), n, C.c_void_p(pout.data_ptr()))
             tb = time.perf_counter()
             assert st == abi.OK
-            if i >= args.warmup:
+            if i >= e2e_warm:
                 e2e_times.append(tb - ta)
     e2e_total = sum(e2e_times)
 
@@ -240,7 +245,9 @@ def run_gpu(args):
             "e2e": {"value": e2e_value, "unit": "scenarios/s",
                     "h2d_bytes_per_step": int(ss.nbytes_in()),
                     "d2h_bytes_per_step": int(n * abi.result_dtype.itemsize),
-                    "ms_per_step": e2e_total / args.steps * 1e3},
+                    "ms_per_step": e2e_total / args.steps * 1e3,
+                    "warmup_calls": max(args.warmup, E2E_WARMUP_CALLS),
+                    "l2": "flushed before every call"},
             "gpu_launches": launches_all,
             "roofline": {
                 "bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
