@@ -29,6 +29,7 @@ constexpr int kWarpsPerBlock = 4;
 #define BSG_WPB 4
 #endif
 constexpr int kPredictWarps = BSG_WPB;
+
 // Resident-warp target per SM for the 32-member kernels: 32 warps/SM needs
 // <= 64 registers/thread (measured: see profiles/).
 #ifndef BSG_K1_WARPS_PER_SM
@@ -158,9 +159,13 @@ __device__ __forceinline__ void predict_one(const DevCfg* __restrict__ cfgs, int
     }
     return;
   }
+  // One window width per kernel (a second instantiation costs more in spills
+  // than it saves): 128-step windows for 32-member sets, 32-step windows for
+  // wide / KV-pressure sets, where admissions and preemptions cut windows short
+  // (measured: cfg3 8.1 ms at J=1 vs 9.6 ms at J=4; cfg1 prefers J=4, 238 vs 310 us).
   constexpr int WJ = (K == 1 && !OPT) ? BSG_WIN_J_PREDICT : BSG_WIN_J_WIDE;
   simulate_scenario<K, false, false, POW2, true, OPT, WJ>(cfg, prompt, est, prefill, decoded, sc, smem, o,
-                                                     TraceSink{nullptr, 0});
+                                                         TraceSink{nullptr, 0});
 }
 
 template <int K, bool POW2, bool OPT = false>
