@@ -125,10 +125,19 @@ def run_gpu(args):
     from paper_2508_03611_b200 import abi, native
 
     world, rank, local = dist_setup()
+    # BSG_DIST_ONE_GPU=1: every rank on cuda:0 with gloo collectives — only for
+    # exercising the multi-rank code path on a one-GPU box (timings meaningless)
+    one_gpu = os.environ.get("BSG_DIST_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
+    coll_dev = None if one_gpu else dev  # gloo reduces host tensors
     ctx = native.Context(local)
 
     # ---- setup (untimed): capture this rank's scenario set --------------------
@@ -211,7 +220,7 @@ def run_gpu(args):
     from paper_2508_03611_b200 import shard
     if world > 1:
         (total_ms, e2e_total), (n_all, ms_all, launches_all) = shard.reduce_max_sum(
-            [total_ms, e2e_total], [n, member_steps, launches], device=dev)
+            [total_ms, e2e_total], [n, member_steps, launches], device=coll_dev)
     else:
         n_all, ms_all, launches_all = n, member_steps, launches
 
@@ -270,7 +279,7 @@ def run_gpu(args):
         if args.cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(ss, cfg)
     if args.latency:
-        lat = mc_latency(ctx, world, rank, dev)
+        lat = mc_latency(ctx, world, rank, coll_dev)
         if rank == 0:
             line["dispatch_latency"] = lat
             line["dispatch_latency_mirror"] = fleet_latency(ctx)
@@ -324,6 +333,12 @@ def mc_latency(ctx, world: int = 1, rank: int = 0, device=None, n_calls: int = 4
         assert st == abi.OK and pick >= 0
         if i >= len(calls):  # first pass is warm-up
             lat.append((t1 - t0) * 1e6)
+        elif world > 1 and os.environ.get("BSG_DIST_ONE_GPU") == "1":
+            # test mode: the sharded decision must equal the one-GPU decision
+            g = picks[i]
+            full = cap.compact(g * n_inst + np.arange(n_inst))
+            ch1, _, _, _ = ctx.dispatch_mc(full, np.arange(n_inst, dtype=np.int32), n_inst, lens)
+            assert int(ch1[0]) == pick, (g, int(ch1[0]), pick)
     lat = np.array(lat)
     return {"p50_us": float(np.percentile(lat, 50)), "p99_us": float(np.percentile(lat, 99)),
             "max_us": float(lat.max()), "calls": len(lat), "gpus": world,

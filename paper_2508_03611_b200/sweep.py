@@ -81,8 +81,12 @@ def main(argv=None):
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("BSG_DIST_ONE_GPU") == "1":  # multi-rank code path on one GPU (tests)
+            local = 0
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     prov = None if args.provision == "static" else dict(
         provision_kind={"preempt": abi.PROVISION_PREEMPT, "relief": abi.PROVISION_RELIEF}[args.provision],
         extra_instances=args.extra_instances)
