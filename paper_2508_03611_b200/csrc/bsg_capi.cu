@@ -53,6 +53,11 @@ constexpr int min_blocks(int k) {
 // warps run the rest in the caller's order (which keeps memory locality),
 // skipping the heavy ones. No sort, no atomics on the simulation path.
 constexpr int kCostBuckets = 128;
+// A scenario queued behind more than kDeepWait waiting entries admits/preempts
+// often, so its pure-decode windows are short: the optimistic pass runs 32-step
+// windows when such scenarios are >= 1/4 of the set, 128-step windows otherwise
+// (cfg3 8.1 ms with 32 vs 9.6 ms with 128; cfg1 310 vs 238 us).
+constexpr int32_t kDeepWait = 8;
 
 __device__ __forceinline__ int cost_bucket(int32_t cand_est) {
   const uint32_t x = static_cast<uint32_t>(max(cand_est, 0)) + 1u;
@@ -66,6 +71,7 @@ __device__ __forceinline__ int cost_bucket(int32_t cand_est) {
 struct WorkQueue {
   int32_t threshold, blocks_done;
   int32_t heavy_count, retry_count;
+  int32_t deep_wait, use_wide;  // window-width vote of the optimistic pass
   int32_t hist[kCostBuckets];
   // followed by the heavy list: int32_t heavy[n / 16 + 32], then the retry
   // list of the optimistic narrow pass: int32_t retry[n]
@@ -101,9 +107,14 @@ __global__ void __launch_bounds__(256) heavy_threshold_kernel(const bsg_scenario
   __shared__ bool last;
   for (int b = threadIdx.x; b < kCostBuckets; b += blockDim.x) h[b] = 0;
   __syncthreads();
+  int32_t deep = 0;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     atomicAdd(&h[cost_bucket(sc[i].cand_est)], 1);
+    deep += sc[i].wait_n > kDeepWait ? 1 : 0;
+  }
+  deep = static_cast<int32_t>(__reduce_add_sync(kFull, static_cast<uint32_t>(deep)));
+  if ((threadIdx.x & 31) == 0 && deep) atomicAdd(&q->deep_wait, deep);
   __syncthreads();
   for (int b = threadIdx.x; b < kCostBuckets; b += blockDim.x)
     if (h[b]) atomicAdd(&q->hist[b], h[b]);
@@ -130,10 +141,14 @@ __global__ void __launch_bounds__(256) heavy_threshold_kernel(const bsg_scenario
     if (acc <= cap && c[j] > 0) thr = kCostBuckets - 1 - (lane * 4 + j);
   }
   thr = static_cast<int32_t>(__reduce_min_sync(kFull, static_cast<uint32_t>(thr)));
-  if (lane == 0) q->threshold = thr;
+  if (lane == 0) {
+    q->threshold = thr;
+    // wide windows unless a quarter of the set queues behind a deep waiting line
+    q->use_wide = static_cast<int64_t>(__ldcg(&q->deep_wait)) * 4 < n ? 1 : 0;
+  }
 }
 
-template <int K, bool POW2, bool OPT = false>
+template <int K, bool POW2, bool OPT, int WJ>
 __device__ __forceinline__ void predict_one(const DevCfg* __restrict__ cfgs, int32_t ncfg,
                                             const int32_t* __restrict__ prompt,
                                             const int32_t* __restrict__ est,
@@ -163,12 +178,15 @@ __device__ __forceinline__ void predict_one(const DevCfg* __restrict__ cfgs, int
   // than it saves): 128-step windows for 32-member sets, 32-step windows for
   // wide / KV-pressure sets, where admissions and preemptions cut windows short
   // (measured: cfg3 8.1 ms at J=1 vs 9.6 ms at J=4; cfg1 prefers J=4, 238 vs 310 us).
-  constexpr int WJ = (K == 1 && !OPT) ? BSG_WIN_J_PREDICT : BSG_WIN_J_WIDE;
   simulate_scenario<K, false, false, POW2, true, OPT, WJ>(cfg, prompt, est, prefill, decoded, sc, smem, o,
                                                          TraceSink{nullptr, 0});
 }
 
-template <int K, bool POW2, bool OPT = false>
+// WJ: event-skipping window width (steps per lane). Measured choices: 128-step
+// windows for 32-member sets and for latency-bound small sets (one wave: the
+// longest scenario is the critical path), 32-step windows for large wide sets
+// and KV pressure, where admissions/preemptions cut windows short.
+template <int K, bool POW2, bool OPT, int WJ>
 __global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K))
     predict_kernel(const DevCfg* __restrict__ cfgs, int32_t ncfg,
                    const int32_t* __restrict__ prompt, const int32_t* __restrict__ est,
@@ -178,6 +196,9 @@ __global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K))
   __shared__ int32_t smem_all[kPredictWarps * smem_words(K)];
   const int warp = threadIdx.x >> 5;
   int32_t* smem = smem_all + warp * smem_words(K);
+  if constexpr (OPT) {  // two optimistic passes are launched; the vote keeps one
+    if ((__ldcg(&q->use_wide) != 0) != (WJ > 1)) return;
+  }
   // warps [0, nh) run the heavy list; warp nh + i runs scenario i unless it is heavy
   int64_t w = static_cast<int64_t>(blockIdx.x) * kPredictWarps + warp;
   if (q) {
@@ -193,7 +214,7 @@ __global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K))
     return;
   }
   const bsg_scenario sc = scen[w];
-  predict_one<K, POW2, OPT>(cfgs, ncfg, prompt, est, prefill, decoded, sc, smem, out + w);
+  predict_one<K, POW2, OPT, WJ>(cfgs, ncfg, prompt, est, prefill, decoded, sc, smem, out + w);
   if constexpr (OPT) {  // too wide for this pass: list it for the wide kernel
     __syncwarp();
     if ((threadIdx.x & 31) == 0 && out[w].status == kStatusRetryWider)
@@ -218,7 +239,7 @@ __global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K))
        j += static_cast<int64_t>(gridDim.x) * kPredictWarps) {
     const int64_t w = __ldcg(&rl[j]);
     const bsg_scenario sc = scen[w];
-    predict_one<K, POW2>(cfgs, ncfg, prompt, est, prefill, decoded, sc, smem, out + w);
+    predict_one<K, POW2, false, BSG_WIN_J_WIDE>(cfgs, ncfg, prompt, est, prefill, decoded, sc, smem, out + w);
   }
 }
 
@@ -433,7 +454,7 @@ bsg_status launch_predict_t(bsg_ctx* ctx, int64_t n, const bsg_entries& e, const
   auto* cf = static_cast<const DevCfg*>(ctx->cfgs.p);
   const int64_t blocks = (n + kPredictWarps - 1) / kPredictWarps;
   if (no_queue || n < BSG_QUEUE_MIN) {
-    predict_kernel<K, POW2><<<static_cast<unsigned>(blocks), kPredictWarps * 32, 0, s>>>(
+    predict_kernel<K, POW2, false, BSG_WIN_J_PREDICT><<<static_cast<unsigned>(blocks), kPredictWarps * 32, 0, s>>>(
         cf, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, nullptr, out);
     ctx->launches += 1;
     BSG_CUDA(ctx, cudaGetLastError());
@@ -455,18 +476,21 @@ bsg_status launch_predict_t(bsg_ctx* ctx, int64_t n, const bsg_entries& e, const
       // the batch cap admits more (KV pressure keeps running sets small); the
       // 32-slot kernel runs at 32 warps/SM with half the per-member work, and hands
       // the rest to the wide kernel.
-      predict_kernel<1, POW2, true><<<static_cast<unsigned>(pb), kPredictWarps * 32, 0, s>>>(
+      predict_kernel<1, POW2, true, BSG_WIN_J_PREDICT><<<static_cast<unsigned>(pb), kPredictWarps * 32, 0, s>>>(
+          cf, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
+      predict_kernel<1, POW2, true, BSG_WIN_J_WIDE><<<static_cast<unsigned>(pb), kPredictWarps * 32, 0, s>>>(
           cf, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
       const int64_t rb = std::min<int64_t>(pb, 148 * 8);
       predict_retry_kernel<K, POW2><<<static_cast<unsigned>(rb), kPredictWarps * 32, 0, s>>>(
           cf, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
-      ctx->launches += 4;
+      ctx->launches += 5;
       BSG_CUDA(ctx, cudaGetLastError());
       BSG_CUDA(ctx, cudaFreeAsync(mem, s));
       return BSG_OK;
     }
   }
-  predict_kernel<K, POW2><<<static_cast<unsigned>(pb), kPredictWarps * 32, 0, s>>>(
+  predict_kernel<K, POW2, false, K == 1 ? BSG_WIN_J_PREDICT : BSG_WIN_J_WIDE>
+      <<<static_cast<unsigned>(pb), kPredictWarps * 32, 0, s>>>(
       cf, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
   ctx->launches += 3;
   BSG_CUDA(ctx, cudaGetLastError());
