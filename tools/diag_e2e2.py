@@ -19,7 +19,9 @@ for _ in range(3): dev.copy_(big, non_blocking=True)
 torch.cuda.synchronize(); t=time.perf_counter()
 for _ in range(20): dev.copy_(big, non_blocking=True)
 torch.cuda.synchronize(); print("H2D %.1f MB: %.3f ms" % (big.numel()/1e6, (time.perf_counter()-t)/20*1e3))
-for chunk, tail, head in [("20000", "0", "0"), ("20000", "0", "4096"), ("20000", "0", "8192"), ("20000", "0", "2048"), ("30000", "0", "8192"), ("20000", "1", "8192")]:
+for _ in range(60):
+    ctx.L.bsg_predict_batch(ctx.h, C.byref(e), host.n_entries, abi.ptr(host.scenarios), len(ss), abi.ptr(out))
+for chunk, tail, head in [("20000", "0", "0"), ("15000", "0", "0"), ("12000", "0", "0"), ("30000", "0", "0"), ("20000", "0", "4096"), ("10000", "0", "0"), ("20000", "0", "0")]:
     os.environ["BSG_PIPE_CHUNK"] = chunk; os.environ["BSG_PIPE_TAIL"] = tail; os.environ["BSG_PIPE_HEAD"] = head
     for _ in range(3): ctx.L.bsg_predict_batch(ctx.h, C.byref(e), host.n_entries, abi.ptr(host.scenarios), len(ss), abi.ptr(out))
     ts=[]
