@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <map>
 #include <cstring>
 #include <vector>
 
@@ -838,14 +839,24 @@ struct FleetDev {
 
 constexpr int kFleetWarps = 4;
 
+// Per-call inputs of a fleet dispatch, staged in pinned memory and copied by the
+// call's CUDA graph (so a dispatch is one graph launch).
+struct FleetParams {
+  int64_t now;
+  int32_t prompt, est, output, S, objective, drain;
+  int32_t lens[1024];  // sorted MC lengths, S of them
+};
+
 template <int K, bool POW2, bool MC>
 __global__ void __launch_bounds__(kFleetWarps * 32)
     fleet_dispatch_kernel(const DevCfg* __restrict__ cfgs, int32_t cfg_index, int32_t n_inst, int32_t n_cap,
                           Arena ar, ClInst* __restrict__ inst, FleetDev* __restrict__ fd,
-                          bsg_request_outcome* __restrict__ outs, int64_t now, int32_t prompt,
-                          int32_t est, int32_t output, const int32_t* __restrict__ sorted_len,
-                          int32_t S, int32_t objective, bsg_result* __restrict__ res,
-                          int64_t* __restrict__ scores, int32_t drain) {
+                          bsg_request_outcome* __restrict__ outs, const FleetParams* __restrict__ P,
+                          bsg_result* __restrict__ res, int64_t* __restrict__ scores) {
+  const int64_t now = P->now;
+  const int32_t prompt = P->prompt, est = P->est, output = P->output, S = P->S,
+                objective = P->objective, drain = P->drain;
+  const int32_t* sorted_len = P->lens;
   extern __shared__ __align__(16) int32_t fsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t i = blockIdx.x * kFleetWarps + warp;
@@ -1141,16 +1152,19 @@ struct bsg_fleet {
   bsg_request_outcome* outs = nullptr;
   bsg_result* res = nullptr;
   int64_t* scores = nullptr;
-  int32_t* lens = nullptr;  // sorted MC lengths (device)
-  void* pinned = nullptr;   // host staging: lengths in, (chosen, status) + scores out
+  FleetParams* dparams = nullptr;  // device copy of the call's inputs
+  FleetParams* hparams = nullptr;  // pinned staging of the call's inputs
+  void* pinned = nullptr;          // pinned (chosen, status) + scores out
   int64_t last_now = -1;
+  // one instantiated graph (params H2D -> kernel -> decision D2H) per sample count
+  std::map<int32_t, cudaGraphExec_t> graphs;
 };
 
 namespace {
 
+// Enqueues the fleet kernel on the context stream; inputs come from f->dparams.
 template <int K, bool POW2, bool MC>
-cudaError_t launch_fleet(bsg_fleet* f, int64_t now, int32_t prompt, int32_t est, int32_t output,
-                         int32_t S, int32_t objective, int32_t drain) {
+cudaError_t launch_fleet(bsg_fleet* f, int32_t S) {
   const size_t sm = static_cast<size_t>(kFleetWarps) * (smem_words(K) + S) * 4;
   if (sm > 48 * 1024)
     cudaFuncSetAttribute(fleet_dispatch_kernel<K, POW2, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1158,19 +1172,15 @@ cudaError_t launch_fleet(bsg_fleet* f, int64_t now, int32_t prompt, int32_t est,
   const int blocks = (f->n_inst + kFleetWarps - 1) / kFleetWarps;
   fleet_dispatch_kernel<K, POW2, MC><<<blocks, kFleetWarps * 32, sm, f->ctx->stream>>>(
       static_cast<const DevCfg*>(f->ctx->cfgs.p), f->cfg, f->n_inst, f->n_cap, f->ar, f->inst, f->fd,
-      f->outs, now, prompt, est, output, f->lens, S, objective, f->res, f->scores, drain);
-  f->ctx->launches += 1;
+      f->outs, f->dparams, f->res, f->scores);
   return cudaGetLastError();
 }
 
-cudaError_t launch_fleet_any(bsg_fleet* f, int64_t now, int32_t prompt, int32_t est, int32_t output,
-                             int32_t S, int32_t objective, int32_t drain, bool mc) {
+cudaError_t launch_fleet_any(bsg_fleet* f, int32_t S, bool mc) {
 #define BSG_FLEET_CASE(KK)                                                                           \
   case KK:                                                                                           \
-    if (mc) return f->pow2 ? launch_fleet<KK, true, true>(f, now, prompt, est, output, S, objective, drain)  \
-                           : launch_fleet<KK, false, true>(f, now, prompt, est, output, S, objective, drain); \
-    return f->pow2 ? launch_fleet<KK, true, false>(f, now, prompt, est, output, S, objective, drain)          \
-                   : launch_fleet<KK, false, false>(f, now, prompt, est, output, S, objective, drain);
+    if (mc) return f->pow2 ? launch_fleet<KK, true, true>(f, S) : launch_fleet<KK, false, true>(f, S); \
+    return f->pow2 ? launch_fleet<KK, true, false>(f, S) : launch_fleet<KK, false, false>(f, S);
   switch (f->k) {
     BSG_FLEET_CASE(1)
     BSG_FLEET_CASE(2)
@@ -1179,6 +1189,19 @@ cudaError_t launch_fleet_any(bsg_fleet* f, int64_t now, int32_t prompt, int32_t 
       BSG_FLEET_CASE(8)
   }
 #undef BSG_FLEET_CASE
+}
+
+// The dispatch sequence: params H2D, the kernel, the decision (+ scores) D2H.
+cudaError_t enqueue_dispatch(bsg_fleet* f, int32_t S, bool mc) {
+  cudaStream_t s = f->ctx->stream;
+  auto* hout = reinterpret_cast<int32_t*>(f->pinned);
+  auto* hsc = reinterpret_cast<int64_t*>(static_cast<char*>(f->pinned) + 64);
+  cudaError_t e = cudaMemcpyAsync(f->dparams, f->hparams, offsetof(FleetParams, lens) + S * 4,
+                                  cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = launch_fleet_any(f, S, mc);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hout, &f->fd->chosen, 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hsc, f->scores, f->n_inst * 8, cudaMemcpyDeviceToHost, s);
+  return e;
 }
 
 }  // namespace
@@ -1206,7 +1229,8 @@ extern "C" bsg_status bsg_fleet_create(bsg_ctx* ctx, int32_t cfg, int32_t n_inst
   auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
   const size_t b_col = up(static_cast<size_t>(entries) * 4), b_inst = up(n_instances * sizeof(ClInst)),
                b_fd = up(sizeof(FleetDev)), b_out = up(static_cast<size_t>(max_requests) * sizeof(bsg_request_outcome)),
-               b_res = up(n_instances * sizeof(bsg_result)), b_sc = up(n_instances * 8), b_len = up(1024 * 4);
+               b_res = up(n_instances * sizeof(bsg_result)), b_sc = up(n_instances * 8),
+               b_len = up(sizeof(FleetParams));
   const size_t total = 7 * b_col + b_inst + b_fd + b_out + b_res + b_sc + b_len;
   if (cudaMalloc(&f->base, total) != cudaSuccess) {
     cudaGetLastError();
@@ -1230,17 +1254,19 @@ extern "C" bsg_status bsg_fleet_create(bsg_ctx* ctx, int32_t cfg, int32_t n_inst
   p += b_res;
   f->scores = reinterpret_cast<int64_t*>(p);
   p += b_sc;
-  f->lens = reinterpret_cast<int32_t*>(p);
+  f->dparams = reinterpret_cast<FleetParams*>(p);
   std::vector<ClInst> init(static_cast<size_t>(n_instances));
   for (auto& x : init) x = ClInst{0, c.max_batch_size, c.max_batch_size, c.total_blocks, 0, 0, 0};
   FleetDev fd0{-1, 0, 0, -1, BSG_OK, 0};
-  bool ok = cudaHostAlloc(&f->pinned, 1024 * 4 + 64 + static_cast<size_t>(n_instances) * 8, cudaHostAllocDefault) == cudaSuccess;
+  bool ok = cudaHostAlloc(&f->pinned, 64 + static_cast<size_t>(n_instances) * 8, cudaHostAllocDefault) == cudaSuccess;
+  ok = ok && cudaHostAlloc(reinterpret_cast<void**>(&f->hparams), sizeof(FleetParams), cudaHostAllocDefault) == cudaSuccess;
   ok = ok && cudaMemcpyAsync(f->inst, init.data(), n_instances * sizeof(ClInst), cudaMemcpyHostToDevice, ctx->stream) == cudaSuccess;
   ok = ok && cudaMemcpyAsync(f->fd, &fd0, sizeof(fd0), cudaMemcpyHostToDevice, ctx->stream) == cudaSuccess;
   ok = ok && cudaStreamSynchronize(ctx->stream) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
     if (f->pinned) cudaFreeHost(f->pinned);
+    if (f->hparams) cudaFreeHost(f->hparams);
     cudaFree(f->base);
     delete f;
     ctx->last_error = "fleet initialisation failed";
@@ -1254,7 +1280,9 @@ extern "C" void bsg_fleet_destroy(bsg_fleet* f) {
   if (!f) return;
   cudaSetDevice(f->ctx->device);
   cudaStreamSynchronize(f->ctx->stream);
+  for (auto& g : f->graphs) cudaGraphExecDestroy(g.second);
   if (f->pinned) cudaFreeHost(f->pinned);
+  if (f->hparams) cudaFreeHost(f->hparams);
   cudaFree(f->base);
   delete f;
 }
@@ -1275,24 +1303,49 @@ extern "C" bsg_status bsg_fleet_dispatch(bsg_fleet* f, int64_t now_ticks, int32_
   const bsg_instance_cfg& c = ctx->host_cfgs[f->cfg];
   if ((static_cast<int64_t>(prompt) + output + c.block_size - 1) / c.block_size > c.total_blocks)
     return BSG_TOO_LARGE_CANDIDATE;
-  auto* hl = static_cast<int32_t*>(f->pinned);
-  auto* hout = reinterpret_cast<int32_t*>(static_cast<char*>(f->pinned) + 1024 * 4);
-  auto* hsc = reinterpret_cast<int64_t*>(static_cast<char*>(f->pinned) + 1024 * 4 + 64);
+  auto* hout = reinterpret_cast<int32_t*>(f->pinned);
+  auto* hsc = reinterpret_cast<int64_t*>(static_cast<char*>(f->pinned) + 64);
   cudaStream_t s = ctx->stream;
-  int32_t S = 0;
+  const int32_t S = mc ? n_samples : 0;
+  FleetParams& P = *f->hparams;
+  P.now = now_ticks;
+  P.prompt = prompt;
+  P.est = est;
+  P.output = output;
+  P.S = S;
+  P.objective = objective;
+  P.drain = 0;
   if (mc) {
-    S = n_samples;
-    std::memcpy(hl, lengths, S * 4);
-    std::sort(hl, hl + S);  // the kernel walks the samples in ascending order
-    cudaError_t e = cudaMemcpyAsync(f->lens, hl, S * 4, cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) return bsg_cuda_fail(ctx, e, "fleet lengths");
+    std::memcpy(P.lens, lengths, S * 4);
+    std::sort(P.lens, P.lens + S);  // the kernel walks the samples in ascending order
   }
-  cudaError_t e = launch_fleet_any(f, now_ticks, prompt, est, output, S, objective, 0, mc);
-  if (e != cudaSuccess) return bsg_cuda_fail(ctx, e, "fleet_dispatch_kernel");
-  e = cudaMemcpyAsync(hout, &f->fd->chosen, 8, cudaMemcpyDeviceToHost, s);  // chosen, status
-  if (e == cudaSuccess && scores) e = cudaMemcpyAsync(hsc, f->scores, f->n_inst * 8, cudaMemcpyDeviceToHost, s);
+  // One CUDA graph per sample count (params H2D -> kernel -> decision D2H),
+  // captured on first use: a dispatch is a single graph launch.
+  static const bool no_graph = std::getenv("BSG_FLEET_NO_GRAPH") != nullptr;
+  cudaError_t e = cudaSuccess;
+  if (no_graph) {
+    e = enqueue_dispatch(f, S, mc);
+  } else {
+    auto it = f->graphs.find(mc ? S : 0);
+    if (it == f->graphs.end()) {
+      cudaGraph_t g = nullptr;
+      cudaGraphExec_t x = nullptr;
+      e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+      if (e == cudaSuccess) {
+        const cudaError_t qe = enqueue_dispatch(f, S, mc);
+        e = cudaStreamEndCapture(s, &g);
+        if (e == cudaSuccess) e = qe;
+      }
+      if (e == cudaSuccess) e = cudaGraphInstantiate(&x, g, 0);
+      if (g) cudaGraphDestroy(g);
+      if (e != cudaSuccess) return bsg_cuda_fail(ctx, e, "fleet graph capture");
+      it = f->graphs.emplace(mc ? S : 0, x).first;
+    }
+    e = cudaGraphLaunch(it->second, s);
+  }
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return bsg_cuda_fail(ctx, e, "fleet dispatch");
+  ctx->launches += 1;
   f->last_now = now_ticks;
   ctx->scenarios += static_cast<int64_t>(f->n_inst) * (mc ? S : 1);
   *chosen = hout[0];
@@ -1311,7 +1364,16 @@ extern "C" bsg_status bsg_fleet_finish(bsg_fleet* f, bsg_request_outcome* outcom
   std::lock_guard<std::mutex> lock(ctx->mu);
   cudaSetDevice(ctx->device);
   cudaStream_t s = ctx->stream;
-  cudaError_t e = launch_fleet_any(f, INT64_MAX, 1, 1, 1, 0, 0, 1, false);  // drain: run every step
+  FleetParams& P = *f->hparams;  // drain: run every remaining step
+  P.now = INT64_MAX;
+  P.prompt = P.est = P.output = 1;
+  P.S = 0;
+  P.objective = 0;
+  P.drain = 1;
+  cudaError_t e = cudaMemcpyAsync(f->dparams, f->hparams, offsetof(FleetParams, lens),
+                                  cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = launch_fleet_any(f, 0, false);
+  ctx->launches += 1;
   FleetDev fd{};
   if (e == cudaSuccess) e = cudaMemcpyAsync(&fd, f->fd, sizeof(fd), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
