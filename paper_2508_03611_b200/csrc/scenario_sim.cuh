@@ -458,7 +458,39 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
       else if (h < wait_n) hp = ld_entry<LDG>(g_prompt + sc.wait_off + h);
       else hp = sc.cand_prompt;
       const int32_t hc = chunked ? (hp < budget ? hp : budget) : hp;
-      if (bnt<POW2>(hc + (hc == hp ? 1 : 0), cfg) > free_blocks - run_delta) try_admit = false;
+      if (bnt<POW2>(hc + (hc == hp ? 1 : 0), cfg) > free_blocks - run_delta) {
+        try_admit = false;
+      } else if (chunked && hp >= budget && n < CAP) {  // (n == CAP: the general path decides)
+        // Single admission: the head fits and its first chunk takes the whole
+        // remaining budget, so the loop stops right after it (backend.cpp:136):
+        // admit exactly the head without materialising the queue.
+        try_admit = false;
+        a = 1;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const int32_t p = lane * K + k;
+          if (p == n) {
+            if (p >= L) {
+              if (h < wait_n) {
+                const int32_t g = sc.wait_off + h;
+                prompt[k] = hp;
+                const int32_t est = ld_entry<LDG>(g_est + g);
+                const int32_t dec = ld_entry<LDG>(g_decoded + g);
+                target[k] = dec >= est ? dec + 10 : est;  // correct_lengths on waiting too
+                org[k] = run_n + h + 1;
+              } else {
+                prompt[k] = sc.cand_prompt;
+                target[k] = cand_target;
+                org[k] = kCandOrg;
+              }
+              prefill[k] = 0;
+              decoded[k] = 0;
+            }
+            chunk[k] = hc;
+            delta[k] = bnt<POW2>(hc + (hc == hp ? 1 : 0), cfg);
+          }
+        }
+      }
     }
     if (try_admit) {
       const int32_t pf = free_blocks - run_delta;  // projected_free (backend.cpp:131-133 / 158-164)
