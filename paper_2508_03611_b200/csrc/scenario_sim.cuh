@@ -608,6 +608,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
       int32_t* h_sst = smem + W;      // their stored tokens at window start
       int32_t* h_dem = smem + 2 * W;  // block demand of step t
       int32_t* h_frd = smem + 3 * W;  // blocks released at the end of step s
+      __syncwarp();  // the previous iteration's reads of this scratch are complete
 #pragma unroll
       for (int i = 0; i < 4 * J; ++i) smem[i * 32 + lane] = 0;
       __syncwarp();

@@ -9,4 +9,4 @@ make -s -j$(nproc) -C paper_2508_03611_b200/csrc OUTDIR=$d EXTRA="$flags" > /dev
 cp $d/libblocksim_b200.so $d/lib.so
 cp $d/lib.so gpurun_out/lib_$tag.so
 BSG_LIB_PATH=$d/lib.so timeout 600 ncu --set full --import-source on --clock-control none \
-  -k regex:predict_kernel -c 1 -o gpurun_out/prof_$tag python tools/ncu_one.py ${3:-cfg2} > gpurun_out/ncu_$tag.log 2>&1
+  -k regex:predict_kernel -s ${4:-0} -c 1 -o gpurun_out/prof_$tag python tools/ncu_one.py ${3:-cfg2} > gpurun_out/ncu_$tag.log 2>&1
