@@ -471,6 +471,10 @@ bsg_status bsg_fleet_finish(bsg_fleet* f, bsg_request_outcome* outcomes, int32_t
  * to the requests' distinct instance_configs. */
 bsg_status bsg_predict_json(bsg_ctx* ctx, const char* const* requests, int32_t n, char* out,
                             int64_t out_cap, int64_t* out_off, int32_t* status);
+/* A double as the reference's JSON layer prints it (nlohmann::json::dump:
+ * Grisu2 digits, fixed notation for decimal exponents in (-4, 15]); returns the
+ * length, or -(bytes needed) when cap is too small. No GPU needed. */
+int32_t bsg_format_double(double v, char* out, int32_t cap);
 
 /* Synthetic trace + estimates + Poisson arrival ticks (no GPU needed). */
 bsg_status bsg_make_workload(const bsg_workload* w, int32_t* prompt, int32_t* output,

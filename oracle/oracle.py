@@ -105,6 +105,8 @@ class Reference:
         L.ref_capture_copy.argtypes = [C.c_void_p] * 7
         L.ref_request_json.restype = C.c_int
         L.ref_request_json.argtypes = [C.c_void_p, E, C.c_void_p, C.c_char_p, C.c_int64]
+        L.ref_dump_double.restype = C.c_int
+        L.ref_dump_double.argtypes = [C.c_double, C.c_char_p, C.c_int64]
         L.ref_service_predict.restype = C.c_int
         L.ref_service_predict.argtypes = [C.c_char_p, C.c_char_p, C.c_int64]
         L.ref_run_report.restype = C.c_int
@@ -164,6 +166,11 @@ class Reference:
         cf = np.ascontiguousarray(np.asarray(cfgs)[int(sc["cfg"][0]):int(sc["cfg"][0]) + 1])
         n = self.lib.ref_request_json(_vp(cf), C.byref(e), _vp(sc), buf, len(buf))
         assert n >= 0
+        return buf.value.decode()
+
+    def dump_double(self, v: float) -> str:
+        buf = C.create_string_buffer(64)
+        assert self.lib.ref_dump_double(v, buf, 64) >= 0
         return buf.value.decode()
 
     def service_predict(self, body: str):

@@ -29,6 +29,7 @@
 #include "blocksim/error.h"
 #include "blocksim/event_loop.h"
 #include "blocksim/json_io.h"
+#include <nlohmann/json.hpp>
 #include "blocksim/metrics.h"
 #include "blocksim/predictor.h"
 #include "blocksim/scheduler.h"
@@ -725,6 +726,12 @@ int ref_service_predict(const char* body, char* out, int64_t cap) {
   }
   const int n = put_text(text, out, cap);
   return n < 0 ? n : code;
+}
+
+
+// How the reference's JSON layer prints a double (nlohmann::json::dump).
+int ref_dump_double(double v, char* out, int64_t cap) {
+  return put_text(nlohmann::json(v).dump(), out, cap);
 }
 
 }  // extern "C"

@@ -6,9 +6,9 @@
 //
 // Parsing follows json_io.cpp's field names and its bad-schema behaviour (a
 // missing field or a wrong type rejects the request); numbers are printed the
-// way nlohmann::json::dump prints them (shortest round-trip digits, fixed
-// notation for decimal exponents in (-4, 15], otherwise d.ddde±XX), so the
-// response text matches the reference's prediction_result_to_json.
+// way nlohmann::json::dump prints them (Grisu2 digits, fixed notation for
+// decimal exponents in (-4, 15], otherwise d.ddde±XX), so the response text is
+// byte-identical to the reference's prediction_result_to_json.
 #include <charconv>
 #include <cmath>
 #include <cstdint>
@@ -315,6 +315,203 @@ Request request_from(const JVal& j) {  // prediction_request_from_json (json_io.
 }
 
 // ---- nlohmann::json::dump number formatting -----------------------------------
+// The reference prints doubles with nlohmann's dtoa: Grisu2 (Loitsch, "Printing
+// Floating-Point Numbers Quickly and Accurately with Integers", PLDI 2010) with
+// the boundaries narrowed by one unit, which is round-trip exact but not always
+// shortest (e.g. 199.28768350000001). To answer byte-identically the digits are
+// generated by the same algorithm here; the decimal layout follows dump():
+// fixed notation for decimal exponents in (-4, 15], else d.ddde±XX.
+struct DiyFp {
+  uint64_t f;
+  int e;
+};
+
+DiyFp diy_mul(DiyFp x, DiyFp y) {  // (x.f * y.f + 2^63) >> 64, rounded half up
+  const unsigned __int128 p = static_cast<unsigned __int128>(x.f) * y.f;
+  uint64_t h = static_cast<uint64_t>(p >> 64);
+  h += static_cast<uint64_t>(p) >> 63;
+  return DiyFp{h, x.e + y.e + 64};
+}
+
+DiyFp diy_normalize(DiyFp x) {
+  while ((x.f >> 63) == 0) {
+    x.f <<= 1;
+    --x.e;
+  }
+  return x;
+}
+
+// Normalised 64-bit significands of 10^k, k = -300, -292, ..., 340 (round to
+// nearest; generated with exact integer arithmetic).
+struct CachedPower {
+  uint64_t f;
+  int e;
+  int k;
+};
+constexpr CachedPower kCachedPowers[] = {
+    {0xAB70FE17C79AC6CAULL, -1060, -300},
+    {0xFF77B1FCBEBCDC4FULL, -1034, -292},
+    {0xBE5691EF416BD60CULL, -1007, -284},
+    {0x8DD01FAD907FFC3CULL, -980, -276},
+    {0xD3515C2831559A83ULL, -954, -268},
+    {0x9D71AC8FADA6C9B5ULL, -927, -260},
+    {0xEA9C227723EE8BCBULL, -901, -252},
+    {0xAECC49914078536DULL, -874, -244},
+    {0x823C12795DB6CE57ULL, -847, -236},
+    {0xC21094364DFB5637ULL, -821, -228},
+    {0x9096EA6F3848984FULL, -794, -220},
+    {0xD77485CB25823AC7ULL, -768, -212},
+    {0xA086CFCD97BF97F4ULL, -741, -204},
+    {0xEF340A98172AACE5ULL, -715, -196},
+    {0xB23867FB2A35B28EULL, -688, -188},
+    {0x84C8D4DFD2C63F3BULL, -661, -180},
+    {0xC5DD44271AD3CDBAULL, -635, -172},
+    {0x936B9FCEBB25C996ULL, -608, -164},
+    {0xDBAC6C247D62A584ULL, -582, -156},
+    {0xA3AB66580D5FDAF6ULL, -555, -148},
+    {0xF3E2F893DEC3F126ULL, -529, -140},
+    {0xB5B5ADA8AAFF80B8ULL, -502, -132},
+    {0x87625F056C7C4A8BULL, -475, -124},
+    {0xC9BCFF6034C13053ULL, -449, -116},
+    {0x964E858C91BA2655ULL, -422, -108},
+    {0xDFF9772470297EBDULL, -396, -100},
+    {0xA6DFBD9FB8E5B88FULL, -369, -92},
+    {0xF8A95FCF88747D94ULL, -343, -84},
+    {0xB94470938FA89BCFULL, -316, -76},
+    {0x8A08F0F8BF0F156BULL, -289, -68},
+    {0xCDB02555653131B6ULL, -263, -60},
+    {0x993FE2C6D07B7FACULL, -236, -52},
+    {0xE45C10C42A2B3B06ULL, -210, -44},
+    {0xAA242499697392D3ULL, -183, -36},
+    {0xFD87B5F28300CA0EULL, -157, -28},
+    {0xBCE5086492111AEBULL, -130, -20},
+    {0x8CBCCC096F5088CCULL, -103, -12},
+    {0xD1B71758E219652CULL, -77, -4},
+    {0x9C40000000000000ULL, -50, 4},
+    {0xE8D4A51000000000ULL, -24, 12},
+    {0xAD78EBC5AC620000ULL, 3, 20},
+    {0x813F3978F8940984ULL, 30, 28},
+    {0xC097CE7BC90715B3ULL, 56, 36},
+    {0x8F7E32CE7BEA5C70ULL, 83, 44},
+    {0xD5D238A4ABE98068ULL, 109, 52},
+    {0x9F4F2726179A2245ULL, 136, 60},
+    {0xED63A231D4C4FB27ULL, 162, 68},
+    {0xB0DE65388CC8ADA8ULL, 189, 76},
+    {0x83C7088E1AAB65DBULL, 216, 84},
+    {0xC45D1DF942711D9AULL, 242, 92},
+    {0x924D692CA61BE758ULL, 269, 100},
+    {0xDA01EE641A708DEAULL, 295, 108},
+    {0xA26DA3999AEF774AULL, 322, 116},
+    {0xF209787BB47D6B85ULL, 348, 124},
+    {0xB454E4A179DD1877ULL, 375, 132},
+    {0x865B86925B9BC5C2ULL, 402, 140},
+    {0xC83553C5C8965D3DULL, 428, 148},
+    {0x952AB45CFA97A0B3ULL, 455, 156},
+    {0xDE469FBD99A05FE3ULL, 481, 164},
+    {0xA59BC234DB398C25ULL, 508, 172},
+    {0xF6C69A72A3989F5CULL, 534, 180},
+    {0xB7DCBF5354E9BECEULL, 561, 188},
+    {0x88FCF317F22241E2ULL, 588, 196},
+    {0xCC20CE9BD35C78A5ULL, 614, 204},
+    {0x98165AF37B2153DFULL, 641, 212},
+    {0xE2A0B5DC971F303AULL, 667, 220},
+    {0xA8D9D1535CE3B396ULL, 694, 228},
+    {0xFB9B7CD9A4A7443CULL, 720, 236},
+    {0xBB764C4CA7A44410ULL, 747, 244},
+    {0x8BAB8EEFB6409C1AULL, 774, 252},
+    {0xD01FEF10A657842CULL, 800, 260},
+    {0x9B10A4E5E9913129ULL, 827, 268},
+    {0xE7109BFBA19C0C9DULL, 853, 276},
+    {0xAC2820D9623BF429ULL, 880, 284},
+    {0x80444B5E7AA7CF85ULL, 907, 292},
+    {0xBF21E44003ACDD2DULL, 933, 300},
+    {0x8E679C2F5E44FF8FULL, 960, 308},
+    {0xD433179D9C8CB841ULL, 986, 316},
+    {0x9E19DB92B4E31BA9ULL, 1013, 324},
+    {0xEB96BF6EBADF77D9ULL, 1039, 332},
+    {0xAF87023B9BF0EE6BULL, 1066, 340},
+};
+constexpr int kCachedMinDecExp = -300, kCachedDecStep = 8;
+constexpr int kAlpha = -60, kGamma = -32;  // target exponent range of the scaled values
+
+CachedPower cached_power_for(int e) {  // c = 10^k with kAlpha <= e + c.e + 64 <= kGamma
+  const int f = kAlpha - e - 1;
+  const int k = (f * 78913) / (1 << 18) + (f > 0 ? 1 : 0);  // ceil(f * log10(2))
+  const int index = (-kCachedMinDecExp + k + (kCachedDecStep - 1)) / kCachedDecStep;
+  return kCachedPowers[index];
+}
+
+void grisu_round(char* buf, int len, uint64_t dist, uint64_t delta, uint64_t rest, uint64_t ten_k) {
+  // move the last digit closer to w while the candidate stays inside (M-, M+)
+  while (rest < dist && delta - rest >= ten_k &&
+         (rest + ten_k < dist || dist - rest > rest + ten_k - dist)) {
+    --buf[len - 1];
+    rest += ten_k;
+  }
+}
+
+// Digits of v (finite, > 0) and the decimal exponent: v ~ digits * 10^exp.
+void grisu2(double value, char* buf, int* len, int* exp10) {
+  uint64_t bits;
+  std::memcpy(&bits, &value, 8);
+  const uint64_t F = bits & ((uint64_t{1} << 52) - 1);
+  const int E = static_cast<int>((bits >> 52) & 0x7ff);
+  constexpr int kBias = 1075, kMinExp = 1 - kBias;
+  const DiyFp v = E == 0 ? DiyFp{F, kMinExp} : DiyFp{F + (uint64_t{1} << 52), E - kBias};
+  const bool lower_closer = F == 0 && E > 1;
+  const DiyFp m_plus = diy_normalize(DiyFp{2 * v.f + 1, v.e - 1});
+  DiyFp m_minus = lower_closer ? DiyFp{4 * v.f - 1, v.e - 2} : DiyFp{2 * v.f - 1, v.e - 1};
+  m_minus.f <<= (m_minus.e - m_plus.e);
+  m_minus.e = m_plus.e;
+  const DiyFp w = diy_normalize(v);
+  const CachedPower c = cached_power_for(m_plus.e);
+  const DiyFp cp{c.f, c.e};
+  const DiyFp sw = diy_mul(w, cp), sm = diy_mul(m_minus, cp), sp = diy_mul(m_plus, cp);
+  const DiyFp M_minus{sm.f + 1, sm.e}, M_plus{sp.f - 1, sp.e};
+  int dexp = -c.k;
+  uint64_t delta = M_plus.f - M_minus.f, dist = M_plus.f - sw.f;
+  const int shift = -M_plus.e;
+  const uint64_t one_f = uint64_t{1} << shift;
+  uint32_t p1 = static_cast<uint32_t>(M_plus.f >> shift);
+  uint64_t p2 = M_plus.f & (one_f - 1);
+  uint32_t pow10 = 1;
+  int n = 1;
+  while (n < 10 && p1 >= pow10 * 10u) {
+    pow10 *= 10;
+    ++n;
+  }
+  int L = 0;
+  while (n > 0) {  // integral digits
+    const uint32_t d = p1 / pow10, r = p1 % pow10;
+    buf[L++] = static_cast<char>('0' + d);
+    p1 = r;
+    --n;
+    const uint64_t rest = (static_cast<uint64_t>(p1) << shift) + p2;
+    if (rest <= delta) {
+      dexp += n;
+      grisu_round(buf, L, dist, delta, rest, static_cast<uint64_t>(pow10) << shift);
+      *len = L;
+      *exp10 = dexp;
+      return;
+    }
+    pow10 /= 10;
+  }
+  int m = 0;
+  for (;;) {  // fractional digits
+    p2 *= 10;
+    delta *= 10;
+    dist *= 10;
+    buf[L++] = static_cast<char>('0' + (p2 >> shift));
+    p2 &= one_f - 1;
+    ++m;
+    if (p2 <= delta) break;
+  }
+  dexp -= m;
+  grisu_round(buf, L, dist, delta, p2, one_f);
+  *len = L;
+  *exp10 = dexp;
+}
+
 void append_double(std::string* out, double v) {
   if (!std::isfinite(v)) {
     out->append("null");
@@ -324,22 +521,15 @@ void append_double(std::string* out, double v) {
     out->append(std::signbit(v) ? "-0.0" : "0.0");
     return;
   }
-  char buf[64];
-  auto r = std::to_chars(buf, buf + sizeof(buf), v, std::chars_format::scientific);
-  std::string sci(buf, r.ptr);
-  std::string digits;
-  size_t i = 0;
-  bool neg = false;
-  if (sci[i] == '-') {
-    neg = true;
-    ++i;
+  if (v < 0) {
+    out->push_back('-');
+    v = -v;
   }
-  for (; i < sci.size() && sci[i] != 'e'; ++i)
-    if (sci[i] != '.') digits.push_back(sci[i]);
-  const int e10 = std::atoi(sci.c_str() + i + 1);  // value = d.ddd x 10^e10
-  const int k = static_cast<int>(digits.size());
-  const int n = e10 + 1;  // value = 0.ddd x 10^n
-  if (neg) out->push_back('-');
+  char buf[32];
+  int k = 0, dexp = 0;
+  grisu2(v, buf, &k, &dexp);
+  const std::string digits(buf, buf + k);
+  const int n = k + dexp;  // value = 0.ddd x 10^n
   if (k <= n && n <= 15) {
     out->append(digits);
     out->append(static_cast<size_t>(n - k), '0');
@@ -531,4 +721,12 @@ extern "C" bsg_status bsg_predict_json(bsg_ctx* ctx, const char* const* requests
   }
   out_off[n] = off;
   return off <= out_cap ? BSG_OK : BSG_INVALID_ARGUMENT;  // out_off[n] = bytes needed
+}
+
+extern "C" int32_t bsg_format_double(double v, char* out, int32_t cap) {
+  std::string t;
+  append_double(&t, v);
+  if (!out || cap < static_cast<int32_t>(t.size()) + 1) return -static_cast<int32_t>(t.size() + 1);
+  std::memcpy(out, t.c_str(), t.size() + 1);
+  return static_cast<int32_t>(t.size());
 }

@@ -69,6 +69,7 @@ def load() -> C.CDLL:
                                          C.c_int32, V, V]),
         "bsg_fleet_finish": (C.c_int, [V, V, V, V]),
         "bsg_predict_json": (C.c_int, [V, V, C.c_int32, V, C.c_int64, V, V]),
+        "bsg_format_double": (C.c_int32, [C.c_double, C.c_char_p, C.c_int32]),
         "bsg_fleet_snapshot": (C.c_int, [V, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                          V, V, V, V, C.c_int32]),
     }
@@ -86,7 +87,7 @@ def exported_symbols_declared_in_header() -> list[str]:
     """Function names declared in include/blocksim_b200.h (for the export check)."""
     import re
     txt = open(HEADER).read()
-    decl = re.compile(r"^\s*(?:bsg_status|void|int|int64_t|double|const char\*)\s+(bsg_[a-z_0-9]+)\s*\(",
+    decl = re.compile(r"^\s*(?:bsg_status|void|int|int32_t|int64_t|double|const char\*)\s+(bsg_[a-z_0-9]+)\s*\(",
                       re.M)
     return sorted(set(decl.findall(txt)))
 
@@ -125,6 +126,14 @@ def mc_lengths(est: int, request_id: int, n_samples: int = 256, seed: int = 1,
     if st != abi.OK:
         raise BsgError(st, "bsg_mc_lengths")
     return out
+
+
+def format_double(v: float) -> str:
+    """A double as the reference's JSON layer prints it (bsg_format_double)."""
+    buf = C.create_string_buffer(64)
+    n = load().bsg_format_double(float(v), buf, 64)
+    assert n >= 0
+    return buf.value.decode()
 
 
 def make_workload_host(w: np.ndarray):

@@ -139,3 +139,23 @@ def test_c_struct_layouts_match_numpy(tmp_path):
         exp.append(dt.itemsize)
         exp.extend(dt.fields[f][1] for f in dt.names)
     assert got == exp
+
+
+def test_wire_number_text_matches_reference_json(lib, ref):
+    """bsg_format_double prints doubles exactly as the reference's JSON layer
+    (nlohmann::json::dump, Grisu2 — not always the shortest form), so wire
+    responses are byte-identical: tick-derived latencies, random bit patterns,
+    and the edge layouts (exponent notation, 15-digit integers, tiny values)."""
+    import random
+    import struct
+    rng = random.Random(2026)
+    vals = [199.2876835, 0.0612, 0.05848, 1.0, 0.1, 1e-9, 1e21, 1e-5, 2.5e-7, 1 / 3, 1e15, 1e16,
+            123456789012345.0, 9007199254740993.0, 5e-324, 1.7976931348623157e308, 0.5, 2.0 ** -1022]
+    vals += [rng.randrange(1, 10 ** 13) * 1e-9 for _ in range(4000)]
+    vals += [struct.unpack("<d", struct.pack("<Q", rng.getrandbits(63)))[0] for _ in range(4000)]
+    vals += [rng.lognormvariate(0, 25) for _ in range(2000)]
+    for v in vals:
+        if v != v or v == float("inf"):
+            continue
+        assert native.format_double(v) == ref.dump_double(v), repr(v)
+        assert float(native.format_double(v)) == v  # round trip
