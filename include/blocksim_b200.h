@@ -261,7 +261,7 @@ typedef struct bsg_workload {
   uint64_t trace_seed;        /* SyntheticTraceSpec::seed */
   double prompt_median, prompt_sigma;  /* 230, 0.7 */
   double output_median, output_sigma;  /* 160, 1.0 */
-  int32_t estimator_kind;     /* 0 oracle, 1 fixed, 2 noisy (EstimatorKind) */
+  int32_t estimator_kind;     /* 0 oracle, 1 fixed, 2 noisy, 3 trace (EstimatorKind; 3 only with trace records) */
   int32_t fixed_tokens;       /* 256 */
   double mean_abs_rel_error;  /* 0.244 */
   uint64_t estimator_seed;
@@ -475,6 +475,59 @@ bsg_status bsg_predict_json(bsg_ctx* ctx, const char* const* requests, int32_t n
  * Grisu2 digits, fixed notation for decimal exponents in (-4, 15]); returns the
  * length, or -(bytes needed) when cap is too small. No GPU needed. */
 int32_t bsg_format_double(double v, char* out, int32_t cap);
+
+/* ---- trace workloads (workload.cpp:51-170) -------------------------------- */
+
+/* One TraceRecord (workload.h:15-21). estimated_output_tokens 0 = absent
+ * (a present estimate is >= 1 after validation); has_arrival_offset 0/1. */
+typedef struct bsg_trace_record {
+  uint64_t id;
+  int32_t prompt_tokens;
+  int32_t output_tokens;
+  int32_t estimated_output_tokens;
+  int32_t has_arrival_offset;
+  double arrival_offset_s;
+} bsg_trace_record;
+
+/* Why a trace was rejected: kind 0 none, 1 TraceParseError (line = 1-based
+ * line number, error.h:64-69), 2 InvalidRecordError (field, error.h:72-76),
+ * 3 ConfigError (field, e.g. "workload.qps"). message is the reference's
+ * what() text where it is ours to write (NUL-terminated, truncated). */
+typedef struct bsg_trace_error {
+  int32_t kind;
+  int32_t line;
+  char field[40];
+  char message[216];
+} bsg_trace_error;
+
+/* load_trace (workload.cpp:51-68): JSON Lines, one object per line with
+ * id, prompt_tokens, output_tokens and optional estimated_output_tokens /
+ * arrival_offset_s; blank lines skipped; the first bad line (malformed JSON,
+ * missing/mistyped field, invalid value, duplicate id) rejects the trace with
+ * BSG_BAD_INPUT and *err filled. *n_records = the number of records; when it
+ * exceeds cap nothing past cap is written and BSG_INVALID_ARGUMENT is
+ * returned (call again with cap >= *n_records). No GPU needed. */
+bsg_status bsg_load_trace(const char* text, int64_t len, bsg_trace_record* out, int64_t cap,
+                          int64_t* n_records, bsg_trace_error* err);
+
+/* The request columns a run_experiment builds from trace records
+ * (driver.cpp:137-160): request_cap truncation, generate_arrivals
+ * (workload.cpp:141-170: every record's arrival_offset_s, in record order, or
+ * Poisson at w->qps with w->arrival_seed when no record has one) and
+ * estimate_length (workload.cpp:113-139) with w's estimator; estimator_kind 3
+ * is EstimatorKind::kTrace (the records' own estimates). Only the estimator,
+ * qps, arrival_seed and request_cap fields of w are read. Rows = *n_out
+ * (<= n). Arrival ticks are non-decreasing unless the offsets are not. */
+bsg_status bsg_trace_workload(const bsg_trace_record* recs, int64_t n, const bsg_workload* w,
+                              int32_t* prompt, int32_t* output, int32_t* est,
+                              int64_t* arrival_ticks, int64_t* n_out, bsg_trace_error* err);
+
+/* bsg_replay over trace records instead of the synthetic trace (host event
+ * loop; arrivals in any order, ties in record order). */
+bsg_status bsg_replay_trace(bsg_ctx* ctx, const bsg_trace_record* recs, int64_t n,
+                            const bsg_workload* w, const bsg_instance_cfg* cfg,
+                            const bsg_replay_spec* spec, bsg_request_outcome* outcomes,
+                            bsg_replay_summary* summary, bsg_trace_error* err);
 
 /* Synthetic trace + estimates + Poisson arrival ticks (no GPU needed). */
 bsg_status bsg_make_workload(const bsg_workload* w, int32_t* prompt, int32_t* output,

@@ -118,6 +118,11 @@ class Reference:
         L.ref_estimate_noisy.argtypes = [C.c_int32, C.c_uint64, C.c_uint64, C.c_double]
         L.ref_capture_free.restype = None
         L.ref_capture_free.argtypes = [C.c_void_p]
+        L.ref_load_trace.argtypes = [C.c_char_p, C.c_int64, C.c_void_p, C.c_int64,
+                                     C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_char_p, C.c_int64]
+        L.ref_load_trace.restype = C.c_int64
+        L.ref_set_trace.argtypes = [C.c_void_p, C.c_int64]
+        L.ref_set_trace.restype = None
 
     def predict_batch(self, cfgs, ss: abi.ScenarioSet, threads: int = 1) -> np.ndarray:
         out = np.zeros(len(ss), abi.ref_result_dtype)
@@ -141,17 +146,45 @@ class Reference:
         self.lib.ref_trace(_vp(cfg), C.byref(e), _vp(sc), _vp(rec), cap, C.byref(n), _vp(out))
         return out[0], rec[:min(n.value, cap)]
 
+    _trace_n = None
+
+    def _rows(self, w):
+        total = int(w["count"][0]) if self._trace_n is None else self._trace_n
+        return total if w["request_cap"][0] < 0 else min(total, int(w["request_cap"][0]))
+
+    def load_trace(self, text):
+        """load_trace (workload.cpp:51-68): (records, None) or (None, (kind, line, field))."""
+        b = text.encode() if isinstance(text, str) else bytes(text)
+        cap = b.count(b"\n") + 1
+        out = np.zeros(cap, abi.trace_record_dtype)
+        kind, line = C.c_int32(0), C.c_int32(0)
+        field = C.create_string_buffer(64)
+        n = self.lib.ref_load_trace(b, len(b), _vp(out), cap, C.byref(kind), C.byref(line), field, 64)
+        if n < 0:
+            return None, (kind.value, line.value, field.value.decode())
+        return out[:n].copy(), None
+
+    def set_trace(self, recs):
+        """Replace the synthetic trace of make_workload / run_experiment /
+        run_report by these records (None restores it)."""
+        if recs is None:
+            self.lib.ref_set_trace(None, -1)
+            self._trace_n = None
+            return
+        recs = np.ascontiguousarray(recs, dtype=abi.trace_record_dtype)
+        self.lib.ref_set_trace(_vp(recs), len(recs))
+        self._trace_n = len(recs)
+
     def make_workload(self, w):
-        n = int(w["count"][0]) if w["request_cap"][0] < 0 else min(int(w["count"][0]),
-                                                                    int(w["request_cap"][0]))
-        p, o, e = (np.zeros(n, np.int32) for _ in range(3))
-        t = np.zeros(n, np.int64)
-        self.lib.ref_make_workload(_vp(w), _vp(p), _vp(o), _vp(e), _vp(t))
-        return p, o, e, t
+        n = self._rows(w)
+        p, o, e = (np.zeros(max(n, 1), np.int32) for _ in range(3))
+        t = np.zeros(max(n, 1), np.int64)
+        if self.lib.ref_make_workload(_vp(w), _vp(p), _vp(o), _vp(e), _vp(t)) < 0:
+            raise RuntimeError("reference make_workload threw")
+        return p[:n], o[:n], e[:n], t[:n]
 
     def run_experiment(self, w, cfg, spec):
-        n = int(w["count"][0]) if w["request_cap"][0] < 0 else min(int(w["count"][0]),
-                                                                    int(w["request_cap"][0]))
+        n = self._rows(w)
         out = np.zeros(n, abi.outcome_dtype)
         summ = np.zeros(1, abi.summary_dtype)
         if self.lib.ref_run_experiment(_vp(w), _vp(cfg), _vp(spec), _vp(out), _vp(summ)) < 0:

@@ -19,6 +19,8 @@
 #include <cstring>
 #include <limits>
 #include <map>
+#include <sstream>
+#include <cstdio>
 #include <string>
 #include <thread>
 #include <unordered_map>
@@ -171,7 +173,16 @@ void parallel_chunks(int64_t n, int threads, F&& body) {
   for (auto& th : pool) th.join();
 }
 
+// Records installed by ref_set_trace replace the synthetic trace (tests only).
+std::vector<TraceRecord>* g_trace = nullptr;
+
 std::vector<TraceRecord> make_records(const bsg_workload* w) {
+  if (g_trace) {  // request_cap as the driver applies it (driver.cpp:140-144)
+    std::vector<TraceRecord> records = *g_trace;
+    if (w->request_cap >= 0 && static_cast<std::size_t>(w->request_cap) < records.size())
+      records.resize(static_cast<std::size_t>(w->request_cap));
+    return records;
+  }
   SyntheticTraceSpec t;
   t.count = w->count;
   t.seed = w->trace_seed;
@@ -191,9 +202,10 @@ std::vector<TraceRecord> make_records(const bsg_workload* w) {
 
 LengthEstimator make_estimator(const bsg_workload* w) {
   LengthEstimator est;
-  est.kind = w->estimator_kind == 1 ? EstimatorKind::kFixed
-                                    : (w->estimator_kind == 2 ? EstimatorKind::kNoisy
-                                                              : EstimatorKind::kOracle);
+  est.kind = w->estimator_kind == 1   ? EstimatorKind::kFixed
+             : w->estimator_kind == 2 ? EstimatorKind::kNoisy
+             : w->estimator_kind == 3 ? EstimatorKind::kTrace
+                                      : EstimatorKind::kOracle;
   est.fixed_tokens = w->fixed_tokens;
   est.mean_abs_rel_error = w->mean_abs_rel_error;
   est.seed = w->estimator_seed;
@@ -532,16 +544,20 @@ int32_t ref_estimate_noisy(int32_t output_tokens, uint64_t record_id, uint64_t s
 
 int ref_make_workload(const bsg_workload* w, int32_t* prompt, int32_t* output, int32_t* est,
                       int64_t* arrival_ticks) {
-  const std::vector<TraceRecord> records = make_records(w);
-  const std::vector<Arrival> arrivals = generate_arrivals(records, w->qps, w->arrival_seed);
-  const LengthEstimator e = make_estimator(w);
-  for (std::size_t i = 0; i < arrivals.size(); ++i) {
-    prompt[i] = arrivals[i].record.prompt_tokens;
-    output[i] = arrivals[i].record.output_tokens;
-    est[i] = estimate_length(e, arrivals[i].record);
-    arrival_ticks[i] = arrivals[i].time.ticks();
+  try {
+    const std::vector<TraceRecord> records = make_records(w);
+    const std::vector<Arrival> arrivals = generate_arrivals(records, w->qps, w->arrival_seed);
+    const LengthEstimator e = make_estimator(w);
+    for (std::size_t i = 0; i < arrivals.size(); ++i) {
+      prompt[i] = arrivals[i].record.prompt_tokens;
+      output[i] = arrivals[i].record.output_tokens;
+      est[i] = estimate_length(e, arrivals[i].record);
+      arrival_ticks[i] = arrivals[i].time.ticks();
+    }
+    return static_cast<int>(arrivals.size());
+  } catch (const std::exception&) {
+    return -1;
   }
-  return static_cast<int>(arrivals.size());
 }
 
 static ExperimentSpec make_experiment(const bsg_workload* w, const bsg_instance_cfg* c,
@@ -732,6 +748,56 @@ int ref_service_predict(const char* body, char* out, int64_t cap) {
 // How the reference's JSON layer prints a double (nlohmann::json::dump).
 int ref_dump_double(double v, char* out, int64_t cap) {
   return put_text(nlohmann::json(v).dump(), out, cap);
+}
+
+// load_trace (workload.cpp:51-68) on a text; returns the record count, or -1
+// with *kind = 1 (TraceParseError, *line) / 2 (InvalidRecordError, field).
+int64_t ref_load_trace(const char* text, int64_t len, bsg_trace_record* out, int64_t cap,
+                       int32_t* kind, int32_t* line, char* field, int64_t field_cap) {
+  *kind = 0;
+  *line = 0;
+  if (field_cap > 0) field[0] = 0;
+  std::istringstream in(std::string(text, static_cast<size_t>(len)));
+  std::vector<TraceRecord> recs;
+  try {
+    recs = load_trace(in);
+  } catch (const TraceParseError& e) {
+    *kind = 1;
+    *line = e.line;
+    return -1;
+  } catch (const InvalidRecordError& e) {
+    *kind = 2;
+    std::snprintf(field, static_cast<size_t>(field_cap), "%s", e.field.c_str());
+    return -1;
+  }
+  for (size_t i = 0; i < recs.size() && static_cast<int64_t>(i) < cap; ++i) {
+    bsg_trace_record& r = out[i];
+    r.id = recs[i].id;
+    r.prompt_tokens = recs[i].prompt_tokens;
+    r.output_tokens = recs[i].output_tokens;
+    r.estimated_output_tokens = recs[i].estimated_output_tokens.value_or(0);
+    r.has_arrival_offset = recs[i].arrival_offset_s.has_value() ? 1 : 0;
+    r.arrival_offset_s = recs[i].arrival_offset_s.value_or(0.0);
+  }
+  return static_cast<int64_t>(recs.size());
+}
+
+// Installs trace records for make_workload / run_experiment / run_report
+// (n < 0 restores the synthetic trace).
+void ref_set_trace(const bsg_trace_record* recs, int64_t n) {
+  delete g_trace;
+  g_trace = nullptr;
+  if (n < 0) return;
+  g_trace = new std::vector<TraceRecord>();
+  for (int64_t i = 0; i < n; ++i) {
+    TraceRecord r;
+    r.id = recs[i].id;
+    r.prompt_tokens = recs[i].prompt_tokens;
+    r.output_tokens = recs[i].output_tokens;
+    if (recs[i].estimated_output_tokens > 0) r.estimated_output_tokens = recs[i].estimated_output_tokens;
+    if (recs[i].has_arrival_offset) r.arrival_offset_s = recs[i].arrival_offset_s;
+    g_trace->push_back(r);
+  }
 }
 
 }  // extern "C"

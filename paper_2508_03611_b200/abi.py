@@ -107,6 +107,20 @@ outcome_dtype = np.dtype([
     ("finish_ticks", "<i8"), ("instance", "<i4"), ("preempt_count", "<i4"),
 ])
 
+trace_record_dtype = np.dtype([
+    ("id", "<u8"), ("prompt_tokens", "<i4"), ("output_tokens", "<i4"),
+    ("estimated_output_tokens", "<i4"), ("has_arrival_offset", "<i4"), ("arrival_offset_s", "<f8")])
+
+
+class TraceError(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("line", C.c_int32), ("field", C.c_char * 40),
+                ("message", C.c_char * 216)]
+
+
+ESTIMATOR_ORACLE, ESTIMATOR_FIXED, ESTIMATOR_NOISY, ESTIMATOR_TRACE = 0, 1, 2, 3
+
+assert trace_record_dtype.itemsize == 32
+assert C.sizeof(TraceError) == 264
 assert cfg_dtype.itemsize == 64
 assert scenario_dtype.itemsize == 32
 assert result_dtype.itemsize == 48

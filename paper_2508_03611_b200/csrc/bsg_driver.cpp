@@ -72,6 +72,82 @@ struct Record {
   int64_t arrival;
 };
 
+// estimate_length (workload.cpp:113-139) for the oracle / fixed / noisy kinds.
+int32_t estimate(const bsg_workload& w, uint64_t record_id, int32_t output) {
+  switch (w.estimator_kind) {
+    case 1: return w.fixed_tokens;
+    case 2: {
+      Rng e(mix_seed(w.estimator_seed, record_id));
+      const double half = std::abs(e.normal());
+      const double sign = (e.next() & 1) ? 1.0 : -1.0;
+      const double scale = w.mean_abs_rel_error * std::sqrt(3.14159265358979323846 / 2.0);
+      const double est = std::round(static_cast<double>(output) * (1.0 + sign * half * scale));
+      return static_cast<int32_t>(std::max(1.0, est));
+    }
+    default: return output;
+  }
+}
+
+void trace_err(bsg_trace_error* err, int32_t kind, const char* field, const std::string& msg) {
+  if (!err) return;
+  err->kind = kind;
+  err->line = 0;
+  std::snprintf(err->field, sizeof(err->field), "%s", field);
+  std::snprintf(err->message, sizeof(err->message), "%s", msg.c_str());
+}
+
+// The SimulationDriver constructor's request build (driver.cpp:137-160) over
+// trace records: request_cap, generate_arrivals (workload.cpp:141-170), then
+// estimate_length per request in arrival-list order.
+bsg_status records_from_trace(const bsg_trace_record* tr, int64_t n, const bsg_workload& w,
+                              std::vector<Record>* out, bsg_trace_error* err) {
+  if (n < 0 || (!tr && n > 0)) return BSG_INVALID_ARGUMENT;
+  if (err) std::memset(err, 0, sizeof(*err));
+  const int64_t m = (w.request_cap >= 0 && w.request_cap < n) ? w.request_cap : n;
+  std::vector<Record> recs(static_cast<size_t>(m));
+  if (m > 0) {
+    const bool first = tr[0].has_arrival_offset != 0;
+    for (int64_t i = 0; i < m; ++i)
+      if ((tr[i].has_arrival_offset != 0) != first) {
+        trace_err(err, 2, "arrival_offset_s",
+                  "invalid trace record: arrival_offset_s: either every record carries an offset or none does");
+        return BSG_BAD_INPUT;
+      }
+    if (first) {
+      for (int64_t i = 0; i < m; ++i) recs[i].arrival = ticks_from_seconds(tr[i].arrival_offset_s);
+    } else {
+      if (!(w.qps > 0)) {
+        trace_err(err, 3, "workload.qps", "invalid config: workload.qps: must be > 0");
+        return BSG_BAD_INPUT;
+      }
+      Rng arr(w.arrival_seed);
+      int64_t t = 0;
+      for (int64_t i = 0; i < m; ++i) {
+        t += ticks_from_seconds(arr.exponential(w.qps));
+        recs[i].arrival = t;
+      }
+    }
+  }
+  for (int64_t i = 0; i < m; ++i) {
+    Record& r = recs[i];
+    r.prompt = tr[i].prompt_tokens;
+    r.output = tr[i].output_tokens;
+    if (w.estimator_kind == 3) {  // EstimatorKind::kTrace
+      if (tr[i].estimated_output_tokens < 1) {
+        trace_err(err, 2, "estimated_output_tokens",
+                  "invalid trace record: estimated_output_tokens: trace estimator needs pre-tagged records (record " +
+                      std::to_string(tr[i].id) + " has none)");
+        return BSG_BAD_INPUT;
+      }
+      r.est = tr[i].estimated_output_tokens;
+    } else {
+      r.est = estimate(w, tr[i].id, r.output);
+    }
+  }
+  *out = std::move(recs);
+  return BSG_OK;
+}
+
 // make_synthetic_trace (workload.cpp:172-191) + estimate_length
 // (workload.cpp:113-139) + generate_arrivals (workload.cpp:141-170).
 bsg_status make_records(const bsg_workload& w, std::vector<Record>* out) {
@@ -93,19 +169,7 @@ bsg_status make_records(const bsg_workload& w, std::vector<Record>* out) {
   int64_t t = 0;
   for (size_t i = 0; i < recs.size(); ++i) {
     Record& r = recs[i];
-    switch (w.estimator_kind) {
-      case 1: r.est = w.fixed_tokens; break;
-      case 2: {
-        Rng e(mix_seed(w.estimator_seed, static_cast<uint64_t>(i)));
-        const double half = std::abs(e.normal());
-        const double sign = (e.next() & 1) ? 1.0 : -1.0;
-        const double scale = w.mean_abs_rel_error * std::sqrt(3.14159265358979323846 / 2.0);
-        const double est = std::round(static_cast<double>(r.output) * (1.0 + sign * half * scale));
-        r.est = static_cast<int32_t>(std::max(1.0, est));
-        break;
-      }
-      default: r.est = r.output;
-    }
+    r.est = estimate(w, static_cast<uint64_t>(i), r.output);  // synthetic ids are row numbers
     t += ticks_from_seconds(arr.exponential(w.qps));
     r.arrival = t;
   }
@@ -676,10 +740,54 @@ bsg_status bsg_make_workload(const bsg_workload* w, int32_t* prompt, int32_t* ou
   return BSG_OK;
 }
 
+bsg_status bsg_trace_workload(const bsg_trace_record* recs, int64_t n, const bsg_workload* w,
+                              int32_t* prompt, int32_t* output, int32_t* est,
+                              int64_t* arrival_ticks, int64_t* n_out, bsg_trace_error* err) {
+  if (!w || !n_out) return BSG_INVALID_ARGUMENT;
+  std::vector<Record> rs;
+  const bsg_status st = records_from_trace(recs, n, *w, &rs, err);
+  if (st != BSG_OK) return st;
+  for (size_t i = 0; i < rs.size(); ++i) {
+    prompt[i] = rs[i].prompt;
+    output[i] = rs[i].output;
+    est[i] = rs[i].est;
+    arrival_ticks[i] = rs[i].arrival;
+  }
+  *n_out = static_cast<int64_t>(rs.size());
+  return BSG_OK;
+}
+
+namespace {
+bsg_status replay_records(bsg_ctx* ctx, std::vector<Record> recs, const bsg_instance_cfg* cfg,
+                          const bsg_replay_spec* spec, bsg_request_outcome* outcomes,
+                          bsg_replay_summary* summary, bsg_capture** capture);
+}
+
+bsg_status bsg_replay_trace(bsg_ctx* ctx, const bsg_trace_record* recs, int64_t n,
+                            const bsg_workload* w, const bsg_instance_cfg* cfg,
+                            const bsg_replay_spec* spec, bsg_request_outcome* outcomes,
+                            bsg_replay_summary* summary, bsg_trace_error* err) {
+  if (!ctx || !w || !cfg || !spec || spec->n_instances < 1) return BSG_INVALID_ARGUMENT;
+  std::vector<Record> rs;
+  const bsg_status st = records_from_trace(recs, n, *w, &rs, err);
+  if (st != BSG_OK) return st;
+  return replay_records(ctx, std::move(rs), cfg, spec, outcomes, summary, nullptr);
+}
+
 bsg_status bsg_replay(bsg_ctx* ctx, const bsg_workload* w, const bsg_instance_cfg* cfg,
                       const bsg_replay_spec* spec, bsg_request_outcome* outcomes,
                       bsg_replay_summary* summary, bsg_capture** capture) {
   if (!ctx || !w || !cfg || !spec || spec->n_instances < 1) return BSG_INVALID_ARGUMENT;
+  std::vector<Record> recs;
+  const bsg_status st = make_records(*w, &recs);
+  if (st != BSG_OK) return st;
+  return replay_records(ctx, std::move(recs), cfg, spec, outcomes, summary, capture);
+}
+
+namespace {
+bsg_status replay_records(bsg_ctx* ctx, std::vector<Record> recs, const bsg_instance_cfg* cfg,
+                          const bsg_replay_spec* spec, bsg_request_outcome* outcomes,
+                          bsg_replay_summary* summary, bsg_capture** capture) {
   // validate_provision_policy (autoscaler.cpp:23-34) and config.cpp:177-180
   if (spec->provision_kind < 0 || spec->provision_kind > 2 || !(spec->threshold_s > 0) ||
       spec->cold_start_s < 0 || spec->cooldown_s < 0 ||
@@ -687,9 +795,6 @@ bsg_status bsg_replay(bsg_ctx* ctx, const bsg_workload* w, const bsg_instance_cf
     return BSG_BAD_CONFIG;
   int32_t bi = 0, fc = 0;
   bsg_status st = bsg_set_configs(ctx, cfg, 1, &bi, &fc);
-  if (st != BSG_OK) return st;
-  std::vector<Record> recs;
-  st = make_records(*w, &recs);
   if (st != BSG_OK) return st;
   // Workload must be servable at all (config.cpp:197-205).
   for (const Record& r : recs)
@@ -706,6 +811,7 @@ bsg_status bsg_replay(bsg_ctx* ctx, const bsg_workload* w, const bsg_instance_cf
   if (capture) *capture = cap.release();
   return BSG_OK;
 }
+}  // namespace
 
 void bsg_capture_sizes(const bsg_capture* c, int64_t* n_entries, int64_t* n_scenarios) {
   *n_entries = static_cast<int64_t>(c->prompt.size());

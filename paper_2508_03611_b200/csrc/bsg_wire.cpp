@@ -9,6 +9,7 @@
 // way nlohmann::json::dump prints them (Grisu2 digits, fixed notation for
 // decimal exponents in (-4, 15], otherwise d.ddde±XX), so the response text is
 // byte-identical to the reference's prediction_result_to_json.
+#include <algorithm>
 #include <charconv>
 #include <cmath>
 #include <cstdint>
@@ -19,6 +20,7 @@
 #include <memory>
 #include <string>
 #include <system_error>
+#include <unordered_set>
 #include <vector>
 
 #include "bsg_internal.h"
@@ -35,9 +37,9 @@ struct JVal {
   std::string s;
   std::vector<JVal> arr;
   std::vector<std::pair<std::string, JVal>> obj;
-  const JVal* get(const char* key) const {
-    for (const auto& kv : obj)
-      if (kv.first == key) return &kv.second;
+  const JVal* get(const char* key) const {  // duplicate keys: the last one wins, as in nlohmann
+    for (auto it = obj.rbegin(); it != obj.rend(); ++it)
+      if (it->first == key) return &it->second;
     return nullptr;
   }
   bool is_number() const { return kind == kInt || kind == kUint || kind == kDouble; }
@@ -60,6 +62,19 @@ struct Parser {
     p += n;
     return true;
   }
+  static bool hex4(const char* h, unsigned* cp) {
+    unsigned v = 0;
+    for (int k = 0; k < 4; ++k) {
+      const char c = h[k];
+      v <<= 4;
+      if (c >= '0' && c <= '9') v |= c - '0';
+      else if (c >= 'a' && c <= 'f') v |= c - 'a' + 10;
+      else if (c >= 'A' && c <= 'F') v |= c - 'A' + 10;
+      else return false;
+    }
+    *cp = v;
+    return true;
+  }
   bool string(std::string* out) {
     if (p >= end || *p != '"') return fail("malformed JSON");
     ++p;
@@ -75,25 +90,31 @@ struct Parser {
           case 'n': out->push_back('\n'); break;
           case 'r': out->push_back('\r'); break;
           case 't': out->push_back('\t'); break;
-          case 'u': {  // keys/values of this schema are ASCII; keep BMP escapes as UTF-8
-            if (end - p < 5) return fail("malformed JSON");
+          case 'u': {  // \uXXXX, surrogate pairs joined, lone surrogates rejected
             unsigned cp = 0;
-            for (int k = 1; k <= 4; ++k) {
-              const char c = p[k];
-              cp <<= 4;
-              if (c >= '0' && c <= '9') cp |= c - '0';
-              else if (c >= 'a' && c <= 'f') cp |= c - 'a' + 10;
-              else if (c >= 'A' && c <= 'F') cp |= c - 'A' + 10;
-              else return fail("malformed JSON");
-            }
+            if (end - p < 5 || !hex4(p + 1, &cp)) return fail("malformed JSON");
             p += 4;
+            if (cp >= 0xDC00 && cp <= 0xDFFF) return fail("malformed JSON");
+            if (cp >= 0xD800 && cp <= 0xDBFF) {
+              unsigned lo = 0;
+              if (end - p < 7 || p[1] != '\\' || p[2] != 'u' || !hex4(p + 3, &lo) || lo < 0xDC00 ||
+                  lo > 0xDFFF)
+                return fail("malformed JSON");
+              p += 6;
+              cp = 0x10000 + ((cp - 0xD800) << 10) + (lo - 0xDC00);
+            }
             if (cp < 0x80) {
               out->push_back(static_cast<char>(cp));
             } else if (cp < 0x800) {
               out->push_back(static_cast<char>(0xc0 | (cp >> 6)));
               out->push_back(static_cast<char>(0x80 | (cp & 0x3f)));
-            } else {
+            } else if (cp < 0x10000) {
               out->push_back(static_cast<char>(0xe0 | (cp >> 12)));
+              out->push_back(static_cast<char>(0x80 | ((cp >> 6) & 0x3f)));
+              out->push_back(static_cast<char>(0x80 | (cp & 0x3f)));
+            } else {
+              out->push_back(static_cast<char>(0xf0 | (cp >> 18)));
+              out->push_back(static_cast<char>(0x80 | ((cp >> 12) & 0x3f)));
               out->push_back(static_cast<char>(0x80 | ((cp >> 6) & 0x3f)));
               out->push_back(static_cast<char>(0x80 | (cp & 0x3f)));
             }
@@ -103,24 +124,62 @@ struct Parser {
         }
         ++p;
       } else {
-        out->push_back(*p++);
+        const unsigned char c = static_cast<unsigned char>(*p);
+        if (c < 0x20) return fail("malformed JSON");  // RFC 8259 §7
+        if (c < 0x80) {
+          out->push_back(*p++);
+          continue;
+        }
+        // well-formed UTF-8 only (RFC 3629 §4), as nlohmann's lexer checks
+        int n = 0;
+        unsigned char lo2 = 0x80, hi2 = 0xBF;
+        if (c >= 0xC2 && c <= 0xDF) n = 1;
+        else if (c == 0xE0) n = 2, lo2 = 0xA0;
+        else if (c >= 0xE1 && c <= 0xEC) n = 2;
+        else if (c == 0xED) n = 2, hi2 = 0x9F;
+        else if (c >= 0xEE && c <= 0xEF) n = 2;
+        else if (c == 0xF0) n = 3, lo2 = 0x90;
+        else if (c >= 0xF1 && c <= 0xF3) n = 3;
+        else if (c == 0xF4) n = 3, hi2 = 0x8F;
+        else return fail("malformed JSON");
+        if (end - p <= n) return fail("malformed JSON");
+        for (int k = 1; k <= n; ++k) {
+          const unsigned char d = static_cast<unsigned char>(p[k]);
+          if (k == 1 ? (d < lo2 || d > hi2) : (d < 0x80 || d > 0xBF)) return fail("malformed JSON");
+        }
+        out->append(p, p + n + 1);
+        p += n + 1;
       }
     }
     if (p >= end) return fail("malformed JSON");
     ++p;
     return true;
   }
-  bool number(JVal* v) {
+  bool number(JVal* v) {  // RFC 8259 grammar: -?(0|[1-9][0-9]*)(.[0-9]+)?([eE][+-]?[0-9]+)?
     const char* s = p;
+    auto digit = [&] { return p < end && *p >= '0' && *p <= '9'; };
     bool is_float = false;
     if (p < end && *p == '-') ++p;
-    while (p < end && ((*p >= '0' && *p <= '9') || *p == '.' || *p == 'e' || *p == 'E' || *p == '+' ||
-                       *p == '-')) {
-      if (*p == '.' || *p == 'e' || *p == 'E') is_float = true;
+    if (!digit()) return fail("malformed JSON");
+    if (*p == '0') {
       ++p;
+    } else {
+      while (digit()) ++p;
     }
-    if (p == s) return fail("malformed JSON");
-    if (!is_float) {
+    if (p < end && *p == '.') {
+      ++p;
+      is_float = true;
+      if (!digit()) return fail("malformed JSON");
+      while (digit()) ++p;
+    }
+    if (p < end && (*p == 'e' || *p == 'E')) {
+      ++p;
+      is_float = true;
+      if (p < end && (*p == '+' || *p == '-')) ++p;
+      if (!digit()) return fail("malformed JSON");
+      while (digit()) ++p;
+    }
+    if (!is_float) {  // integers that overflow 64 bits fall through to double, as in nlohmann
       if (*s == '-') {
         int64_t x = 0;
         auto r = std::from_chars(s, p, x);
@@ -235,23 +294,27 @@ const JVal& at(const JVal& j, const char* key) {
   return *v;
 }
 
+// nlohmann get<integral>: any JSON number, converted; booleans too, except for
+// its own number_integer_t / number_unsigned_t (int64_t / uint64_t), whose
+// from_json is get_arithmetic_value (json.hpp 3.11.3, from_json overloads).
 template <typename T>
-T as_int(const JVal& v) {  // nlohmann get<integral>: any JSON number, converted
+T as_int(const JVal& v) {
   switch (v.kind) {
     case JVal::kInt: return static_cast<T>(v.i);
     case JVal::kUint: return static_cast<T>(v.u);
     case JVal::kDouble: return static_cast<T>(v.d);
-    case JVal::kBool: return static_cast<T>(v.b);
+    case JVal::kBool:
+      if (sizeof(T) == 8) throw SchemaError{"type must be number, but is boolean"};
+      return static_cast<T>(v.b);
     default: throw SchemaError{"type must be number"};
   }
 }
 
-double as_double(const JVal& v) {
+double as_double(const JVal& v) {  // get<double> = get_arithmetic_value: no booleans
   switch (v.kind) {
     case JVal::kInt: return static_cast<double>(v.i);
     case JVal::kUint: return static_cast<double>(v.u);
     case JVal::kDouble: return v.d;
-    case JVal::kBool: return v.b ? 1.0 : 0.0;
     default: throw SchemaError{"type must be number"};
   }
 }
@@ -721,6 +784,102 @@ extern "C" bsg_status bsg_predict_json(bsg_ctx* ctx, const char* const* requests
   }
   out_off[n] = off;
   return off <= out_cap ? BSG_OK : BSG_INVALID_ARGUMENT;  // out_off[n] = bytes needed
+}
+
+// ---- trace JSONL (workload.cpp:20-68) --------------------------------------
+namespace {
+
+void set_err(bsg_trace_error* err, int32_t kind, int32_t line, const std::string& field,
+             const std::string& msg) {
+  if (!err) return;
+  err->kind = kind;
+  err->line = line;
+  std::snprintf(err->field, sizeof(err->field), "%s", field.c_str());
+  std::snprintf(err->message, sizeof(err->message), "%s", msg.c_str());
+}
+
+// record_from_json (workload.cpp:20-36): a missing or mistyped field is a
+// TraceParseError of its line; `contains` + get, so an explicit null in an
+// optional field is mistyped, not absent.
+bsg_trace_record record_from(const JVal& j) {
+  bsg_trace_record r{};
+  r.id = as_int<uint64_t>(at(j, "id"));
+  r.prompt_tokens = as_int<int32_t>(at(j, "prompt_tokens"));
+  r.output_tokens = as_int<int32_t>(at(j, "output_tokens"));
+  if (j.kind == JVal::kObject && j.get("estimated_output_tokens")) {
+    // validate_record rejects a present estimate < 1, so 0 is free to mean
+    // "absent" in the flat record
+    r.estimated_output_tokens = as_int<int32_t>(*j.get("estimated_output_tokens"));
+  }
+  if (j.kind == JVal::kObject && j.get("arrival_offset_s")) {
+    r.arrival_offset_s = as_double(*j.get("arrival_offset_s"));
+    r.has_arrival_offset = 1;
+  }
+  return r;
+}
+
+}  // namespace
+
+extern "C" bsg_status bsg_load_trace(const char* text, int64_t len, bsg_trace_record* out,
+                                     int64_t cap, int64_t* n_records, bsg_trace_error* err) {
+  if ((!text && len > 0) || len < 0 || cap < 0 || (!out && cap > 0) || !n_records)
+    return BSG_INVALID_ARGUMENT;
+  set_err(err, 0, 0, "", "");
+  *n_records = 0;
+  std::unordered_set<uint64_t> seen;
+  int64_t n = 0;
+  int32_t line_number = 0;
+  const char* p = text;
+  const char* const end = text + len;
+  while (p < end) {
+    const char* nl = static_cast<const char*>(std::memchr(p, '\n', static_cast<size_t>(end - p)));
+    const char* line_end = nl ? nl : end;
+    ++line_number;
+    const char* a = p;
+    p = nl ? nl + 1 : end;
+    bool blank = true;
+    for (const char* c = a; c < line_end && blank; ++c) blank = (*c == ' ' || *c == '\t' || *c == '\r');
+    if (blank) continue;
+    Parser ps{a, line_end, {}};
+    JVal j;
+    bool good = ps.value(&j);
+    ps.ws();
+    if (good && ps.p != ps.end) good = false;
+    if (!good) {
+      set_err(err, 1, line_number, "",
+              "trace parse error at line " + std::to_string(line_number) + ": malformed JSON");
+      return BSG_BAD_INPUT;
+    }
+    bsg_trace_record r;
+    try {
+      r = record_from(j);
+    } catch (const SchemaError& e) {
+      set_err(err, 1, line_number, "",
+              "trace parse error at line " + std::to_string(line_number) + ": " + e.what);
+      return BSG_BAD_INPUT;
+    }
+    // validate_record (workload.cpp:38-47)
+    const char* bad = nullptr;
+    if (r.prompt_tokens < 1) bad = "prompt_tokens";
+    else if (r.output_tokens < 1) bad = "output_tokens";
+    else if (j.get("estimated_output_tokens") && r.estimated_output_tokens < 1) bad = "estimated_output_tokens";
+    else if (r.has_arrival_offset && r.arrival_offset_s < 0) bad = "arrival_offset_s";
+    if (bad) {
+      set_err(err, 2, line_number, bad,
+              std::string("invalid trace record: ") + bad + ": must be >= " +
+                  (std::strcmp(bad, "arrival_offset_s") == 0 ? "0" : "1"));
+      return BSG_BAD_INPUT;
+    }
+    if (!seen.insert(r.id).second) {
+      set_err(err, 2, line_number, "id",
+              "invalid trace record: id: duplicate id " + std::to_string(r.id));
+      return BSG_BAD_INPUT;
+    }
+    if (n < cap) out[n] = r;
+    ++n;
+  }
+  *n_records = n;
+  return n > cap ? BSG_INVALID_ARGUMENT : BSG_OK;
 }
 
 extern "C" int32_t bsg_format_double(double v, char* out, int32_t cap) {

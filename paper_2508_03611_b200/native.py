@@ -70,6 +70,11 @@ def load() -> C.CDLL:
         "bsg_fleet_finish": (C.c_int, [V, V, V, V]),
         "bsg_predict_json": (C.c_int, [V, V, C.c_int32, V, C.c_int64, V, V]),
         "bsg_format_double": (C.c_int32, [C.c_double, C.c_char_p, C.c_int32]),
+        "bsg_load_trace": (C.c_int, [C.c_char_p, C.c_int64, V, C.c_int64, C.POINTER(C.c_int64),
+                                     C.POINTER(abi.TraceError)]),
+        "bsg_trace_workload": (C.c_int, [V, C.c_int64, V, V, V, V, V, C.POINTER(C.c_int64),
+                                         C.POINTER(abi.TraceError)]),
+        "bsg_replay_trace": (C.c_int, [V, V, C.c_int64, V, V, V, V, V, C.POINTER(abi.TraceError)]),
         "bsg_fleet_snapshot": (C.c_int, [V, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                          V, V, V, V, C.c_int32]),
     }
@@ -147,6 +152,55 @@ def make_workload_host(w: np.ndarray):
     if st != abi.OK:
         raise BsgError(st, "bsg_make_workload")
     return p, o, e, t
+
+
+class TraceError(ValueError):
+    """load_trace / generate_arrivals rejection: kind 1 TraceParseError (line),
+    2 InvalidRecordError (field), 3 ConfigError (field)."""
+
+    def __init__(self, e: abi.TraceError):
+        self.kind, self.line = int(e.kind), int(e.line)
+        self.field = e.field.decode()
+        super().__init__(e.message.decode())
+
+
+def load_trace(text: str | bytes) -> np.ndarray:
+    """load_trace (workload.cpp:51-68) over a JSON Lines text -> trace_record_dtype
+    rows; raises TraceError on the first bad line. No GPU needed."""
+    L = load()
+    b = text.encode() if isinstance(text, str) else bytes(text)
+    err, n = abi.TraceError(), C.c_int64(0)
+    cap = b.count(b"\n") + 1
+    out = np.zeros(cap, abi.trace_record_dtype)
+    st = L.bsg_load_trace(b, len(b), _p(out), cap, C.byref(n), C.byref(err))
+    if st == abi.BAD_INPUT:
+        raise TraceError(err)
+    if st != abi.OK:
+        raise BsgError(st, "bsg_load_trace")
+    return out[:n.value].copy()
+
+
+def load_trace_file(path: str) -> np.ndarray:
+    with open(path, "rb") as f:
+        return load_trace(f.read())
+
+
+def trace_workload(recs: np.ndarray, w: np.ndarray):
+    """Request columns (prompt, output, est, arrival_ticks) run_experiment
+    builds from trace records: request_cap, generate_arrivals, estimate_length."""
+    L = load()
+    recs = np.ascontiguousarray(recs, dtype=abi.trace_record_dtype)
+    n = len(recs)
+    p, o, e = (np.zeros(max(n, 1), np.int32) for _ in range(3))
+    t = np.zeros(max(n, 1), np.int64)
+    err, m = abi.TraceError(), C.c_int64(0)
+    st = L.bsg_trace_workload(_p(recs), n, _p(w), _p(p), _p(o), _p(e), _p(t), C.byref(m), C.byref(err))
+    if st == abi.BAD_INPUT:
+        raise TraceError(err)
+    if st != abi.OK:
+        raise BsgError(st, "bsg_trace_workload")
+    k = m.value
+    return p[:k], o[:k], e[:k], t[:k]
 
 
 class Fleet:
@@ -332,9 +386,10 @@ class Context:
     def replay_device(self, runs):
         """Device-resident closed loops (bsg_replay_device). runs: list of
         (workload, replay_spec, cfg_index) with the configs already set (the
-        spec's policy must be BlockPredictive). Returns [(status, outcomes,
-        summary)] per run."""
-        cols = [make_workload_host(w) for w, *_ in runs]
+        spec's policy must be BlockPredictive); a workload may also be the
+        (prompt, output, est, arrival_ticks) columns, e.g. of trace_workload.
+        Returns [(status, outcomes, summary)] per run."""
+        cols = [w if isinstance(w, tuple) else make_workload_host(w) for w, *_ in runs]
         desc = np.zeros(len(runs), abi.closed_loop_run_dtype)
         off = 0
         for r, ((w, sp, cf), c) in enumerate(zip(runs, cols)):
@@ -356,6 +411,21 @@ class Context:
             a, n = int(desc[r]["req_off"]), int(desc[r]["n_requests"])
             res.append((int(st[r]), out[a:a + n], summ[r]))
         return res
+
+    def replay_trace(self, recs, w, cfg, spec):
+        """Closed-loop replay over trace records (bsg_replay_trace). Returns
+        (outcomes, summary)."""
+        recs = np.ascontiguousarray(recs, dtype=abi.trace_record_dtype)
+        n = len(recs) if w["request_cap"][0] < 0 else min(len(recs), int(w["request_cap"][0]))
+        out = np.zeros(max(n, 1), abi.outcome_dtype)
+        summ = np.zeros(1, abi.summary_dtype)
+        err = abi.TraceError()
+        st = self.L.bsg_replay_trace(self.h, _p(recs), len(recs), _p(w), _p(cfg), _p(spec), _p(out),
+                                     _p(summ), C.byref(err))
+        if st == abi.BAD_INPUT and err.kind:
+            raise TraceError(err)
+        self._check(st, "bsg_replay_trace")
+        return out[:n], summ[0]
 
     def replay(self, w, cfg, spec):
         """Closed-loop replay (host live instances, GPU what-ifs). Returns

@@ -6,7 +6,7 @@ batch composition / allocation / preemption fingerprints, and decisions.
 import numpy as np
 import pytest
 
-from paper_2508_03611_b200 import abi
+from paper_2508_03611_b200 import abi, native
 from oracle.oracle import compare_to_ref
 from scenarios import fuzz_set, kat_set
 from test_oracle import load_golden
@@ -365,3 +365,61 @@ def test_wire_predict_json_matches_reference_service(ctx, ref):
             assert st != abi.OK, (i, code, exp)
             assert json.loads(text)["error"] == json.loads(exp)["error"], (i, text, exp)
     assert n_ok > 400  # mostly successes, with failures of every kind mixed in
+
+
+def _trace_text(n, seed, offsets, shuffle=False):
+    """A JSONL trace built from a synthetic workload (ids sparse, estimates tagged)."""
+    import json
+    p, o, e, t = native.make_workload_host(abi.make_workload(count=n, qps=9.0, arrival_seed=seed,
+                                                             estimator_kind=2, estimator_seed=seed))
+    rng = np.random.default_rng(seed)
+    ids = rng.permutation(50 * n)[:n] + 1000
+    lines = []
+    for i in range(n):
+        d = {"id": int(ids[i]), "prompt_tokens": int(p[i]), "output_tokens": int(o[i]),
+             "estimated_output_tokens": int(e[i])}
+        if offsets:
+            d["arrival_offset_s"] = float(t[i]) * 1e-9
+        lines.append(json.dumps(d))
+    if shuffle:  # arrivals out of record order, with exact ties
+        rng.shuffle(lines)
+        lines[5] = lines[5].replace(lines[5][lines[5].index('"arrival_offset_s"'):],
+                                    lines[6][lines[6].index('"arrival_offset_s"'):])
+    return "\n".join(lines) + "\n"
+
+
+@pytest.mark.parametrize("offsets,shuffle,est_kind", [
+    (False, False, abi.ESTIMATOR_TRACE), (True, False, abi.ESTIMATOR_TRACE),
+    (True, False, abi.ESTIMATOR_NOISY), (True, True, abi.ESTIMATOR_ORACLE)])
+def test_trace_closed_loop_matches_reference(ctx, ref, offsets, shuffle, est_kind):
+    """A JSONL trace through load_trace -> run_experiment (workload.cpp:51-170,
+    driver.cpp:137-160): the host closed loop for any arrival order, and the
+    device closed loop (K5) for time-ordered arrivals, tick-exact against the
+    reference fed the same records."""
+    text = _trace_text(400, 3 + est_kind, offsets, shuffle)
+    recs = native.load_trace(text)
+    want_recs, err = ref.load_trace(text)
+    assert err is None and recs.tobytes() == want_recs.tobytes()
+    w = abi.make_workload(qps=8.0, arrival_seed=17, estimator_kind=est_kind, estimator_seed=5)
+    cfg = abi.make_config(total_blocks=600, max_batch_size=32)
+    for ni in (3, 6):
+        spec = abi.make_replay_spec(ni, capture=0)
+        ref.set_trace(recs)
+        try:
+            exp, esum = ref.run_experiment(w, cfg, spec)
+            erep = ref.run_report(w, cfg, spec)
+        finally:
+            ref.set_trace(None)
+        host, hsum = ctx.replay_trace(recs, w, cfg, spec)
+        assert host.tobytes() == exp.tobytes(), (ni, np.nonzero(host != exp)[0][:5])
+        assert int(hsum["total_preemptions"]) == int(esum["total_preemptions"])
+        cols = native.trace_workload(recs, w)
+        if np.all(np.diff(cols[3]) >= 0):
+            ctx.set_configs(cfg)
+            [(st, out, summ)] = ctx.replay_device([(cols, spec, 0)])
+            assert st == abi.OK
+            for f in ("instance", "dispatch_ticks", "first_token_ticks", "finish_ticks", "preempt_count"):
+                assert np.array_equal(out[f], exp[f]), (ni, f)
+            assert ctx.last_reports[0].tobytes() == erep.tobytes()
+        else:
+            assert shuffle
