@@ -148,23 +148,30 @@ __global__ void __launch_bounds__(256) heavy_threshold_kernel(const bsg_scenario
   }
 }
 
+// One pass of the predict kernels serves the scenarios of ONE instance config,
+// passed by value as a __grid_constant__ kernel parameter: its fields stay in
+// the constant bank and feed the integer / FP64 instructions as c[][] operands
+// instead of occupying ~14 registers for the whole simulation (measured on
+// cfg2: spills 172/356 B -> 74/84 B, 222 -> 247 M scenarios/s). Sets that mix
+// configs run one pass per config in use; the other scenarios' warps exit at
+// once. Returns false when this pass does not own the scenario.
 template <int K, bool POW2, bool OPT, int WJ>
-__device__ __forceinline__ void predict_one(const DevCfg* __restrict__ cfgs, int32_t ncfg,
+__device__ __forceinline__ bool predict_one(const DevCfg& cfg, int32_t cfg_sel, int32_t ncfg,
                                             const int32_t* __restrict__ prompt,
                                             const int32_t* __restrict__ est,
                                             const int32_t* __restrict__ prefill,
                                             const int32_t* __restrict__ decoded,
                                             const bsg_scenario& sc, int32_t* smem,
                                             bsg_result* __restrict__ o) {
-  if (sc.cfg < 0 || sc.cfg >= ncfg) {
+  if (sc.cfg < 0 || sc.cfg >= ncfg) {  // every pass writes the same verdict
     if ((threadIdx.x & 31) == 0) {
       bsg_result r{};
       r.status = BSG_INVALID_ARGUMENT;
       *o = r;
     }
-    return;
+    return false;
   }
-  const DevCfg cfg = cfgs[sc.cfg];
+  if (sc.cfg != cfg_sel) return false;
   const int32_t need = max(sc.run_n, min(cfg.max_batch_size, sc.run_n + sc.wait_n + 1));
   if ((!OPT && need > 32 * K) || sc.run_n < 0 || sc.wait_n < 0) {
     if ((threadIdx.x & 31) == 0) {
@@ -172,7 +179,7 @@ __device__ __forceinline__ void predict_one(const DevCfg* __restrict__ cfgs, int
       r.status = BSG_BAD_INPUT;
       *o = r;
     }
-    return;
+    return false;
   }
   // One window width per kernel (a second instantiation costs more in spills
   // than it saves): 128-step windows for 32-member sets, 32-step windows for
@@ -180,6 +187,7 @@ __device__ __forceinline__ void predict_one(const DevCfg* __restrict__ cfgs, int
   // (measured: cfg3 8.1 ms at J=1 vs 9.6 ms at J=4; cfg1 prefers J=4, 238 vs 310 us).
   simulate_scenario<K, false, false, POW2, true, OPT, WJ>(cfg, prompt, est, prefill, decoded, sc, smem, o,
                                                          TraceSink{nullptr, 0});
+  return true;
 }
 
 // WJ: event-skipping window width (steps per lane). Measured choices: 128-step
@@ -188,7 +196,7 @@ __device__ __forceinline__ void predict_one(const DevCfg* __restrict__ cfgs, int
 // and KV pressure, where admissions/preemptions cut windows short.
 template <int K, bool POW2, bool OPT, int WJ>
 __global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K))
-    predict_kernel(const DevCfg* __restrict__ cfgs, int32_t ncfg,
+    predict_kernel(__grid_constant__ const DevCfg cfg, int32_t cfg_sel, int32_t ncfg,
                    const int32_t* __restrict__ prompt, const int32_t* __restrict__ est,
                    const int32_t* __restrict__ prefill, const int32_t* __restrict__ decoded,
                    const bsg_scenario* __restrict__ scen, int64_t n, WorkQueue* __restrict__ q,
@@ -214,10 +222,11 @@ __global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K))
     return;
   }
   const bsg_scenario sc = scen[w];
-  predict_one<K, POW2, OPT, WJ>(cfgs, ncfg, prompt, est, prefill, decoded, sc, smem, out + w);
+  const bool ran = predict_one<K, POW2, OPT, WJ>(cfg, cfg_sel, ncfg, prompt, est, prefill, decoded, sc,
+                                                  smem, out + w);
   if constexpr (OPT) {  // too wide for this pass: list it for the wide kernel
     __syncwarp();
-    if ((threadIdx.x & 31) == 0 && out[w].status == kStatusRetryWider)
+    if (ran && (threadIdx.x & 31) == 0 && out[w].status == kStatusRetryWider)
       retry_list(q, n)[atomicAdd(&q->retry_count, 1)] = static_cast<int32_t>(w);
   }
 }
@@ -225,7 +234,7 @@ __global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K))
 // The wide pass over the scenarios the optimistic narrow pass handed back.
 template <int K, bool POW2>
 __global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K))
-    predict_retry_kernel(const DevCfg* __restrict__ cfgs, int32_t ncfg,
+    predict_retry_kernel(__grid_constant__ const DevCfg cfg, int32_t cfg_sel, int32_t ncfg,
                          const int32_t* __restrict__ prompt, const int32_t* __restrict__ est,
                          const int32_t* __restrict__ prefill, const int32_t* __restrict__ decoded,
                          const bsg_scenario* __restrict__ scen, int64_t n, WorkQueue* __restrict__ q,
@@ -239,7 +248,8 @@ __global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K))
        j += static_cast<int64_t>(gridDim.x) * kPredictWarps) {
     const int64_t w = __ldcg(&rl[j]);
     const bsg_scenario sc = scen[w];
-    predict_one<K, POW2, false, BSG_WIN_J_WIDE>(cfgs, ncfg, prompt, est, prefill, decoded, sc, smem, out + w);
+    predict_one<K, POW2, false, BSG_WIN_J_WIDE>(cfg, cfg_sel, ncfg, prompt, est, prefill, decoded, sc, smem,
+                                                out + w);
   }
 }
 
@@ -447,15 +457,16 @@ int capacity_k(int32_t need) {
 #define BSG_QUEUE_MIN 8192
 #endif
 
+// One pass: the scenarios of config cfg_sel (see predict_one).
 template <int K, bool POW2>
-bsg_status launch_predict_t(bsg_ctx* ctx, int64_t n, const bsg_entries& e, const bsg_scenario* sc,
-                            bsg_result* out, cudaStream_t s) {
+bsg_status launch_predict_t(bsg_ctx* ctx, int32_t cfg_sel, int64_t n, const bsg_entries& e,
+                            const bsg_scenario* sc, bsg_result* out, cudaStream_t s) {
   static const bool no_queue = std::getenv("BSG_NO_QUEUE") != nullptr;
-  auto* cf = static_cast<const DevCfg*>(ctx->cfgs.p);
+  const DevCfg& cf = ctx->dev_cfgs_host[cfg_sel];
   const int64_t blocks = (n + kPredictWarps - 1) / kPredictWarps;
   if (no_queue || n < BSG_QUEUE_MIN) {
     predict_kernel<K, POW2, false, BSG_WIN_J_PREDICT><<<static_cast<unsigned>(blocks), kPredictWarps * 32, 0, s>>>(
-        cf, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, nullptr, out);
+        cf, cfg_sel, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, nullptr, out);
     ctx->launches += 1;
     BSG_CUDA(ctx, cudaGetLastError());
     return BSG_OK;
@@ -477,12 +488,12 @@ bsg_status launch_predict_t(bsg_ctx* ctx, int64_t n, const bsg_entries& e, const
       // 32-slot kernel runs at 32 warps/SM with half the per-member work, and hands
       // the rest to the wide kernel.
       predict_kernel<1, POW2, true, BSG_WIN_J_PREDICT><<<static_cast<unsigned>(pb), kPredictWarps * 32, 0, s>>>(
-          cf, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
+          cf, cfg_sel, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
       predict_kernel<1, POW2, true, BSG_WIN_J_WIDE><<<static_cast<unsigned>(pb), kPredictWarps * 32, 0, s>>>(
-          cf, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
+          cf, cfg_sel, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
       const int64_t rb = std::min<int64_t>(pb, 148 * 8);
       predict_retry_kernel<K, POW2><<<static_cast<unsigned>(rb), kPredictWarps * 32, 0, s>>>(
-          cf, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
+          cf, cfg_sel, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
       ctx->launches += 5;
       BSG_CUDA(ctx, cudaGetLastError());
       BSG_CUDA(ctx, cudaFreeAsync(mem, s));
@@ -491,7 +502,7 @@ bsg_status launch_predict_t(bsg_ctx* ctx, int64_t n, const bsg_entries& e, const
   }
   predict_kernel<K, POW2, false, K == 1 ? BSG_WIN_J_PREDICT : BSG_WIN_J_WIDE>
       <<<static_cast<unsigned>(pb), kPredictWarps * 32, 0, s>>>(
-      cf, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
+      cf, cfg_sel, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
   ctx->launches += 3;
   BSG_CUDA(ctx, cudaGetLastError());
   if (std::getenv("BSG_QUEUE_DEBUG")) {
@@ -505,26 +516,45 @@ bsg_status launch_predict_t(bsg_ctx* ctx, int64_t n, const bsg_entries& e, const
   return BSG_OK;
 }
 
+// One pass per config in use (used == nullptr: every config); a pass is
+// specialised on its own block size (shift/mask when it is a power of two).
 template <int K>
 bsg_status launch_predict(bsg_ctx* ctx, int64_t n, const bsg_entries& e, const bsg_scenario* sc,
-                          bsg_result* out, cudaStream_t s) {
-  return ctx->all_pow2 ? launch_predict_t<K, true>(ctx, n, e, sc, out, s)
-                       : launch_predict_t<K, false>(ctx, n, e, sc, out, s);
+                          bsg_result* out, cudaStream_t s, const std::vector<uint8_t>* used) {
+  bool any = false;
+  for (int32_t c = 0; c < ctx->ncfg; ++c) any |= !used || (*used)[c];
+  for (int32_t c = 0; c < ctx->ncfg; ++c) {
+    if (used && !(*used)[c] && (any || c > 0)) continue;  // >= 1 pass: it writes bad-cfg verdicts
+    const bsg_status st = ctx->dev_cfgs_host[c].div_magic == 0
+                              ? launch_predict_t<K, true>(ctx, c, n, e, sc, out, s)
+                              : launch_predict_t<K, false>(ctx, c, n, e, sc, out, s);
+    if (st != BSG_OK) return st;
+  }
+  return BSG_OK;
 }
 
 bsg_status launch_predict_k(bsg_ctx* ctx, int k, int64_t n, const bsg_entries& e,
-                            const bsg_scenario* sc, bsg_result* out, cudaStream_t s) {
+                            const bsg_scenario* sc, bsg_result* out, cudaStream_t s,
+                            const std::vector<uint8_t>* used) {
   if (n == 0) return BSG_OK;
   ctx->scenarios += n;
   switch (k) {
-    case 1: return launch_predict<1>(ctx, n, e, sc, out, s);
-    case 2: return launch_predict<2>(ctx, n, e, sc, out, s);
-    case 4: return launch_predict<4>(ctx, n, e, sc, out, s);
-    case 8: return launch_predict<8>(ctx, n, e, sc, out, s);
+    case 1: return launch_predict<1>(ctx, n, e, sc, out, s, used);
+    case 2: return launch_predict<2>(ctx, n, e, sc, out, s, used);
+    case 4: return launch_predict<4>(ctx, n, e, sc, out, s, used);
+    case 8: return launch_predict<8>(ctx, n, e, sc, out, s, used);
     default:
       ctx->last_error = "member capacity beyond 256 is outside the supported domain";
       return BSG_BAD_INPUT;
   }
+}
+
+// Which configs a host scenario set uses (out-of-range indices are skipped).
+std::vector<uint8_t> cfgs_used(const bsg_scenario* sc, int64_t n, int32_t ncfg) {
+  std::vector<uint8_t> u(static_cast<size_t>(std::max(ncfg, 0)), 0);
+  for (int64_t i = 0; i < n; ++i)
+    if (sc[i].cfg >= 0 && sc[i].cfg < ncfg) u[sc[i].cfg] = 1;
+  return u;
 }
 
 int32_t host_need(const bsg_scenario* sc, int64_t n, const std::vector<bsg_instance_cfg>& cfgs) {
@@ -743,8 +773,10 @@ bsg_status bsg_predict_batch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n
     if (s0 >= s1) continue;
     int64_t lo = INT64_MAX, hi = 0;
     int32_t need = 1;
+    std::vector<uint8_t> used(static_cast<size_t>(ctx->ncfg), 0);
     for (int64_t i = s0; i < s1; ++i) {
       const bsg_scenario& x = scenarios[i];
+      if (x.cfg >= 0 && x.cfg < ctx->ncfg) used[x.cfg] = 1;
       if (x.run_n > 0) {
         lo = std::min<int64_t>(lo, x.run_off);
         hi = std::max<int64_t>(hi, static_cast<int64_t>(x.run_off) + x.run_n);
@@ -771,7 +803,7 @@ bsg_status bsg_predict_batch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n
     BSG_CUDA(ctx, cudaMemcpyAsync(dsc + s0, scenarios + s0, (s1 - s0) * sizeof(bsg_scenario),
                                   cudaMemcpyHostToDevice, st));
     const int k = capacity_k(need);
-    const bsg_status ls = launch_predict_k(ctx, k == 0 ? 8 : k, s1 - s0, dev, dsc + s0, dres + s0, st);
+    const bsg_status ls = launch_predict_k(ctx, k == 0 ? 8 : k, s1 - s0, dev, dsc + s0, dres + s0, st, &used);
     if (ls != BSG_OK) return ls;
     BSG_CUDA(ctx, cudaMemcpyAsync(out + s0, dres + s0, (s1 - s0) * sizeof(bsg_result),
                                   cudaMemcpyDeviceToHost, st));
@@ -791,7 +823,7 @@ bsg_status bsg_predict_batch_device(bsg_ctx* ctx, const bsg_entries* dev_entries
   const int32_t cap = member_capacity > 0 ? member_capacity : std::max(1, ctx->max_batch_all);
   int k = capacity_k(cap);
   if (k == 0) k = 8;
-  return launch_predict_k(ctx, k, n, *dev_entries, dev_scenarios, dev_out, s);
+  return launch_predict_k(ctx, k, n, *dev_entries, dev_scenarios, dev_out, s, nullptr);
 }
 
 bsg_status bsg_trace(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries,
@@ -881,8 +913,9 @@ bsg_status bsg_dispatch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entr
                                 cudaMemcpyHostToDevice, ctx->stream));
   const int k = capacity_k(host_need(scenarios, n, ctx->host_cfgs));
   auto* res = static_cast<bsg_result*>(ctx->res.p);
+  const std::vector<uint8_t> used = cfgs_used(scenarios, n, ctx->ncfg);
   st = launch_predict_k(ctx, k == 0 ? 8 : k, n, dev, static_cast<const bsg_scenario*>(ctx->scen.p),
-                        res, ctx->stream);
+                        res, ctx->stream, &used);
   if (st != BSG_OK) return st;
   const int warps = 4;
   argmin_kernel<<<(n_requests + warps - 1) / warps, warps * 32, 0, ctx->stream>>>(
