@@ -30,17 +30,24 @@ constexpr int kWarpsPerBlock = 4;
 #endif
 constexpr int kPredictWarps = BSG_WPB;
 
-// Resident-warp target per SM for the 32-member kernels: 32 warps/SM needs
-// <= 64 registers/thread (measured: see profiles/).
+// Resident-warp target per SM for the 32-member kernels: 28 warps/SM = 72
+// registers/thread (measured on cfg2 with the config in the constant bank:
+// 28 -> 249 M/s, 32 -> 246.5 M/s); the optimistic narrow passes of wide sets
+// keep 32 (64 registers; cfg3 7.44 ms at 28 vs 7.32 ms at 32).
 #ifndef BSG_K1_WARPS_PER_SM
-#define BSG_K1_WARPS_PER_SM 32
+#define BSG_K1_WARPS_PER_SM 28
+#endif
+#ifndef BSG_OPT_WARPS_PER_SM
+#define BSG_OPT_WARPS_PER_SM 32
 #endif
 // ... and for the 64-member kernels (KV-pressure sets with deep waiting queues)
 #ifndef BSG_K2_WARPS_PER_SM
 #define BSG_K2_WARPS_PER_SM 24
 #endif
-constexpr int min_blocks(int k) {
-  return k == 1 ? BSG_K1_WARPS_PER_SM / kPredictWarps : (k == 2 ? BSG_K2_WARPS_PER_SM / kPredictWarps : 1);
+constexpr int min_blocks(int k, bool opt = false) {
+  return opt ? BSG_OPT_WARPS_PER_SM / kPredictWarps
+             : k == 1 ? BSG_K1_WARPS_PER_SM / kPredictWarps
+                      : (k == 2 ? BSG_K2_WARPS_PER_SM / kPredictWarps : 1);
 }
 
 // ---- cost-aware launch order ----------------------------------------------------
@@ -195,7 +202,7 @@ __device__ __forceinline__ bool predict_one(const DevCfg& cfg, int32_t cfg_sel, 
 // longest scenario is the critical path), 32-step windows for large wide sets
 // and KV pressure, where admissions/preemptions cut windows short.
 template <int K, bool POW2, bool OPT, int WJ>
-__global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K))
+__global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K, OPT))
     predict_kernel(__grid_constant__ const DevCfg cfg, int32_t cfg_sel, int32_t ncfg,
                    const int32_t* __restrict__ prompt, const int32_t* __restrict__ est,
                    const int32_t* __restrict__ prefill, const int32_t* __restrict__ decoded,
