@@ -543,8 +543,7 @@ __device__ __forceinline__ void autoscale(ClShared<K>& S, const ClRun& run, int3
 
 template <int K, bool POW2>
 __global__ void __launch_bounds__(kClWarps * 32, BSG_CL_MINB)
-    closed_loop_kernel(__grid_constant__ const DevCfg cfg, __grid_constant__ const DevCfg live_cfg,
-                       int32_t cfg_sel, const ClRun* __restrict__ runs,
+    closed_loop_kernel(const DevCfg* __restrict__ cfgs, const ClRun* __restrict__ runs,
                        const int32_t* __restrict__ rq_prompt, const int32_t* __restrict__ rq_output,
                        const int32_t* __restrict__ rq_est, const int64_t* __restrict__ rq_arrival,
                        Arena ar, bsg_request_outcome* __restrict__ outcomes,
@@ -554,11 +553,11 @@ __global__ void __launch_bounds__(kClWarps * 32, BSG_CL_MINB)
   ClShared<K>& S = *reinterpret_cast<ClShared<K>*>(cl_smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const ClRun run = runs[blockIdx.x];
-  // One launch per config in use (concurrent streams): the config and its
-  // live-instance copy (cache off: live instances price steps with
-  // batch_latency itself, driver.cpp:274; only predict() uses the cache) are
-  // kernel parameters, read from the constant bank instead of registers.
-  if (run.cfg != cfg_sel) return;
+  const DevCfg cfg = cfgs[run.cfg];
+  // live instances price steps with batch_latency itself (driver.cpp:274 calls
+  // begin_step() without a latency function); only predict() uses the cache
+  DevCfg live_cfg = cfg;
+  live_cfg.cache_mode = BSG_CACHE_OFF;
   const int32_t I0 = run.n_inst, N = run.n_req, maxb = cfg.max_batch_size;
   const int32_t IMAX = run.prov_kind == 0 ? I0 : run.max_inst;  // instance slots
   const int64_t stride = inst_stride(maxb, N);
@@ -992,45 +991,17 @@ using namespace bsg;
 
 namespace {
 
-#define CL_CUDA(call)                                                   \
-  do {                                                                  \
-    const cudaError_t _e = (call);                                      \
-    if (_e != cudaSuccess) return bsg_cuda_fail(ctx, _e, #call);        \
-  } while (0)
-
 template <int K, bool POW2>
-bsg_status launch_closed_loop(bsg_ctx* ctx, const std::vector<uint8_t>& used, int32_t n_runs,
-                              const ClRun* runs,
+bsg_status launch_closed_loop(bsg_ctx* ctx, int32_t n_runs, const ClRun* runs,
                               const int32_t* p, const int32_t* o, const int32_t* e,
                               const int64_t* arr, const Arena& ar, bsg_request_outcome* outs,
                               bsg_replay_summary* sums, int32_t* st, bsg_run_report* rep) {
   const size_t sm = sizeof(ClShared<K>);
   cudaFuncSetAttribute(closed_loop_kernel<K, POW2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(sm));
-  int32_t n_used = 0, only = 0;
-  for (int32_t c = 0; c < ctx->ncfg; ++c)
-    if (used[c]) ++n_used, only = c;
-  auto launch = [&](int32_t c, cudaStream_t s) {
-    DevCfg live = ctx->dev_cfgs_host[c];
-    live.cache_mode = BSG_CACHE_OFF;
-    closed_loop_kernel<K, POW2><<<n_runs, kClWarps * 32, sm, s>>>(
-        ctx->dev_cfgs_host[c], live, c, runs, p, o, e, arr, ar, outs, sums, st, rep);
-    ctx->launches += 1;
-  };
-  if (n_used <= 1) {
-    launch(only, ctx->stream);
-  } else {  // several configs: their launches overlap on the pipeline streams
-    cudaEvent_t ready = ctx->pipe_done[0];
-    CL_CUDA(cudaEventRecord(ready, ctx->stream));
-    for (int i = 0; i < 3; ++i) CL_CUDA(cudaStreamWaitEvent(ctx->pipe[i], ready, 0));
-    int32_t k = 0;
-    for (int32_t c = 0; c < ctx->ncfg; ++c)
-      if (used[c]) launch(c, ctx->pipe[k++ % 3]);
-    for (int i = 0; i < 3; ++i) {
-      CL_CUDA(cudaEventRecord(ctx->pipe_done[i], ctx->pipe[i]));
-      CL_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->pipe_done[i], 0));
-    }
-  }
+  closed_loop_kernel<K, POW2><<<n_runs, kClWarps * 32, sm, ctx->stream>>>(
+      static_cast<const DevCfg*>(ctx->cfgs.p), runs, p, o, e, arr, ar, outs, sums, st, rep);
+  ctx->launches += 1;
   const cudaError_t err = cudaGetLastError();
   return err == cudaSuccess ? BSG_OK : bsg_cuda_fail(ctx, err, "closed_loop_kernel launch");
 }
@@ -1055,7 +1026,6 @@ extern "C" bsg_status bsg_replay_device(bsg_ctx* ctx, const bsg_closed_loop_run*
   int64_t arena = 0;
   int32_t maxb_all = 1;
   bool pow2 = true;
-  std::vector<uint8_t> used(static_cast<size_t>(ctx->ncfg), 0);
   for (int32_t r = 0; r < n_runs; ++r) {
     const bsg_closed_loop_run& x = runs[r];
     if (x.cfg < 0 || x.cfg >= ctx->ncfg || x.n_instances < 1 || x.n_instances > kClMaxInst ||
@@ -1071,7 +1041,6 @@ extern "C" bsg_status bsg_replay_device(bsg_ctx* ctx, const bsg_closed_loop_run*
       return BSG_BAD_CONFIG;
     const int32_t slots = x.provision_kind == 0 ? x.n_instances : x.max_instances;
     const bsg_instance_cfg& c = ctx->host_cfgs[x.cfg];
-    used[x.cfg] = 1;
     maxb_all = std::max(maxb_all, c.max_batch_size);
     pow2 &= ctx->dev_cfgs_host[x.cfg].div_magic == 0;
     for (int64_t q = x.req_off; q < x.req_off + x.n_requests; ++q) {
@@ -1144,14 +1113,14 @@ extern "C" bsg_status bsg_replay_device(bsg_ctx* ctx, const bsg_closed_loop_run*
   BSG_CL_CHECK(cudaMemcpyAsync(d_out, init.data(), b_out, cudaMemcpyHostToDevice, s));
   if (st == BSG_OK) {
     switch (k * 2 + (pow2 ? 1 : 0)) {
-      case 2: st = launch_closed_loop<1, false>(ctx, used, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
-      case 3: st = launch_closed_loop<1, true>(ctx, used, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
-      case 4: st = launch_closed_loop<2, false>(ctx, used, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
-      case 5: st = launch_closed_loop<2, true>(ctx, used, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
-      case 8: st = launch_closed_loop<4, false>(ctx, used, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
-      case 9: st = launch_closed_loop<4, true>(ctx, used, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
-      case 16: st = launch_closed_loop<8, false>(ctx, used, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
-      default: st = launch_closed_loop<8, true>(ctx, used, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
+      case 2: st = launch_closed_loop<1, false>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
+      case 3: st = launch_closed_loop<1, true>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
+      case 4: st = launch_closed_loop<2, false>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
+      case 5: st = launch_closed_loop<2, true>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
+      case 8: st = launch_closed_loop<4, false>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
+      case 9: st = launch_closed_loop<4, true>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
+      case 16: st = launch_closed_loop<8, false>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
+      default: st = launch_closed_loop<8, true>(ctx, n_runs, d_runs, d_p, d_o, d_e, d_a, ar, d_out, d_sum, d_st, d_rep); break;
     }
   }
   if (st == BSG_OK) {
