@@ -206,7 +206,7 @@ struct Parser {
     return true;
   }
   bool value(JVal* v, int depth = 0) {
-    if (depth > 64) return fail("malformed JSON");
+    if (depth > 512) return fail("malformed JSON");  // bounded recursion (nlohmann has none)
     ws();
     if (p >= end) return fail("malformed JSON");
     switch (*p) {
