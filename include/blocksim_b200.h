@@ -510,6 +510,12 @@ typedef struct bsg_trace_error {
 bsg_status bsg_load_trace(const char* text, int64_t len, bsg_trace_record* out, int64_t cap,
                           int64_t* n_records, bsg_trace_error* err);
 
+/* write_trace (workload.cpp:78-89): the records as JSON Lines, byte-identical
+ * to the reference's (nlohmann object key order, dump() number format).
+ * *len = bytes needed; BSG_INVALID_ARGUMENT (nothing written) when > cap. */
+bsg_status bsg_write_trace(const bsg_trace_record* recs, int64_t n, char* out, int64_t cap,
+                           int64_t* len);
+
 /* The request columns a run_experiment builds from trace records
  * (driver.cpp:137-160): request_cap truncation, generate_arrivals
  * (workload.cpp:141-170: every record's arrival_offset_s, in record order, or

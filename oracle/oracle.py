@@ -121,6 +121,8 @@ class Reference:
         L.ref_load_trace.argtypes = [C.c_char_p, C.c_int64, C.c_void_p, C.c_int64,
                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_char_p, C.c_int64]
         L.ref_load_trace.restype = C.c_int64
+        L.ref_write_trace.argtypes = [C.c_void_p, C.c_int64, C.c_char_p, C.c_int64]
+        L.ref_write_trace.restype = C.c_int64
         L.ref_set_trace.argtypes = [C.c_void_p, C.c_int64]
         L.ref_set_trace.restype = None
 
@@ -163,6 +165,13 @@ class Reference:
         if n < 0:
             return None, (kind.value, line.value, field.value.decode())
         return out[:n].copy(), None
+
+    def write_trace(self, recs) -> bytes:
+        recs = np.ascontiguousarray(recs, dtype=abi.trace_record_dtype)
+        buf = C.create_string_buffer(len(recs) * 160 + 16)
+        n = self.lib.ref_write_trace(_vp(recs), len(recs), buf, len(buf))
+        assert n >= 0
+        return buf.raw[:n]
 
     def set_trace(self, recs):
         """Replace the synthetic trace of make_workload / run_experiment /

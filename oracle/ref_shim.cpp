@@ -800,4 +800,24 @@ void ref_set_trace(const bsg_trace_record* recs, int64_t n) {
   }
 }
 
+// write_trace (workload.cpp:78-89) into out; returns the length (or -needed).
+int64_t ref_write_trace(const bsg_trace_record* recs, int64_t n, char* out, int64_t cap) {
+  std::vector<TraceRecord> v;
+  for (int64_t i = 0; i < n; ++i) {
+    TraceRecord r;
+    r.id = recs[i].id;
+    r.prompt_tokens = recs[i].prompt_tokens;
+    r.output_tokens = recs[i].output_tokens;
+    if (recs[i].estimated_output_tokens > 0) r.estimated_output_tokens = recs[i].estimated_output_tokens;
+    if (recs[i].has_arrival_offset) r.arrival_offset_s = recs[i].arrival_offset_s;
+    v.push_back(r);
+  }
+  std::ostringstream os;
+  write_trace(os, v);
+  const std::string s = os.str();
+  if (static_cast<int64_t>(s.size()) > cap) return -static_cast<int64_t>(s.size());
+  std::memcpy(out, s.data(), s.size());
+  return static_cast<int64_t>(s.size());
+}
+
 }  // extern "C"

@@ -882,6 +882,40 @@ extern "C" bsg_status bsg_load_trace(const char* text, int64_t len, bsg_trace_re
   return n > cap ? BSG_INVALID_ARGUMENT : BSG_OK;
 }
 
+// write_trace (workload.cpp:78-89): one nlohmann object per line — its keys
+// in std::map order, no whitespace, numbers as dump() prints them.
+extern "C" bsg_status bsg_write_trace(const bsg_trace_record* recs, int64_t n, char* out,
+                                      int64_t cap, int64_t* len) {
+  if ((!recs && n > 0) || n < 0 || cap < 0 || (!out && cap > 0) || !len) return BSG_INVALID_ARGUMENT;
+  std::string s;
+  s.reserve(static_cast<size_t>(n) * 96);
+  for (int64_t i = 0; i < n; ++i) {
+    const bsg_trace_record& r = recs[i];
+    s.push_back('{');
+    if (r.has_arrival_offset) {
+      s.append("\"arrival_offset_s\":");
+      append_double(&s, r.arrival_offset_s);
+      s.push_back(',');
+    }
+    if (r.estimated_output_tokens > 0) {
+      s.append("\"estimated_output_tokens\":");
+      s.append(std::to_string(r.estimated_output_tokens));
+      s.push_back(',');
+    }
+    s.append("\"id\":");
+    s.append(std::to_string(r.id));
+    s.append(",\"output_tokens\":");
+    s.append(std::to_string(r.output_tokens));
+    s.append(",\"prompt_tokens\":");
+    s.append(std::to_string(r.prompt_tokens));
+    s.append("}\n");
+  }
+  *len = static_cast<int64_t>(s.size());
+  if (*len > cap) return BSG_INVALID_ARGUMENT;
+  std::memcpy(out, s.data(), s.size());
+  return BSG_OK;
+}
+
 extern "C" int32_t bsg_format_double(double v, char* out, int32_t cap) {
   std::string t;
   append_double(&t, v);

@@ -72,6 +72,7 @@ def load() -> C.CDLL:
         "bsg_format_double": (C.c_int32, [C.c_double, C.c_char_p, C.c_int32]),
         "bsg_load_trace": (C.c_int, [C.c_char_p, C.c_int64, V, C.c_int64, C.POINTER(C.c_int64),
                                      C.POINTER(abi.TraceError)]),
+        "bsg_write_trace": (C.c_int, [V, C.c_int64, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]),
         "bsg_trace_workload": (C.c_int, [V, C.c_int64, V, V, V, V, V, C.POINTER(C.c_int64),
                                          C.POINTER(abi.TraceError)]),
         "bsg_replay_trace": (C.c_int, [V, V, C.c_int64, V, V, V, V, V, C.POINTER(abi.TraceError)]),
@@ -178,6 +179,19 @@ def load_trace(text: str | bytes) -> np.ndarray:
     if st != abi.OK:
         raise BsgError(st, "bsg_load_trace")
     return out[:n.value].copy()
+
+
+def write_trace(recs: np.ndarray) -> bytes:
+    """write_trace (workload.cpp:78-89): JSON Lines, byte-identical to the reference."""
+    L = load()
+    recs = np.ascontiguousarray(recs, dtype=abi.trace_record_dtype)
+    need = C.c_int64(0)
+    L.bsg_write_trace(_p(recs), len(recs), None, 0, C.byref(need))
+    buf = C.create_string_buffer(max(need.value, 1))
+    st = L.bsg_write_trace(_p(recs), len(recs), buf, len(buf), C.byref(need))
+    if st != abi.OK:
+        raise BsgError(st, "bsg_write_trace")
+    return buf.raw[:need.value]
 
 
 def load_trace_file(path: str) -> np.ndarray:

@@ -242,3 +242,21 @@ def test_oracle_and_pretagged_trace_estimators_agree():  # test_workload.cpp:147
     b = native.trace_workload(r, w)
     for x, y in zip(a, b):
         np.testing.assert_array_equal(x, y)
+
+
+def test_write_trace_matches_reference(ref):
+    """write_trace (workload.cpp:78-89): byte-identical JSONL (key order, number
+    text), and load_trace(write_trace(r)) == r."""
+    rng = np.random.default_rng(3)
+    r = _records(300, 8, offsets=True)
+    r["estimated_output_tokens"][::3] = 0                      # absent
+    r["has_arrival_offset"][::5] = 0                           # (mixed is legal to write)
+    r["arrival_offset_s"][1::5] = rng.choice([0.0, 1e-7, 1e16, 123456789.125, 2.5e-5, 1e21, 0.1], 60)
+    r["id"][7] = np.uint64(2**64 - 1)
+    got = native.write_trace(r)
+    assert got == ref.write_trace(r)
+    back = native.load_trace(got)
+    keep = r.copy()
+    keep["arrival_offset_s"][keep["has_arrival_offset"] == 0] = 0.0
+    assert back.tobytes() == keep.tobytes()
+    assert native.write_trace(r[:0]) == b""
