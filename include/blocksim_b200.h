@@ -510,6 +510,10 @@ typedef struct bsg_trace_error {
 bsg_status bsg_load_trace(const char* text, int64_t len, bsg_trace_record* out, int64_t cap,
                           int64_t* n_records, bsg_trace_error* err);
 
+/* make_synthetic_trace (workload.cpp:172-191) as records: w->count rows,
+ * id = row, no estimates or offsets (only the trace fields of w are read). */
+bsg_status bsg_make_trace(const bsg_workload* w, bsg_trace_record* out);
+
 /* write_trace (workload.cpp:78-89): the records as JSON Lines, byte-identical
  * to the reference's (nlohmann object key order, dump() number format).
  * *len = bytes needed; BSG_INVALID_ARGUMENT (nothing written) when > cap. */

@@ -150,13 +150,13 @@ bsg_status records_from_trace(const bsg_trace_record* tr, int64_t n, const bsg_w
 
 // make_synthetic_trace (workload.cpp:172-191) + estimate_length
 // (workload.cpp:113-139) + generate_arrivals (workload.cpp:141-170).
-bsg_status make_records(const bsg_workload& w, std::vector<Record>* out) {
-  if (!(w.qps > 0)) return BSG_INVALID_ARGUMENT;
+// make_synthetic_trace (workload.cpp:172-191): lognormal prompt / output
+// lengths, record i has id i.
+std::vector<Record> synthetic_trace(const bsg_workload& w) {
   Rng rng(w.trace_seed);
-  int n = w.count;
   std::vector<Record> recs;
-  recs.reserve(n);
-  for (int i = 0; i < n; ++i) {
+  recs.reserve(static_cast<size_t>(std::max(w.count, 0)));
+  for (int i = 0; i < w.count; ++i) {
     const double p = w.prompt_median * std::exp(w.prompt_sigma * rng.normal());
     const double o = w.output_median * std::exp(w.output_sigma * rng.normal());
     Record r{};
@@ -164,6 +164,13 @@ bsg_status make_records(const bsg_workload& w, std::vector<Record>* out) {
     r.output = static_cast<int32_t>(std::clamp<double>(std::round(o), w.min_tokens, w.max_output_tokens));
     recs.push_back(r);
   }
+  return recs;
+}
+
+bsg_status make_records(const bsg_workload& w, std::vector<Record>* out) {
+  if (!(w.qps > 0)) return BSG_INVALID_ARGUMENT;
+  const int n = w.count;
+  std::vector<Record> recs = synthetic_trace(w);
   if (w.request_cap >= 0 && w.request_cap < n) recs.resize(w.request_cap);
   Rng arr(w.arrival_seed);
   int64_t t = 0;
@@ -736,6 +743,18 @@ bsg_status bsg_make_workload(const bsg_workload* w, int32_t* prompt, int32_t* ou
     output[i] = recs[i].output;
     est[i] = recs[i].est;
     arrival_ticks[i] = recs[i].arrival;
+  }
+  return BSG_OK;
+}
+
+bsg_status bsg_make_trace(const bsg_workload* w, bsg_trace_record* out) {
+  if (!w || (!out && w->count > 0) || w->count < 0) return BSG_INVALID_ARGUMENT;
+  const std::vector<Record> rs = synthetic_trace(*w);
+  for (size_t i = 0; i < rs.size(); ++i) {
+    out[i] = bsg_trace_record{};
+    out[i].id = static_cast<uint64_t>(i);
+    out[i].prompt_tokens = rs[i].prompt;
+    out[i].output_tokens = rs[i].output;
   }
   return BSG_OK;
 }

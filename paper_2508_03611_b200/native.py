@@ -72,6 +72,7 @@ def load() -> C.CDLL:
         "bsg_format_double": (C.c_int32, [C.c_double, C.c_char_p, C.c_int32]),
         "bsg_load_trace": (C.c_int, [C.c_char_p, C.c_int64, V, C.c_int64, C.POINTER(C.c_int64),
                                      C.POINTER(abi.TraceError)]),
+        "bsg_make_trace": (C.c_int, [V, V]),
         "bsg_write_trace": (C.c_int, [V, C.c_int64, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]),
         "bsg_trace_workload": (C.c_int, [V, C.c_int64, V, V, V, V, V, C.POINTER(C.c_int64),
                                          C.POINTER(abi.TraceError)]),
@@ -179,6 +180,16 @@ def load_trace(text: str | bytes) -> np.ndarray:
     if st != abi.OK:
         raise BsgError(st, "bsg_load_trace")
     return out[:n.value].copy()
+
+
+def make_trace(w: np.ndarray) -> np.ndarray:
+    """make_synthetic_trace (workload.cpp:172-191) as trace records."""
+    L = load()
+    out = np.zeros(max(int(w["count"][0]), 1), abi.trace_record_dtype)
+    st = L.bsg_make_trace(_p(w), _p(out))
+    if st != abi.OK:
+        raise BsgError(st, "bsg_make_trace")
+    return out[:int(w["count"][0])]
 
 
 def write_trace(recs: np.ndarray) -> bytes:

@@ -260,3 +260,16 @@ def test_write_trace_matches_reference(ref):
     keep["arrival_offset_s"][keep["has_arrival_offset"] == 0] = 0.0
     assert back.tobytes() == keep.tobytes()
     assert native.write_trace(r[:0]) == b""
+
+
+def test_make_trace_is_the_reference_synthetic_trace(ref):
+    """make-trace: make_synthetic_trace (workload.cpp:172-191) records, written
+    as the reference writes them."""
+    w = abi.make_workload(count=500, trace_seed=99)
+    recs = native.make_trace(w)
+    assert recs["id"].tolist() == list(range(500))
+    ref.set_trace(None)
+    p, o, _, _ = ref.make_workload(w)
+    np.testing.assert_array_equal(recs["prompt_tokens"], p)
+    np.testing.assert_array_equal(recs["output_tokens"], o)
+    assert native.write_trace(recs) == ref.write_trace(recs)
