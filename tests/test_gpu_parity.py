@@ -423,3 +423,30 @@ def test_trace_closed_loop_matches_reference(ctx, ref, offsets, shuffle, est_kin
             assert ctx.last_reports[0].tobytes() == erep.tobytes()
         else:
             assert shuffle
+
+
+def test_edge_inputs(ctx, ref):
+    """Empty batches, a scenario naming a config that does not exist (every
+    per-config pass writes its INVALID_ARGUMENT verdict, the rest are
+    unaffected), and a set whose configs are all unused but one."""
+    cfgs, ss = fuzz_set(41, 9000)  # >= the queue threshold: heavy list + per-config passes
+    ctx.set_configs(cfgs)
+    empty = abi.ScenarioSet(ss.prompt[:0], ss.est[:0], ss.prefill[:0], ss.decoded[:0], ss.scenarios[:0])
+    assert len(ctx.predict_batch(empty)) == 0
+    base = ctx.predict_batch(ss)
+    bad = ss.scenarios.copy()
+    bad["cfg"][[5, 4000, 8999]] = len(cfgs)
+    bad["cfg"][77] = -1
+    ss2 = abi.ScenarioSet(ss.prompt, ss.est, ss.prefill, ss.decoded, bad)
+    got = ctx.predict_batch(ss2)
+    hit = np.zeros(len(ss), bool)
+    hit[[5, 77, 4000, 8999]] = True
+    assert (got["status"][hit] == abi.INVALID_ARGUMENT).all()
+    assert got[~hit].tobytes() == base[~hit].tobytes()
+    # only config 0 in use: one pass; results equal the reference's
+    one = ss.scenarios.copy()
+    one["cfg"] = 0
+    ss3 = abi.ScenarioSet(ss.prompt, ss.est, ss.prefill, ss.decoded, one)
+    got3 = ctx.predict_batch(ss3)
+    exp3 = ref.predict_batch(cfgs, ss3, threads=8)
+    assert compare_to_ref(got3, exp3).sum() == 0
