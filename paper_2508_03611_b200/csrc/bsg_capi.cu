@@ -75,16 +75,22 @@ __device__ __forceinline__ int cost_bucket(int32_t cand_est) {
 
 // Work-queue state of one launch (zeroed before it): 2 tickets, the heavy
 // bucket threshold, a block-completion count, then the bucket histogram.
+// At most n / kHeavyDiv scenarios (whole cost buckets) form the heavy list.
+#ifndef BSG_HEAVY_DIV
+#define BSG_HEAVY_DIV 16
+#endif
+constexpr int64_t kHeavyDiv = BSG_HEAVY_DIV;
+
 struct WorkQueue {
   int32_t threshold, blocks_done;
   int32_t heavy_count, retry_count;
   int32_t deep_wait, use_wide;  // window-width vote of the optimistic pass
   int32_t hist[kCostBuckets];
-  // followed by the heavy list: int32_t heavy[n / 16 + 32], then the retry
+  // followed by the heavy list: int32_t heavy[n / kHeavyDiv + 32], then the retry
   // list of the optimistic narrow pass: int32_t retry[n]
 };
 __device__ __forceinline__ int32_t* heavy_list(WorkQueue* q) { return reinterpret_cast<int32_t*>(q + 1); }
-__device__ __forceinline__ int32_t* retry_list(WorkQueue* q, int64_t n) { return heavy_list(q) + n / 16 + 32; }
+__device__ __forceinline__ int32_t* retry_list(WorkQueue* q, int64_t n) { return heavy_list(q) + n / kHeavyDiv + 32; }
 
 // Lists the heavy scenarios (order inside the list is arbitrary).
 __global__ void __launch_bounds__(256) heavy_list_kernel(const bsg_scenario* __restrict__ sc, int64_t n,
@@ -140,7 +146,7 @@ __global__ void __launch_bounds__(256) heavy_threshold_kernel(const bsg_scenario
     tot += c[j];
   }
   int32_t acc = warp_incl_scan(tot) - tot;  // count in strictly higher buckets
-  const int64_t cap = n / 16;
+  const int64_t cap = n / kHeavyDiv;
   int32_t thr = kCostBuckets;  // no heavy bucket
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -480,13 +486,13 @@ bsg_status launch_predict_t(bsg_ctx* ctx, int32_t cfg_sel, int64_t n, const bsg_
   }
   // stream-ordered scratch: safe for concurrent calls on different streams
   void* mem = nullptr;
-  BSG_CUDA(ctx, cudaMallocAsync(&mem, sizeof(WorkQueue) + (n / 16 + 32 + n) * sizeof(int32_t), s));
+  BSG_CUDA(ctx, cudaMallocAsync(&mem, sizeof(WorkQueue) + (n / kHeavyDiv + 32 + n) * sizeof(int32_t), s));
   auto* q = static_cast<WorkQueue*>(mem);
   BSG_CUDA(ctx, cudaMemsetAsync(q, 0, sizeof(WorkQueue), s));
   const int64_t hb = std::min<int64_t>((n + 1023) / 1024, 148);
   heavy_threshold_kernel<<<static_cast<unsigned>(hb), 256, 0, s>>>(sc, n, q);
   heavy_list_kernel<<<static_cast<unsigned>(hb), 256, 0, s>>>(sc, n, q);
-  const int64_t pb = (n + n / 16 + 32 + kPredictWarps - 1) / kPredictWarps;  // >= heavy + n warps
+  const int64_t pb = (n + n / kHeavyDiv + 32 + kPredictWarps - 1) / kPredictWarps;  // >= heavy + n warps
   static const bool no_opt = std::getenv("BSG_NO_OPT") != nullptr;
   if constexpr (K > 1) {
     if (!no_opt) {
