@@ -75,9 +75,11 @@ __device__ __forceinline__ int cost_bucket(int32_t cand_est) {
 
 // Work-queue state of one launch (zeroed before it): 2 tickets, the heavy
 // bucket threshold, a block-completion count, then the bucket histogram.
-// At most n / kHeavyDiv scenarios (whole cost buckets) form the heavy list.
+// At most n / kHeavyDiv scenarios (whole cost buckets) form the heavy list
+// (cfg2, 60k scenarios: n/16 245.0 us, n/64 241.0, n/128 238.8, n/256 243.0;
+// cfg3 flat).
 #ifndef BSG_HEAVY_DIV
-#define BSG_HEAVY_DIV 16
+#define BSG_HEAVY_DIV 128
 #endif
 constexpr int64_t kHeavyDiv = BSG_HEAVY_DIV;
 
