@@ -220,7 +220,8 @@ __global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K, OPT))
   const int warp = threadIdx.x >> 5;
   int32_t* smem = smem_all + warp * smem_words(K);
   if constexpr (OPT) {  // two optimistic passes are launched; the vote keeps one
-    if ((__ldcg(&q->use_wide) != 0) != (WJ > 1)) return;
+    static_assert(BSG_WIN_J_WIDE != BSG_WIN_J_PREDICT, "the two optimistic passes need distinct widths");
+    if ((__ldcg(&q->use_wide) != 0) != (WJ == BSG_WIN_J_WIDE)) return;
   }
   // warps [0, nh) run the heavy list; warp nh + i runs scenario i unless it is heavy
   int64_t w = static_cast<int64_t>(blockIdx.x) * kPredictWarps + warp;

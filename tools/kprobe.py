@@ -37,7 +37,9 @@ def timeit(scen_np, reps=20):
     return np.median(ts) * 1e3, res
 t0, res = timeit(ss.scenarios)
 steps = res["steps"]; ms = res["member_steps"]
-print(f"{which}: n={n} entries={ss.n_entries} natural {t0:.1f} us -> {n/t0:.1f}M scen/s")
+nbad = int((res["status"] != abi.OK).sum())
+print(f"{which}: n={n} entries={ss.n_entries} natural {t0:.1f} us -> {n/t0:.1f}M scen/s"
+      + (f"  [{nbad} scenarios not OK: timing invalid]" if nbad else ""))
 print("steps pct 50/90/99/99.9/max", np.percentile(steps, [50, 90, 99, 99.9]).round(), steps.max(), "mean", steps.mean().round(1))
 print("member_steps mean", ms.mean().round(1), "max", ms.max())
 order = np.argsort(-steps, kind="stable")
