@@ -221,7 +221,9 @@ __global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K, OPT))
   int32_t* smem = smem_all + warp * smem_words(K);
   if constexpr (OPT) {  // two optimistic passes are launched; the vote keeps one
     static_assert(BSG_WIN_J_WIDE != BSG_WIN_J_PREDICT, "the two optimistic passes need distinct widths");
-    if ((__ldcg(&q->use_wide) != 0) != (WJ == BSG_WIN_J_WIDE)) return;
+    // use_wide = the vote chose wide (BSG_WIN_J_PREDICT-step) windows; else the
+    // BSG_WIN_J_WIDE pass (the width for wide member sets) runs
+    if ((__ldcg(&q->use_wide) != 0) != (WJ == BSG_WIN_J_PREDICT)) return;
   }
   // warps [0, nh) run the heavy list; warp nh + i runs scenario i unless it is heavy
   int64_t w = static_cast<int64_t>(blockIdx.x) * kPredictWarps + warp;
