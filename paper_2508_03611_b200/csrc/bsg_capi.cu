@@ -55,7 +55,7 @@ constexpr int min_blocks(int k, bool opt = false) {
 // its step count is ~ the candidate's estimate plus its queueing): one long
 // scenario that starts late is the kernel's tail. Blocks are dispatched in
 // index order, so predict_kernel's first warps run the HEAVY scenarios (cost
-// bucket >= a threshold picked by heavy_threshold_kernel: at most the top 1/16
+// bucket >= a threshold picked by heavy_threshold_kernel: at most the top n / kHeavyDiv
 // by quarter-octave of cand_est, listed by heavy_list_kernel); the following
 // warps run the rest in the caller's order (which keeps memory locality),
 // skipping the heavy ones. No sort, no atomics on the simulation path.
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(256) heavy_list_kernel(const bsg_scenario* __r
 }
 
 // Histogram of cost buckets; the last block picks the threshold: the highest
-// buckets whose cumulative count stays within n/16 (none if the top bucket alone
+// buckets whose cumulative count stays within n / kHeavyDiv (none if the top bucket alone
 // exceeds it).
 __global__ void __launch_bounds__(256) heavy_threshold_kernel(const bsg_scenario* __restrict__ sc,
                                                               int64_t n, WorkQueue* q) {
