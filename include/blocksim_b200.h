@@ -248,6 +248,27 @@ bsg_status bsg_dispatch_mc(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_e
 bsg_status bsg_mc_lengths(int32_t est, uint64_t request_id, int32_t n_samples, uint64_t seed,
                           double mean_abs_rel_error, int32_t* out);
 
+/* bsg_dispatch_mc with the samples drawn ON THE DEVICE inside the call (K3):
+ * request r's n_samples lengths are bsg_mc_lengths(cand_est, request_ids[r],
+ * n_samples, seed, mean_abs_rel_error) of its scenarios' (common) cand_est,
+ * generated and sorted per warp in shared memory, so the sampling cost is
+ * part of the dispatch. Optional outputs: scores [n_req*n_inst], lengths_out
+ * [n_req*n_samples] (the drawn samples, sample order), per_instance, and
+ * dev_keys — a DEVICE buffer [n_req] receiving the packed argmin key
+ * (min(score, 2^47-1) << 16 | id, or -1 when the request failed) for a
+ * cross-GPU MIN reduction (instance ids must then be < 65535),
+ * complete when the call returns. HOST buffers otherwise. */
+bsg_status bsg_dispatch_mc_sampled(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries,
+                                   const bsg_scenario* scenarios, const int32_t* instance_ids,
+                                   int32_t n_inst, int32_t n_requests, const uint64_t* request_ids,
+                                   int32_t n_samples, uint64_t seed, double mean_abs_rel_error,
+                                   int32_t objective, int32_t* chosen, int64_t* scores,
+                                   int32_t* lengths_out, bsg_result* per_instance, int64_t* dev_keys);
+
+/* Name(s) of the simulation kernel(s) this context's last predict / dispatch
+ * call launched (template arguments included), for measurement records. */
+const char* bsg_last_launch(const bsg_ctx* ctx);
+
 /* ---- closed-loop replay (the scenario source; driver.cpp:134-289) -------- */
 
 /* Synthetic ShareGPT-shaped workload: make_synthetic_trace (workload.cpp:172-191,
@@ -448,6 +469,13 @@ void bsg_fleet_destroy(bsg_fleet* f);
 bsg_status bsg_fleet_dispatch(bsg_fleet* f, int64_t now_ticks, int32_t prompt, int32_t est,
                               int32_t output, const int32_t* lengths, int32_t n_samples,
                               int32_t objective, int32_t* chosen, int64_t* scores);
+/* bsg_fleet_dispatch with the candidate's n_samples MC lengths drawn ON THE
+ * DEVICE inside the call (K3; bsg_mc_lengths(est, request_id, n_samples, seed,
+ * mean_abs_rel_error)): per call only the candidate's scalars go in. */
+bsg_status bsg_fleet_dispatch_sampled(bsg_fleet* f, int64_t now_ticks, int32_t prompt, int32_t est,
+                                      int32_t output, uint64_t request_id, int32_t n_samples,
+                                      uint64_t seed, double mean_abs_rel_error, int32_t objective,
+                                      int32_t* chosen, int64_t* scores);
 /* The mirror's Status API (Instance::snapshot, backend.cpp:351-373) as of the
  * last dispatch: run_n running entries (admission order) then wait_n waiting
  * entries (head first) into the caller's columns (any may be NULL); when
@@ -471,6 +499,14 @@ bsg_status bsg_fleet_finish(bsg_fleet* f, bsg_request_outcome* outcomes, int32_t
  * to the requests' distinct instance_configs. */
 bsg_status bsg_predict_json(bsg_ctx* ctx, const char* const* requests, int32_t n, char* out,
                             int64_t out_cap, int64_t* out_off, int32_t* status);
+
+/* The /predict role's request checks that precede simulation, on the host
+ * (no device needed): parses `body` as prediction_request_from_json
+ * (json_io.cpp:136-146) and validates its instance_config
+ * (validate_instance_config, types.cpp:47-61). Returns BSG_OK when the request
+ * would be simulated; otherwise its status and, in `out`, the exact error body
+ * the reference role answers (json_io.cpp:148-152; service.cpp:229-241). */
+int32_t bsg_wire_check(const char* body, char* out, int64_t cap);
 /* A double as the reference's JSON layer prints it (nlohmann::json::dump:
  * Grisu2 digits, fixed notation for decimal exponents in (-4, 15]); returns the
  * length, or -(bytes needed) when cap is too small. No GPU needed. */

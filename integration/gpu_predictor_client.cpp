@@ -142,6 +142,11 @@ std::map<InstanceId, PredictionResult> GpuPredictorClient::predict_across(
           throw PredictionError(tag + "candidate vanished from the forward simulation");
         case BSG_EMPTY_PLAN:
           throw EmptyPlanError("no runnable work fits the batch");
+        case BSG_BAD_INPUT:
+          // outside the GPU simulator's integer domain: a prediction
+          // failure the caller sees, never a silent switch to the fallback policy
+          throw PredictionError(tag + "snapshot outside the GPU simulator's supported domain "
+                                      "(prompt <= 2^22, estimate <= 2^24, member capacity <= 256)");
         default:
           throw PredictorUnavailableError("GPU predictor rejected the input (status " +
                                           std::to_string(r.status) + ")");

@@ -13,7 +13,9 @@
 // "instance N: ..." for the first failing snapshot in input order,
 // EmptyPlanError / ConfigError propagate as themselves, NoInstancesError on an
 // empty fan-out, and any device failure surfaces as PredictorUnavailableError
-// so the Dispatcher's Llumnix- fallback engages (scheduler.cpp:129-136).
+// so the Dispatcher's Llumnix- fallback engages (scheduler.cpp:129-136). A
+// snapshot outside the GPU simulator's integer domain is a PredictionError
+// (it propagates out of dispatch), never a silent fallback.
 #pragma once
 
 #include <cstdint>

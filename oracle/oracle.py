@@ -125,6 +125,8 @@ class Reference:
         L.ref_write_trace.restype = C.c_int64
         L.ref_set_trace.argtypes = [C.c_void_p, C.c_int64]
         L.ref_set_trace.restype = None
+        L.ref_sweep.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
+        L.ref_sweep.restype = C.c_double
 
     def predict_batch(self, cfgs, ss: abi.ScenarioSet, threads: int = 1) -> np.ndarray:
         out = np.zeros(len(ss), abi.ref_result_dtype)
@@ -235,6 +237,14 @@ class Reference:
         n = int(out["n_tested"][0])
         return st, out[0], list(zip(tq[:n].tolist(), tp[:n].astype(bool).tolist()))
 
+    def sweep(self, cells, threads: int):
+        """capacity_search of every cell, parallel over (cell, qps) points on
+        `threads` threads (ref_sweep). Returns (sweep_out rows, wall seconds)."""
+        cells = np.ascontiguousarray(cells, abi.sweep_cell_dtype)
+        out = np.zeros(len(cells), abi.sweep_out_dtype)
+        secs = self.lib.ref_sweep(_vp(cells), len(cells), threads, _vp(out))
+        return out, secs
+
     def replay(self, w, cfg, spec, capture: bool = True):
         n = int(w["count"][0]) if w["request_cap"][0] < 0 else min(int(w["count"][0]),
                                                                     int(w["request_cap"][0]))
@@ -292,11 +302,14 @@ def mc_reference_dispatch(ref, cfg, ss, n_inst, lengths, threads=8):
 def compare_to_ref(gpu_res: np.ndarray, ref_res: np.ndarray) -> np.ndarray:
     """Boolean mask of scenarios whose product result (ticks) differs from the
     reference's (double seconds): status, steps, and e2e/ttft/qdelay compared
-    bit-exactly as ticks * 1e-9 (time.h:25)."""
+    bit-exactly as ticks * 1e-9 (time.h:25); failures compare status + detail."""
     ok = gpu_res["status"] == ref_res["status"]
     good = ok & (gpu_res["status"] == abi.OK)
     for tk, sk in (("e2e_ticks", "e2e_s"), ("ttft_ticks", "ttft_s"), ("qdelay_ticks", "qdelay_s")):
         sec = abi.ticks_to_seconds(gpu_res[tk])
         ok &= ~good | (sec.view(np.int64) == ref_res[sk].view(np.int64))
     ok &= ~good | (gpu_res["steps"] == ref_res["steps"])
+    # failures: the error detail too (deadlocked member's origin, the candidate's
+    # block need for TOO_LARGE_CANDIDATE; 0 where the reference message has none)
+    ok &= good | (gpu_res["detail"] == ref_res["detail"])
     return ~ok

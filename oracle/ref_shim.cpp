@@ -662,6 +662,83 @@ int ref_capacity_search(const bsg_workload* w, const bsg_instance_cfg* c, const 
   }
 }
 
+// capacity_search (metrics.cpp:139-178) of many cells, scheduled at (cell, qps)
+// granularity on `threads` std::threads: every integer point of every cell,
+// then every cell's tenths — the same runner as ref_capacity_search
+// (spec_for_cell + run_experiment + aggregate, driver.cpp:398-418), so each
+// cell's result equals capacity_search's (tested against it). This is the
+// all-core CPU baseline of the cfg5 sweep: no core idles while one cell's
+// sequential search runs. Returns the wall seconds.
+double ref_sweep(const bsg_sweep_cell* cells, int32_t n_cells, int32_t threads, bsg_sweep_out* out) {
+  struct Pt {
+    int32_t cell;
+    double qps;
+    int8_t pass;
+  };
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<ExperimentSpec> base(static_cast<size_t>(n_cells));
+  for (int32_t c = 0; c < n_cells; ++c) base[c] = make_experiment(&cells[c].workload, &cells[c].cfg, &cells[c].spec);
+  auto run = [&](std::vector<Pt>& pts) {
+    // longest first: more instances and more load per run
+    std::vector<size_t> order(pts.size());
+    for (size_t i = 0; i < pts.size(); ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+      return cells[pts[a].cell].spec.n_instances * pts[a].qps > cells[pts[b].cell].spec.n_instances * pts[b].qps;
+    });
+    std::atomic<size_t> next{0};
+    auto work = [&]() {
+      for (size_t k; (k = next.fetch_add(1)) < order.size();) {
+        Pt& p = pts[order[k]];
+        ExperimentSpec spec = spec_for_cell(base[p.cell], base[p.cell].policy.kind, p.qps, cells[p.cell].seed);
+        spec.collect_events = false;
+        const RunReport r = aggregate(run_experiment(spec));
+        p.pass = r.p99_ttft_s < cells[p.cell].slo_p99_ttft_s ? 1 : 0;
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < std::max(1, threads); ++t) pool.emplace_back(work);
+    for (auto& th : pool) th.join();
+  };
+  std::vector<Pt> ints;
+  for (int32_t c = 0; c < n_cells; ++c)
+    for (int32_t q = cells[c].qps_min; q <= cells[c].qps_max; ++q) ints.push_back(Pt{c, static_cast<double>(q), 0});
+  run(ints);
+  std::vector<std::vector<bool>> ip(static_cast<size_t>(n_cells));
+  for (const Pt& p : ints) ip[p.cell].push_back(p.pass != 0);
+  std::vector<Pt> tenths;
+  for (int32_t c = 0; c < n_cells; ++c) {
+    std::memset(&out[c], 0, sizeof(out[c]));
+    bsg_capacity_result& r = out[c].result;
+    if (cells[c].qps_min > cells[c].qps_max) {
+      out[c].status = BSG_BAD_CONFIG;
+      continue;
+    }
+    if (!ip[c].front()) {
+      out[c].status = BSG_NO_CAPACITY;
+      r.n_tested = static_cast<int32_t>(ip[c].size());
+      continue;
+    }
+    int last = 0;
+    while (last + 1 < static_cast<int>(ip[c].size()) && ip[c][last + 1]) ++last;
+    r.monotone = 1;
+    for (int i = last + 1; i < static_cast<int>(ip[c].size()); ++i)
+      if (ip[c][i]) r.monotone = 0;
+    r.bracket_pass = cells[c].qps_min + last;
+    r.bracket_fail = r.bracket_pass + 1;
+    r.capacity_qps = r.bracket_pass;
+    r.n_tested = static_cast<int32_t>(ip[c].size());
+    if (r.bracket_pass < cells[c].qps_max)
+      for (int t = 1; t <= 9; ++t) tenths.push_back(Pt{c, static_cast<double>(r.bracket_pass * 10 + t) / 10.0, 0});
+  }
+  run(tenths);
+  for (const Pt& p : tenths) {
+    bsg_capacity_result& r = out[p.cell].result;
+    ++r.n_tested;
+    if (p.pass) r.capacity_qps = std::max(r.capacity_qps, p.qps);
+  }
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
 int ref_replay(const bsg_workload* w, const bsg_instance_cfg* cfg, const bsg_replay_spec* spec,
                bsg_request_outcome* out, bsg_replay_summary* summary, ref_capture** capture) {
   ref_capture* cap = capture ? new ref_capture() : nullptr;

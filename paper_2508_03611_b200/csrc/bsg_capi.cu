@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "bsg_internal.h"
+#include "mc_sampler.cuh"
 #include "scenario_sim.cuh"
 
 namespace bsg {
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(256) heavy_list_kernel(const bsg_scenario* __r
 // buckets whose cumulative count stays within n / kHeavyDiv (none if the top bucket alone
 // exceeds it).
 __global__ void __launch_bounds__(256) heavy_threshold_kernel(const bsg_scenario* __restrict__ sc,
-                                                              int64_t n, WorkQueue* q) {
+                                                              int64_t n, WorkQueue* q, int32_t force_vote) {
   __shared__ int32_t h[kCostBuckets];
   __shared__ bool last;
   for (int b = threadIdx.x; b < kCostBuckets; b += blockDim.x) h[b] = 0;
@@ -159,7 +160,8 @@ __global__ void __launch_bounds__(256) heavy_threshold_kernel(const bsg_scenario
   if (lane == 0) {
     q->threshold = thr;
     // wide windows unless a quarter of the set queues behind a deep waiting line
-    q->use_wide = static_cast<int64_t>(__ldcg(&q->deep_wait)) * 4 < n ? 1 : 0;
+    q->use_wide = force_vote >= 0 ? force_vote
+                                  : (static_cast<int64_t>(__ldcg(&q->deep_wait)) * 4 < n ? 1 : 0);
   }
 }
 
@@ -319,13 +321,27 @@ __global__ void argmin_kernel(const bsg_result* __restrict__ res,
   if (lane == 0) chosen[r] = fail ? -1 : best_id;
 }
 
+// Per-request MC sampling arguments of the device-sampled dispatch.
+struct McSampling {
+  const uint64_t* request_id;  // [n_req], nullptr: lengths are given (sorted_len)
+  uint64_t seed;
+  double scale;                // mean_abs_rel_error * sqrt(pi / 2), computed on the host
+  int32_t* lengths_out;        // optional [n_req * S], sample order
+};
+
+// Packed cross-GPU argmin key: min(score, 2^47 - 1) << 16 | id,
+// -1 when the request failed on this shard (the MIN reduction then fails it).
+constexpr int64_t kKeySat = (int64_t{1} << 47) - 1;
+
 // Monte-Carlo BlockPredictive dispatch (cfg4): warp w simulates instance
 // w % n_inst of request w / n_inst once, with the request's sorted sample
 // lengths staged in shared memory (prefix sharing), and the
 // last warp of each request to finish takes the argmin over the per-instance
 // scores (sum of per-sample e2e ticks), lowest instance id on ties
-// (scheduler.cpp:138-150).
-template <int K, bool POW2>
+// (scheduler.cpp:138-150). SAMPLE: each warp draws the request's S samples
+// itself (K3 above, lane-parallel) and bitonic-sorts them in shared memory,
+// so sampling is inside the call with no extra launch or host pass.
+template <int K, bool POW2, bool SAMPLE>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     dispatch_mc_kernel(const DevCfg* __restrict__ cfgs, int32_t ncfg,
                        const int32_t* __restrict__ prompt, const int32_t* __restrict__ est,
@@ -334,18 +350,25 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
                        int32_t n_inst, int32_t n_req, const int32_t* __restrict__ sorted_len,
                        int32_t S, int32_t objective, int64_t* __restrict__ scores,
                        int64_t* __restrict__ sample_e2e, bsg_result* __restrict__ res,
-                       unsigned* __restrict__ counters, int32_t* __restrict__ chosen) {
+                       unsigned* __restrict__ counters, int32_t* __restrict__ chosen,
+                       McSampling smp, int64_t* __restrict__ keys) {
   extern __shared__ int32_t dsm[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t w = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + warp;
   if (w >= static_cast<int64_t>(n_inst) * n_req) return;
   const int32_t r = static_cast<int32_t>(w / n_inst);
-  int32_t* smem = dsm + warp * (smem_words(K) + S);
+  const int32_t Sp = SAMPLE ? pow2_ceil(S) : S;
+  int32_t* smem = dsm + warp * (smem_words(K) + Sp);
   int32_t* len = smem + smem_words(K);
-  for (int32_t j = lane; j < S; j += 32) len[j] = sorted_len[static_cast<int64_t>(r) * S + j];
-  __syncwarp();
   const bsg_scenario sc = scen[w];
+  if constexpr (SAMPLE) {
+    stage_mc_samples(len, sc.cand_est, smp.request_id[r], S, smp.seed, smp.scale,
+                     (smp.lengths_out && w % n_inst == 0) ? smp.lengths_out + static_cast<int64_t>(r) * S : nullptr);
+  } else {
+    for (int32_t j = lane; j < S; j += 32) len[j] = sorted_len[static_cast<int64_t>(r) * S + j];
+    __syncwarp();
+  }
   bsg_result* o = res + w;
   if (sc.cfg < 0 || sc.cfg >= ncfg) {
     if (lane == 0) {
@@ -403,6 +426,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   fail = __any_sync(kFull, fail);
   if (lane == 0) {
     chosen[r] = fail ? -1 : best_id;
+    if (keys) keys[r] = fail ? -1 : ((best_v < kKeySat ? best_v : kKeySat) << 16) | best_id;
     counters[r] = 0;  // ready for the next call
   }
 }
@@ -482,7 +506,10 @@ bsg_status launch_predict_t(bsg_ctx* ctx, int32_t cfg_sel, int64_t n, const bsg_
   static const bool no_queue = std::getenv("BSG_NO_QUEUE") != nullptr;
   const DevCfg& cf = ctx->dev_cfgs_host[cfg_sel];
   const int64_t blocks = (n + kPredictWarps - 1) / kPredictWarps;
+  const std::string tp = std::string(POW2 ? "true" : "false");
   if (no_queue || n < BSG_QUEUE_MIN) {
+    ctx->last_launch = "predict_kernel<" + std::to_string(K) + "," + tp + ",false," +
+                       std::to_string(BSG_WIN_J_PREDICT) + ">";
     predict_kernel<K, POW2, false, BSG_WIN_J_PREDICT><<<static_cast<unsigned>(blocks), kPredictWarps * 32, 0, s>>>(
         cf, cfg_sel, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, nullptr, out);
     ctx->launches += 1;
@@ -495,7 +522,11 @@ bsg_status launch_predict_t(bsg_ctx* ctx, int32_t cfg_sel, int64_t n, const bsg_
   auto* q = static_cast<WorkQueue*>(mem);
   BSG_CUDA(ctx, cudaMemsetAsync(q, 0, sizeof(WorkQueue), s));
   const int64_t hb = std::min<int64_t>((n + 1023) / 1024, 148);
-  heavy_threshold_kernel<<<static_cast<unsigned>(hb), 256, 0, s>>>(sc, n, q);
+  // BSG_FORCE_VOTE=0/1 pins the optimistic pass's window-width vote (parity
+  // tests run both passes on the same sets); unset: the vote decides
+  const char* fv = std::getenv("BSG_FORCE_VOTE");
+  const int32_t force_vote = fv ? (std::atoi(fv) != 0 ? 1 : 0) : -1;
+  heavy_threshold_kernel<<<static_cast<unsigned>(hb), 256, 0, s>>>(sc, n, q, force_vote);
   heavy_list_kernel<<<static_cast<unsigned>(hb), 256, 0, s>>>(sc, n, q);
   const int64_t pb = (n + n / kHeavyDiv + 32 + kPredictWarps - 1) / kPredictWarps;  // >= heavy + n warps
   static const bool no_opt = std::getenv("BSG_NO_OPT") != nullptr;
@@ -509,6 +540,9 @@ bsg_status launch_predict_t(bsg_ctx* ctx, int32_t cfg_sel, int64_t n, const bsg_
           cf, cfg_sel, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
       predict_kernel<1, POW2, true, BSG_WIN_J_WIDE><<<static_cast<unsigned>(pb), kPredictWarps * 32, 0, s>>>(
           cf, cfg_sel, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
+      ctx->last_launch = "predict_kernel<1," + tp + ",true," + std::to_string(BSG_WIN_J_PREDICT) + "|" +
+                         std::to_string(BSG_WIN_J_WIDE) + "> (vote) + predict_retry_kernel<" +
+                         std::to_string(K) + "," + tp + ">";
       const int64_t rb = std::min<int64_t>(pb, 148 * 8);
       predict_retry_kernel<K, POW2><<<static_cast<unsigned>(rb), kPredictWarps * 32, 0, s>>>(
           cf, cfg_sel, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
@@ -518,6 +552,8 @@ bsg_status launch_predict_t(bsg_ctx* ctx, int32_t cfg_sel, int64_t n, const bsg_
       return BSG_OK;
     }
   }
+  ctx->last_launch = "predict_kernel<" + std::to_string(K) + "," + tp + ",false," +
+                     std::to_string(K == 1 ? BSG_WIN_J_PREDICT : BSG_WIN_J_WIDE) + ">";
   predict_kernel<K, POW2, false, K == 1 ? BSG_WIN_J_PREDICT : BSG_WIN_J_WIDE>
       <<<static_cast<unsigned>(pb), kPredictWarps * 32, 0, s>>>(
       cf, cfg_sel, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
@@ -586,9 +622,29 @@ int32_t host_need(const bsg_scenario* sc, int64_t n, const std::vector<bsg_insta
   return need;
 }
 
+// Every scenario's running / waiting slice must lie inside [0, n_entries): a
+// bad offset would otherwise read past a column (silently wrong) or fault the
+// device (a sticky error that ends the process's CUDA context).
+bsg_status check_ranges(bsg_ctx* ctx, const bsg_scenario* sc, int64_t n, int64_t n_entries) {
+  for (int64_t i = 0; i < n; ++i) {
+    const bsg_scenario& x = sc[i];
+    const bool bad_run = x.run_n > 0 && (x.run_off < 0 || static_cast<int64_t>(x.run_off) + x.run_n > n_entries);
+    const bool bad_wait = x.wait_n > 0 && (x.wait_off < 0 || static_cast<int64_t>(x.wait_off) + x.wait_n > n_entries);
+    if (bad_run || bad_wait) {
+      ctx->last_error = "scenario " + std::to_string(i) + " references entries outside [0, n_entries)";
+      return BSG_INVALID_ARGUMENT;
+    }
+  }
+  return BSG_OK;
+}
+
 // Uploads host entry columns + scenarios into the context's device buffers.
 bsg_status upload(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries,
                   const bsg_scenario* sc, int64_t n, bsg_entries* dev) {
+  {
+    const bsg_status v = check_ranges(ctx, sc, n, n_entries);
+    if (v != BSG_OK) return v;
+  }
   const size_t eb = static_cast<size_t>(std::max<int64_t>(n_entries, 1)) * sizeof(int32_t);
   if (!ctx->prompt.ensure(eb) || !ctx->est.ensure(eb) || !ctx->prefill.ensure(eb) ||
       !ctx->decoded.ensure(eb) || !ctx->scen.ensure(n * sizeof(bsg_scenario)) ||
@@ -619,7 +675,9 @@ bsg_status dispatch_fused(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_en
                           const bsg_scenario* scenarios, const int32_t* instance_ids,
                           int32_t n_inst, int32_t n_requests, const int32_t* lengths,
                           int32_t n_samples, int32_t objective, int32_t* chosen, int64_t* scores,
-                          int64_t* sample_e2e, bsg_result* per_instance);
+                          int64_t* sample_e2e, bsg_result* per_instance,
+                          const uint64_t* request_ids, uint64_t seed, double mean_abs_rel_error,
+                          int32_t* lengths_out, int64_t* dev_keys);
 }  // namespace
 
 extern "C" {
@@ -682,6 +740,33 @@ int64_t bsg_launch_count(const bsg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 int64_t bsg_scenario_count(const bsg_ctx* ctx) { return ctx ? ctx->scenarios : 0; }
 
+const char* bsg_last_launch(const bsg_ctx* ctx) { return ctx ? ctx->last_launch.c_str() : ""; }
+
+}  // extern "C"
+
+// validate_instance_config (types.cpp:47-61, same check order): BSG_BAD_CONFIG
+// with the field code; then the supported integer domain (all
+// token sums fit int32): BSG_BAD_INPUT.
+bsg_status bsg_check_config(const bsg_instance_cfg& c, int32_t* field_code) {
+  int32_t f = 0;
+  if (c.total_blocks < 1) f = 1;
+  else if (c.block_size < 1) f = 2;
+  else if (c.max_batch_size < 1) f = 3;
+  else if (c.chunk_budget < c.block_size) f = 4;
+  else if (!(c.c0_s > 0)) f = 5;
+  else if (c.prefill_s_per_token < 0) f = 6;
+  else if (c.decode_s_per_seq < 0) f = 7;
+  else if (c.context_s_per_token < 0) f = 8;
+  *field_code = f;
+  if (f) return BSG_BAD_CONFIG;
+  if (static_cast<int64_t>(c.total_blocks) * c.block_size > (1LL << 30) || c.block_size > (1 << 20) ||
+      c.chunk_budget > (1 << 30))
+    return BSG_BAD_INPUT;
+  return BSG_OK;
+}
+
+extern "C" {
+
 bsg_status bsg_set_configs(bsg_ctx* ctx, const bsg_instance_cfg* cfgs, int32_t n,
                            int32_t* bad_index, int32_t* field_code) {
   if (!ctx || !cfgs || n <= 0) return BSG_INVALID_ARGUMENT;
@@ -691,28 +776,13 @@ bsg_status bsg_set_configs(bsg_ctx* ctx, const bsg_instance_cfg* cfgs, int32_t n
   int32_t maxb = 0;
   for (int32_t i = 0; i < n; ++i) {
     const bsg_instance_cfg& c = cfgs[i];
-    int32_t f = 0;  // validate_instance_config, types.cpp:47-61 (same order)
-    if (c.total_blocks < 1) f = 1;
-    else if (c.block_size < 1) f = 2;
-    else if (c.max_batch_size < 1) f = 3;
-    else if (c.chunk_budget < c.block_size) f = 4;
-    else if (!(c.c0_s > 0)) f = 5;
-    else if (c.prefill_s_per_token < 0) f = 6;
-    else if (c.decode_s_per_seq < 0) f = 7;
-    else if (c.context_s_per_token < 0) f = 8;
-    if (f) {
+    int32_t f = 0;
+    const bsg_status v = bsg_check_config(c, &f);
+    if (v != BSG_OK) {
       if (bad_index) *bad_index = i;
       if (field_code) *field_code = f;
-      ctx->last_error = "invalid config";
-      return BSG_BAD_CONFIG;
-    }
-    // Supported integer domain: all token sums fit in int32.
-    if (static_cast<int64_t>(c.total_blocks) * c.block_size > (1LL << 30) ||
-        c.block_size > (1 << 20) || c.chunk_budget > (1 << 30)) {
-      if (bad_index) *bad_index = i;
-      if (field_code) *field_code = 0;
-      ctx->last_error = "config outside the supported integer domain";
-      return BSG_BAD_INPUT;
+      ctx->last_error = v == BSG_BAD_CONFIG ? "invalid config" : "config outside the supported integer domain";
+      return v;
     }
     dev[i] = to_dev(c);
     maxb = std::max(maxb, c.max_batch_size);
@@ -919,7 +989,8 @@ bsg_status bsg_dispatch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entr
   }
   if (uniform)
     return dispatch_fused(ctx, entries, n_entries, scenarios, instance_ids, n_inst, n_requests,
-                          est.data(), 1, objective, chosen, nullptr, nullptr, per_instance);
+                          est.data(), 1, objective, chosen, nullptr, nullptr, per_instance, nullptr, 0,
+                          0.0, nullptr, nullptr);
   cudaSetDevice(ctx->device);
   const int64_t n = static_cast<int64_t>(n_inst) * n_requests;
   bsg_entries dev{};
@@ -956,31 +1027,49 @@ bsg_status bsg_dispatch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entr
 namespace {
 
 // Fused what-if fan-out + argmin with one packed host->device copy: the
-// latency path of both bsg_dispatch (one "sample" = the candidate's estimate)
-// and bsg_dispatch_mc. Caller holds ctx->mu.
+// latency path of bsg_dispatch (one "sample" = the candidate's estimate),
+// bsg_dispatch_mc (samples given) and bsg_dispatch_mc_sampled (samples drawn
+// on the device: request_ids != nullptr, lengths == nullptr). Caller holds ctx->mu.
 bsg_status dispatch_fused(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries,
                           const bsg_scenario* scenarios, const int32_t* instance_ids,
                           int32_t n_inst, int32_t n_requests, const int32_t* lengths,
                           int32_t n_samples, int32_t objective, int32_t* chosen, int64_t* scores,
-                          int64_t* sample_e2e, bsg_result* per_instance) {
+                          int64_t* sample_e2e, bsg_result* per_instance,
+                          const uint64_t* request_ids, uint64_t seed, double mean_abs_rel_error,
+                          int32_t* lengths_out, int64_t* dev_keys) {
   cudaSetDevice(ctx->device);
   const int64_t n = static_cast<int64_t>(n_inst) * n_requests;
   const int64_t S = n_samples;
-  // sort each request's samples, remembering the permutation for sample_e2e
-  std::vector<int32_t> sorted(static_cast<size_t>(n_requests * S));
-  std::vector<int32_t> perm(static_cast<size_t>(n_requests * S));
-  for (int32_t r = 0; r < n_requests; ++r) {
-    int32_t* pr = perm.data() + r * S;
-    for (int32_t j = 0; j < S; ++j) pr[j] = j;
-    const int32_t* lr = lengths + r * S;
-    std::stable_sort(pr, pr + S, [&](int32_t a, int32_t b) { return lr[a] < lr[b]; });
-    for (int32_t j = 0; j < S; ++j) sorted[r * S + j] = lr[pr[j]];
+  const bool sample = request_ids != nullptr;
+  {
+    const bsg_status v = check_ranges(ctx, scenarios, n, n_entries);
+    if (v != BSG_OK) return v;
   }
-  // one packed host->device copy: 4 entry columns | scenarios | ids | sorted lengths
+  if (dev_keys) {  // the packed key holds 16-bit instance ids
+    for (int64_t i = 0; i < n; ++i)
+      if (instance_ids[i] < 0 || instance_ids[i] >= 0xffff) {
+        ctx->last_error = "instance ids must be in [0, 65535) for the packed cross-GPU key";
+        return BSG_INVALID_ARGUMENT;
+      }
+  }
+  // given samples: sort each request's, remembering the permutation for sample_e2e
+  std::vector<int32_t> sorted, perm;
+  if (!sample) {
+    sorted.resize(static_cast<size_t>(n_requests * S));
+    perm.resize(static_cast<size_t>(n_requests * S));
+    for (int32_t r = 0; r < n_requests; ++r) {
+      int32_t* pr = perm.data() + r * S;
+      for (int32_t j = 0; j < S; ++j) pr[j] = j;
+      const int32_t* lr = lengths + r * S;
+      std::stable_sort(pr, pr + S, [&](int32_t a, int32_t b) { return lr[a] < lr[b]; });
+      for (int32_t j = 0; j < S; ++j) sorted[r * S + j] = lr[pr[j]];
+    }
+  }
+  // one packed host->device copy: 4 entry columns | scenarios | ids | sorted lengths or request ids
   const size_t ne = static_cast<size_t>(n_entries);
   auto r16 = [](size_t b) { return (b + 15) & ~size_t(15); };
-  const size_t bytes = 4 * r16(ne * 4) + r16(n * sizeof(bsg_scenario)) + r16(n * 4) +
-                       r16(sorted.size() * 4);
+  const size_t tail = sample ? static_cast<size_t>(n_requests) * 8 : sorted.size() * 4;
+  const size_t bytes = 4 * r16(ne * 4) + r16(n * sizeof(bsg_scenario)) + r16(n * 4) + r16(tail);
   if (ctx->pinned_cap < bytes) {
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     ctx->pinned = nullptr;
@@ -989,7 +1078,8 @@ bsg_status dispatch_fused(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_en
     ctx->pinned_cap = bytes * 2;
   }
   if (!ctx->blob.ensure(bytes) || !ctx->scores.ensure(n * 8) || !ctx->res.ensure(n * sizeof(bsg_result)) ||
-      !ctx->chosen.ensure(n_requests * 4) || !ctx->ids.ensure(4)) {
+      !ctx->chosen.ensure(n_requests * 4) || !ctx->ids.ensure(4) ||
+      (lengths_out && !ctx->samples.ensure(n_requests * S * 4))) {
     ctx->last_error = "device allocation failed";
     return BSG_CUDA_ERROR;
   }
@@ -1009,7 +1099,7 @@ bsg_status dispatch_fused(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_en
   const size_t o_p = put(entries->prompt, ne * 4), o_e = put(entries->est, ne * 4),
                o_f = put(entries->prefill, ne * 4), o_d = put(entries->decoded, ne * 4),
                o_s = put(scenarios, n * sizeof(bsg_scenario)), o_i = put(instance_ids, n * 4),
-               o_l = put(sorted.data(), sorted.size() * 4);
+               o_l = sample ? put(request_ids, tail) : put(sorted.data(), tail);
   BSG_CUDA(ctx, cudaMemcpyAsync(ctx->blob.p, h, off, cudaMemcpyHostToDevice, ctx->stream));
   char* d = static_cast<char*>(ctx->blob.p);
   int32_t cap = 1;
@@ -1029,22 +1119,33 @@ bsg_status dispatch_fused(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_en
   auto* ds = reinterpret_cast<const bsg_scenario*>(d + o_s);
   auto* di = reinterpret_cast<const int32_t*>(d + o_i);
   auto* dl = reinterpret_cast<const int32_t*>(d + o_l);
+  McSampling smp{sample ? reinterpret_cast<const uint64_t*>(d + o_l) : nullptr, seed,
+                 mean_abs_rel_error * std::sqrt(3.14159265358979323846 / 2.0),
+                 lengths_out ? static_cast<int32_t*>(ctx->samples.p) : nullptr};
   auto* dsc = static_cast<int64_t*>(ctx->scores.p);
   auto* dse = sample_e2e ? static_cast<int64_t*>(ctx->samples.p) : nullptr;
   auto* dres = static_cast<bsg_result*>(ctx->res.p);
   auto* dcnt = static_cast<unsigned*>(ctx->counters.p);
   auto* dch = static_cast<int32_t*>(ctx->chosen.p);
   auto* dcf = static_cast<const DevCfg*>(ctx->cfgs.p);
-#define BSG_LAUNCH_MC1(KK, P2)                                                                  \
+  const int32_t Sp = sample ? pow2_ceil(n_samples) : n_samples;
+#define BSG_LAUNCH_MC2(KK, P2, SM)                                                              \
   {                                                                                             \
-    const size_t sm = static_cast<size_t>(kWarpsPerBlock) * (smem_words(KK) + S) * 4;         \
+    const size_t sm = static_cast<size_t>(kWarpsPerBlock) * (smem_words(KK) + Sp) * 4;        \
     if (sm > 48 * 1024)                                                                         \
-      cudaFuncSetAttribute(dispatch_mc_kernel<KK, P2>,                                          \
+      cudaFuncSetAttribute(dispatch_mc_kernel<KK, P2, SM>,                                      \
                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));  \
-    dispatch_mc_kernel<KK, P2><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, sm,       \
-                                 ctx->stream>>>(dcf, ctx->ncfg, dp, de, df, dd, ds, di, n_inst,  \
-                                                n_requests, dl, n_samples, objective, dsc, dse,  \
-                                                dres, dcnt, dch);                                \
+    dispatch_mc_kernel<KK, P2, SM><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, sm,   \
+                                     ctx->stream>>>(dcf, ctx->ncfg, dp, de, df, dd, ds, di,     \
+                                                    n_inst, n_requests, dl, n_samples,          \
+                                                    objective, dsc, dse, dres, dcnt, dch, smp,  \
+                                                    dev_keys);                                  \
+  }
+#define BSG_LAUNCH_MC1(KK, P2)        \
+  if (sample) {                       \
+    BSG_LAUNCH_MC2(KK, P2, true)      \
+  } else {                            \
+    BSG_LAUNCH_MC2(KK, P2, false)     \
   }
 #define BSG_LAUNCH_MC(KK)             \
   if (ctx->all_pow2) {                \
@@ -1060,14 +1161,20 @@ bsg_status dispatch_fused(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_en
   }
 #undef BSG_LAUNCH_MC
 #undef BSG_LAUNCH_MC1
+#undef BSG_LAUNCH_MC2
   ctx->launches += 1;
   ctx->scenarios += n * S;
+  ctx->last_launch = std::string("dispatch_mc_kernel<") + std::to_string(k) + "," +
+                     (ctx->all_pow2 ? "true" : "false") + "," + (sample ? "true" : "false") + ">";
   BSG_CUDA(ctx, cudaGetLastError());
   BSG_CUDA(ctx, cudaMemcpyAsync(chosen, dch, n_requests * 4, cudaMemcpyDeviceToHost, ctx->stream));
   if (scores)
     BSG_CUDA(ctx, cudaMemcpyAsync(scores, dsc, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
   if (per_instance)
     BSG_CUDA(ctx, cudaMemcpyAsync(per_instance, dres, n * sizeof(bsg_result), cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+  if (lengths_out)
+    BSG_CUDA(ctx, cudaMemcpyAsync(lengths_out, ctx->samples.p, n_requests * S * 4, cudaMemcpyDeviceToHost,
                                   ctx->stream));
   std::vector<int64_t> tmp;
   if (sample_e2e) {
@@ -1101,7 +1208,26 @@ bsg_status bsg_dispatch_mc(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_e
   if (ctx->ncfg == 0) return BSG_INVALID_ARGUMENT;
   std::lock_guard<std::mutex> lock(ctx->mu);
   return dispatch_fused(ctx, entries, n_entries, scenarios, instance_ids, n_inst, n_requests,
-                        lengths, n_samples, objective, chosen, scores, sample_e2e, per_instance);
+                        lengths, n_samples, objective, chosen, scores, sample_e2e, per_instance, nullptr,
+                        0, 0.0, nullptr, nullptr);
+}
+
+bsg_status bsg_dispatch_mc_sampled(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries,
+                                   const bsg_scenario* scenarios, const int32_t* instance_ids,
+                                   int32_t n_inst, int32_t n_requests, const uint64_t* request_ids,
+                                   int32_t n_samples, uint64_t seed, double mean_abs_rel_error,
+                                   int32_t objective, int32_t* chosen, int64_t* scores,
+                                   int32_t* lengths_out, bsg_result* per_instance, int64_t* dev_keys) {
+  if (!ctx || !entries || !scenarios || !instance_ids || !request_ids || !chosen)
+    return BSG_INVALID_ARGUMENT;
+  if (n_inst <= 0) return BSG_NO_INSTANCES;
+  if (n_samples < 1 || n_samples > 1024 || !(mean_abs_rel_error >= 0)) return BSG_INVALID_ARGUMENT;
+  if (n_requests <= 0) return BSG_OK;
+  if (ctx->ncfg == 0) return BSG_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  return dispatch_fused(ctx, entries, n_entries, scenarios, instance_ids, n_inst, n_requests, nullptr,
+                        n_samples, objective, chosen, scores, nullptr, per_instance, request_ids, seed,
+                        mean_abs_rel_error, lengths_out, dev_keys);
 }
 
 }  // extern "C"

@@ -37,6 +37,7 @@ struct bsg_ctx {
   cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};  // chunked host-buffer pipeline
   cudaEvent_t pipe_done[3] = {nullptr, nullptr, nullptr};
   std::string last_error;
+  std::string last_launch;  // the simulation kernel(s) the last call launched
   int64_t launches = 0;
   int64_t scenarios = 0;  // predict() scenarios simulated (MC: request x instance x sample)
   std::vector<bsg_instance_cfg> host_cfgs;

@@ -283,14 +283,36 @@ struct Parser {
 };
 
 // ---- schema (json_io.cpp) ---------------------------------------------------
+// Errors carry nlohmann::json 3.11.3's exception text (what()), which the
+// reference wraps as "bad-schema: <what>" (parse_with, json_io.cpp:86-95).
 struct SchemaError {
   std::string what;
 };
 
-const JVal& at(const JVal& j, const char* key) {
-  if (j.kind != JVal::kObject) throw SchemaError{std::string("type must be object, but is other")};
+const char* type_name(const JVal& v) {  // basic_json::type_name()
+  switch (v.kind) {
+    case JVal::kNull: return "null";
+    case JVal::kBool: return "boolean";
+    case JVal::kInt:
+    case JVal::kUint:
+    case JVal::kDouble: return "number";
+    case JVal::kString: return "string";
+    case JVal::kArray: return "array";
+    case JVal::kObject: return "object";
+  }
+  return "discarded";
+}
+
+[[noreturn]] void type_error_302(const char* want, const JVal& v) {
+  throw SchemaError{std::string("[json.exception.type_error.302] type must be ") + want + ", but is " +
+                    type_name(v)};
+}
+
+const JVal& at(const JVal& j, const char* key) {  // basic_json::at(key)
+  if (j.kind != JVal::kObject)
+    throw SchemaError{std::string("[json.exception.type_error.304] cannot use at() with ") + type_name(j)};
   const JVal* v = j.get(key);
-  if (!v) throw SchemaError{std::string("key '") + key + "' not found"};
+  if (!v) throw SchemaError{std::string("[json.exception.out_of_range.403] key '") + key + "' not found"};
   return *v;
 }
 
@@ -304,9 +326,9 @@ T as_int(const JVal& v) {
     case JVal::kUint: return static_cast<T>(v.u);
     case JVal::kDouble: return static_cast<T>(v.d);
     case JVal::kBool:
-      if (sizeof(T) == 8) throw SchemaError{"type must be number, but is boolean"};
+      if (sizeof(T) == 8) type_error_302("number", v);
       return static_cast<T>(v.b);
-    default: throw SchemaError{"type must be number"};
+    default: type_error_302("number", v);
   }
 }
 
@@ -315,8 +337,35 @@ double as_double(const JVal& v) {  // get<double> = get_arithmetic_value: no boo
     case JVal::kInt: return static_cast<double>(v.i);
     case JVal::kUint: return static_cast<double>(v.u);
     case JVal::kDouble: return v.d;
-    default: throw SchemaError{"type must be number"};
+    default: type_error_302("number", v);
   }
+}
+
+const std::string& as_string(const JVal& v) {
+  if (v.kind != JVal::kString) type_error_302("string", v);
+  return v.s;
+}
+
+// Range-for over a basic_json (json_io.cpp:49-50): an array yields its
+// elements, an object its values in key order (std::map, duplicates: last
+// wins), null nothing, any other value itself once.
+std::vector<const JVal*> json_range(const JVal& j) {
+  std::vector<const JVal*> out;
+  if (j.kind == JVal::kArray) {
+    for (const JVal& x : j.arr) out.push_back(&x);
+  } else if (j.kind == JVal::kObject) {
+    std::vector<std::pair<std::string, const JVal*>> m;
+    for (auto it = j.obj.rbegin(); it != j.obj.rend(); ++it) {
+      bool seen = false;
+      for (const auto& e : m) seen |= e.first == it->first;
+      if (!seen) m.emplace_back(it->first, &it->second);
+    }
+    std::sort(m.begin(), m.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    for (const auto& e : m) out.push_back(e.second);
+  } else if (j.kind != JVal::kNull) {
+    out.push_back(&j);
+  }
+  return out;
 }
 
 struct Entry {
@@ -325,17 +374,22 @@ struct Entry {
 };
 
 void entries_from(const JVal& arr, std::vector<Entry>* out) {
-  if (arr.kind != JVal::kArray) throw SchemaError{"type must be array"};
-  for (const JVal& r : arr.arr) {
+  for (const JVal* r : json_range(arr)) {  // snapshot_request_from_json_obj (json_io.cpp:21-29)
     Entry e{};
-    e.id = as_int<uint64_t>(at(r, "id"));
-    e.prompt = as_int<int32_t>(at(r, "prompt_tokens"));
-    e.est = as_int<int32_t>(at(r, "estimated_output_tokens"));
-    e.prefill = as_int<int32_t>(at(r, "prefill_progress"));
-    e.decoded = as_int<int32_t>(at(r, "decoded_tokens"));
+    e.id = as_int<uint64_t>(at(*r, "id"));
+    e.prompt = as_int<int32_t>(at(*r, "prompt_tokens"));
+    e.est = as_int<int32_t>(at(*r, "estimated_output_tokens"));
+    e.prefill = as_int<int32_t>(at(*r, "prefill_progress"));
+    e.decoded = as_int<int32_t>(at(*r, "decoded_tokens"));
     out->push_back(e);
   }
 }
+
+// A ConfigError (error.h:14-18) raised while parsing: passes parse_with's
+// json::exception handler untouched.
+struct ConfigErr {
+  std::string what;
+};
 
 struct Request {
   std::vector<Entry> running, waiting;
@@ -362,11 +416,10 @@ Request request_from(const JVal& j) {  // prediction_request_from_json (json_io.
   r.cfg.block_size = as_int<int32_t>(at(c, "block_size"));
   r.cfg.max_batch_size = as_int<int32_t>(at(c, "max_batch_size"));
   r.cfg.chunk_budget = as_int<int32_t>(at(c, "chunk_budget"));
-  const JVal& pol = at(c, "local_policy");
-  if (pol.kind != JVal::kString) throw SchemaError{"type must be string"};
-  if (pol.s == "chunked_prefill") r.cfg.local_policy = BSG_CHUNKED_PREFILL;  // parse_local_policy
-  else if (pol.s == "prefill_priority") r.cfg.local_policy = BSG_PREFILL_PRIORITY;
-  else throw SchemaError{"unknown local policy '" + pol.s + "'"};
+  const std::string& pol = as_string(at(c, "local_policy"));
+  if (pol == "chunked_prefill") r.cfg.local_policy = BSG_CHUNKED_PREFILL;  // parse_local_policy (types.cpp:41-45)
+  else if (pol == "prefill_priority") r.cfg.local_policy = BSG_PREFILL_PRIORITY;
+  else throw ConfigErr{"invalid config: cluster.local_policy: unknown policy '" + pol + "'"};
   const JVal& cost = at(c, "cost_model");
   r.cfg.c0_s = as_double(at(cost, "c0_s"));
   r.cfg.prefill_s_per_token = as_double(at(cost, "prefill_s_per_token"));
@@ -626,6 +679,9 @@ std::string escape(const std::string& s) {
     if (c == '"' || c == '\\') {
       o.push_back('\\');
       o.push_back(c);
+    } else if (c == '\b' || c == '\t' || c == '\n' || c == '\f' || c == '\r') {  // dump's short escapes
+      o.push_back('\\');
+      o.push_back(c == '\b' ? 'b' : c == '\t' ? 't' : c == '\n' ? 'n' : c == '\f' ? 'f' : 'r');
     } else if (static_cast<unsigned char>(c) < 0x20) {
       char b[8];
       std::snprintf(b, sizeof(b), "\\u%04x", c);
@@ -638,9 +694,114 @@ std::string escape(const std::string& s) {
 }
 
 std::string error_body(const std::string& code, const std::string& detail) {  // json_io.cpp:148-152
-  std::string o = "{\"error\":\"" + escape(code) + "\"";
-  if (!detail.empty()) o += ",\"detail\":\"" + escape(detail) + "\"";
-  return o + "}";
+  // nlohmann objects dump in key order: "detail" before "error"
+  std::string o = "{";
+  if (!detail.empty()) o += "\"detail\":\"" + escape(detail) + "\",";
+  return o + "\"error\":\"" + escape(code) + "\"}";
+}
+
+// "invalid config: <field>: <rule>" of validate_instance_config (types.cpp:47-61)
+// by bsg_check_config's field code.
+std::string config_error_text(int32_t f) {
+  static const char* const field[] = {"", "total_blocks", "block_size", "max_batch_size", "chunk_budget",
+                                      "cost_model.c0_s", "cost_model.prefill_s_per_token",
+                                      "cost_model.decode_s_per_seq", "cost_model.context_s_per_token"};
+  static const char* const rule[] = {"", "must be >= 1", "must be >= 1", "must be >= 1",
+                                     "must be >= block_size", "must be > 0", "must be >= 0", "must be >= 0",
+                                     "must be >= 0"};
+  return std::string("invalid config: ") + field[f] + ": " + rule[f];
+}
+
+// Parses one /predict body exactly as prediction_request_from_json
+// (json_io.cpp:136-146) and runs predict()'s checks that precede simulation
+// (the Instance ctor's validate_instance_config, backend.cpp:16-18). Returns
+// true, or false with the reference's status / error body (json_io.cpp:148-152
+// via service.cpp:229-241).
+bool parse_predict_request(const char* t, Request* req, int32_t* status, std::string* body) {
+  Parser ps{t, t + std::strlen(t), {}};
+  JVal j;
+  bool good = ps.value(&j);
+  ps.ws();
+  if (good && ps.p != ps.end) good = ps.fail("malformed JSON");
+  if (!good) {
+    *status = BSG_BAD_INPUT;
+    *body = error_body("bad-schema", "bad-schema: malformed JSON");
+    return false;
+  }
+  try {
+    *req = request_from(j);
+  } catch (const SchemaError& e) {
+    *status = BSG_BAD_INPUT;
+    *body = error_body("bad-schema", "bad-schema: " + e.what);
+    return false;
+  } catch (const ConfigErr& e) {
+    *status = BSG_BAD_CONFIG;
+    *body = error_body("bad-schema", e.what);
+    return false;
+  }
+  int32_t f = 0;
+  const bsg_status v = bsg_check_config(req->cfg, &f);
+  if (v == BSG_BAD_CONFIG) {  // ConfigError is an Error: 400
+    *status = BSG_BAD_CONFIG;
+    *body = error_body("bad-schema", config_error_text(f));
+    return false;
+  }
+  if (v != BSG_OK) {  // outside the supported integer domain: a prediction failure, never a silent fallback
+    *status = BSG_BAD_INPUT;
+    *body = error_body("prediction-failure", "instance config outside the GPU simulator's supported domain "
+                                             "(total_blocks * block_size <= 2^30, block_size <= 2^20, "
+                                             "chunk_budget <= 2^30)");
+    return false;
+  }
+  return true;
+}
+
+// The response body of a simulated request (service.cpp:229-241): the
+// PredictionResult, or PredictionError's message (predictor.cpp:101-136),
+// rebuilt from the result's status and detail.
+std::string result_body(const Request& r, const bsg_result& x) {
+  auto entry_id = [&](int32_t origin) -> uint64_t {  // origin: running i, waiting run_n + j, candidate -1
+    uint64_t cand = 0;  // candidate id: max snapshot id + 1 (predictor.cpp:79-82)
+    for (const Entry& e : r.running) cand = std::max(cand, e.id);
+    for (const Entry& e : r.waiting) cand = std::max(cand, e.id);
+    cand += 1;
+    const int32_t rn = static_cast<int32_t>(r.running.size());
+    if (origin < 0) return cand;
+    return origin < rn ? r.running[origin].id : r.waiting[origin - rn].id;
+  };
+  switch (x.status) {
+    case BSG_OK: {  // prediction_result_to_json (json_io.cpp:103-108): std::map key order
+      std::string o = "{\"metrics\":{\"predicted_e2e_latency\":";
+      append_double(&o, bsg_ticks_to_seconds(x.e2e_ticks));
+      o += ",\"predicted_queueing_delay\":";
+      append_double(&o, bsg_ticks_to_seconds(x.qdelay_ticks));
+      o += ",\"predicted_ttft\":";
+      append_double(&o, bsg_ticks_to_seconds(x.ttft_ticks));
+      o += "},\"simulated_steps\":" + std::to_string(x.steps) + "}";
+      return o;
+    }
+    case BSG_TOO_LARGE_RUNNING:  // backend.cpp:42-44, re-thrown at predictor.cpp:134-135
+      return error_body("prediction-failure",
+                        "candidate does not fit the instance: snapshot running set exceeds total memory blocks");
+    case BSG_TOO_LARGE_CANDIDATE:  // backend.cpp:76-83
+      return error_body("prediction-failure", "candidate does not fit the instance: request " +
+                                                  std::to_string(entry_id(-1)) + " needs " +
+                                                  std::to_string(x.detail) + " blocks, instance has " +
+                                                  std::to_string(r.cfg.total_blocks));
+    case BSG_DEADLOCK:  // backend.cpp:274-277, predictor.cpp:132-133
+      return error_body("prediction-failure", "backend deadlock during forward simulation: request " +
+                                                  std::to_string(entry_id(x.detail)) +
+                                                  " cannot proceed with the whole memory free");
+    case BSG_STEP_LIMIT:
+      return error_body("prediction-failure", "forward simulation exceeded the step limit");
+    case BSG_VANISHED:
+      return error_body("prediction-failure", "candidate vanished from the forward simulation");
+    case BSG_EMPTY_PLAN:  // EmptyPlanError is an Error, not a PredictionError: 400 (backend.cpp:245)
+      return error_body("bad-schema", "no runnable work fits the batch");
+    default:  // out-of-domain snapshot values: the GPU simulator refuses them explicitly
+      return error_body("prediction-failure",
+                        "snapshot outside the GPU simulator's supported domain (DESIGN.md §4)");
+  }
 }
 
 }  // namespace
@@ -652,28 +813,12 @@ extern "C" bsg_status bsg_predict_json(bsg_ctx* ctx, const char* const* requests
   std::vector<std::string> body(static_cast<size_t>(n));
   std::vector<Request> reqs(static_cast<size_t>(n));
   std::vector<int> ok(static_cast<size_t>(n), 0);
-  // parse (parse_with, json_io.cpp:86-95): malformed JSON / missing fields -> bad-schema
+  // parse + per-request config validation: each request fails on its own, like
+  // the reference role handles each /predict independently
   std::vector<bsg_instance_cfg> cfgs;
   std::vector<int32_t> cfg_of(static_cast<size_t>(n), 0);
   for (int32_t q = 0; q < n; ++q) {
-    const char* t = requests[q] ? requests[q] : "";
-    Parser ps{t, t + std::strlen(t), {}};
-    JVal j;
-    bool good = ps.value(&j);
-    ps.ws();
-    if (good && ps.p != ps.end) good = ps.fail("malformed JSON");
-    if (!good) {
-      status[q] = BSG_BAD_INPUT;
-      body[q] = error_body("bad-schema", "bad-schema: malformed JSON");
-      continue;
-    }
-    try {
-      reqs[q] = request_from(j);
-    } catch (const SchemaError& e) {
-      status[q] = BSG_BAD_INPUT;
-      body[q] = error_body("bad-schema", "bad-schema: " + e.what);
-      continue;
-    }
+    if (!parse_predict_request(requests[q] ? requests[q] : "", &reqs[q], &status[q], &body[q])) continue;
     int32_t ci = -1;
     for (size_t c = 0; c < cfgs.size() && ci < 0; ++c)
       if (std::memcmp(&cfgs[c], &reqs[q].cfg, sizeof(bsg_instance_cfg)) == 0) ci = static_cast<int32_t>(c);
@@ -684,36 +829,13 @@ extern "C" bsg_status bsg_predict_json(bsg_ctx* ctx, const char* const* requests
     cfg_of[q] = ci;
     ok[q] = 1;
   }
-  // one GPU batch over every well-formed request
-  std::vector<int32_t> rows;
+  // one GPU batch over every well-formed request (its configs all validated)
   if (!cfgs.empty()) {
     int32_t bi = -1, fc = 0;
     const bsg_status cs = bsg_set_configs(ctx, cfgs.data(), static_cast<int32_t>(cfgs.size()), &bi, &fc);
-    if (cs != BSG_OK && cs != BSG_BAD_CONFIG && cs != BSG_BAD_INPUT) return cs;
-    if (cs != BSG_OK) {  // a config failed validation (ConfigError): reject its requests
-      for (int32_t q = 0; q < n; ++q)
-        if (ok[q] && cfg_of[q] == bi) {
-          ok[q] = 0;
-          status[q] = BSG_BAD_CONFIG;
-          body[q] = error_body("bad-schema", "invalid instance_config");
-        }
-      // retry with the remaining configs
-      std::vector<bsg_instance_cfg> keep;
-      std::vector<int32_t> remap(cfgs.size(), -1);
-      for (size_t c = 0; c < cfgs.size(); ++c)
-        if (static_cast<int32_t>(c) != bi) {
-          remap[c] = static_cast<int32_t>(keep.size());
-          keep.push_back(cfgs[c]);
-        }
-      for (int32_t q = 0; q < n; ++q)
-        if (ok[q]) cfg_of[q] = remap[cfg_of[q]];
-      cfgs.swap(keep);
-      if (!cfgs.empty()) {
-        const bsg_status c2 = bsg_set_configs(ctx, cfgs.data(), static_cast<int32_t>(cfgs.size()), &bi, &fc);
-        if (c2 != BSG_OK) return c2;  // one bad config per call is reported per request
-      }
-    }
+    if (cs != BSG_OK) return cs;
   }
+  std::vector<int32_t> rows;
   std::vector<uint64_t> id;
   std::vector<int32_t> prompt, est, prefill, decoded;
   std::vector<bsg_scenario> scen;
@@ -747,30 +869,8 @@ extern "C" bsg_status bsg_predict_json(bsg_ctx* ctx, const char* const* requests
                                             static_cast<int64_t>(scen.size()), res.data());
     if (st != BSG_OK) return st;
     for (size_t k = 0; k < rows.size(); ++k) {
-      const int32_t q = rows[k];
-      const bsg_result& x = res[k];
-      status[q] = x.status;
-      if (x.status == BSG_OK) {  // prediction_result_to_json (json_io.cpp:103-108): std::map key order
-        std::string o = "{\"metrics\":{\"predicted_e2e_latency\":";
-        append_double(&o, bsg_ticks_to_seconds(x.e2e_ticks));
-        o += ",\"predicted_queueing_delay\":";
-        append_double(&o, bsg_ticks_to_seconds(x.qdelay_ticks));
-        o += ",\"predicted_ttft\":";
-        append_double(&o, bsg_ticks_to_seconds(x.ttft_ticks));
-        o += "},\"simulated_steps\":" + std::to_string(x.steps) + "}";
-        body[q] = std::move(o);
-      } else if (x.status == BSG_TOO_LARGE_RUNNING || x.status == BSG_TOO_LARGE_CANDIDATE) {
-        // RequestTooLarge is re-thrown as PredictionError (predictor.cpp:134-135) -> 422
-        body[q] = error_body("prediction-failure", "candidate does not fit the instance");
-      } else if (x.status == BSG_DEADLOCK) {
-        body[q] = error_body("prediction-failure", "backend deadlock during forward simulation");
-      } else if (x.status == BSG_STEP_LIMIT) {
-        body[q] = error_body("prediction-failure", "forward simulation exceeded the step limit");
-      } else if (x.status == BSG_VANISHED) {
-        body[q] = error_body("prediction-failure", "candidate vanished from the forward simulation");
-      } else {  // EmptyPlanError / ConfigError / out-of-domain input: an Error -> 400
-        body[q] = error_body("bad-schema", "invalid request");
-      }
+      status[rows[k]] = res[k].status;
+      body[rows[k]] = result_body(reqs[rows[k]], res[k]);
     }
   }
   int64_t off = 0;
@@ -784,6 +884,16 @@ extern "C" bsg_status bsg_predict_json(bsg_ctx* ctx, const char* const* requests
   }
   out_off[n] = off;
   return off <= out_cap ? BSG_OK : BSG_INVALID_ARGUMENT;  // out_off[n] = bytes needed
+}
+
+extern "C" int32_t bsg_wire_check(const char* body, char* out, int64_t cap) {
+  if (!body) return BSG_INVALID_ARGUMENT;
+  Request r;
+  int32_t st = BSG_OK;
+  std::string text;
+  if (parse_predict_request(body, &r, &st, &text)) return BSG_OK;
+  if (out && cap > 0) std::snprintf(out, static_cast<size_t>(cap), "%s", text.c_str());
+  return st;
 }
 
 // ---- trace JSONL (workload.cpp:20-68) --------------------------------------

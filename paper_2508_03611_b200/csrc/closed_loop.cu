@@ -33,6 +33,7 @@
 #include <vector>
 
 #include "bsg_ctx.cuh"
+#include "mc_sampler.cuh"
 #include "bsg_internal.h"
 
 namespace bsg {
@@ -844,7 +845,10 @@ constexpr int kFleetWarps = 4;
 struct FleetParams {
   int64_t now;
   int32_t prompt, est, output, S, objective, drain;
-  int32_t lens[1024];  // sorted MC lengths, S of them
+  int32_t sample, pad;  // sample: draw the S lengths on the device (K3) instead of lens
+  uint64_t request_id, seed;
+  double scale;         // mean_abs_rel_error * sqrt(pi / 2)
+  int32_t lens[1024];   // sorted MC lengths, S of them (sample == 0)
 };
 
 template <int K, bool POW2, bool MC>
@@ -861,7 +865,7 @@ __global__ void __launch_bounds__(kFleetWarps * 32)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t i = blockIdx.x * kFleetWarps + warp;
   if (i >= n_inst) return;
-  int32_t* smem = fsm + warp * (smem_words(K) + S);
+  int32_t* smem = fsm + warp * (smem_words(K) + pow2_ceil(S));
   int32_t* len = smem + smem_words(K);
   const DevCfg cfg = cfgs[cfg_index];
   DevCfg live_cfg = cfg;
@@ -902,8 +906,12 @@ __global__ void __launch_bounds__(kFleetWarps * 32)
     sc.cfg = cfg_index;
     sc.reserved = 0;
     if constexpr (MC) {
-      for (int32_t j = lane; j < S; j += 32) len[j] = sorted_len[j];
-      __syncwarp();
+      if (P->sample) {
+        stage_mc_samples(len, est, P->request_id, S, P->seed, P->scale, nullptr);
+      } else {
+        for (int32_t j = lane; j < S; j += 32) len[j] = sorted_len[j];
+        __syncwarp();
+      }
       simulate_scenario<K, false, true, POW2, false, false, BSG_WIN_J_LATENCY>(cfg, ar.prompt, ar.est, ar.prefill, ar.decoded, sc,
                                                     smem, &res[i], TraceSink{nullptr, 0},
                                                     McArgs{len, S, nullptr, &scores[i], objective});
@@ -1165,7 +1173,7 @@ namespace {
 // Enqueues the fleet kernel on the context stream; inputs come from f->dparams.
 template <int K, bool POW2, bool MC>
 cudaError_t launch_fleet(bsg_fleet* f, int32_t S) {
-  const size_t sm = static_cast<size_t>(kFleetWarps) * (smem_words(K) + S) * 4;
+  const size_t sm = static_cast<size_t>(kFleetWarps) * (smem_words(K) + pow2_ceil(S)) * 4;
   if (sm > 48 * 1024)
     cudaFuncSetAttribute(fleet_dispatch_kernel<K, POW2, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sm));
@@ -1287,14 +1295,20 @@ extern "C" void bsg_fleet_destroy(bsg_fleet* f) {
   delete f;
 }
 
-extern "C" bsg_status bsg_fleet_dispatch(bsg_fleet* f, int64_t now_ticks, int32_t prompt, int32_t est,
-                                         int32_t output, const int32_t* lengths, int32_t n_samples,
-                                         int32_t objective, int32_t* chosen, int64_t* scores) {
+namespace {
+
+// One fleet dispatch: given sorted-on-host lengths (lengths != nullptr), device-
+// drawn samples (sample), or the estimate alone.
+bsg_status fleet_dispatch(bsg_fleet* f, int64_t now_ticks, int32_t prompt, int32_t est, int32_t output,
+                          const int32_t* lengths, bool sample, uint64_t request_id, uint64_t seed,
+                          double mean_abs_rel_error, int32_t n_samples, int32_t objective, int32_t* chosen,
+                          int64_t* scores) {
   if (!f || !chosen || now_ticks < 0 || objective < 0 || objective > 1) return BSG_INVALID_ARGUMENT;
   if (now_ticks < f->last_now) return BSG_INVALID_ARGUMENT;  // arrivals in time order
   if (prompt < 1 || prompt > (1 << 22) || est < 0 || est > (1 << 24) || output < 1 || output > (1 << 24))
     return BSG_BAD_INPUT;
-  const bool mc = lengths != nullptr;
+  if (sample && !(mean_abs_rel_error >= 0)) return BSG_INVALID_ARGUMENT;
+  const bool mc = lengths != nullptr || sample;
   if (mc && (n_samples < 1 || n_samples > 1024)) return BSG_INVALID_ARGUMENT;
   bsg_ctx* ctx = f->ctx;
   std::lock_guard<std::mutex> lock(ctx->mu);
@@ -1315,7 +1329,11 @@ extern "C" bsg_status bsg_fleet_dispatch(bsg_fleet* f, int64_t now_ticks, int32_
   P.S = S;
   P.objective = objective;
   P.drain = 0;
-  if (mc) {
+  P.sample = sample ? 1 : 0;
+  P.request_id = request_id;
+  P.seed = seed;
+  P.scale = mean_abs_rel_error * std::sqrt(3.14159265358979323846 / 2.0);
+  if (lengths) {
     std::memcpy(P.lens, lengths, S * 4);
     std::sort(P.lens, P.lens + S);  // the kernel walks the samples in ascending order
   }
@@ -1326,7 +1344,8 @@ extern "C" bsg_status bsg_fleet_dispatch(bsg_fleet* f, int64_t now_ticks, int32_
   if (no_graph) {
     e = enqueue_dispatch(f, S, mc);
   } else {
-    auto it = f->graphs.find(mc ? S : 0);
+    const int32_t gkey = mc ? (sample ? -S : S) : 0;  // the graph's H2D copies lens only when given
+    auto it = f->graphs.find(gkey);
     if (it == f->graphs.end()) {
       cudaGraph_t g = nullptr;
       cudaGraphExec_t x = nullptr;
@@ -1339,7 +1358,7 @@ extern "C" bsg_status bsg_fleet_dispatch(bsg_fleet* f, int64_t now_ticks, int32_
       if (e == cudaSuccess) e = cudaGraphInstantiate(&x, g, 0);
       if (g) cudaGraphDestroy(g);
       if (e != cudaSuccess) return bsg_cuda_fail(ctx, e, "fleet graph capture");
-      it = f->graphs.emplace(mc ? S : 0, x).first;
+      it = f->graphs.emplace(gkey, x).first;
     }
     e = cudaGraphLaunch(it->second, s);
   }
@@ -1355,6 +1374,23 @@ extern "C" bsg_status bsg_fleet_dispatch(bsg_fleet* f, int64_t now_ticks, int32_
     return static_cast<bsg_status>(hout[1]);
   }
   return BSG_OK;
+}
+
+}  // namespace
+
+extern "C" bsg_status bsg_fleet_dispatch(bsg_fleet* f, int64_t now_ticks, int32_t prompt, int32_t est,
+                                         int32_t output, const int32_t* lengths, int32_t n_samples,
+                                         int32_t objective, int32_t* chosen, int64_t* scores) {
+  return fleet_dispatch(f, now_ticks, prompt, est, output, lengths, false, 0, 0, 0.0, n_samples, objective,
+                        chosen, scores);
+}
+
+extern "C" bsg_status bsg_fleet_dispatch_sampled(bsg_fleet* f, int64_t now_ticks, int32_t prompt, int32_t est,
+                                                 int32_t output, uint64_t request_id, int32_t n_samples,
+                                                 uint64_t seed, double mean_abs_rel_error, int32_t objective,
+                                                 int32_t* chosen, int64_t* scores) {
+  return fleet_dispatch(f, now_ticks, prompt, est, output, nullptr, true, request_id, seed,
+                        mean_abs_rel_error, n_samples, objective, chosen, scores);
 }
 
 extern "C" bsg_status bsg_fleet_finish(bsg_fleet* f, bsg_request_outcome* outcomes, int32_t* n_requests,

@@ -79,6 +79,14 @@ def load() -> C.CDLL:
         "bsg_replay_trace": (C.c_int, [V, V, C.c_int64, V, V, V, V, V, C.POINTER(abi.TraceError)]),
         "bsg_fleet_snapshot": (C.c_int, [V, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                          V, V, V, V, C.c_int32]),
+        "bsg_dispatch_mc_sampled": (C.c_int, [V, E, C.c_int64, V, V, C.c_int32, C.c_int32, V,
+                                              C.c_int32, C.c_uint64, C.c_double, C.c_int32, V, V, V,
+                                              V, V]),
+        "bsg_last_launch": (C.c_char_p, [V]),
+        "bsg_fleet_dispatch_sampled": (C.c_int, [V, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                                                 C.c_uint64, C.c_int32, C.c_uint64, C.c_double,
+                                                 C.c_int32, V, V]),
+        "bsg_wire_check": (C.c_int32, [C.c_char_p, C.c_char_p, C.c_int64]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -133,6 +141,13 @@ def mc_lengths(est: int, request_id: int, n_samples: int = 256, seed: int = 1,
     if st != abi.OK:
         raise BsgError(st, "bsg_mc_lengths")
     return out
+
+
+def wire_check(body: str) -> tuple[int, str]:
+    """bsg_wire_check: (status, the reference role's error body or "")."""
+    buf = C.create_string_buffer(1 << 16)
+    st = load().bsg_wire_check(body.encode(), buf, len(buf))
+    return int(st), buf.value.decode()
 
 
 def format_double(v: float) -> str:
@@ -247,6 +262,17 @@ class Fleet:
                                            lp, ns, objective, C.byref(self._chosen),
                                            None if scores is None else _p(scores))
         self.ctx._check(st, "bsg_fleet_dispatch")
+        return self._chosen.value
+
+    def dispatch_sampled(self, now_ticks: int, prompt: int, est: int, output: int, request_id: int,
+                         n_samples: int = 256, seed: int = 1, mean_abs_rel_error: float = 0.244,
+                         objective: int = 0, scores: np.ndarray | None = None) -> int:
+        """Monte-Carlo dispatch with the samples drawn on the device (K3)."""
+        st = self.ctx.L.bsg_fleet_dispatch_sampled(self.h, int(now_ticks), int(prompt), int(est),
+                                                   int(output), int(request_id), n_samples, seed,
+                                                   mean_abs_rel_error, objective, C.byref(self._chosen),
+                                                   None if scores is None else _p(scores))
+        self.ctx._check(st, "bsg_fleet_dispatch_sampled")
         return self._chosen.value
 
     def snapshot(self, instance: int):
@@ -377,6 +403,29 @@ class Context:
                                            _p(chosen), _p(scores), _p(samples), _p(per)),
                     "bsg_dispatch_mc")
         return chosen, scores, samples, per
+
+    def dispatch_mc_sampled(self, ss: abi.ScenarioSet, instance_ids: np.ndarray, n_inst: int,
+                            request_ids, n_samples: int = 256, seed: int = 1,
+                            mean_abs_rel_error: float = 0.244, objective: int = 0,
+                            want_lengths: bool = False, dev_keys_ptr: int | None = None):
+        """bsg_dispatch_mc_sampled: Monte-Carlo dispatch with the length samples
+        drawn on the device (K3). Returns (chosen, scores, lengths or None)."""
+        n_req = len(ss) // n_inst
+        ids = np.ascontiguousarray(instance_ids, dtype=np.int32)
+        rid = np.ascontiguousarray(request_ids, dtype=np.uint64).reshape(n_req)
+        chosen = np.zeros(n_req, np.int32)
+        scores = np.zeros(len(ss), np.int64)
+        lens = np.zeros((n_req, n_samples), np.int32) if want_lengths else None
+        e = ss.entries()
+        self._check(self.L.bsg_dispatch_mc_sampled(
+            self.h, C.byref(e), ss.n_entries, _p(ss.scenarios), _p(ids), n_inst, n_req, _p(rid),
+            n_samples, seed, mean_abs_rel_error, objective, _p(chosen), _p(scores), _p(lens), None,
+            C.c_void_p(dev_keys_ptr) if dev_keys_ptr else None), "bsg_dispatch_mc_sampled")
+        return chosen, scores, lens
+
+    @property
+    def last_launch(self) -> str:
+        return self.L.bsg_last_launch(self.h).decode()
 
     def capacity_search(self, w, cfg, spec, seed: int, qps_min: int, qps_max: int, slo: float):
         """capacity_search over GPU closed loops. Returns (status, result, [(qps, passed)])."""

@@ -47,7 +47,44 @@ PACK_BITS = 16                            # instance id field of the packed key
 PACK_SAT = (1 << (63 - PACK_BITS)) - 1    # largest score the packed key holds exactly
 
 
-def global_argmin(scores: np.ndarray, ids: np.ndarray, device=None, group=None) -> int:
+def group_range(n_groups: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous arrival groups [g0, g1) of ``rank`` in strong scaling (all
+    what-ifs of one arrival stay on one GPU, so its argmin is local)."""
+    return n_groups * rank // world, n_groups * (rank + 1) // world
+
+
+def pack_key(score: int, inst: int, failed: bool = False) -> int:
+    """The packed argmin key: min(score, 2^47 - 1) << 16 | id; -1 = failed
+    (an empty shard packs (INT64_MAX, 0xffff), which loses to any real key)."""
+    if failed:
+        return -1
+    if score == INT64_MAX:
+        return (PACK_SAT << PACK_BITS) | ((1 << PACK_BITS) - 1)
+    return (min(score, PACK_SAT) << PACK_BITS) | inst
+
+
+def reduce_key(key, scores: np.ndarray, ids: np.ndarray, device=None, group=None) -> int:
+    """Cross-rank argmin from the per-rank packed key the dispatch kernel left
+    in device memory (bsg_dispatch_mc_sampled dev_keys): ONE all_reduce MIN
+    over NCCL on the device tensor, then one 8-byte read. Returns -1 on every
+    rank when any rank's shard failed (key -1 wins the MIN), and falls back to
+    the exact two-pass reduce (with this rank's host scores) only when the
+    winning score saturated the 47-bit field."""
+    import torch
+    import torch.distributed as dist
+    t = key if device is not None else key.cpu()  # gloo (one-GPU test mode) reduces host tensors
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    k = int(t.item())
+    if k < 0:
+        return -1
+    if (k >> PACK_BITS) < PACK_SAT:
+        return k & ((1 << PACK_BITS) - 1)
+    s, i = local_best(scores, ids)
+    return _global_argmin_two_pass(s, i, device, group)
+
+
+def global_argmin(scores: np.ndarray, ids: np.ndarray, device=None, group=None,
+                  failed: bool = False) -> int:
     """Exact cross-rank argmin with lowest-id ties (scheduler.cpp:138-150).
 
     One collective in the common case: all_reduce MIN of the packed
@@ -58,14 +95,17 @@ def global_argmin(scores: np.ndarray, ids: np.ndarray, device=None, group=None) 
     the score, then MIN of the ids attaining it)."""
     import torch
     import torch.distributed as dist
-    if len(ids) and int(np.max(ids)) >= (1 << PACK_BITS) - 1:
-        raise ValueError("instance ids must be < 65535")  # every rank decides the same way
+    # A local problem (this rank's prediction failed, or an id the key cannot
+    # hold) must not raise before the collective — the other ranks would block
+    # in all_reduce. It packs key -1, so the reduced key fails on EVERY rank.
+    bad_ids = bool(len(ids)) and (int(np.max(ids)) >= (1 << PACK_BITS) - 1 or int(np.min(ids)) < 0)
     s, i = local_best(scores, ids)
-    key = (min(s, PACK_SAT) << PACK_BITS) | (i if s != INT64_MAX else (1 << PACK_BITS) - 1)
-    t = torch.tensor([key], dtype=torch.int64, device=device)
+    t = torch.tensor([pack_key(s, i, failed or bad_ids)], dtype=torch.int64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
     k = int(t.item())
-    if (k >> PACK_BITS) < PACK_SAT:  # the same reduced value on every rank: a uniform branch
+    if k < 0:  # the same reduced value on every rank: uniform branches
+        return -1
+    if (k >> PACK_BITS) < PACK_SAT:
         return k & ((1 << PACK_BITS) - 1)
     return _global_argmin_two_pass(s, i, device, group)
 

@@ -159,3 +159,65 @@ def test_wire_number_text_matches_reference_json(lib, ref):
             continue
         assert native.format_double(v) == ref.dump_double(v), repr(v)
         assert float(native.format_double(v)) == v  # round trip
+
+
+def _mutations(base):
+    """Request bodies that fail before simulation, one defect each."""
+    import copy
+    import json
+    out = ["{not json", "", "[]", "3", "null", json.dumps({"snapshot": 1})]
+    paths = [("snapshot",), ("candidate",), ("instance_config",), ("snapshot", "running"),
+             ("snapshot", "qpm"), ("snapshot", "snapshot_time"), ("candidate", "prompt_tokens"),
+             ("instance_config", "cost_model"), ("instance_config", "cost_model", "c0_s"),
+             ("instance_config", "local_policy"), ("instance_config", "total_blocks")]
+    for path in paths:
+        for val in (None, "x", True, [1], {"a": 1}, 1.5, -3, "DELETE"):
+            d = copy.deepcopy(base)
+            o = d
+            for k in path[:-1]:
+                o = o[k]
+            if val == "DELETE":
+                del o[path[-1]]
+            else:
+                o[path[-1]] = val
+            out.append(json.dumps(d))
+    for field, val in [("total_blocks", 0), ("block_size", 0), ("max_batch_size", 0), ("chunk_budget", 1),
+                       ("local_policy", "round_robin")]:
+        d = copy.deepcopy(base)
+        d["instance_config"][field] = val
+        out.append(json.dumps(d))
+    for field, val in [("c0_s", 0.0), ("prefill_s_per_token", -1.0), ("decode_s_per_seq", -1e-9),
+                       ("context_s_per_token", -2.0)]:
+        d = copy.deepcopy(base)
+        d["instance_config"]["cost_model"][field] = val
+        out.append(json.dumps(d))
+    # running given as an object / a string / null: nlohmann's range-for semantics
+    entry = base["snapshot"]["running"][0] if base["snapshot"]["running"] else None
+    for val in ({"b": entry, "a": entry}, "str", None, [entry, 5]):
+        d = copy.deepcopy(base)
+        d["snapshot"]["running"] = val
+        out.append(json.dumps(d))
+    return out
+
+
+def test_wire_check_error_bodies_match_reference(lib, ref):
+    """/predict requests rejected before simulation (schema, types, config
+    validation): bsg_wire_check answers the reference role's status class and
+    the byte-identical error body (nlohmann's exception text; ConfigError's
+    "invalid config: <field>: <rule>"); accepted bodies are accepted by both."""
+    import json
+    from paper_2508_03611_b200 import native
+    from scenarios import kat_set
+    names, kc, ks = kat_set()
+    base = json.loads(ref.request_json(kc, ks, 1))
+    assert base["snapshot"]["running"], "need a running entry to mutate"
+    n_err = 0
+    for body in _mutations(base):
+        code, exp = ref.service_predict(body)
+        st, got = native.wire_check(body)
+        if code == 400:
+            assert st != 0 and got == exp, (body, got, exp)
+            n_err += 1
+        else:  # simulated by the reference (200 / 422): simulated here too
+            assert st == 0, (body, code, exp, got)
+    assert n_err > 60

@@ -43,6 +43,18 @@ def _worker(rank, world, port, q):
                 scores = rng.integers(1 << 47, 1 << 48, n_inst).astype(np.int64) // 3 * 3  # ties, all saturated
             mine = shard.instance_shard(n_inst, world, rank)
             out[case] = (shard.global_argmin(scores[mine], mine), int(np.argmin(scores)))
+        # a failure (or an id the packed key cannot hold) on ONE rank: no hang,
+        # and every rank sees the failed decision (shard.py:61)
+        out["fail"] = (shard.global_argmin(np.array([5, 6]), np.array([rank, 2 + rank]),
+                                           failed=(rank == 1)), -1)
+        out["bad_id"] = (shard.global_argmin(np.array([5]), np.array([70000 if rank == 0 else 1])), -1)
+        # the device-key path (bench cfg4 multi-GPU): per-rank packed keys -> one MIN
+        import torch
+        for case, (keys, exp) in enumerate([((shard.pack_key(9, 3), shard.pack_key(4, 8)), 8),
+                                            ((shard.pack_key(4, 5), shard.pack_key(4, 2)), 2),
+                                            ((shard.pack_key(4, 5), -1), -1)]):
+            t = torch.tensor([keys[rank]], dtype=torch.int64)
+            out[f"key{case}"] = (shard.reduce_key(t, np.array([0]), np.array([0])), exp)
         maxes, sums = shard.reduce_max_sum([1.5 + rank, 10.0 * rank], [100 + rank, 7])
         q.put((rank, out, maxes, sums))
     finally:
@@ -84,3 +96,27 @@ def test_lpt_assignment_balanced_and_deterministic():
     assert sorted(sum(a, [])) == list(range(300))
     loads = [costs[x].sum() for x in a]
     assert max(loads) <= (sum(loads) / 8) * 1.05 + costs.max()
+
+
+def test_strong_scaling_groups_partition():
+    from paper_2508_03611_b200 import shard
+    for g in (1, 5, 4999, 5000):
+        for w in (1, 2, 3, 8):
+            rs = [shard.group_range(g, w, r) for r in range(w)]
+            assert rs[0][0] == 0 and rs[-1][1] == g
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+            assert max(b - a for a, b in rs) - min(b - a for a, b in rs) <= 1
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """`bench.py --gpus 2` outside torchrun launches 2 ranks itself (rendezvous
+    on 127.0.0.1); --dist-probe runs only the rank plumbing (gloo, no GPU)."""
+    import json
+    import subprocess
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dist-probe"],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert lines == [{"probe": "dist", "world": 2, "rank_sum": 1, "ranks": 2}]

@@ -160,3 +160,25 @@ def test_reference_shim_replay_equals_run_experiment(ref):
     b, pb = ref.run_experiment(w, cfg, spec)
     assert np.array_equal(a, b) and pa["total_preemptions"] == pb["total_preemptions"]
     assert len(ss) == 4 * 600
+
+
+def test_reference_sweep_equals_capacity_search(ref):
+    """ref_sweep (the all-core cfg5 baseline, parallel over (cell, qps) points)
+    gives every cell exactly the reference's own capacity_search result
+    (metrics.cpp:139-178): same bracket, capacity, monotone flag, tests."""
+    import numpy as np
+    from paper_2508_03611_b200 import abi, sweep
+    cells, _ = sweep.make_cells([1, 3], sweep.load_profiles(), request_cap=120, qps_max=10, slo=1.0)
+    cells["qps_min"][0] = 6  # a cell with no capacity at its lowest qps
+    got, secs = ref.sweep(cells, threads=8)
+    assert secs > 0
+    for c, o in zip(cells, got):
+        w = np.array([c["workload"]], abi.workload_dtype)
+        st, exp, tested = ref.capacity_search(w, np.array([c["cfg"]], abi.cfg_dtype),
+                                              np.array([c["spec"]], abi.replay_spec_dtype),
+                                              int(c["seed"]), int(c["qps_min"]), int(c["qps_max"]),
+                                              float(c["slo_p99_ttft_s"]))
+        assert int(o["status"]) == st
+        if st == abi.OK:
+            assert o["result"].tolist() == exp.tolist()
+    assert (got["status"] == abi.NO_CAPACITY).any() and (got["status"] == abi.OK).any()
