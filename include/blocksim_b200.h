@@ -269,6 +269,44 @@ bsg_status bsg_dispatch_mc_sampled(bsg_ctx* ctx, const bsg_entries* entries, int
  * call launched (template arguments included), for measurement records. */
 const char* bsg_last_launch(const bsg_ctx* ctx);
 
+/* ---- several GPUs in one process ---------------------------
+ * One context per device, one persistent host worker thread per context: the
+ * devices' copies and kernels run concurrently. No data-path collective —
+ * scenarios are independent; the only exchange is the per-request argmin,
+ * which stays on one device when requests are split and is merged exactly on
+ * the host (lowest id on ties, scheduler.cpp:138-150) when one request's
+ * instances are split. A device may appear more than once (several contexts
+ * on one GPU). This is what a PredictorClient fanning out over a box's GPUs
+ * binds (the reference's predictor replicas, service.cpp:218-246, and its
+ * concurrent sweep cells, driver.cpp:375-388). HOST buffers throughout. */
+typedef struct bsg_multi bsg_multi;
+bsg_status bsg_multi_create(const int* devices, int32_t n_devices, bsg_multi** out);
+void bsg_multi_destroy(bsg_multi* m);
+int32_t bsg_multi_device_count(const bsg_multi* m);
+const char* bsg_multi_last_error(const bsg_multi* m);
+int64_t bsg_multi_launch_count(const bsg_multi* m);
+/* bsg_set_configs on every device. */
+bsg_status bsg_multi_set_configs(bsg_multi* m, const bsg_instance_cfg* cfgs, int32_t n,
+                                 int32_t* bad_index, int32_t* field_code);
+/* bsg_predict_batch with the batch split into contiguous ranges of whole
+ * `group`s (e.g. group = instances per arrival) across the devices. */
+bsg_status bsg_multi_predict_batch(bsg_multi* m, const bsg_entries* entries, int64_t n_entries,
+                                   const bsg_scenario* scenarios, int64_t n, int32_t group,
+                                   bsg_result* out);
+/* bsg_dispatch with the requests split across the devices. */
+bsg_status bsg_multi_dispatch(bsg_multi* m, const bsg_entries* entries, int64_t n_entries,
+                              const bsg_scenario* scenarios, const int32_t* instance_ids,
+                              int32_t n_inst, int32_t n_requests, int32_t objective,
+                              int32_t* chosen, bsg_result* per_instance);
+/* ONE Monte-Carlo dispatch (bsg_dispatch_mc_sampled semantics, one request)
+ * with its instances split i % n_devices; per-device (score, id) minima
+ * merged on the host. scores (optional) in instance order. */
+bsg_status bsg_multi_dispatch_mc_sampled(bsg_multi* m, const bsg_entries* entries, int64_t n_entries,
+                                         const bsg_scenario* scenarios, const int32_t* instance_ids,
+                                         int32_t n_inst, uint64_t request_id, int32_t n_samples,
+                                         uint64_t seed, double mean_abs_rel_error, int32_t objective,
+                                         int32_t* chosen, int64_t* scores);
+
 /* ---- closed-loop replay (the scenario source; driver.cpp:134-289) -------- */
 
 /* Synthetic ShareGPT-shaped workload: make_synthetic_trace (workload.cpp:172-191,

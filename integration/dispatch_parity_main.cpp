@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "blocksim/backend.h"
+#include "blocksim/predictor.h"
 #include "blocksim/error.h"
 #include "blocksim/scheduler.h"
 #include "blocksim/workload.h"
@@ -185,6 +186,67 @@ int main() {
         if (in.has_work()) in.execute_step();
     }
     check(compared > 50, "replay compared enough arrivals");
+  }
+
+  // the same fixtures through a client fanning out over several contexts
+  // (bsg_multi_*; two contexts on device 0 here: the splitting is under test)
+  {
+    GpuPredictorClient multi(cfg, std::vector<int>{0, 0});
+    for (std::size_t i = 0; i < fixtures.size(); ++i)
+      compare(multi, local, fixtures[i], {300, 80}, "multi_c11_fixture_" + std::to_string(i));
+    compare(multi, local, {snapshot_with(0, {}, {})}, {16000, 2000}, "multi_too_large_candidate");
+  }
+
+  // direct predict() callers (driver.cpp:204-208 preempt provisioning, service.cpp:232):
+  // GpuPredictorClient::predict vs the reference predict(), per request config,
+  // results and exception messages identical
+  {
+    auto direct = [&](const PredictionRequest& req, const std::string& name) {
+      std::string eg, el, tg, tl;
+      PredictionResult rg, rl;
+      auto run = [&](const std::function<PredictionResult()>& f, PredictionResult& r, std::string& e,
+                     std::string& t) {
+        try {
+          r = f();
+        } catch (const PredictionError& x) {
+          t = "PredictionError";
+          e = x.what();
+        } catch (const EmptyPlanError& x) {
+          t = "EmptyPlanError";
+          e = x.what();
+        } catch (const ConfigError& x) {
+          t = "ConfigError";
+          e = x.what();
+        }
+      };
+      run([&] { return gpu.predict(req); }, rg, eg, tg);
+      run([&] { return predict(req, &cache); }, rl, el, tl);
+      check(tg == tl && eg == el, name + ": exception " + tg + " '" + eg + "' vs " + tl + " '" + el + "'");
+      check(rg.metrics == rl.metrics && rg.simulated_steps == rl.simulated_steps, name + ": prediction differs");
+    };
+    int k = 0;
+    for (const auto& fx : fixtures)
+      for (const auto& snap : fx) {
+        PredictionRequest req;
+        req.snapshot = snap;
+        req.candidate = {300, 80};
+        req.instance_config = cfg;
+        direct(req, "direct_" + std::to_string(k));
+        req.instance_config.total_blocks = 700 + 37 * k;  // a different config per request
+        req.instance_config.max_batch_size = 24 + k;
+        req.instance_config.local_policy = k % 2 ? LocalPolicy::kPrefillPriority : LocalPolicy::kChunkedPrefill;
+        direct(req, "direct_cfg_" + std::to_string(k));
+        ++k;
+      }
+    PredictionRequest bad;
+    bad.snapshot = snapshot_with(0, {}, {});
+    bad.candidate = {10, 10};
+    bad.instance_config = cfg;
+    bad.instance_config.chunk_budget = 8;  // < block_size: ConfigError
+    direct(bad, "direct_config_error");
+    bad.instance_config = cfg;
+    bad.candidate = {16000, 2000};
+    direct(bad, "direct_too_large");
   }
 
   // predictor unavailable -> the Dispatcher's own Llumnix- fallback

@@ -87,6 +87,16 @@ def load() -> C.CDLL:
                                                  C.c_uint64, C.c_int32, C.c_uint64, C.c_double,
                                                  C.c_int32, V, V]),
         "bsg_wire_check": (C.c_int32, [C.c_char_p, C.c_char_p, C.c_int64]),
+        "bsg_multi_create": (C.c_int, [V, C.c_int32, C.POINTER(C.c_void_p)]),
+        "bsg_multi_destroy": (None, [V]),
+        "bsg_multi_device_count": (C.c_int32, [V]),
+        "bsg_multi_last_error": (C.c_char_p, [V]),
+        "bsg_multi_launch_count": (C.c_int64, [V]),
+        "bsg_multi_set_configs": (C.c_int, [V, V, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+        "bsg_multi_predict_batch": (C.c_int, [V, E, C.c_int64, V, C.c_int64, C.c_int32, V]),
+        "bsg_multi_dispatch": (C.c_int, [V, E, C.c_int64, V, V, C.c_int32, C.c_int32, C.c_int32, V, V]),
+        "bsg_multi_dispatch_mc_sampled": (C.c_int, [V, E, C.c_int64, V, V, C.c_int32, C.c_uint64,
+                                                    C.c_int32, C.c_uint64, C.c_double, C.c_int32, V, V]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -305,6 +315,77 @@ class Fleet:
             self.close()
         except Exception:
             pass
+
+
+class MultiContext:
+    """Several GPUs in one process (bsg_multi_*): one context + host worker
+    thread per device; batches split by arrival group, dispatches by request,
+    one Monte-Carlo dispatch by instance (exact host argmin merge)."""
+
+    def __init__(self, devices):
+        self.L = load()
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        st = self.L.bsg_multi_create(devs, len(devices), C.byref(h))
+        if st != abi.OK:
+            raise BsgError(st, "bsg_multi_create", "(CUDA devices are required)")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.bsg_multi_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st, where):
+        if st != abi.OK:
+            raise BsgError(st, where, self.L.bsg_multi_last_error(self.h).decode())
+
+    @property
+    def launches(self) -> int:
+        return int(self.L.bsg_multi_launch_count(self.h))
+
+    def set_configs(self, cfgs: np.ndarray):
+        cfgs = np.ascontiguousarray(cfgs, dtype=abi.cfg_dtype)
+        bi, fc = C.c_int32(-1), C.c_int32(0)
+        self._check(self.L.bsg_multi_set_configs(self.h, _p(cfgs), len(cfgs), C.byref(bi), C.byref(fc)),
+                    "bsg_multi_set_configs")
+
+    def predict_batch(self, ss: abi.ScenarioSet, group: int = 1) -> np.ndarray:
+        out = np.zeros(len(ss), abi.result_dtype)
+        e = ss.entries()
+        self._check(self.L.bsg_multi_predict_batch(self.h, C.byref(e), ss.n_entries, _p(ss.scenarios),
+                                                   len(ss), group, _p(out)), "bsg_multi_predict_batch")
+        return out
+
+    def dispatch(self, ss: abi.ScenarioSet, instance_ids: np.ndarray, n_inst: int, objective: int = 0):
+        n_req = len(ss) // n_inst
+        ids = np.ascontiguousarray(instance_ids, dtype=np.int32)
+        chosen = np.zeros(n_req, np.int32)
+        per = np.zeros(len(ss), abi.result_dtype)
+        e = ss.entries()
+        self._check(self.L.bsg_multi_dispatch(self.h, C.byref(e), ss.n_entries, _p(ss.scenarios), _p(ids),
+                                              n_inst, n_req, objective, _p(chosen), _p(per)),
+                    "bsg_multi_dispatch")
+        return chosen, per
+
+    def dispatch_mc_sampled(self, ss: abi.ScenarioSet, instance_ids: np.ndarray, request_id: int,
+                            n_samples: int = 256, seed: int = 1, mean_abs_rel_error: float = 0.244,
+                            objective: int = 0):
+        ids = np.ascontiguousarray(instance_ids, dtype=np.int32)
+        chosen = C.c_int32(-1)
+        scores = np.zeros(len(ss), np.int64)
+        e = ss.entries()
+        self._check(self.L.bsg_multi_dispatch_mc_sampled(
+            self.h, C.byref(e), ss.n_entries, _p(ss.scenarios), _p(ids), len(ss), int(request_id),
+            n_samples, seed, mean_abs_rel_error, objective, C.byref(chosen), _p(scores)),
+            "bsg_multi_dispatch_mc_sampled")
+        return chosen.value, scores
 
 
 class Context:

@@ -51,6 +51,8 @@ def test_no_cpu_fallback_without_device(lib):
     assert lib.bsg_ctx_create(0, C.byref(h)) == abi.CUDA_ERROR
     with pytest.raises(native.BsgError):
         native.Context(0)
+    with pytest.raises(native.BsgError):
+        native.MultiContext([0, 0])
 
 
 @pytest.mark.parametrize("kw", [

@@ -197,3 +197,31 @@ def test_fleet_device_sampling_equals_host_lengths(ctx):
     assert oa.tobytes() == ob.tobytes()
     fa.close()
     fb.close()
+
+
+def test_multi_device_fanout_equals_one_device(ctx):
+    """bsg_multi_* (one context + worker thread per device; here 3 contexts on
+    cuda:0, the host-side splitting and merging is what is under test): batch
+    results, per-request decisions and the instance-split Monte-Carlo argmin
+    equal the single-context calls bit for bit."""
+    cfg, ss = captured(ctx, "cfg2")
+    ctx.set_configs(cfg)
+    one = ctx.predict_batch(ss)
+    m = native.MultiContext([0, 0, 0])
+    m.set_configs(cfg)
+    assert m.predict_batch(ss, group=12).tobytes() == one.tobytes()
+    sub = abi.ScenarioSet(ss.prompt, ss.est, ss.prefill, ss.decoded, ss.scenarios[:12 * 500])
+    ids = np.tile(np.arange(12, dtype=np.int32), 500)
+    c1, p1 = ctx.dispatch(sub, ids, 12)
+    c2, p2 = m.dispatch(sub, ids, 12)
+    assert np.array_equal(c1, c2) and p1.tobytes() == p2.tobytes()
+    w = abi.make_workload(count=600, qps=130.0, arrival_seed=1)
+    _, _, cap = ctx.replay(w, cfg, abi.make_replay_spec(64))
+    ctx.set_configs(cfg)
+    for g in (50, 300, 599):
+        one = cap.compact(g * 64 + np.arange(64))
+        ch, sc, _ = ctx.dispatch_mc_sampled(one, np.arange(64, dtype=np.int32), 64, [g], 256, seed=1)
+        mc, msc = m.dispatch_mc_sampled(one, np.arange(64, dtype=np.int32), g, 256, seed=1)
+        assert mc == int(ch[0]) and np.array_equal(msc, sc), g
+    assert m.launches > 0
+    m.close()
