@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(256) heavy_threshold_kernel(const bsg_scenario
 // cfg2: spills 172/356 B -> 74/84 B, 222 -> 247 M scenarios/s). Sets that mix
 // configs run one pass per config in use; the other scenarios' warps exit at
 // once. Returns false when this pass does not own the scenario.
-template <int K, bool POW2, bool OPT, int WJ>
+template <int K, bool POW2, bool OPT, int WJ, bool CYC>
 __device__ __forceinline__ bool predict_one(const DevCfg& cfg, int32_t cfg_sel, int32_t ncfg,
                                             const int32_t* __restrict__ prompt,
                                             const int32_t* __restrict__ est,
@@ -202,8 +202,8 @@ __device__ __forceinline__ bool predict_one(const DevCfg& cfg, int32_t cfg_sel, 
   // than it saves): 128-step windows for 32-member sets, 32-step windows for
   // wide / KV-pressure sets, where admissions and preemptions cut windows short
   // (measured: cfg3 8.1 ms at J=1 vs 9.6 ms at J=4; cfg1 prefers J=4, 238 vs 310 us).
-  simulate_scenario<K, false, false, POW2, true, OPT, WJ>(cfg, prompt, est, prefill, decoded, sc, smem, o,
-                                                         TraceSink{nullptr, 0});
+  simulate_scenario<K, false, false, POW2, true, OPT, WJ, CYC>(cfg, prompt, est, prefill, decoded, sc, smem, o,
+                                                              TraceSink{nullptr, 0});
   return true;
 }
 
@@ -242,7 +242,9 @@ __global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K, OPT))
     return;
   }
   const bsg_scenario sc = scen[w];
-  const bool ran = predict_one<K, POW2, OPT, WJ>(cfg, cfg_sel, ncfg, prompt, est, prefill, decoded, sc,
+  // admit / self-preempt cycle absorption (scenario_sim.cuh) only where queues
+  // are deep (KV-pressure / wide sets): it costs the 32-member kernel registers
+  const bool ran = predict_one<K, POW2, OPT, WJ, (OPT || K >= 2)>(cfg, cfg_sel, ncfg, prompt, est, prefill, decoded, sc,
                                                   smem, out + w);
   if constexpr (OPT) {  // too wide for this pass: list it for the wide kernel
     __syncwarp();
@@ -268,12 +270,12 @@ __global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K))
        j += static_cast<int64_t>(gridDim.x) * kPredictWarps) {
     const int64_t w = __ldcg(&rl[j]);
     const bsg_scenario sc = scen[w];
-    predict_one<K, POW2, false, BSG_WIN_J_WIDE>(cfg, cfg_sel, ncfg, prompt, est, prefill, decoded, sc, smem,
+    predict_one<K, POW2, false, BSG_WIN_J_WIDE, true>(cfg, cfg_sel, ncfg, prompt, est, prefill, decoded, sc, smem,
                                                 out + w);
   }
 }
 
-template <int K, bool POW2, int WJ>
+template <int K, bool POW2, int WJ, bool CYC>
 __global__ void __launch_bounds__(32)
     trace_kernel(const DevCfg* __restrict__ cfgs, const int32_t* __restrict__ prompt,
                  const int32_t* __restrict__ est, const int32_t* __restrict__ prefill,
@@ -282,8 +284,8 @@ __global__ void __launch_bounds__(32)
   __shared__ int32_t smem[smem_words(K)];
   const bsg_scenario sc = scen[0];
   const DevCfg cfg = cfgs[sc.cfg];
-  simulate_scenario<K, true, false, POW2, true, false, WJ>(cfg, prompt, est, prefill, decoded, sc, smem, out,
-                                         TraceSink{rec, cap});
+  simulate_scenario<K, true, false, POW2, true, false, WJ, CYC>(cfg, prompt, est, prefill, decoded, sc, smem,
+                                                              out, TraceSink{rec, cap});
 }
 
 // BlockPredictive argmin (scheduler.cpp:138-150): one warp per request, value
@@ -936,14 +938,21 @@ bsg_status bsg_trace(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries
   // 4 (32-member sets, latency path); BSG_TRACE_J picks which per-step trace to emit
   const char* tj = std::getenv("BSG_TRACE_J");
   const int wj = tj ? std::atoi(tj) : 1;
+  // BSG_TRACE_CYC=0 traces the windows without admit/self-preempt cycle absorption
+  // (the 32-member throughput kernels); default: with it (every other kernel)
+  const char* tc = std::getenv("BSG_TRACE_CYC");
+  const bool cyc = tc ? std::atoi(tc) != 0 : true;
+#define BSG_TRACE_LAUNCH_C(KK, P2, WW)                                                           \
+  {                                                                                              \
+    if (cyc) trace_kernel<KK, P2, WW, true><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap); \
+    else trace_kernel<KK, P2, WW, false><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap); \
+  }
 #define BSG_TRACE_LAUNCH(KK)                                                                     \
   {                                                                                              \
     if (wj == 4) {                                                                               \
-      if (ctx->all_pow2) trace_kernel<KK, true, 4><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap); \
-      else trace_kernel<KK, false, 4><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap); \
+      if (ctx->all_pow2) BSG_TRACE_LAUNCH_C(KK, true, 4) else BSG_TRACE_LAUNCH_C(KK, false, 4)   \
     } else {                                                                                     \
-      if (ctx->all_pow2) trace_kernel<KK, true, 1><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap); \
-      else trace_kernel<KK, false, 1><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap); \
+      if (ctx->all_pow2) BSG_TRACE_LAUNCH_C(KK, true, 1) else BSG_TRACE_LAUNCH_C(KK, false, 1)   \
     }                                                                                            \
   }
   switch (k) {
@@ -954,6 +963,7 @@ bsg_status bsg_trace(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries
     default: ctx->last_error = "member capacity beyond 256"; return BSG_BAD_INPUT;
   }
 #undef BSG_TRACE_LAUNCH
+#undef BSG_TRACE_LAUNCH_C
   ctx->launches += 1;
   BSG_CUDA(ctx, cudaGetLastError());
   BSG_CUDA(ctx, cudaMemcpyAsync(out, res, sizeof(bsg_result), cudaMemcpyDeviceToHost, ctx->stream));

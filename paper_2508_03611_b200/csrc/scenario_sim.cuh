@@ -259,7 +259,7 @@ __device__ __forceinline__ int32_t ld_entry(const int32_t* p) {
 constexpr int32_t kStatusRetryWider = 100;
 
 template <int K, bool TRACE, bool MC = false, bool POW2 = false, bool LDG = true, bool OPT = false,
-          int WJ = 1>
+          int WJ = 1, bool CYC = true>
 __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__ g_prompt,
                                   const int32_t* __restrict__ g_est,
                                   const int32_t* __restrict__ g_prefill,
@@ -443,6 +443,11 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
     // ---------------- waiting admissions ----------------
     int32_t a = 0;  // admitted waiting heads
     int32_t run_delta = 0;
+    // this step admits a preemption victim's first chunk (< its prompt) and
+    // nothing else: the first step of an admit / self-preempt cycle the window
+    // below may absorb
+    bool cyc0 = false;
+    int32_t cyc_hp = 0;  // its prompt
     bool try_admit = waiting_nonempty && n < maxb && (chunked ? budget > 0 : true);
     if (try_admit) {
       running_deltas();
@@ -466,6 +471,8 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
         // admit exactly the head without materialising the queue.
         try_admit = false;
         a = 1;
+        cyc0 = CYC && L > n && hp > budget;
+        cyc_hp = hp;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           const int32_t p = lane * K + k;
@@ -599,7 +606,49 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
     static_assert(WJ >= 1 && WJ <= kMaxWinJ, "window width");
     int64_t win_pre[WJ];
     int64_t win_base = 0;
-    if (a == 0 && D == n && n > 0 && !prefill_step) {
+    bool win = (a == 0 || cyc0) && D == n && n > 0 && !prefill_step;
+    if constexpr (CYC) {
+      // Exact pre-checks of the window's first steps, so that a window which
+      // would retire nothing is never set up (KV-pressure sets otherwise pay a
+      // window per general step): a plain window stops at step 0 iff its decode
+      // demand needs a victim; a cycle window is cut before its A step iff the
+      // B step after it would not evict exactly the head (same tests as below).
+      if (win) {
+        bool d0[K], c0[K], d1[K];
+        int32_t fr0[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const bool alive = lane * K + k < n;
+          d0[k] = alive && modt<POW2>(stored[k], cfg) == 0;
+          c0[k] = alive && target[k] - decoded[k] == 1;
+          d1[k] = alive && !c0[k] && modt<POW2>(stored[k] + 1, cfg) == 0;
+          fr0[k] = c0[k] ? bnt<POW2>(stored[k] + 1, cfg) : 0;
+        }
+        const int32_t dem0 = count<K>(d0);
+        if (!cyc0) {
+          win = dem0 <= free_blocks;
+        } else {
+          const int32_t nc0 = count<K>(c0);
+          const int32_t D1 = n - nc0;
+          const int32_t A1 = free_blocks - dem0 + (nc0 > 0 ? warp_sum<K>(fr0) : 0);
+          const int32_t dem1 = count<K>(d1);
+          const int32_t cA = cfg.chunk_budget - n;
+          const int32_t hA = bnt<POW2>(cA, cfg);
+          const int32_t bud1 = cfg.chunk_budget - D1;
+          const int32_t rem = cyc_hp - cA;
+          const int32_t ch = rem < bud1 ? rem : bud1;
+          const int32_t dB = bnt<POW2>(cA + ch + (ch == rem ? 1 : 0), cfg) - hA;
+          win = !(D1 == 0 || bud1 <= 0 || dem1 + dB <= A1 - hA || dem1 > A1);
+        }
+      }
+    }
+#ifdef BSG_PROFILE_T0
+    bool prof_entered = false;
+#endif
+    if (win) {
+#ifdef BSG_PROFILE_T0
+      prof_entered = true;
+#endif
 #ifdef BSG_PROFILE_WENTRY
       ++prof_pre;  // debug: window entries (reported in the preempt counter's slot)
 #endif
@@ -734,28 +783,111 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
         else if (h < wait_n) hp = ld_entry<LDG>(g_prompt + sc.wait_off + h);
         else hp = sc.cand_prompt;
       }
-      int32_t Dt[J], Ct[J];
+      // Admit / self-preempt cycles (chunked prefill under KV pressure). When
+      // the waiting head is a preemption victim (prefill = decoded = 0) whose
+      // first chunk c = budget < prompt fits, step A admits it with that chunk
+      // (the budget is then exhausted: a single admission, backend.cpp:135-147);
+      // in the next step B its remaining chunk does not fit, so the newest
+      // member — the head itself — is evicted (263-288) and returns to the
+      // waiting front exactly as before A. The pair leaves free blocks as two
+      // pure-decode steps would (A takes bn(c), B refunds it), so A(t) below
+      // stays exact on every non-B step. A step is A iff the head fits, is such
+      // a victim, and the previous step was not A: in a run of consecutive
+      // fitting steps starting at s, steps s, s+2, ... are A (a max-scan of run
+      // starts). B must evict the head and nothing else, else the window ends
+      // before its A. Repeats until the head misfits, a member completes and
+      // budgets change, or decode demand needs a victim.
+      const bool cyc_head = CYC && chunked && L > n;
+      int32_t Dt[J], Ct[J], At[J], bud[J];
+      bool fits[J], fa[J];
+      int32_t rs_lane = -1;  // lane-local inclusive max of cycle-run starts
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const int32_t t = t0 + j;
+        Dt[j] = n - cnt_x[j];                          // alive in step t
+        Ct[j] = (s_tot - sst_x[j]) + t * Dt[j];        // context of step t
+        At[j] = free_blocks - dem_x[j] + frd_x[j];     // free before step t (no A at t-1)
+        bud[j] = cfg.chunk_budget - Dt[j];
+        // would the waiting head be admitted at step t? (backend.cpp:132-148 / 158-175)
+        bool f = false;
+        if (t == 0) {
+          f = a > 0;
+        } else if (waiting_nonempty && Dt[j] > 0) {
+          if (chunked) {
+            const int32_t c = hp < bud[j] ? hp : bud[j];
+            f = bud[j] > 0 && Dt[j] < maxb && bnt<POW2>(c + (c == hp ? 1 : 0), cfg) <= At[j] - c_dem[j];
+          } else {
+            f = Dt[j] < maxb && bnt<POW2>(hp + 1, cfg) <= At[j];
+          }
+        }
+        fits[j] = f;
+        fa[j] = f && cyc_head && hp > bud[j];
+      }
+      bool isA[J], isB[J];
+#pragma unroll
+      for (int j = 0; j < J; ++j) isA[j] = false;
+      bool a_prev_lane = false;
+      int32_t bud_prev_lane = 0;
+      bool any_fa = false;
+#pragma unroll
+      for (int j = 0; j < J; ++j) any_fa |= fa[j];
+      if (CYC && __any_sync(kFull, any_fa)) {
+        // previous step's flags / budget (lane - 1's last slot for j = 0)
+        const bool fa_prev_lane = __shfl_up_sync(kFull, fa[J - 1], 1) && lane > 0;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const bool prev = j == 0 ? fa_prev_lane : fa[j - 1];
+          if (fa[j] && !prev) rs_lane = t0 + j;
+        }
+        int32_t rs_carry = rs_lane;  // inclusive max-scan over lanes
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int32_t y = __shfl_up_sync(kFull, rs_carry, d);
+          if (lane >= d) rs_carry = max(rs_carry, y);
+        }
+        rs_carry = __shfl_up_sync(kFull, rs_carry, 1);
+        if (lane == 0) rs_carry = -1;
+        int32_t rs = rs_carry;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const bool prev = j == 0 ? fa_prev_lane : fa[j - 1];
+          if (fa[j] && !prev) rs = t0 + j;
+          isA[j] = fa[j] && (((t0 + j - rs) & 1) == 0);
+        }
+        a_prev_lane = __shfl_up_sync(kFull, isA[J - 1], 1) && lane > 0;
+        bud_prev_lane = __shfl_up_sync(kFull, bud[J - 1], 1);
+      }
       int32_t first_stop = W;
 #pragma unroll
       for (int j = J - 1; j >= 0; --j) {
         const int32_t t = t0 + j;
-        Dt[j] = n - cnt_x[j];                          // alive in step t
-        Ct[j] = (s_tot - sst_x[j]) + t * Dt[j];        // context of step t
-        const int32_t At = free_blocks - dem_x[j] + frd_x[j];  // free before step t
-        bool stop = Dt[j] == 0 || c_dem[j] > At;
-        if (waiting_nonempty && t > 0 && !stop) {
-          // would the waiting head be admitted at step t? (backend.cpp:132-148 / 158-175)
-          if (chunked) {
-            const int32_t bud = cfg.chunk_budget - Dt[j];
-            const int32_t c = hp < bud ? hp : bud;
-            stop = bud > 0 && Dt[j] < maxb && bnt<POW2>(c + (c == hp ? 1 : 0), cfg) <= At - c_dem[j];
-          } else {
-            stop = Dt[j] < maxb && bnt<POW2>(hp + 1, cfg) <= At;
-          }
+        isB[j] = j == 0 ? a_prev_lane : isA[j - 1];
+        bool stop;
+        if (isB[j]) {
+          // the head holds bn(cA) after A; its next chunk must not fit (it alone is
+          // evicted: F(n+1) < 0 <= F(n))
+          const int32_t cA = j == 0 ? bud_prev_lane : bud[j - 1];
+          const int32_t rem = hp - cA;
+          const int32_t ch = rem < bud[j] ? rem : bud[j];
+          const int32_t hA = bnt<POW2>(cA, cfg);
+          const int32_t dB = bnt<POW2>(cA + ch + (ch == rem ? 1 : 0), cfg) - hA;
+          stop = Dt[j] == 0 || bud[j] <= 0 || c_dem[j] + dB <= At[j] - hA || c_dem[j] > At[j];
+        } else if (isA[j]) {
+          stop = t == W - 1;  // its B would fall outside the window
+        } else {
+          stop = Dt[j] == 0 || c_dem[j] > At[j] || fits[j];
         }
         if (stop) first_stop = t;
       }
       T = static_cast<int32_t>(__reduce_min_sync(kFull, static_cast<uint32_t>(first_stop)));
+      // never end right after an A step (the head would be mid-prefill)
+      if constexpr (CYC) {
+        bool a_last = false;
+#pragma unroll
+        for (int j = 0; j < J; ++j)
+          if (t0 + j == T - 1) a_last = isA[j];
+        if (__any_sync(kFull, a_last)) T -= 1;
+      }
       const int32_t t_cand = static_cast<int32_t>(__reduce_min_sync(kFull, static_cast<uint32_t>(lc)));
       if (t_cand < W - 1) T = min(T, t_cand + 1);
       const int64_t lim = kMaxSimulatedSteps + 1 - steps;
@@ -767,16 +899,9 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
 #pragma unroll
         for (int j = 0; j < J; ++j) {
           const bool in = t0 + j < T;
-#ifdef BSG_ABL_TICKS
-          {  // ablation (timing experiments only): branch-free pricing
-            const int64_t tk = step_ticks(cfg, 0, Dt[j], Ct[j]);
-            d[j] = in ? tk : 0;
-          }
-#else
-          d[j] = in ? step_ticks(cfg, 0, Dt[j], Ct[j]) : 0;
-#endif
+          d[j] = in ? step_ticks(cfg, isA[j] ? bud[j] : 0, Dt[j], Ct[j]) : 0;
           dsum += d[j];
-          msum += in ? Dt[j] + 1 : 0;
+          msum += in ? Dt[j] + 1 + (isA[j] ? 1 : 0) : 0;
         }
         const int64_t sum = warp_sum_i64(dsum);
         if constexpr (MC) {
@@ -805,9 +930,14 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
           int32_t rr[K];
 #pragma unroll
           for (int k = 0; k < K; ++k) rr[k] = (lane * K + k) < n ? target[k] - decoded[k] - 1 : -1;
-          int32_t fa[J];
+          int32_t fafter[J], kind[J];  // free after step t; 1 = A step, 2 = B step
 #pragma unroll
-          for (int j = 0; j < J; ++j) fa[j] = free_blocks - dem_i[j] + frd_x[j] + c_frd[j];
+          for (int j = 0; j < J; ++j) {
+            fafter[j] = free_blocks - dem_i[j] + frd_x[j] + c_frd[j] -
+                        (isA[j] ? bnt<POW2>(bud[j], cfg) : 0);
+            kind[j] = isA[j] ? 1 : (isB[j] ? 2 : 0);
+          }
+          const int32_t head_o = cyc_head ? org_origin(read_pos<K>(org, n)) : 0;
           for (int32_t t = 0; t < T; ++t) {
             int32_t al[K], ral[K], cp[K], rcp[K], z[K], rz[K];
 #pragma unroll
@@ -839,15 +969,19 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
             const int64_t dt = __shfl_sync(kFull, dl, t / J);
             const int32_t ct = read_pos<J>(Ct, t);
             const int32_t nd = read_pos<J>(Dt, t);
-            const int32_t fat = read_pos<J>(fa, t);
+            const int32_t fat = read_pos<J>(fafter, t);
+            const int32_t kt = read_pos<J>(kind, t);
+            const int32_t ca = read_pos<J>(bud, t);
+            if (kt == 1) hplan += hash_term(BSG_TAG_PLAN + 16u, 0, head_o, ca);
+            if (kt == 2) hev += hash_term(BSG_TAG_PREEMPT, 0, head_o, 0);
             if (lane == 0 && steps + t < trace.cap) {
               bsg_step_record& rec = trace.rec[steps + t];
               rec.duration_ticks = dt;
               rec.context_tokens = ct;
               rec.n_decode = nd;
-              rec.prefill_tokens = 0;
-              rec.n_prefill = 0;
-              rec.n_preempted = 0;
+              rec.prefill_tokens = kt == 1 ? ca : 0;
+              rec.n_prefill = kt == 1 ? 1 : 0;
+              rec.n_preempted = kt == 2 ? 1 : 0;
               rec.n_completed = ncp;
               rec.free_blocks_after = fat;
               rec.plan_hash = hplan;
@@ -879,8 +1013,14 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
     }
 #ifdef BSG_PROFILE_ITERS
     if (T == 0) ++prof_gen; else ++prof_win;
+#ifdef BSG_PROFILE_T0
+    // debug: general steps after a window that retired nothing (cycle entry / plain)
+    if (T == 0 && prof_entered && a > 0) ++prof_adm;
+    if (T == 0 && prof_entered && a == 0) ++prof_prf;
+#else
     if (T == 0 && a > 0) ++prof_adm;
     if (T == 0 && any_nonready) ++prof_prf;
+#endif
 #endif
     if (T == 0 && !delta_ready) running_deltas();
     if (T == 0) {

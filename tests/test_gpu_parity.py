@@ -36,13 +36,14 @@ def test_gpu_matches_reference_fuzz(ctx, ref, seed):
     assert bad.sum() == 0, [(i, got[i], exp[i]) for i in np.nonzero(bad)[0][:5]]
 
 
-@pytest.mark.parametrize("win_j", ["1", "4"])
-def test_gpu_trace_matches_reference(ctx, ref, monkeypatch, win_j):
+@pytest.mark.parametrize("win_j,cyc", [("1", "1"), ("4", "1"), ("4", "0"), ("1", "0")])
+def test_gpu_trace_matches_reference(ctx, ref, monkeypatch, win_j, cyc):
     """Per-step batch composition, allocations, preemption victims, first
     tokens, completions and durations (bsg_step_record) for every step — with
     the event-skipping window at both widths the kernels use (32 and 128 steps
     per iteration), so every window-retired step is checked too."""
     monkeypatch.setenv("BSG_TRACE_J", win_j)
+    monkeypatch.setenv("BSG_TRACE_CYC", cyc)
     cfgs, ss = fuzz_set(12, 400)
     ctx.set_configs(cfgs)
     names, kc, ks = kat_set()
@@ -54,6 +55,29 @@ def test_gpu_trace_matches_reference(ctx, ref, monkeypatch, win_j):
             assert a["status"] == b["status"], (i, a, b)
             assert len(ta) == len(tb), (i, len(ta), len(tb))
             assert np.array_equal(ta, tb), (i, np.nonzero(ta != tb)[0][:3])
+
+
+@pytest.mark.parametrize("win_j", ["1", "4"])
+def test_gpu_trace_kv_pressure_cycles(ctx, ref, monkeypatch, win_j):
+    """cfg3-shaped scenarios (KV pressure, chunked prefill, deep queues) spend
+    most general steps in admit / self-preempt cycles, which the windows
+    absorb: every step record (plan, preemption victim, free blocks, duration)
+    must equal the reference's, and the scenarios must actually contain cycles."""
+    monkeypatch.setenv("BSG_TRACE_J", win_j)
+    cfg = abi.make_config()
+    w = abi.make_workload(count=1000, prompt_median=600, output_median=600, qps=5.0, arrival_seed=1)
+    _, _, ss = ref.replay(w, cfg, abi.make_replay_spec(12))
+    ctx.set_configs(cfg)
+    cycles = 0
+    for i in range(len(ss) - 1, len(ss) - 1 - 48 * 12, -12):  # late arrivals queue deepest
+        a, ta = ctx.trace(ss, i, cap=1 << 15)
+        b, tb = ref.trace(cfg, ss, i, cap=1 << 15)
+        assert a["status"] == b["status"] and len(ta) == len(tb), (i, a, b)
+        assert np.array_equal(ta, tb), (i, np.nonzero(ta != tb)[0][:3])
+        A = (tb["n_prefill"] == 1) & (tb["n_preempted"] == 0)
+        B = (tb["n_prefill"] == 0) & (tb["n_preempted"] == 1)
+        cycles += int((A[:-1] & B[1:]).sum())
+    assert cycles > 5000, cycles
 
 
 def test_gpu_kats(ctx):
