@@ -264,7 +264,11 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
                                   const int32_t* __restrict__ g_est,
                                   const int32_t* __restrict__ g_prefill,
                                   const int32_t* __restrict__ g_decoded, const bsg_scenario sc,
-                                  int32_t* __restrict__ smem,  // smem_words(K) int32 per warp
+                                  // smem_words(K) int32 per warp. Not __restrict__: lanes
+                                  // exchange values through it across __syncwarp(), which
+                                  // a restrict-qualified pointer lets the compiler reorder
+                                  // loads across (the barrier does not take the pointer)
+                                  int32_t* smem,
                                   bsg_result* __restrict__ out, TraceSink trace,
                                   McArgs mc = McArgs{}) {
   constexpr int CAP = 32 * K;
@@ -611,8 +615,9 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
       // Exact pre-checks of the window's first steps, so that a window which
       // would retire nothing is never set up (KV-pressure sets otherwise pay a
       // window per general step): a plain window stops at step 0 iff its decode
-      // demand needs a victim; a cycle window is cut before its A step iff the
-      // B step after it would not evict exactly the head (same tests as below).
+      // demand needs a victim; a cycle window is cut before its A1 step when
+      // step 1 shows the cycle cannot close (the head would finish its prefill,
+      // or more than the head would be evicted) — the tests the window applies.
       if (win) {
         bool d0[K], c0[K], d1[K];
         int32_t fr0[K];
@@ -638,7 +643,10 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
           const int32_t rem = cyc_hp - cA;
           const int32_t ch = rem < bud1 ? rem : bud1;
           const int32_t dB = bnt<POW2>(cA + ch + (ch == rem ? 1 : 0), cfg) - hA;
-          win = !(D1 == 0 || bud1 <= 0 || dem1 + dB <= A1 - hA || dem1 > A1);
+          // step 1 evicts the head alone (a two-step cycle), or the head's next
+          // chunk fits without finishing its prefill (a longer cycle may follow)
+          const bool evict = dem1 + dB > A1 - hA;
+          win = !(D1 == 0 || bud1 <= 0 || (evict && dem1 > A1) || (!evict && ch == rem));
         }
       }
     }
@@ -785,18 +793,19 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
       }
       // Admit / self-preempt cycles (chunked prefill under KV pressure). When
       // the waiting head is a preemption victim (prefill = decoded = 0) whose
-      // first chunk c = budget < prompt fits, step A admits it with that chunk
+      // first chunk c1 = budget < prompt fits, step A1 admits it with that chunk
       // (the budget is then exhausted: a single admission, backend.cpp:135-147);
-      // in the next step B its remaining chunk does not fit, so the newest
-      // member — the head itself — is evicted (263-288) and returns to the
-      // waiting front exactly as before A. The pair leaves free blocks as two
-      // pure-decode steps would (A takes bn(c), B refunds it), so A(t) below
-      // stays exact on every non-B step. A step is A iff the head fits, is such
-      // a victim, and the previous step was not A: in a run of consecutive
-      // fitting steps starting at s, steps s, s+2, ... are A (a max-scan of run
-      // starts). B must evict the head and nothing else, else the window ends
-      // before its A. Repeats until the head misfits, a member completes and
-      // budgets change, or decode demand needs a victim.
+      // in the following steps A2, A3, ... its next full-budget chunks fit, until
+      // at step B its next chunk does not, and the newest member — the head
+      // itself — is evicted (263-288) and returns to the waiting front exactly
+      // as before A1. While it runs, the head holds bn(progress) blocks, and B
+      // refunds them, so after B the free count is what pure-decode steps would
+      // leave, and A(t) below stays exact outside cycles. Per step t the window
+      // computes where a cycle starting at t would end (e(t), a lane-parallel
+      // walk over its steps), then follows the chain of cycles from step 0
+      // (next event: a fitting step starts a cycle, a stop ends the window). A
+      // cycle whose head would finish its prefill, or whose B would evict more
+      // than the head, or that runs past the window, ends the window before it.
       const bool cyc_head = CYC && chunked && L > n;
       int32_t Dt[J], Ct[J], At[J], bud[J];
       bool fits[J], fa[J];
@@ -823,71 +832,168 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
         fits[j] = f;
         fa[j] = f && cyc_head && hp > bud[j];
       }
+      int32_t first_stop = W;
       bool isA[J], isB[J];
+      int32_t hprog[J];  // head's prefill progress before step t (cycle steps)
 #pragma unroll
-      for (int j = 0; j < J; ++j) isA[j] = false;
-      bool a_prev_lane = false;
-      int32_t bud_prev_lane = 0;
+      for (int j = 0; j < J; ++j) {
+        isA[j] = false;
+        isB[j] = false;
+        hprog[j] = 0;
+      }
       bool any_fa = false;
 #pragma unroll
       for (int j = 0; j < J; ++j) any_fa |= fa[j];
       if (CYC && __any_sync(kFull, any_fa)) {
-        // previous step's flags / budget (lane - 1's last slot for j = 0)
-        const bool fa_prev_lane = __shfl_up_sync(kFull, fa[J - 1], 1) && lane > 0;
+        // per-step values in shared memory (the histograms are in registers now)
+        int32_t* s_D = smem;
+        int32_t* s_bud = smem + W;
+        int32_t* s_At = smem + 2 * W;
+        int32_t* s_dem = smem + 3 * W;
+        __syncwarp();
 #pragma unroll
         for (int j = 0; j < J; ++j) {
-          const bool prev = j == 0 ? fa_prev_lane : fa[j - 1];
-          if (fa[j] && !prev) rs_lane = t0 + j;
+          s_D[t0 + j] = Dt[j];
+          s_bud[t0 + j] = bud[j];
+          s_At[t0 + j] = At[j];
+          s_dem[t0 + j] = c_dem[j];
         }
-        int32_t rs_carry = rs_lane;  // inclusive max-scan over lanes
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const int32_t y = __shfl_up_sync(kFull, rs_carry, d);
-          if (lane >= d) rs_carry = max(rs_carry, y);
-        }
-        rs_carry = __shfl_up_sync(kFull, rs_carry, 1);
-        if (lane == 0) rs_carry = -1;
-        int32_t rs = rs_carry;
+        __syncwarp();
+        // e(t): the B step of a cycle whose A1 is step t (-1: cut before t)
+        int32_t e[J], P[J];
+        bool open[J];
 #pragma unroll
         for (int j = 0; j < J; ++j) {
-          const bool prev = j == 0 ? fa_prev_lane : fa[j - 1];
-          if (fa[j] && !prev) rs = t0 + j;
-          isA[j] = fa[j] && (((t0 + j - rs) & 1) == 0);
+          e[j] = -1;
+          P[j] = bud[j];
+          open[j] = fa[j];
         }
-        a_prev_lane = __shfl_up_sync(kFull, isA[J - 1], 1) && lane > 0;
-        bud_prev_lane = __shfl_up_sync(kFull, bud[J - 1], 1);
-      }
-      int32_t first_stop = W;
+        for (int32_t d = 1;; ++d) {
+          bool any_open = false;
 #pragma unroll
-      for (int j = J - 1; j >= 0; --j) {
-        const int32_t t = t0 + j;
-        isB[j] = j == 0 ? a_prev_lane : isA[j - 1];
-        bool stop;
-        if (isB[j]) {
-          // the head holds bn(cA) after A; its next chunk must not fit (it alone is
-          // evicted: F(n+1) < 0 <= F(n))
-          const int32_t cA = j == 0 ? bud_prev_lane : bud[j - 1];
-          const int32_t rem = hp - cA;
-          const int32_t ch = rem < bud[j] ? rem : bud[j];
-          const int32_t hA = bnt<POW2>(cA, cfg);
-          const int32_t dB = bnt<POW2>(cA + ch + (ch == rem ? 1 : 0), cfg) - hA;
-          stop = Dt[j] == 0 || bud[j] <= 0 || c_dem[j] + dB <= At[j] - hA || c_dem[j] > At[j];
-        } else if (isA[j]) {
-          stop = t == W - 1;  // its B would fall outside the window
-        } else {
-          stop = Dt[j] == 0 || c_dem[j] > At[j] || fits[j];
+          for (int j = 0; j < J; ++j) {
+            if (open[j]) {
+              const int32_t st = t0 + j + d;
+              if (st >= W) {
+                open[j] = false;
+              } else {
+                const int32_t Ds = s_D[st], bs_ = s_bud[st], As = s_At[st], cd = s_dem[st];
+                const int32_t rem = hp - P[j];
+                const int32_t ch = rem < bs_ ? rem : bs_;
+                const int32_t hA = bnt<POW2>(P[j], cfg);
+                const int32_t dl = bnt<POW2>(P[j] + ch + (ch == rem ? 1 : 0), cfg) - hA;
+                if (Ds == 0 || bs_ <= 0) {
+                  open[j] = false;
+                } else if (cd + dl > As - hA) {  // F(n+1) < 0: the head is evicted
+                  open[j] = false;
+                  if (cd <= As) e[j] = st;       // F(n) >= 0: and nobody else
+                } else if (ch == rem) {          // it would finish its prefill
+                  open[j] = false;
+                } else {
+                  P[j] += ch;
+                }
+              }
+              any_open |= open[j];
+            }
+          }
+          if (!__any_sync(kFull, any_open)) break;
         }
-        if (stop) first_stop = t;
-      }
-      T = static_cast<int32_t>(__reduce_min_sync(kFull, static_cast<uint32_t>(first_stop)));
-      // never end right after an A step (the head would be mid-prefill)
-      if constexpr (CYC) {
-        bool a_last = false;
+        // next event at or after t: a fitting step (cycle start or cut) or a stop
+        int32_t ev[J];
+        {
+          int32_t nx = W;
 #pragma unroll
-        for (int j = 0; j < J; ++j)
-          if (t0 + j == T - 1) a_last = isA[j];
-        if (__any_sync(kFull, a_last)) T -= 1;
+          for (int j = J - 1; j >= 0; --j) {
+            const bool pstop = Dt[j] == 0 || c_dem[j] > At[j] || (fits[j] && !fa[j]);
+            if (fa[j] || pstop) nx = t0 + j;
+            ev[j] = nx;
+          }
+          // suffix-min over lanes: lane l gets min over lanes > l of their first event
+          int32_t sfx = nx;  // this lane's first event
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_down_sync(kFull, sfx, o);
+            if (lane + o < 32) sfx = min(sfx, y);
+          }
+          int32_t after = __shfl_down_sync(kFull, sfx, 1);
+          if (lane == 31) after = W;
+#pragma unroll
+          for (int j = 0; j < J; ++j) ev[j] = min(ev[j], after);
+        }
+        int32_t* s_e = s_D;     // reused: e(t) of fitting steps, -1 otherwise
+        int32_t* s_ev = s_bud;  // next event
+        int32_t* s_cs = s_At;   // 1 = a cycle starts here
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          s_e[t0 + j] = fa[j] ? e[j] : -1;
+          s_ev[t0 + j] = ev[j];
+          s_cs[t0 + j] = 0;
+        }
+        __syncwarp();
+        // the chain of cycles from step 0 (warp-uniform walk over broadcast reads)
+        int32_t cur = 0;
+        for (;;) {
+          const int32_t pos = cur < W ? s_ev[cur] : W;
+          if (pos >= W) break;
+          const int32_t eb = s_e[pos];
+          if (eb < 0) {
+            first_stop = pos;
+            break;
+          }
+          if (lane == 0) s_cs[pos] = 1;
+          cur = eb + 1;
+        }
+        __syncwarp();
+        // each step's cycle: the latest start at or before it (prefix max)
+        int32_t rs[J];
+        {
+          int32_t m = -1;
+#pragma unroll
+          for (int j = 0; j < J; ++j) {
+            if (s_cs[t0 + j]) m = t0 + j;
+            rs[j] = m;
+          }
+          int32_t pm = m;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(kFull, pm, o);
+            if (lane >= o) pm = max(pm, y);
+          }
+          int32_t before = __shfl_up_sync(kFull, pm, 1);
+          if (lane == 0) before = -1;
+#pragma unroll
+          for (int j = 0; j < J; ++j) rs[j] = max(rs[j], before);
+        }
+        // head progress: exclusive prefix of chunks (= budgets) from the cycle start
+        int32_t Sx[J];
+        excl_scan<J>(bud, Sx);
+        int32_t* s_S = s_dem;
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < J; ++j) s_S[t0 + j] = Sx[j];
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const int32_t t = t0 + j;
+          if (rs[j] >= 0 && t < first_stop) {
+            const int32_t eb = s_e[rs[j]];
+            if (t <= eb) {
+              isB[j] = t == eb;
+              isA[j] = t < eb;
+              hprog[j] = Sx[j] - s_S[rs[j]];
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = J - 1; j >= 0; --j) {
+          const bool stop = Dt[j] == 0 || c_dem[j] > At[j] || fits[j];
+          if (stop) first_stop = t0 + j;
+        }
+        first_stop = static_cast<int32_t>(__reduce_min_sync(kFull, static_cast<uint32_t>(first_stop)));
       }
+      T = first_stop;
       const int32_t t_cand = static_cast<int32_t>(__reduce_min_sync(kFull, static_cast<uint32_t>(lc)));
       if (t_cand < W - 1) T = min(T, t_cand + 1);
       const int64_t lim = kMaxSimulatedSteps + 1 - steps;
@@ -934,7 +1040,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
 #pragma unroll
           for (int j = 0; j < J; ++j) {
             fafter[j] = free_blocks - dem_i[j] + frd_x[j] + c_frd[j] -
-                        (isA[j] ? bnt<POW2>(bud[j], cfg) : 0);
+                        (isA[j] ? bnt<POW2>(hprog[j] + bud[j], cfg) : 0);
             kind[j] = isA[j] ? 1 : (isB[j] ? 2 : 0);
           }
           const int32_t head_o = cyc_head ? org_origin(read_pos<K>(org, n)) : 0;
@@ -981,6 +1087,9 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
               rec.n_decode = nd;
               rec.prefill_tokens = kt == 1 ? ca : 0;
               rec.n_prefill = kt == 1 ? 1 : 0;
+#ifdef BSG_PROFILE_T0
+              rec.n_prefill |= 1 << 20;  // debug: retired by a window
+#endif
               rec.n_preempted = kt == 2 ? 1 : 0;
               rec.n_completed = ncp;
               rec.free_blocks_after = fat;
