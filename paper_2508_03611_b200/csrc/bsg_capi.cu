@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         scores[w] = INT64_MAX;
       }
     } else {
-      simulate_scenario<K, false, true, POW2, true, false, BSG_WIN_J_LATENCY>(
+      simulate_scenario<K, false, true, POW2, true, false, BSG_WIN_J_LATENCY, BSG_CYC_LATENCY>(
           cfg, prompt, est, prefill, decoded, sc, smem, o, TraceSink{nullptr, 0},
           McArgs{len, S, sample_e2e ? sample_e2e + w * S : nullptr, scores + w, objective});
     }

@@ -722,7 +722,7 @@ __global__ void __launch_bounds__(kClWarps * 32, BSG_CL_MINB)
       sc.cand_est = ce;
       sc.cfg = run.cfg;
       sc.reserved = 0;
-      simulate_scenario<K, false, false, POW2, false, false, BSG_WIN_J_CLOSED>(
+      simulate_scenario<K, false, false, POW2, false, false, BSG_WIN_J_CLOSED, BSG_CYC_CLOSED>(
           cfg, ar.prompt, ar.est, ar.prefill, ar.decoded, sc, S.scratch[warp], &S.res[i],
           TraceSink{nullptr, 0});
     }
@@ -912,11 +912,11 @@ __global__ void __launch_bounds__(kFleetWarps * 32)
         for (int32_t j = lane; j < S; j += 32) len[j] = sorted_len[j];
         __syncwarp();
       }
-      simulate_scenario<K, false, true, POW2, false, false, BSG_WIN_J_LATENCY>(cfg, ar.prompt, ar.est, ar.prefill, ar.decoded, sc,
+      simulate_scenario<K, false, true, POW2, false, false, BSG_WIN_J_LATENCY, BSG_CYC_LATENCY>(cfg, ar.prompt, ar.est, ar.prefill, ar.decoded, sc,
                                                     smem, &res[i], TraceSink{nullptr, 0},
                                                     McArgs{len, S, nullptr, &scores[i], objective});
     } else {
-      simulate_scenario<K, false, false, POW2, false, false, BSG_WIN_J_LATENCY>(
+      simulate_scenario<K, false, false, POW2, false, false, BSG_WIN_J_LATENCY, BSG_CYC_LATENCY>(
           cfg, ar.prompt, ar.est, ar.prefill, ar.decoded, sc, smem, &res[i], TraceSink{nullptr, 0});
       __syncwarp();
       if (lane == 0) {

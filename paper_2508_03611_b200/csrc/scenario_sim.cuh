@@ -54,6 +54,17 @@ constexpr int kMaxWinJ = BSG_MAX_WIN_J;
 #ifndef BSG_WIN_J_CLOSED
 #define BSG_WIN_J_CLOSED 1    // K5 closed-loop what-ifs
 #endif
+// Admit / self-preempt cycle absorption in the windows (simulate_scenario's
+// CYC) for the latency path (dispatch_mc, fleet) and the K5 closed loop; the
+// throughput kernels choose per launch shape (bsg_capi.cu). Off by measurement:
+// cfg4 p99 116 vs 123 us, cfg5 full grid 0.333 vs 0.355 s (their instances
+// rarely thrash; the extra registers cost more than the cycles save).
+#ifndef BSG_CYC_LATENCY
+#define BSG_CYC_LATENCY 0
+#endif
+#ifndef BSG_CYC_CLOSED
+#define BSG_CYC_CLOSED 0
+#endif
 // Per-warp shared-memory words of simulate_scenario: the completion-compaction
 // area (5 x 32K) / the window histograms (4 x 32 x kMaxWinJ), whichever is larger.
 __host__ __device__ constexpr int smem_words(int K) {
