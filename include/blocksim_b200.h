@@ -340,8 +340,11 @@ typedef enum bsg_policy {
   BSG_POLICY_BLOCK_PREDICTIVE = 5
 } bsg_policy;
 
-/* Zero-overhead, probe-free closed loop (ExperimentSpec, config.h:58-70
- * subset) with the autoscaler (ProvisionPolicy, autoscaler.h:10-27). */
+/* Probe-free closed loop (ExperimentSpec, config.h:58-70 subset) with the
+ * autoscaler (ProvisionPolicy, autoscaler.h:10-27) and the dispatch-overhead
+ * mode (overhead.dispatch_s, config.h:65: the decision is taken at the
+ * arrival, the request lands at the chosen instance overhead seconds later,
+ * driver.cpp:213-218). */
 typedef struct bsg_replay_spec {
   int32_t n_instances;     /* cluster.instances */
   int32_t policy;          /* bsg_policy */
@@ -353,6 +356,7 @@ typedef struct bsg_replay_spec {
   double threshold_s;      /* provision.threshold_s (70) */
   double cold_start_s;     /* provision.cold_start_s (30) */
   double cooldown_s;       /* provision.cooldown_s (15) */
+  double dispatch_overhead_s; /* overhead.dispatch_s (0: admit at the decision) */
 } bsg_replay_spec;
 
 /* RunLog totals (metrics.h:18-54 subset). */
@@ -403,6 +407,7 @@ typedef struct bsg_run_report {
    * produced by bsg_replay_device's device reports (bsg_aggregate, which has
    * no dispatch points, leaves them 0) */
   double free_blocks_mean_avg, free_blocks_var_avg;
+  double mean_overhead_s;  /* mean of dispatch - arrival over finished requests */
 } bsg_run_report;
 bsg_status bsg_aggregate(const bsg_request_outcome* outcomes, int64_t n,
                          const bsg_replay_summary* summary, bsg_run_report* out);
@@ -443,24 +448,72 @@ typedef struct bsg_sweep_out {
   double wall_s;                 /* host path: summed closed-loop time; device path: the
                                     wall time of the batched launches holding its points */
 } bsg_sweep_out;
-/* Runs the cells' capacity searches. When every cell is a BlockPredictive
- * cluster of <= 256 instances (max_instances when provisioning), every (cell, qps)
- * point is a device-resident closed loop (bsg_replay_device): all integer
- * points in one batched launch, then all tenths in a second one (records
- * generated on `threads` host threads). Otherwise the closed loops run on
- * `threads` host threads, each with its own context on `device` (GPU what-ifs
- * per arrival). BSG_SWEEP_HOST=1 forces the host path. */
+/* Runs the cells' capacity searches. When every cell is a cluster of <= 256
+ * instances (max_instances when provisioning) with max_batch_size <= 256, every
+ * (cell, qps) point is a device-resident closed loop (bsg_replay_device, any
+ * policy): all integer points in one batched launch, then all tenths in a
+ * second one (records generated on `threads` host threads). Otherwise the
+ * closed loops run on `threads` host threads, each with its own context on
+ * `device` (GPU what-ifs per arrival). BSG_SWEEP_HOST=1 forces the host path. */
 bsg_status bsg_sweep_run(int device, const bsg_sweep_cell* cells, int32_t n_cells,
                          int32_t threads, bsg_sweep_out* out);
+
+/* run_sweep (driver.cpp:333-390): one closed loop per (policy, qps, seed) cell,
+ * policies outermost, seeds innermost (the reference's cell order), each
+ * run_experiment(spec_for_cell(base, policy, qps, seed)) (driver.cpp:321-331)
+ * aggregated (metrics.cpp:21-124) into a SweepCell row (driver.h:78-90).
+ * A run that fails (e.g. a deadlock or a what-if error) gives ok = 0 and its
+ * status instead of the reference's error text. All cells run as device-resident
+ * closed loops in one batched launch when they fit (see bsg_sweep_run), else on
+ * `threads` host threads. rows: n_policies * n_qps * n_seeds. */
+typedef struct bsg_sweep_row {
+  int32_t policy;            /* bsg_policy */
+  int32_t ok;                /* 1: ran to completion */
+  double qps;
+  uint64_t seed;
+  int32_t status;            /* BSG_OK, or why the run failed */
+  int32_t finished_requests;
+  double mean_ttft_s, p99_ttft_s, mean_e2e_s, p99_e2e_s;
+  double throughput_rps;
+  int64_t total_preemptions;
+  double free_blocks_var_avg;
+} bsg_sweep_row;
+bsg_status bsg_run_sweep(int device, const bsg_workload* base, const bsg_instance_cfg* cfg,
+                         const bsg_replay_spec* spec, const int32_t* policies, int32_t n_policies,
+                         const double* qps_values, int32_t n_qps, const uint64_t* seeds, int32_t n_seeds,
+                         int32_t threads, bsg_sweep_row* rows);
+
+/* run_capacity (driver.cpp:392-427): capacity_search per policy of `policies`
+ * (the baseline appended when absent), every run spec_for_cell(base, policy,
+ * qps, seed); then the gain of every non-baseline policy over the baseline's
+ * capacity, (c - c_base) / c_base, also formatted like format_percent ("16.7%",
+ * driver.cpp:392-396). rows receive n_policies (+1) entries in that order;
+ * *n_rows their count. Rows of policies with no capacity have status
+ * BSG_NO_CAPACITY (the reference throws NoCapacityError out of run_capacity). */
+typedef struct bsg_capacity_row {
+  int32_t policy;
+  int32_t status;             /* BSG_OK or BSG_NO_CAPACITY or an error */
+  bsg_capacity_result result;
+  int32_t has_gain;           /* non-baseline policy with a positive baseline capacity */
+  int32_t reserved;
+  double gain;                /* (capacity - baseline) / baseline */
+  char gain_text[16];         /* format_percent: "%.1f%%" of gain * 100 */
+} bsg_capacity_row;
+bsg_status bsg_run_capacity(int device, const bsg_workload* base, const bsg_instance_cfg* cfg,
+                            const bsg_replay_spec* spec, const int32_t* policies, int32_t n_policies,
+                            int32_t baseline, uint64_t seed, int32_t qps_min, int32_t qps_max,
+                            double slo_p99_ttft_s, int32_t threads, bsg_capacity_row* rows,
+                            int32_t* n_rows, double* baseline_capacity);
 /* Scenarios simulated by this context so far (all entry points). */
 int64_t bsg_scenario_count(const bsg_ctx* ctx);
 
 /* Device-resident closed loops: each run is one
- * run_experiment (driver.cpp:134-289) with zero dispatch overhead,
- * BlockPredictive dispatch and static / preempt / relief provisioning
- * (autoscaler.cpp:36-52), executed entirely on the GPU — one
- * thread block per run: live instances in HBM, every arrival's per-instance
- * what-ifs + argmin on the block's warps, the event loop on the device.
+ * run_experiment (driver.cpp:134-289) — any dispatch policy (BlockPredictive,
+ * or the heuristics of pick_heuristic, scheduler.cpp:68-113), static / preempt
+ * / relief provisioning (autoscaler.cpp:36-52), optional dispatch overhead
+ * (driver.cpp:213-218) — executed entirely on the GPU, one thread block per
+ * run: live instances in HBM, every arrival's per-instance what-ifs + argmin
+ * (or heuristic scores) on the block's warps, the event loop on the device.
  * Requests of run r are rows [req_off, req_off + n_requests) of the request
  * columns (arrival ticks non-decreasing; request id = row - req_off);
  * outcomes has the same rows. run_status[r] is BSG_OK or the error that ended
@@ -476,6 +529,10 @@ typedef struct bsg_closed_loop_run {
   int32_t provision_kind;
   int32_t max_instances;
   double threshold_s, cold_start_s, cooldown_s;
+  int32_t policy;              /* bsg_policy */
+  int32_t reserved;
+  uint64_t policy_seed;        /* Random's SplitMix64 stream (PolicyConfig::seed) */
+  double dispatch_overhead_s;  /* overhead.dispatch_s */
 } bsg_closed_loop_run;
 /* outcomes may be NULL (not copied back); reports (optional, one per run) is
  * aggregate (metrics.cpp:21-124) computed on the device:

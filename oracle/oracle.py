@@ -127,6 +127,13 @@ class Reference:
         L.ref_set_trace.restype = None
         L.ref_sweep.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
         L.ref_sweep.restype = C.c_double
+        L.ref_run_sweep.argtypes = [C.c_void_p] * 4 + [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
+                                                       C.c_int32, C.c_int32, C.c_void_p]
+        L.ref_run_sweep.restype = C.c_int
+        L.ref_run_capacity.argtypes = [C.c_void_p] * 4 + [C.c_int32, C.c_int32, C.c_uint64, C.c_int32,
+                                                          C.c_int32, C.c_double, C.c_void_p,
+                                                          C.POINTER(C.c_double)]
+        L.ref_run_capacity.restype = C.c_int
 
     def predict_batch(self, cfgs, ss: abi.ScenarioSet, threads: int = 1) -> np.ndarray:
         out = np.zeros(len(ss), abi.ref_result_dtype)
@@ -236,6 +243,28 @@ class Reference:
                                           _vp(out), _vp(tq), _vp(tp), 256)
         n = int(out["n_tested"][0])
         return st, out[0], list(zip(tq[:n].tolist(), tp[:n].astype(bool).tolist()))
+
+    def run_sweep(self, w, cfg, spec, policies, qps_values, seeds, jobs: int = 8):
+        """The reference's run_sweep (driver.cpp:333-390): SweepCell rows."""
+        pol = np.ascontiguousarray(policies, np.int32)
+        qps = np.ascontiguousarray(qps_values, np.float64)
+        sd = np.ascontiguousarray(seeds, np.uint64)
+        rows = np.zeros(len(pol) * len(qps) * len(sd), abi.sweep_row_dtype)
+        n = self.lib.ref_run_sweep(_vp(w), _vp(cfg), _vp(spec), _vp(pol), len(pol), _vp(qps), len(qps),
+                                   _vp(sd), len(sd), jobs, _vp(rows))
+        if n < 0:
+            raise RuntimeError("reference run_sweep threw")
+        return rows[:n]
+
+    def run_capacity(self, w, cfg, spec, policies, baseline, seed, qps_min, qps_max, slo):
+        """The reference's run_capacity (driver.cpp:392-427): (status, rows,
+        baseline capacity); status -12 = NoCapacityError."""
+        pol = np.ascontiguousarray(policies, np.int32)
+        rows = np.zeros(len(pol) + 1, abi.capacity_row_dtype)
+        bc = C.c_double(0)
+        n = self.lib.ref_run_capacity(_vp(w), _vp(cfg), _vp(spec), _vp(pol), len(pol), baseline, seed,
+                                      qps_min, qps_max, slo, _vp(rows), C.byref(bc))
+        return (n if n < 0 else 0), rows[:max(n, 0)], bc.value
 
     def sweep(self, cells, threads: int):
         """capacity_search of every cell, parallel over (cell, qps) points on

@@ -581,6 +581,7 @@ static ExperimentSpec make_experiment(const bsg_workload* w, const bsg_instance_
   spec.provision.cooldown_s = s->cooldown_s;
   spec.cache_mode = to_ref_cache(c->cache_mode);
   spec.cache_bucket = c->context_bucket;
+  spec.dispatch_overhead_s = s->dispatch_overhead_s;
   spec.collect_events = false;
   return spec;
 }
@@ -627,6 +628,7 @@ int ref_run_report(const bsg_workload* w, const bsg_instance_cfg* c, const bsg_r
   out->final_instance_count = r.final_instance_count;
   out->free_blocks_mean_avg = r.free_blocks_mean_avg;
   out->free_blocks_var_avg = r.free_blocks_var_avg;
+  out->mean_overhead_s = r.mean_overhead_s;
   return 0;
 }
 
@@ -895,6 +897,91 @@ int64_t ref_write_trace(const bsg_trace_record* recs, int64_t n, char* out, int6
   if (static_cast<int64_t>(s.size()) > cap) return -static_cast<int64_t>(s.size());
   std::memcpy(out, s.data(), s.size());
   return static_cast<int64_t>(s.size());
+}
+
+}  // extern "C"
+
+
+// ---- run_sweep / run_capacity (driver.cpp:333-427) through the reference itself
+extern "C" {
+
+// run_sweep(base, SweepSpec{policies, qps_values, seeds, jobs}); rows in the
+// reference's cell order. Returns the number of rows, -1 if it threw.
+int ref_run_sweep(const bsg_workload* w, const bsg_instance_cfg* c, const bsg_replay_spec* s,
+                  const int32_t* policies, int32_t n_policies, const double* qps, int32_t n_qps,
+                  const uint64_t* seeds, int32_t n_seeds, int32_t jobs, bsg_sweep_row* rows) {
+  try {
+    const ExperimentSpec base = make_experiment(w, c, s);
+    SweepSpec sw;
+    for (int32_t i = 0; i < n_policies; ++i) sw.policies.push_back(to_ref_policy(policies[i]));
+    sw.qps_values.assign(qps, qps + n_qps);
+    sw.seeds.assign(seeds, seeds + n_seeds);
+    sw.jobs = jobs;
+    const std::vector<SweepCell> cells = run_sweep(base, sw);
+    for (std::size_t i = 0; i < cells.size(); ++i) {
+      const SweepCell& x = cells[i];
+      bsg_sweep_row& r = rows[i];
+      std::memset(&r, 0, sizeof(r));
+      r.policy = static_cast<int32_t>(x.policy);
+      r.ok = x.ok ? 1 : 0;
+      r.qps = x.qps;
+      r.seed = x.seed;
+      r.status = x.ok ? 0 : -1;
+      r.finished_requests = x.finished_requests;
+      r.mean_ttft_s = x.mean_ttft_s;
+      r.p99_ttft_s = x.p99_ttft_s;
+      r.mean_e2e_s = x.mean_e2e_s;
+      r.p99_e2e_s = x.p99_e2e_s;
+      r.throughput_rps = x.throughput_rps;
+      r.total_preemptions = x.total_preemptions;
+      r.free_blocks_var_avg = x.free_blocks_var_avg;
+    }
+    return static_cast<int>(cells.size());
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// run_capacity(base, CapacitySpec{...}): rows in table order, gains as the
+// reference formats them. Returns the row count; -12 on NoCapacityError, -1 on
+// any other exception.
+int ref_run_capacity(const bsg_workload* w, const bsg_instance_cfg* c, const bsg_replay_spec* s,
+                     const int32_t* policies, int32_t n_policies, int32_t baseline, uint64_t seed,
+                     int32_t qps_min, int32_t qps_max, double slo, bsg_capacity_row* rows,
+                     double* baseline_capacity) {
+  try {
+    const ExperimentSpec base = make_experiment(w, c, s);
+    CapacitySpec cs;
+    for (int32_t i = 0; i < n_policies; ++i) cs.policies.push_back(to_ref_policy(policies[i]));
+    cs.baseline = to_ref_policy(baseline);
+    cs.qps_min = qps_min;
+    cs.qps_max = qps_max;
+    cs.slo_p99_ttft_s = slo;
+    cs.seed = seed;
+    const CapacityTable t = run_capacity(base, cs);
+    *baseline_capacity = t.baseline_capacity;
+    for (std::size_t i = 0; i < t.rows.size(); ++i) {
+      const CapacityTableRow& x = t.rows[i];
+      bsg_capacity_row& r = rows[i];
+      std::memset(&r, 0, sizeof(r));
+      r.policy = static_cast<int32_t>(x.policy);
+      r.result.capacity_qps = x.result.capacity_qps;
+      r.result.bracket_pass = x.result.bracket_pass;
+      r.result.bracket_fail = x.result.bracket_fail;
+      r.result.monotone = x.result.monotone ? 1 : 0;
+      r.result.n_tested = static_cast<int32_t>(x.result.tested.size());
+      for (const auto& [name, text] : t.gains)
+        if (name == to_string(x.policy)) {
+          r.has_gain = 1;
+          std::snprintf(r.gain_text, sizeof(r.gain_text), "%s", text.c_str());
+        }
+    }
+    return static_cast<int>(t.rows.size());
+  } catch (const NoCapacityError&) {
+    return -12;
+  } catch (const std::exception&) {
+    return -1;
+  }
 }
 
 }  // extern "C"

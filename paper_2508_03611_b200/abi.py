@@ -71,6 +71,7 @@ replay_spec_dtype = np.dtype([
     ("n_instances", "<i4"), ("policy", "<i4"), ("objective", "<i4"), ("capture", "<i4"),
     ("policy_seed", "<u8"), ("provision_kind", "<i4"), ("max_instances", "<i4"),
     ("threshold_s", "<f8"), ("cold_start_s", "<f8"), ("cooldown_s", "<f8"),
+    ("dispatch_overhead_s", "<f8"),
 ])
 summary_dtype = np.dtype([
     ("total_preemptions", "<i8"), ("end_ticks", "<i8"), ("instances_provisioned", "<i4"),
@@ -82,11 +83,15 @@ report_dtype = np.dtype([
     ("mean_e2e_s", "<f8"), ("p50_e2e_s", "<f8"), ("p99_e2e_s", "<f8"),
     ("total_preemptions", "<i8"), ("instances_provisioned", "<i4"),
     ("final_instance_count", "<i4"), ("free_blocks_mean_avg", "<f8"), ("free_blocks_var_avg", "<f8"),
+    ("mean_overhead_s", "<f8"),
 ])
 capacity_dtype = np.dtype([
     ("capacity_qps", "<f8"), ("bracket_pass", "<i4"), ("bracket_fail", "<i4"),
     ("monotone", "<i4"), ("n_tested", "<i4"),
 ])
+capacity_row_dtype = np.dtype([
+    ("policy", "<i4"), ("status", "<i4"), ("result", capacity_dtype), ("has_gain", "<i4"),
+    ("reserved", "<i4"), ("gain", "<f8"), ("gain_text", "S16")])
 sweep_cell_dtype = np.dtype([
     ("workload", workload_dtype), ("cfg", cfg_dtype), ("spec", replay_spec_dtype),
     ("seed", "<u8"), ("qps_min", "<i4"), ("qps_max", "<i4"), ("slo_p99_ttft_s", "<f8"),
@@ -101,7 +106,13 @@ PROVISION_STATIC, PROVISION_PREEMPT, PROVISION_RELIEF = 0, 1, 2
 closed_loop_run_dtype = np.dtype([
     ("n_instances", "<i4"), ("objective", "<i4"), ("cfg", "<i4"), ("n_requests", "<i4"),
     ("req_off", "<i8"), ("provision_kind", "<i4"), ("max_instances", "<i4"),
-    ("threshold_s", "<f8"), ("cold_start_s", "<f8"), ("cooldown_s", "<f8")])
+    ("threshold_s", "<f8"), ("cold_start_s", "<f8"), ("cooldown_s", "<f8"),
+    ("policy", "<i4"), ("reserved", "<i4"), ("policy_seed", "<u8"), ("dispatch_overhead_s", "<f8")])
+sweep_row_dtype = np.dtype([
+    ("policy", "<i4"), ("ok", "<i4"), ("qps", "<f8"), ("seed", "<u8"), ("status", "<i4"),
+    ("finished_requests", "<i4"), ("mean_ttft_s", "<f8"), ("p99_ttft_s", "<f8"),
+    ("mean_e2e_s", "<f8"), ("p99_e2e_s", "<f8"), ("throughput_rps", "<f8"),
+    ("total_preemptions", "<i8"), ("free_blocks_var_avg", "<f8")])
 outcome_dtype = np.dtype([
     ("arrival_ticks", "<i8"), ("dispatch_ticks", "<i8"), ("first_token_ticks", "<i8"),
     ("finish_ticks", "<i8"), ("instance", "<i4"), ("preempt_count", "<i4"),
@@ -175,7 +186,8 @@ def make_workload(count=1000, trace_seed=1234, prompt_median=230.0, prompt_sigma
 
 def make_replay_spec(n_instances, policy=POLICY_BLOCK_PREDICTIVE, objective=0, capture=1,
                      policy_seed=0, provision_kind=PROVISION_STATIC, max_instances=None,
-                     threshold_s=70.0, cold_start_s=30.0, cooldown_s=15.0) -> np.ndarray:
+                     threshold_s=70.0, cold_start_s=30.0, cooldown_s=15.0,
+                     dispatch_overhead_s=0.0) -> np.ndarray:
     """ExperimentSpec subset + ProvisionPolicy (autoscaler.h:10-27) defaults."""
     s = np.zeros(1, replay_spec_dtype)
     s["n_instances"], s["policy"], s["objective"] = n_instances, policy, objective
@@ -183,6 +195,7 @@ def make_replay_spec(n_instances, policy=POLICY_BLOCK_PREDICTIVE, objective=0, c
     s["provision_kind"] = provision_kind
     s["max_instances"] = n_instances if max_instances is None else max_instances
     s["threshold_s"], s["cold_start_s"], s["cooldown_s"] = threshold_s, cold_start_s, cooldown_s
+    s["dispatch_overhead_s"] = dispatch_overhead_s
     return s
 
 

@@ -405,7 +405,7 @@ class LiveInstance {
 struct Ev {
   int64_t t;
   uint64_t seq;
-  int32_t kind;  // 0 arrival, 1 batch complete
+  int32_t kind;  // 0 arrival, 1 batch complete, 2 provision complete, 3 dispatch (landing)
   int32_t a;
   bool operator>(const Ev& o) const { return t != o.t ? t > o.t : seq > o.seq; }
 };
@@ -443,6 +443,7 @@ class Replay {
     active_ = spec.n_instances;
     next_instance_id_ = spec.n_instances;
     out_.resize(recs_.size());
+    land_inst_.assign(recs_.size(), -1);
     for (size_t i = 0; i < recs_.size(); ++i) {
       out_[i] = bsg_request_outcome{recs_[i].arrival, -1, -1, -1, -1, 0};
       push(recs_[i].arrival, 0, static_cast<int32_t>(i));
@@ -464,8 +465,10 @@ class Replay {
       const Ev ev = q_.top();
       q_.pop();
       now_ = ev.t;
-      const bsg_status st =
-          ev.kind == 0 ? arrival(ev.a) : (ev.kind == 1 ? complete(ev.a) : provision_complete(ev.a));
+      const bsg_status st = ev.kind == 0   ? arrival(ev.a)
+                            : ev.kind == 1 ? complete(ev.a)
+                            : ev.kind == 2 ? provision_complete(ev.a)
+                                           : land(ev.a);
       if (st != BSG_OK) return st;
       open = true;
     }
@@ -473,6 +476,11 @@ class Replay {
   }
 
   const std::vector<bsg_request_outcome>& outcomes() const { return out_; }
+  // means over dispatch points of the snapshot free-block mean / variance (metrics.cpp:79-86)
+  void balance(double* mean_avg, double* var_avg) const {
+    *mean_avg = n_points_ ? fm_sum_ / static_cast<double>(n_points_) : 0.0;
+    *var_avg = n_points_ ? fv_sum_ / static_cast<double>(n_points_) : 0.0;
+  }
   void summary(bsg_replay_summary* s) const {
     s->total_preemptions = preemptions_;
     s->end_ticks = now_;
@@ -544,6 +552,20 @@ class Replay {
     batch_.resize(n);
     for (int i = 0; i < n; ++i)
       inst_[i].snapshot(&snaps_run_[i], &snaps_wait_[i], &free_[i], &batch_[i]);
+    {  // memory-balance sample before this dispatch lands (driver.cpp:142-157)
+      double mean = 0;
+      for (int i = 0; i < n; ++i) mean += free_[i];
+      mean /= static_cast<double>(n);
+      double var = 0;
+      for (int i = 0; i < n; ++i) {
+        const double d = free_[i] - mean;
+        var += d * d;
+      }
+      var /= static_cast<double>(n);
+      fm_sum_ += mean;
+      fv_sum_ += var;
+      n_points_ += 1;
+    }
     int32_t chosen = 0;
     bool have_prediction = false;
     const bsg_status st = decide(rid, &chosen, &have_prediction);
@@ -559,11 +581,26 @@ class Replay {
       }
       maybe_provision(1, static_cast<double>(e2e) * 1e-9);
     }
-    const Record& r = recs_[rid];
-    inst_[chosen].admit(rid, r.prompt, r.output, r.est);
-    out_[rid].dispatch_ticks = now_;
     out_[rid].instance = chosen;
+    if (spec_.dispatch_overhead_s == 0) {  // driver.cpp:213-218
+      admit_to_instance(rid, chosen);
+    } else {
+      land_inst_[rid] = chosen;
+      push(now_ + ticks_from_seconds(spec_.dispatch_overhead_s), 3, rid);
+    }
     return BSG_OK;
+  }
+
+  // kDispatch: the request lands at its instance after the overhead (handle_dispatch)
+  bsg_status land(int32_t rid) {
+    admit_to_instance(rid, land_inst_[rid]);
+    return BSG_OK;
+  }
+
+  void admit_to_instance(int32_t rid, int32_t iid) {  // driver.cpp:224-231
+    const Record& r = recs_[rid];
+    inst_[iid].admit(rid, r.prompt, r.output, r.est);
+    out_[rid].dispatch_ticks = now_;
   }
 
   // Dispatcher::dispatch (scheduler.cpp:115-152) with the heuristics of
@@ -696,6 +733,9 @@ class Replay {
   std::vector<LiveInstance> inst_;
   std::vector<QpmWindow> qpm_;
   std::vector<bsg_request_outcome> out_;
+  std::vector<int32_t> land_inst_;  // overhead mode: the instance a request lands at
+  double fm_sum_ = 0, fv_sum_ = 0;
+  int64_t n_points_ = 0;
   std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> q_;
   uint64_t seq_ = 0;
   int64_t now_ = 0;
@@ -779,7 +819,8 @@ bsg_status bsg_trace_workload(const bsg_trace_record* recs, int64_t n, const bsg
 namespace {
 bsg_status replay_records(bsg_ctx* ctx, std::vector<Record> recs, const bsg_instance_cfg* cfg,
                           const bsg_replay_spec* spec, bsg_request_outcome* outcomes,
-                          bsg_replay_summary* summary, bsg_capture** capture);
+                          bsg_replay_summary* summary, bsg_capture** capture,
+                          bsg_run_report* report = nullptr);
 }
 
 bsg_status bsg_replay_trace(bsg_ctx* ctx, const bsg_trace_record* recs, int64_t n,
@@ -806,11 +847,13 @@ bsg_status bsg_replay(bsg_ctx* ctx, const bsg_workload* w, const bsg_instance_cf
 namespace {
 bsg_status replay_records(bsg_ctx* ctx, std::vector<Record> recs, const bsg_instance_cfg* cfg,
                           const bsg_replay_spec* spec, bsg_request_outcome* outcomes,
-                          bsg_replay_summary* summary, bsg_capture** capture) {
+                          bsg_replay_summary* summary, bsg_capture** capture,
+                          bsg_run_report* report) {
   // validate_provision_policy (autoscaler.cpp:23-34) and config.cpp:177-180
   if (spec->provision_kind < 0 || spec->provision_kind > 2 || !(spec->threshold_s > 0) ||
       spec->cold_start_s < 0 || spec->cooldown_s < 0 ||
-      (spec->provision_kind != 0 && spec->max_instances < spec->n_instances))
+      (spec->provision_kind != 0 && spec->max_instances < spec->n_instances) ||
+      !(spec->dispatch_overhead_s >= 0))  // config.cpp:189-190
     return BSG_BAD_CONFIG;
   int32_t bi = 0, fc = 0;
   bsg_status st = bsg_set_configs(ctx, cfg, 1, &bi, &fc);
@@ -827,6 +870,12 @@ bsg_status replay_records(bsg_ctx* ctx, std::vector<Record> recs, const bsg_inst
     std::memcpy(outcomes, replay.outcomes().data(),
                 replay.outcomes().size() * sizeof(bsg_request_outcome));
   if (summary) replay.summary(summary);
+  if (report) {  // aggregate (metrics.cpp:21-124) incl. the dispatch-point balance
+    bsg_replay_summary sm{};
+    replay.summary(&sm);
+    bsg_aggregate(replay.outcomes().data(), static_cast<int64_t>(replay.outcomes().size()), &sm, report);
+    replay.balance(&report->free_blocks_mean_avg, &report->free_blocks_var_avg);
+  }
   if (capture) *capture = cap.release();
   return BSG_OK;
 }
@@ -878,13 +927,14 @@ extern "C" bsg_status bsg_aggregate(const bsg_request_outcome* o, int64_t n,
                                     const bsg_replay_summary* summary, bsg_run_report* out) {
   if (!o || !out || n < 0) return BSG_INVALID_ARGUMENT;
   std::memset(out, 0, sizeof(*out));
-  std::vector<double> ttft, e2e;
+  std::vector<double> ttft, e2e, overhead;
   int64_t first_arrival = INT64_MAX, last_finish = INT64_MIN;
   for (int64_t i = 0; i < n; ++i) {
     first_arrival = std::min(first_arrival, o[i].arrival_ticks);
     if (o[i].finish_ticks >= 0 && o[i].dispatch_ticks >= 0 && o[i].first_token_ticks >= 0) {
       ttft.push_back(static_cast<double>(o[i].first_token_ticks - o[i].dispatch_ticks) * 1e-9);
       e2e.push_back(static_cast<double>(o[i].finish_ticks - o[i].arrival_ticks) * 1e-9);
+      overhead.push_back(static_cast<double>(o[i].dispatch_ticks - o[i].arrival_ticks) * 1e-9);
       last_finish = std::max(last_finish, o[i].finish_ticks);
       ++out->finished_requests;
     } else {
@@ -897,6 +947,7 @@ extern "C" bsg_status bsg_aggregate(const bsg_request_outcome* o, int64_t n,
   out->mean_e2e_s = mean_of(e2e);
   out->p50_e2e_s = nearest_rank(e2e, 50.0);
   out->p99_e2e_s = nearest_rank(e2e, 99.0);
+  out->mean_overhead_s = mean_of(overhead);
   if (n > 0 && out->finished_requests > 0 && last_finish > first_arrival)
     out->throughput_rps = static_cast<double>(out->finished_requests) /
                           (static_cast<double>(last_finish - first_arrival) * 1e-9);
@@ -1047,7 +1098,9 @@ bsg_status run_points_device(bsg_ctx* ctx, const bsg_sweep_cell* cells, const st
     runs.push_back(bsg_closed_loop_run{c.spec.n_instances, c.spec.objective, pts[i].cell,
                                        static_cast<int32_t>(recs[i].size()), static_cast<int64_t>(p.size()),
                                        c.spec.provision_kind, c.spec.max_instances, c.spec.threshold_s,
-                                       c.spec.cold_start_s, c.spec.cooldown_s});
+                                       c.spec.cold_start_s, c.spec.cooldown_s, c.spec.policy, 0,
+                                       c.seed /* spec_for_cell: policy seed = seed */,
+                                       c.spec.dispatch_overhead_s});
     run_pt.push_back(i);
     for (const Record& r : recs[i]) {
       p.push_back(r.prompt);
@@ -1156,9 +1209,9 @@ extern "C" bsg_status bsg_sweep_run(int device, const bsg_sweep_cell* cells, int
   {
     bool device_ok = n_cells > 0 && std::getenv("BSG_SWEEP_HOST") == nullptr;
     for (int32_t c = 0; c < n_cells && device_ok; ++c)
-      device_ok = cells[c].spec.policy == BSG_POLICY_BLOCK_PREDICTIVE &&
-                  cells[c].spec.n_instances >= 1 && cells[c].spec.n_instances <= 256 &&
-                  (cells[c].spec.provision_kind == 0 || cells[c].spec.max_instances <= 256);
+      device_ok = cells[c].spec.n_instances >= 1 && cells[c].spec.n_instances <= 256 &&
+                  (cells[c].spec.provision_kind == 0 || cells[c].spec.max_instances <= 256) &&
+                  cells[c].cfg.max_batch_size <= 256;
     if (device_ok) return sweep_device(device, cells, n_cells, threads, out);
   }
   // Every closed loop of every cell is independent, so schedule at (cell, qps)
@@ -1280,5 +1333,239 @@ extern "C" bsg_status bsg_sweep_run(int device, const bsg_sweep_cell* cells, int
     for (size_t j = 0; j < tenths[c].size(); ++j)
       if (tpass[c][j] == 1) o.result.capacity_qps = std::max(o.result.capacity_qps, tenths[c][j]);
   }
+  return BSG_OK;
+}
+
+// ---- run_sweep / run_capacity (driver.cpp:333-427) ------------------------------
+namespace {
+
+bool fits_device(const bsg_instance_cfg& cfg, const bsg_replay_spec& sp) {
+  return sp.n_instances >= 1 && sp.n_instances <= 256 &&
+         (sp.provision_kind == 0 || sp.max_instances <= 256) && cfg.max_batch_size <= 256;
+}
+
+// spec_for_cell (driver.cpp:321-331): policy, its seed, the workload's qps and
+// arrival seed, and the estimator's seed.
+void apply_cell(bsg_workload* w, bsg_replay_spec* sp, int32_t policy, double qps, uint64_t seed) {
+  w->qps = qps;
+  w->arrival_seed = seed;
+  w->estimator_seed = seed;
+  sp->policy = policy;
+  sp->policy_seed = seed;
+  sp->capture = 0;
+}
+
+// Independent run_experiment points, each aggregated (metrics.cpp:21-124):
+// device-resident closed loops (batched launches of bounded arena) when every
+// point fits K5, else host closed loops on `threads` threads.
+bsg_status run_reports(int device, const bsg_instance_cfg& cfg, const std::vector<bsg_workload>& ws,
+                       const std::vector<bsg_replay_spec>& sps, int32_t threads,
+                       std::vector<int32_t>* status, std::vector<bsg_run_report>* reps) {
+  const size_t np = ws.size();
+  status->assign(np, BSG_OK);
+  reps->assign(np, bsg_run_report{});
+  if (np == 0) return BSG_OK;
+  bool device_ok = std::getenv("BSG_SWEEP_HOST") == nullptr;
+  for (const bsg_replay_spec& sp : sps) device_ok = device_ok && fits_device(cfg, sp);
+  threads = std::max<int32_t>(1, threads);
+  if (!device_ok) {
+    std::atomic<size_t> next{0};
+    std::atomic<int> fatal{BSG_OK};
+    auto worker = [&]() {
+      bsg_ctx* ctx = nullptr;
+      const bsg_status cs = bsg_ctx_create(device, &ctx);
+      if (cs != BSG_OK) {
+        fatal = cs;
+        return;
+      }
+      for (size_t i; (i = next.fetch_add(1)) < np;) {
+        std::vector<Record> recs;
+        bsg_status st = make_records(ws[i], &recs);
+        if (st == BSG_OK) {
+          const size_t n = recs.size();
+          std::vector<bsg_request_outcome> o(n);
+          bsg_replay_summary sm{};
+          st = replay_records(ctx, std::move(recs), &cfg, &sps[i], o.data(), &sm, nullptr, &(*reps)[i]);
+        }
+        (*status)[i] = st;
+      }
+      bsg_ctx_destroy(ctx);
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < std::min<int>(threads, static_cast<int>(np)); ++t) pool.emplace_back(worker);
+    for (auto& th : pool) th.join();
+    return static_cast<bsg_status>(fatal.load());
+  }
+  bsg_ctx* ctx = nullptr;
+  bsg_status st = bsg_ctx_create(device, &ctx);
+  if (st != BSG_OK) return st;
+  std::unique_ptr<bsg_ctx, void (*)(bsg_ctx*)> guard(ctx, bsg_ctx_destroy);
+  int32_t bi = 0, fc = 0;
+  st = bsg_set_configs(ctx, &cfg, 1, &bi, &fc);
+  if (st != BSG_OK) return st;
+  std::vector<std::vector<Record>> recs(np);
+  std::vector<int32_t> gen_err(np, BSG_OK);
+  {
+    std::atomic<size_t> next{0};
+    auto work = [&]() {
+      for (size_t i; (i = next.fetch_add(1)) < np;) gen_err[i] = make_records(ws[i], &recs[i]);
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < std::min<int>(threads, static_cast<int>(np)); ++t) pool.emplace_back(work);
+    for (auto& th : pool) th.join();
+  }
+  // longest first (blocks are dispatched in index order); launches of bounded arena
+  std::vector<size_t> order;
+  for (size_t i = 0; i < np; ++i) {
+    if (gen_err[i] != BSG_OK) (*status)[i] = gen_err[i];
+    else order.push_back(i);
+  }
+  auto cost = [&](size_t i) {
+    const double ni = sps[i].n_instances;
+    return static_cast<double>(recs[i].size()) * ni * (1.0 + ws[i].qps / ni);
+  };
+  std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return cost(a) > cost(b); });
+  size_t o0 = 0;
+  while (o0 < order.size()) {
+    std::vector<bsg_closed_loop_run> runs;
+    std::vector<int32_t> p, o, e;
+    std::vector<int64_t> t;
+    int64_t arena = 0;
+    size_t o1 = o0;
+    for (; o1 < order.size(); ++o1) {
+      const size_t i = order[o1];
+      const bsg_replay_spec& sp = sps[i];
+      const int64_t slots = sp.provision_kind == 0 ? sp.n_instances : sp.max_instances;
+      const int64_t need = slots * (2 * static_cast<int64_t>(cfg.max_batch_size) + static_cast<int64_t>(recs[i].size()));
+      if (o1 > o0 && arena + need >= (int64_t{1} << 30)) break;
+      arena += need;
+      runs.push_back(bsg_closed_loop_run{sp.n_instances, sp.objective, 0, static_cast<int32_t>(recs[i].size()),
+                                         static_cast<int64_t>(p.size()), sp.provision_kind, sp.max_instances,
+                                         sp.threshold_s, sp.cold_start_s, sp.cooldown_s, sp.policy, 0,
+                                         sp.policy_seed, sp.dispatch_overhead_s});
+      for (const Record& r : recs[i]) {
+        p.push_back(r.prompt);
+        o.push_back(r.output);
+        e.push_back(r.est);
+        t.push_back(r.arrival);
+      }
+    }
+    std::vector<bsg_run_report> rr(runs.size());
+    std::vector<int32_t> rs(runs.size(), BSG_OK);
+    st = bsg_replay_device(ctx, runs.data(), static_cast<int32_t>(runs.size()), p.data(), o.data(), e.data(),
+                           t.data(), static_cast<int64_t>(p.size()), nullptr, nullptr, rs.data(), rr.data());
+    if (st == BSG_BAD_CONFIG || st == BSG_TOO_LARGE_CANDIDATE || st == BSG_BAD_INPUT) {
+      // a descriptor-level rejection: attribute it to every run of the batch
+      for (size_t q = o0; q < o1; ++q) (*status)[order[q]] = st;
+    } else if (st != BSG_OK) {
+      return st;
+    } else {
+      for (size_t q = o0; q < o1; ++q) {
+        (*status)[order[q]] = rs[q - o0];
+        (*reps)[order[q]] = rr[q - o0];
+      }
+    }
+    o0 = o1;
+  }
+  return BSG_OK;
+}
+
+void format_percent(double fraction, char* out) {  // driver.cpp:392-396
+  std::snprintf(out, 16, "%.1f%%", fraction * 100.0);
+}
+
+}  // namespace
+
+extern "C" bsg_status bsg_run_sweep(int device, const bsg_workload* base, const bsg_instance_cfg* cfg,
+                                    const bsg_replay_spec* spec, const int32_t* policies, int32_t n_policies,
+                                    const double* qps_values, int32_t n_qps, const uint64_t* seeds,
+                                    int32_t n_seeds, int32_t threads, bsg_sweep_row* rows) {
+  if (!base || !cfg || !spec || !rows || n_policies < 0 || n_qps < 0 || n_seeds < 0 ||
+      (n_policies && !policies) || (n_qps && !qps_values) || (n_seeds && !seeds))
+    return BSG_INVALID_ARGUMENT;
+  std::vector<bsg_workload> ws;
+  std::vector<bsg_replay_spec> sps;
+  for (int32_t a = 0; a < n_policies; ++a) {
+    if (policies[a] < BSG_POLICY_RANDOM || policies[a] > BSG_POLICY_BLOCK_PREDICTIVE) return BSG_BAD_CONFIG;
+    for (int32_t b = 0; b < n_qps; ++b)
+      for (int32_t c = 0; c < n_seeds; ++c) {  // the reference's cell order (driver.cpp:339-345)
+        bsg_workload w = *base;
+        bsg_replay_spec sp = *spec;
+        apply_cell(&w, &sp, policies[a], qps_values[b], seeds[c]);
+        ws.push_back(w);
+        sps.push_back(sp);
+      }
+  }
+  std::vector<int32_t> st;
+  std::vector<bsg_run_report> reps;
+  const bsg_status s = run_reports(device, *cfg, ws, sps, threads, &st, &reps);
+  if (s != BSG_OK) return s;
+  for (size_t i = 0; i < ws.size(); ++i) {
+    bsg_sweep_row& r = rows[i];
+    std::memset(&r, 0, sizeof(r));
+    r.policy = sps[i].policy;
+    r.qps = ws[i].qps;
+    r.seed = sps[i].policy_seed;
+    r.status = st[i];
+    r.ok = st[i] == BSG_OK ? 1 : 0;
+    if (!r.ok) continue;
+    const bsg_run_report& p = reps[i];
+    r.mean_ttft_s = p.mean_ttft_s;
+    r.p99_ttft_s = p.p99_ttft_s;
+    r.mean_e2e_s = p.mean_e2e_s;
+    r.p99_e2e_s = p.p99_e2e_s;
+    r.throughput_rps = p.throughput_rps;
+    r.total_preemptions = p.total_preemptions;
+    r.finished_requests = p.finished_requests;
+    r.free_blocks_var_avg = p.free_blocks_var_avg;
+  }
+  return BSG_OK;
+}
+
+extern "C" bsg_status bsg_run_capacity(int device, const bsg_workload* base, const bsg_instance_cfg* cfg,
+                                       const bsg_replay_spec* spec, const int32_t* policies,
+                                       int32_t n_policies, int32_t baseline, uint64_t seed, int32_t qps_min,
+                                       int32_t qps_max, double slo_p99_ttft_s, int32_t threads,
+                                       bsg_capacity_row* rows, int32_t* n_rows, double* baseline_capacity) {
+  if (!base || !cfg || !spec || !rows || !n_rows || n_policies < 0 || (n_policies && !policies))
+    return BSG_INVALID_ARGUMENT;
+  std::vector<int32_t> pol(policies, policies + n_policies);
+  if (std::find(pol.begin(), pol.end(), baseline) == pol.end()) pol.push_back(baseline);
+  for (int32_t p : pol)
+    if (p < BSG_POLICY_RANDOM || p > BSG_POLICY_BLOCK_PREDICTIVE) return BSG_BAD_CONFIG;
+  // one capacity_search cell per policy (driver.cpp:404-416), all batched together
+  std::vector<bsg_sweep_cell> cells(pol.size());
+  for (size_t i = 0; i < pol.size(); ++i) {
+    bsg_sweep_cell& c = cells[i];
+    c.workload = *base;
+    c.cfg = *cfg;
+    c.spec = *spec;
+    c.spec.policy = pol[i];
+    c.spec.capture = 0;
+    c.seed = seed;
+    c.qps_min = qps_min;
+    c.qps_max = qps_max;
+    c.slo_p99_ttft_s = slo_p99_ttft_s;
+  }
+  std::vector<bsg_sweep_out> out(pol.size());
+  const bsg_status st = bsg_sweep_run(device, cells.data(), static_cast<int32_t>(cells.size()), threads, out.data());
+  if (st != BSG_OK) return st;
+  double base_cap = 0;
+  for (size_t i = 0; i < pol.size(); ++i)
+    if (pol[i] == baseline && out[i].status == BSG_OK) base_cap = out[i].result.capacity_qps;
+  for (size_t i = 0; i < pol.size(); ++i) {
+    bsg_capacity_row& r = rows[i];
+    std::memset(&r, 0, sizeof(r));
+    r.policy = pol[i];
+    r.status = out[i].status;
+    r.result = out[i].result;
+    if (pol[i] != baseline && base_cap > 0 && out[i].status == BSG_OK) {
+      r.has_gain = 1;
+      r.gain = (r.result.capacity_qps - base_cap) / base_cap;
+      format_percent(r.gain, r.gain_text);
+    }
+  }
+  *n_rows = static_cast<int32_t>(pol.size());
+  if (baseline_capacity) *baseline_capacity = base_cap;
   return BSG_OK;
 }

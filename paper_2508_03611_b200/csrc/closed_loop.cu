@@ -59,6 +59,10 @@ struct ClRun {
   int32_t prov_kind, max_inst;
   double threshold_s;
   int64_t cold_start_ticks, cooldown_ticks;
+  int32_t policy;            // bsg_policy (scheduler.h:16-23)
+  int32_t immediate;         // dispatch_overhead_s == 0: admit at the decision
+  uint64_t policy_seed;      // Random's SplitMix64 stream
+  int64_t overhead_ticks;    // SimTime::from_seconds(dispatch_overhead_s)
 };
 
 // Live-state SoA columns.
@@ -68,12 +72,12 @@ struct Arena {
 
 struct ClInst {
   int32_t n;           // running members R[0, n)
-  int32_t whead;       // waiting = A[whead, wtail)
-  int32_t wtail;
+  int32_t whead;       // waiting = A[whead, wland)
+  int32_t wtail;       // A[wland, wtail): dispatched, still in flight (overhead mode)
   int32_t free_blocks;
   int64_t t_done;      // completion time of the current step
   int32_t mid;         // mid-step
-  int32_t pad;
+  int32_t wland;       // end of the landed waiting requests
 };
 
 // Instance i of a run: R at base, A at base + maxb (A's first maxb slots are
@@ -90,7 +94,7 @@ __device__ int32_t live_begin(const DevCfg& cfg, const Arena& ar, int64_t Rb, in
                               unsigned long long* preempts) {
   constexpr int CAP = 32 * K;
   const int lane = lane_id();
-  const int32_t n = st.n, whead = st.whead, wtail = st.wtail;
+  const int32_t n = st.n, whead = st.whead, wtail = st.wland;
   int32_t free_blocks = st.free_blocks;
   const int32_t maxb = cfg.max_batch_size;
   const bool chunked = cfg.local_policy == BSG_CHUNKED_PREFILL;
@@ -400,6 +404,13 @@ struct ClShared {
   // metric pipeline (aggregate, metrics.cpp:21-124, and the per-dispatch
   // free-block balance, driver.cpp:142-157)
   int32_t snap_free[kClMaxInst];
+  // heuristic dispatch (pick_heuristic, scheduler.cpp:68-113)
+  double hscore[kClMaxInst];
+  int32_t qpm[kClMaxInst];      // dispatches of the last 60 s per instance (QpmTracker)
+  int32_t qhead;                // oldest request still inside the QPM window
+  int32_t chosen;
+  unsigned long long rng;       // Random's SplitMix64 state (rand.h:11-56)
+  unsigned long long rr;        // RoundRobin's cursor
   double fm_sum, fv_sum;
   int32_t n_points;
   int32_t hist[256];
@@ -503,18 +514,20 @@ __device__ void block_report(ClShared<K>& S, const bsg_request_outcome* outs, in
   }
   if (threadIdx.x != 0) return;
   // means: summed in request order, as the reference does
-  double st = 0, se = 0;
+  double st = 0, se = 0, so = 0;
   for (int32_t q = 0; q < N; ++q) {
     const bsg_request_outcome o = outs[q];
     if (!finished(o)) continue;
     st = __dadd_rn(st, static_cast<double>(ttft_ticks(o)) * 1e-9);
     se = __dadd_rn(se, static_cast<double>(e2e_ticks(o)) * 1e-9);
+    so = __dadd_rn(so, static_cast<double>(o.dispatch_ticks - o.arrival_ticks) * 1e-9);
   }
   r.finished_requests = static_cast<int32_t>(n_fin);
   r.censored_requests = N - static_cast<int32_t>(n_fin);
   if (n_fin > 0) {
     r.mean_ttft_s = st / static_cast<double>(n_fin);
     r.mean_e2e_s = se / static_cast<double>(n_fin);
+    r.mean_overhead_s = so / static_cast<double>(n_fin);
     const int64_t first = static_cast<int64_t>(S.min_arr), last = static_cast<int64_t>(S.max_fin);
     if (N > 0 && last > first)
       r.throughput_rps = static_cast<double>(n_fin) / (static_cast<double>(last - first) * 1e-9);
@@ -542,8 +555,13 @@ __device__ __forceinline__ void autoscale(ClShared<K>& S, const ClRun& run, int3
   S.pend[S.n_pend++] = now + run.cold_start_ticks;
 }
 
+// Wide member lists (K >= 4: max_batch_size > 64) hold 4-8 members per lane in
+// registers; at 2 blocks per SM (128 registers) they spilled 150-1800 B per
+// thread, so they get one block per SM and the full register file.
+__host__ __device__ constexpr int cl_min_blocks(int K) { return K >= 4 ? 1 : BSG_CL_MINB; }
+
 template <int K, bool POW2>
-__global__ void __launch_bounds__(kClWarps * 32, BSG_CL_MINB)
+__global__ void __launch_bounds__(kClWarps * 32, cl_min_blocks(K))
     closed_loop_kernel(const DevCfg* __restrict__ cfgs, const ClRun* __restrict__ runs,
                        const int32_t* __restrict__ rq_prompt, const int32_t* __restrict__ rq_output,
                        const int32_t* __restrict__ rq_est, const int64_t* __restrict__ rq_arrival,
@@ -573,6 +591,7 @@ __global__ void __launch_bounds__(kClWarps * 32, BSG_CL_MINB)
     s.n = 0;
     s.whead = maxb;
     s.wtail = maxb;
+    s.wland = maxb;
     s.free_blocks = cfg.total_blocks;
     s.t_done = 0;
     s.mid = 0;
@@ -589,13 +608,28 @@ __global__ void __launch_bounds__(kClWarps * 32, BSG_CL_MINB)
     S.fm_sum = 0;
     S.fv_sum = 0;
     S.n_points = 0;
+    S.qhead = 0;
+    S.rng = run.policy_seed;
+    S.rr = 0;
   }
+  for (int i = threadIdx.x; i < IMAX; i += blockDim.x) S.qpm[i] = 0;
   __syncthreads();
   const bool relief = run.prov_kind == 2;
   int64_t last_done = 0;  // this warp's latest processed completion
   int64_t relief_after = 0;  // relief: earliest trigger time the cooldown allows
   // close the instant tc (its completions, then end_of_instant's begin_step) and
   // advance through every completion strictly before t
+  // overhead mode: the next in-flight request of instance s lands at its
+  // arrival + overhead (kDispatch, driver.cpp:216-231); landings of one
+  // instance are in dispatch order
+  auto next_land = [&](const ClInst& s, int64_t Ab) -> int64_t {
+    if (s.wland >= s.wtail) return kNever;
+    return arrival[__ldcg(&ar.rid[Ab + s.wland])] + run.overhead_ticks;
+  };
+  // close the instant tc (its completions and landings — events at tc after
+  // that instant's arrivals — then end_of_instant's begin_step) and advance
+  // through every event strictly before t. A landing and a completion of the
+  // same instance at one instant commute (finish_step does not read waiting_).
   auto advance = [&](int32_t i, int64_t tc, int64_t t) -> int32_t {
     ClInst& s = S.inst[i];
     const int64_t Rb = run.arena_off + i * stride;
@@ -606,17 +640,24 @@ __global__ void __launch_bounds__(kClWarps * 32, BSG_CL_MINB)
                              relief ? &S.cand_min : nullptr);
         last_done = max(last_done, tc);
       }
-      if (!s.mid && (s.n > 0 || s.whead < s.wtail)) {
+      while (next_land(s, Ab) == tc) s.wland += 1;
+      if (!s.mid && (s.n > 0 || s.whead < s.wland)) {
         const int32_t e = live_begin<K, POW2>(live_cfg, ar, Rb, Ab, s, tc, outs, &S.preempts);
         if (e != BSG_OK) return e;
       }
     }
-    while (s.mid && s.t_done < t) {
-      const int64_t now = s.t_done;
-      live_finish<K, POW2>(cfg, ar, Rb, s, now, outs, run.threshold_s, relief_after,
-                           relief ? &S.cand_min : nullptr);
+    for (;;) {
+      const int64_t tl = next_land(s, Ab);
+      const int64_t td = s.mid ? s.t_done : kNever;
+      const int64_t now = min(tl, td);
+      if (now >= t) break;
+      if (td == now) {
+        live_finish<K, POW2>(cfg, ar, Rb, s, now, outs, run.threshold_s, relief_after,
+                             relief ? &S.cand_min : nullptr);
+      }
+      while (next_land(s, Ab) == now) s.wland += 1;
       last_done = max(last_done, now);
-      if (s.n > 0 || s.whead < s.wtail) {
+      if (!s.mid && (s.n > 0 || s.whead < s.wland)) {
         const int32_t e = live_begin<K, POW2>(live_cfg, ar, Rb, Ab, s, now, outs, &S.preempts);
         if (e != BSG_OK) return e;
       }
@@ -694,30 +735,64 @@ __global__ void __launch_bounds__(kClWarps * 32, BSG_CL_MINB)
       __syncthreads();
     }
     const int32_t I = S.active;
-    // ---- dispatch: per-instance what-ifs (predict_across) + argmin ----
-    if (threadIdx.x == 0) S.next = 0;
+    // ---- dispatch: per-instance what-ifs (predict_across) + argmin, or the
+    // heuristic scores of pick_heuristic (scheduler.cpp:68-113) ----
+    const bool bp = run.policy == BSG_POLICY_BLOCK_PREDICTIVE;
+    if (threadIdx.x == 0) {
+      S.next = 0;
+      if (run.policy == BSG_POLICY_MIN_QPM) {  // QpmTracker: dispatches strictly younger than 60 s
+        const int64_t cutoff = t - 60000000000LL;
+        while (S.qhead < k && arrival[S.qhead] <= cutoff) {
+          S.qpm[outs[S.qhead].instance] -= 1;
+          S.qhead += 1;
+        }
+      }
+    }
     __syncthreads();
     const int32_t cp = rq_prompt[run.req_off + k], ce = rq_est[run.req_off + k];
+    const bool need_stats = reports || run.policy == BSG_POLICY_INFAAS_PP ||
+                            run.policy == BSG_POLICY_LLUMNIX_MINUS;
     for (;;) {
       int32_t i = 0;
       if (lane == 0) i = atomicAdd(&S.next, 1);
       i = __shfl_sync(kFull, i, 0);
       if (i >= I) break;
       const ClInst& s = S.inst[i];
-      if (reports) {  // the snapshot's free blocks (backend.cpp:357-365): total - sum held(stored)
+      if (need_stats) {  // the snapshot's free blocks (backend.cpp:357-365): total - sum held(stored)
         int32_t held = 0;
         for (int32_t p = lane; p < s.n; p += 32) {
           const int64_t g = run.arena_off + i * stride + p;
           held += bnt<POW2>(__ldcg(&ar.prefill[g]) + __ldcg(&ar.decoded[g]), cfg);
         }
         held = static_cast<int32_t>(__reduce_add_sync(kFull, static_cast<uint32_t>(held)));
-        if (lane == 0) S.snap_free[i] = cfg.total_blocks - held;
+        const int32_t snap_free = cfg.total_blocks - held;
+        if (lane == 0) S.snap_free[i] = snap_free;
+        if (!bp) {
+          // load_infaas / load_llumnix (scheduler.cpp:33-46) over the snapshot
+          const double used = static_cast<double>(cfg.total_blocks - snap_free);
+          const double bsz = static_cast<double>(max(s.n, 1));
+          double score = 0;
+          if (run.policy == BSG_POLICY_LLUMNIX_MINUS) {
+            long long pm = 0;  // blocks_needed(prompt - prefill_progress) over waiting
+            for (int32_t q = s.whead + lane; q < s.wland; q += 32) {
+              const int64_t g = run.arena_off + i * stride + maxb + q;
+              pm += bnt<POW2>(__ldcg(&ar.prompt[g]) - __ldcg(&ar.prefill[g]), cfg);
+            }
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) pm += __shfl_xor_sync(kFull, pm, d);
+            score = __ddiv_rn(__dadd_rn(used, static_cast<double>(pm)), bsz);
+          } else if (run.policy == BSG_POLICY_INFAAS_PP) {
+            score = __ddiv_rn(used, bsz);
+          }
+          if (lane == 0) S.hscore[i] = score;
+        }
       }
+      if (!bp) continue;
       bsg_scenario sc;
       sc.run_off = static_cast<int32_t>(run.arena_off + i * stride);
       sc.run_n = s.n;
       sc.wait_off = static_cast<int32_t>(run.arena_off + i * stride + maxb + s.whead);
-      sc.wait_n = s.wtail - s.whead;
+      sc.wait_n = s.wland - s.whead;
       sc.cand_prompt = cp;
       sc.cand_est = ce;
       sc.cfg = run.cfg;
@@ -727,31 +802,86 @@ __global__ void __launch_bounds__(kClWarps * 32, BSG_CL_MINB)
           TraceSink{nullptr, 0});
     }
     __syncthreads();
-    if (warp == 0) {  // BlockPredictive argmin (scheduler.cpp:138-150)
-      int64_t best_v = INT64_MAX;
-      int32_t best_i = INT32_MAX, bad = BSG_OK;
-      for (int32_t i = lane; i < I; i += 32) {
-        const bsg_result& r = S.res[i];
-        if (r.status != BSG_OK && bad == BSG_OK) bad = r.status;
-        const int64_t v = run.objective == 1 ? r.ttft_ticks : r.e2e_ticks;
-        if (v < best_v || (v == best_v && i < best_i)) {
-          best_v = v;
-          best_i = i;
+    if (!bp) {
+      if (threadIdx.x == 0) {
+        int32_t c = 0;
+        if (run.policy == BSG_POLICY_RANDOM) {  // ids[rng.below(n)] over sorted ids
+          const unsigned long long n = static_cast<unsigned long long>(I);
+          const unsigned long long limit = ~0ull - ~0ull % n;
+          unsigned long long r;
+          do {
+            unsigned long long z = (S.rng += 0x9e3779b97f4a7c15ull);
+            z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+            z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+            r = z ^ (z >> 31);
+          } while (r >= limit);
+          c = static_cast<int32_t>(r % n);
+        } else if (run.policy == BSG_POLICY_ROUND_ROBIN) {
+          c = static_cast<int32_t>(S.rr++ % static_cast<unsigned long long>(I));
+        } else {  // lowest score, lowest id on ties (instances in id order)
+          double best = 0;
+          for (int32_t q = 0; q < I; ++q) {
+            const double v = run.policy == BSG_POLICY_MIN_QPM ? static_cast<double>(S.qpm[q]) : S.hscore[q];
+            if (q == 0 || v < best) {
+              best = v;
+              c = q;
+            }
+          }
         }
+        S.chosen = c;
       }
+      __syncthreads();
+      // heuristics carry no prediction: preempt provisioning asks for the chosen
+      // instance's (driver.cpp:202-209)
+      if (run.prov_kind == 1 && warp == 0) {
+        const int32_t i = S.chosen;
+        const ClInst& s = S.inst[i];
+        bsg_scenario sc;
+        sc.run_off = static_cast<int32_t>(run.arena_off + i * stride);
+        sc.run_n = s.n;
+        sc.wait_off = static_cast<int32_t>(run.arena_off + i * stride + maxb + s.whead);
+        sc.wait_n = s.wland - s.whead;
+        sc.cand_prompt = cp;
+        sc.cand_est = ce;
+        sc.cfg = run.cfg;
+        sc.reserved = 0;
+        simulate_scenario<K, false, false, POW2, false, false, BSG_WIN_J_CLOSED, BSG_CYC_CLOSED>(
+            cfg, ar.prompt, ar.est, ar.prefill, ar.decoded, sc, S.scratch[0], &S.res[i],
+            TraceSink{nullptr, 0});
+      }
+      __syncthreads();
+    }
+    if (warp == 0) {
+      int32_t best_i = 0, bad = BSG_OK;
+      if (bp) {  // BlockPredictive argmin (scheduler.cpp:138-150)
+        int64_t best_v = INT64_MAX;
+        best_i = INT32_MAX;
+        for (int32_t i = lane; i < I; i += 32) {
+          const bsg_result& r = S.res[i];
+          if (r.status != BSG_OK && bad == BSG_OK) bad = r.status;
+          const int64_t v = run.objective == 1 ? r.ttft_ticks : r.e2e_ticks;
+          if (v < best_v || (v == best_v && i < best_i)) {
+            best_v = v;
+            best_i = i;
+          }
+        }
 #pragma unroll
-      for (int d = 16; d > 0; d >>= 1) {
-        const int64_t ov = __shfl_xor_sync(kFull, best_v, d);
-        const int32_t oi = __shfl_xor_sync(kFull, best_i, d);
-        if (ov < best_v || (ov == best_v && oi < best_i)) {
-          best_v = ov;
-          best_i = oi;
+        for (int d = 16; d > 0; d >>= 1) {
+          const int64_t ov = __shfl_xor_sync(kFull, best_v, d);
+          const int32_t oi = __shfl_xor_sync(kFull, best_i, d);
+          if (ov < best_v || (ov == best_v && oi < best_i)) {
+            best_v = ov;
+            best_i = oi;
+          }
         }
+        bad = static_cast<int32_t>(__reduce_max_sync(kFull, static_cast<uint32_t>(bad)));
+      } else {
+        best_i = S.chosen;
+        if (run.prov_kind == 1 && S.res[best_i].status != BSG_OK) bad = S.res[best_i].status;
       }
-      bad = static_cast<int32_t>(__reduce_max_sync(kFull, static_cast<uint32_t>(bad)));
       if (bad != BSG_OK) {
         fail(bad);  // PredictionError propagates out of the run (predictor.cpp:132-136)
-      } else if (lane == 0) {  // admit the arrival at the chosen instance's waiting tail
+      } else if (lane == 0) {  // the chosen instance receives the arrival
         if (reports) {  // memory-balance sample of this dispatch (driver.cpp:142-157)
           double mean = 0;
           for (int32_t q = 0; q < I; ++q) mean = __dadd_rn(mean, static_cast<double>(S.snap_free[q]));
@@ -766,8 +896,10 @@ __global__ void __launch_bounds__(kClWarps * 32, BSG_CL_MINB)
           S.fv_sum = __dadd_rn(S.fv_sum, var);
           S.n_points += 1;
         }
+        if (run.policy == BSG_POLICY_MIN_QPM) S.qpm[best_i] += 1;  // record_dispatch
         if (run.prov_kind == 1)  // preempt provisioning on the predicted e2e (driver.cpp:197-211)
           autoscale<K>(S, run, I0, static_cast<double>(S.res[best_i].e2e_ticks) * 1e-9, t);
+        // append at the waiting tail; with overhead it lands later (driver.cpp:213-231)
         ClInst& s = S.inst[best_i];
         const int64_t g = run.arena_off + best_i * stride + maxb + s.wtail;
         ar.prompt[g] = cp;
@@ -777,7 +909,8 @@ __global__ void __launch_bounds__(kClWarps * 32, BSG_CL_MINB)
         ar.target[g] = rq_output[run.req_off + k];
         ar.rid[g] = k;
         s.wtail += 1;
-        outs[k].dispatch_ticks = t;
+        if (run.immediate) s.wland = s.wtail;
+        outs[k].dispatch_ticks = run.immediate ? t : t + run.overhead_ticks;
         outs[k].instance = best_i;
       }
     }
@@ -981,6 +1114,7 @@ __global__ void __launch_bounds__(kFleetWarps * 32)
   ar.target[g] = output;
   ar.rid[g] = k;
   c.wtail += 1;
+  c.wland = c.wtail;
   bsg_request_outcome o;
   o.arrival_ticks = now;
   o.dispatch_ticks = now;
@@ -1039,13 +1173,15 @@ extern "C" bsg_status bsg_replay_device(bsg_ctx* ctx, const bsg_closed_loop_run*
     if (x.cfg < 0 || x.cfg >= ctx->ncfg || x.n_instances < 1 || x.n_instances > kClMaxInst ||
         x.n_requests < 0 || x.req_off < 0 || x.req_off + x.n_requests > n_requests_total ||
         x.objective < 0 || x.objective > 1 || x.provision_kind < 0 || x.provision_kind > 2 ||
-        (x.provision_kind != 0 && x.max_instances > kClMaxInst)) {
+        (x.provision_kind != 0 && x.max_instances > kClMaxInst) || x.policy < BSG_POLICY_RANDOM ||
+        x.policy > BSG_POLICY_BLOCK_PREDICTIVE) {
       ctx->last_error = "bad closed-loop run descriptor";
       return BSG_INVALID_ARGUMENT;
     }
     // validate_provision_policy (autoscaler.cpp:23-34), config.cpp:177-180
     if (!(x.threshold_s > 0) || x.cold_start_s < 0 || x.cooldown_s < 0 ||
-        (x.provision_kind != 0 && x.max_instances < x.n_instances))
+        (x.provision_kind != 0 && x.max_instances < x.n_instances) ||
+        !(x.dispatch_overhead_s >= 0))  // config.cpp:189-190
       return BSG_BAD_CONFIG;
     const int32_t slots = x.provision_kind == 0 ? x.n_instances : x.max_instances;
     const bsg_instance_cfg& c = ctx->host_cfgs[x.cfg];
@@ -1063,7 +1199,9 @@ extern "C" bsg_status bsg_replay_device(bsg_ctx* ctx, const bsg_closed_loop_run*
     }
     dr[r] = ClRun{x.n_instances, x.objective, x.cfg, x.n_requests, x.req_off, arena,
                   x.provision_kind, x.provision_kind == 0 ? x.n_instances : x.max_instances,
-                  x.threshold_s, std::llround(x.cold_start_s * 1e9), std::llround(x.cooldown_s * 1e9)};
+                  x.threshold_s, std::llround(x.cold_start_s * 1e9), std::llround(x.cooldown_s * 1e9),
+                  x.policy, x.dispatch_overhead_s == 0 ? 1 : 0, x.policy_seed,
+                  std::llround(x.dispatch_overhead_s * 1e9)};
     arena += static_cast<int64_t>(slots) * (2 * static_cast<int64_t>(c.max_batch_size) + x.n_requests);
   }
   if (arena >= (int64_t{1} << 31)) {
@@ -1264,7 +1402,7 @@ extern "C" bsg_status bsg_fleet_create(bsg_ctx* ctx, int32_t cfg, int32_t n_inst
   p += b_sc;
   f->dparams = reinterpret_cast<FleetParams*>(p);
   std::vector<ClInst> init(static_cast<size_t>(n_instances));
-  for (auto& x : init) x = ClInst{0, c.max_batch_size, c.max_batch_size, c.total_blocks, 0, 0, 0};
+  for (auto& x : init) x = ClInst{0, c.max_batch_size, c.max_batch_size, c.total_blocks, 0, 0, c.max_batch_size};
   FleetDev fd0{-1, 0, 0, -1, BSG_OK, 0};
   bool ok = cudaHostAlloc(&f->pinned, 64 + static_cast<size_t>(n_instances) * 8, cudaHostAllocDefault) == cudaSuccess;
   ok = ok && cudaHostAlloc(reinterpret_cast<void**>(&f->hparams), sizeof(FleetParams), cudaHostAllocDefault) == cudaSuccess;

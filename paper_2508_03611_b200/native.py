@@ -60,6 +60,11 @@ def load() -> C.CDLL:
         "bsg_capacity_search": (C.c_int, [V, V, V, V, C.c_uint64, C.c_int32, C.c_int32, C.c_double,
                                           V, V, V, C.c_int32]),
         "bsg_sweep_run": (C.c_int, [C.c_int, V, C.c_int32, C.c_int32, V]),
+        "bsg_run_sweep": (C.c_int, [C.c_int, V, V, V, V, C.c_int32, V, C.c_int32, V, C.c_int32,
+                                    C.c_int32, V]),
+        "bsg_run_capacity": (C.c_int, [C.c_int, V, V, V, V, C.c_int32, C.c_int32, C.c_uint64,
+                                       C.c_int32, C.c_int32, C.c_double, C.c_int32, V,
+                                       C.POINTER(C.c_int32), C.POINTER(C.c_double)]),
         "bsg_scenario_count": (C.c_int64, [V]),
         "bsg_mc_lengths": (C.c_int, [C.c_int32, C.c_uint64, C.c_int32, C.c_uint64, C.c_double, V]),
         "bsg_replay_device": (C.c_int, [V, V, C.c_int32, V, V, V, V, C.c_int64, V, V, V, V]),
@@ -140,6 +145,34 @@ def sweep_run(device: int, cells: np.ndarray, threads: int = 8) -> np.ndarray:
     if st != abi.OK:
         raise BsgError(st, "bsg_sweep_run")
     return out
+
+
+def run_sweep(device: int, w, cfg, spec, policies, qps_values, seeds, threads: int = 8) -> np.ndarray:
+    """bsg_run_sweep (run_sweep, driver.cpp:333-390): one SweepCell row per
+    (policy, qps, seed), policies outermost."""
+    pol = np.ascontiguousarray(policies, np.int32)
+    qps = np.ascontiguousarray(qps_values, np.float64)
+    sd = np.ascontiguousarray(seeds, np.uint64)
+    rows = np.zeros(len(pol) * len(qps) * len(sd), abi.sweep_row_dtype)
+    st = load().bsg_run_sweep(device, _p(w), _p(cfg), _p(spec), _p(pol), len(pol), _p(qps), len(qps),
+                              _p(sd), len(sd), threads, _p(rows))
+    if st != abi.OK:
+        raise BsgError(st, "bsg_run_sweep")
+    return rows
+
+
+def run_capacity(device: int, w, cfg, spec, policies, baseline: int, seed: int, qps_min: int,
+                 qps_max: int, slo: float, threads: int = 8):
+    """bsg_run_capacity (run_capacity, driver.cpp:392-427): (rows, baseline capacity)."""
+    pol = np.ascontiguousarray(policies, np.int32)
+    rows = np.zeros(len(pol) + 1, abi.capacity_row_dtype)
+    n = C.c_int32(0)
+    bc = C.c_double(0)
+    st = load().bsg_run_capacity(device, _p(w), _p(cfg), _p(spec), _p(pol), len(pol), baseline, seed,
+                                 qps_min, qps_max, slo, threads, _p(rows), C.byref(n), C.byref(bc))
+    if st != abi.OK:
+        raise BsgError(st, "bsg_run_capacity")
+    return rows[:n.value], bc.value
 
 
 def mc_lengths(est: int, request_id: int, n_samples: int = 256, seed: int = 1,
@@ -540,8 +573,8 @@ class Context:
 
     def replay_device(self, runs):
         """Device-resident closed loops (bsg_replay_device). runs: list of
-        (workload, replay_spec, cfg_index) with the configs already set (the
-        spec's policy must be BlockPredictive); a workload may also be the
+        (workload, replay_spec, cfg_index) with the configs already set (any
+        policy, provisioning and dispatch overhead); a workload may also be the
         (prompt, output, est, arrival_ticks) columns, e.g. of trace_workload.
         Returns [(status, outcomes, summary)] per run."""
         cols = [w if isinstance(w, tuple) else make_workload_host(w) for w, *_ in runs]
@@ -550,7 +583,8 @@ class Context:
         for r, ((w, sp, cf), c) in enumerate(zip(runs, cols)):
             sp = np.asarray(sp).reshape(-1)[0]
             desc[r] = (sp["n_instances"], sp["objective"], cf, len(c[0]), off, sp["provision_kind"],
-                       sp["max_instances"], sp["threshold_s"], sp["cold_start_s"], sp["cooldown_s"])
+                       sp["max_instances"], sp["threshold_s"], sp["cold_start_s"], sp["cooldown_s"],
+                       sp["policy"], 0, sp["policy_seed"], sp["dispatch_overhead_s"])
             off += len(c[0])
         p, o, e, t = (np.ascontiguousarray(np.concatenate([c[j] for c in cols])) for j in range(4))
         out = np.zeros(off, abi.outcome_dtype)

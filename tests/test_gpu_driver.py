@@ -1,0 +1,122 @@
+"""GPU parity of the sweep-driver row beyond BlockPredictive:
+the heuristic dispatch policies (pick_heuristic, scheduler.cpp:68-113) and the
+dispatch-overhead mode (driver.cpp:213-231) inside the device-resident closed
+loop (K5) and the host-driven one, run_sweep's SweepCell table
+(driver.cpp:333-390) and run_capacity's capacity table with its gains
+(driver.cpp:392-427) — each against the reference's own functions
+(oracle/_ref), bit-exactly."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2508_03611_b200 import abi, native
+
+pytestmark = pytest.mark.gpu
+THREADS = os.cpu_count() or 8
+FIELDS = ("instance", "dispatch_ticks", "first_token_ticks", "finish_ticks", "preempt_count")
+HEURISTICS = [abi.POLICY_RANDOM, abi.POLICY_ROUND_ROBIN, abi.POLICY_MIN_QPM, abi.POLICY_INFAAS_PP,
+              abi.POLICY_LLUMNIX_MINUS]
+
+
+def check_runs(ctx, ref, cfg, cases, host=True):
+    """cases: [(workload, spec)]; device closed loops in one batched launch,
+    each also run by the host-driven loop, against run_experiment + aggregate."""
+    ctx.set_configs(cfg)
+    got = ctx.replay_device([(w, sp, 0) for w, sp in cases])
+    reps = ctx.last_reports.copy()
+    for (w, sp), (st, out, summ), rep in zip(cases, got, reps):
+        exp, esum = ref.run_experiment(w, cfg, sp)
+        tag = (int(sp["policy"][0]), float(sp["dispatch_overhead_s"][0]), int(sp["provision_kind"][0]))
+        assert st == abi.OK, tag
+        for f in FIELDS:
+            assert np.array_equal(out[f], exp[f]), (tag, f, np.nonzero(out[f] != exp[f])[0][:5])
+        for f in ("total_preemptions", "instances_provisioned", "final_instance_count"):
+            assert int(summ[f]) == int(esum[f]), (tag, f)
+        erep = ref.run_report(w, cfg, sp)
+        assert rep.tobytes() == erep.tobytes(), (tag, rep, erep)
+        if host:
+            hout, hsum, _ = ctx.replay(w, cfg, sp)
+            ctx.set_configs(cfg)
+            for f in FIELDS:
+                assert np.array_equal(hout[f], exp[f]), ("host", tag, f)
+    return got
+
+
+@pytest.mark.parametrize("policy", HEURISTICS)
+def test_device_closed_loop_heuristics_match_reference(ctx, ref, policy):
+    """Every heuristic policy on K5 (and the host loop): same decisions and
+    timelines as the reference driver, static and preempt provisioning (the
+    heuristics then ask predict() for the chosen instance, driver.cpp:202-209)."""
+    cfg = abi.make_config()
+    cases = []
+    for q, s, ni in [(8.0, 1, 4), (24.0, 2, 12), (40.0, 3, 3)]:
+        w = abi.make_workload(count=300, qps=q, arrival_seed=s, estimator_kind=2, estimator_seed=s)
+        cases.append((w, abi.make_replay_spec(ni, policy=policy, capture=0, policy_seed=s + 10)))
+    w = abi.make_workload(count=400, qps=24.0, arrival_seed=5)
+    cases.append((w, abi.make_replay_spec(4, policy=policy, capture=0, policy_seed=3,
+                                          provision_kind=abi.PROVISION_PREEMPT, max_instances=9,
+                                          threshold_s=15.0, cold_start_s=5.0, cooldown_s=3.0)))
+    check_runs(ctx, ref, cfg, cases)
+
+
+@pytest.mark.parametrize("policy", [abi.POLICY_BLOCK_PREDICTIVE, abi.POLICY_LLUMNIX_MINUS,
+                                    abi.POLICY_ROUND_ROBIN])
+def test_dispatch_overhead_matches_reference(ctx, ref, policy):
+    """Overhead mode: the decision at the arrival, the request lands overhead
+    seconds later (kDispatch events interleaved with the instance's steps and
+    later arrivals). Overheads below, near and above the inter-arrival gap, and
+    one that rounds to zero ticks (lands in the same instant, after it)."""
+    cfg = abi.make_config()
+    cases = []
+    for o, q, s, ni in [(0.08, 12.0, 1, 4), (0.5, 20.0, 2, 6), (2.5, 30.0, 3, 12), (1e-10, 40.0, 4, 3)]:
+        w = abi.make_workload(count=300, qps=q, arrival_seed=s)
+        cases.append((w, abi.make_replay_spec(ni, policy=policy, capture=0, policy_seed=s,
+                                              dispatch_overhead_s=o)))
+    w = abi.make_workload(count=300, qps=30.0, arrival_seed=6)
+    cases.append((w, abi.make_replay_spec(4, policy=policy, capture=0, dispatch_overhead_s=0.3,
+                                          provision_kind=2, max_instances=8, threshold_s=10.0,
+                                          cold_start_s=2.0, cooldown_s=1.0)))
+    got = check_runs(ctx, ref, cfg, cases)
+    # test_driver.cpp:90-102: every finished request reports the constant
+    rep = ctx.last_reports
+    assert abs(rep[0]["mean_overhead_s"] - 0.08) < 1e-9 * 0.08 + 1e-15
+    assert rep[0]["mean_overhead_s"] > 0 and got[0][0] == abi.OK
+
+
+def test_run_sweep_matches_reference(ref):
+    """bsg_run_sweep == the reference's run_sweep: every SweepCell field of the
+    (policy x qps x seed) table, in the reference's cell order."""
+    cfg = abi.make_config()
+    w = abi.make_workload(count=250)
+    spec = abi.make_replay_spec(6, capture=0)
+    pols = [abi.POLICY_ROUND_ROBIN, abi.POLICY_LLUMNIX_MINUS, abi.POLICY_MIN_QPM,
+            abi.POLICY_BLOCK_PREDICTIVE]
+    qps, seeds = [4.0, 9.5, 30.0], [1, 7]
+    got = native.run_sweep(0, w, cfg, spec, pols, qps, seeds, threads=THREADS)
+    exp = ref.run_sweep(w, cfg, spec, pols, qps, seeds, jobs=THREADS)
+    assert len(got) == len(exp) == len(pols) * len(qps) * len(seeds)
+    assert (got["ok"] == 1).all() and (exp["ok"] == 1).all()
+    for f in got.dtype.names:
+        if f == "status":
+            continue
+        assert np.array_equal(got[f], exp[f]), (f, got[f], exp[f])
+
+
+def test_run_capacity_matches_reference(ref):
+    """bsg_run_capacity == the reference's run_capacity: the capacity row of
+    every policy (baseline appended), its tested count and bracket, and the
+    gains table's formatted percentages."""
+    cfg = abi.make_config()
+    w = abi.make_workload(count=200)
+    spec = abi.make_replay_spec(4, capture=0)
+    pols = [abi.POLICY_BLOCK_PREDICTIVE, abi.POLICY_INFAAS_PP, abi.POLICY_ROUND_ROBIN]
+    base = abi.POLICY_LLUMNIX_MINUS
+    st, exp, ebase = ref.run_capacity(w, cfg, spec, pols, base, 3, 1, 16, 3.0)
+    assert st == 0
+    got, gbase = native.run_capacity(0, w, cfg, spec, pols, base, 3, 1, 16, 3.0, threads=THREADS)
+    assert gbase == ebase and len(got) == len(exp) == 4
+    assert (got["status"] == abi.OK).all()
+    for f in ("policy", "result", "has_gain", "gain_text"):
+        assert got[f].tobytes() == exp[f].tobytes(), (f, got[f], exp[f])
+    assert any(got["has_gain"])
