@@ -357,6 +357,7 @@ def run_gpu(args):
         for k, v in line["other_configs"].items():
             line.setdefault("parity", {})[k] = v["parity"]
         line["capacity_sweep"] = capacity_sweep(local)
+        line["capacity_table"] = capacity_table(local)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -597,13 +598,70 @@ def other_configs(ctx, dev):
         sub = ss.compact(np.unique(np.linspace(0, len(ss) - 1, min(sample, len(ss))).astype(np.int64)))
         secs = ref.time_predict(cfg, sub, threads=threads, reps=1)
         exp = ref.predict_batch(cfg, ss, threads=threads)
+        peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {}
+        issue_peak = (torch_sms(dev) * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6)
+        achieved = msteps * 24 * value / len(ss)
         out[name] = {"workload": CONFIGS[name]["desc"], "scenarios": len(ss), "value": value,
                      "unit": "scenarios/s", "member_steps": msteps, "kernel": kernel,
+                     "roofline": {"bound": "issue", "achieved": achieved / 1e12, "peak": issue_peak / 1e12,
+                                  "unit": "T int32-lane-ops/s", "frac": achieved / issue_peak,
+                                  "work": "member-steps x 24 int32 lane-ops (SURVEY 8(d)) per launch time"},
                      "parity": parity(res, exp),
                      "cpu_baseline": {"value": len(sub) / secs, "unit": "scenarios/s", "cores": threads,
                                       "kind": "reference",
                                       "sample": f"{len(sub)} scenarios evenly spaced over the same set"}}
     return out
+
+
+def torch_sms(dev) -> int:
+    import torch
+    return torch.cuda.get_device_properties(dev).multi_processor_count
+
+
+def capacity_table(local: int):
+    """run_capacity (driver.cpp:392-427) — the paper's capacity-gain table: the
+    capacity of BlockPredictive and the heuristics against the Llumnix- baseline
+    (8 instances of the P1 profile, 800 requests, QPS 1-40, SLO p99 TTFT < 3 s),
+    every capacity search's closed loops on the device (bsg_run_capacity), timed
+    against the reference's capacity searches on all host cores (ref_sweep, the
+    same (policy, qps) closed loops), rows and gains checked equal."""
+    from oracle.oracle import Reference
+    from paper_2508_03611_b200 import abi, native, sweep
+    threads = os.cpu_count() or 1
+    cfg = sweep.load_profiles()["P1_llama2_7b"]
+    w = abi.make_workload(count=800)
+    spec = abi.make_replay_spec(8, capture=0)
+    pols = [abi.POLICY_BLOCK_PREDICTIVE, abi.POLICY_INFAAS_PP, abi.POLICY_MIN_QPM,
+            abi.POLICY_ROUND_ROBIN, abi.POLICY_RANDOM]
+    base = abi.POLICY_LLUMNIX_MINUS
+    native.run_capacity(local, w, cfg, spec, pols[:1], base, 1, 1, 2, 3.0, threads=threads)  # warm-up
+    t0 = time.perf_counter()
+    rows, bcap = native.run_capacity(local, w, cfg, spec, pols, base, 1, 1, 40, 3.0, threads=threads)
+    gpu_s = time.perf_counter() - t0
+    cells = np.zeros(len(rows), abi.sweep_cell_dtype)
+    for i, p in enumerate(rows["policy"]):
+        sp = spec.copy()
+        sp["policy"] = p
+        cells[i] = (w[0], np.asarray(cfg).reshape(-1)[0], sp[0], 1, 1, 40, 3.0)
+    rr, ref_s = Reference().sweep(cells, threads=threads)
+    rb = float(rr["result"]["capacity_qps"][list(rows["policy"]).index(base)])
+    egain = [("%.1f%%" % ((c - rb) / rb * 100.0)).encode() if p != base else b""
+             for p, c in zip(rows["policy"], rr["result"]["capacity_qps"])]
+    same = bool(rows["result"].tobytes() == rr["result"].tobytes() and list(rows["gain_text"]) == egain)
+    names = {0: "random", 1: "round_robin", 2: "min_qpm", 3: "infaas_pp", 4: "llumnix_minus",
+             5: "block_predictive"}
+    loops = int(rows["result"]["n_tested"].sum())
+    return {"metric": "run_capacity closed loops/s (device-resident, every policy)",
+            "value": loops / gpu_s, "unit": "closed loops/s", "wall_s": gpu_s, "closed_loops": loops,
+            "baseline": names[base], "baseline_capacity_qps": bcap,
+            "rows": [{"policy": names[int(r["policy"])], "capacity_qps": float(r["result"]["capacity_qps"]),
+                      "gain": r["gain_text"].decode()} for r in rows],
+            "identical_to_reference": same,
+            "config": "8 instances x P1 profile, 800 requests, QPS 1-40 (+tenths), SLO p99 TTFT < 3 s, seed 1",
+            "cpu_baseline": {"value": loops / ref_s, "unit": "closed loops/s", "wall_s": ref_s,
+                             "cores": threads, "kind": "reference",
+                             "sample": "the same capacity searches, every (policy, qps) closed loop on "
+                                       "a pool of all host threads (ref_sweep)"}}
 
 
 def capacity_sweep(local: int):
