@@ -627,9 +627,18 @@ __global__ void __launch_bounds__(kClWarps * 32, cl_min_blocks(K))
   // overhead mode: the next in-flight request of instance s lands at its
   // arrival + overhead (kDispatch, driver.cpp:216-231); landings of one
   // instance are in dispatch order
-  auto next_land = [&](const ClInst& s, int64_t Ab) -> int64_t {
-    if (s.wland >= s.wtail) return kNever;
-    return arrival[__ldcg(&ar.rid[Ab + s.wland])] + run.overhead_ticks;
+  auto next_land = [&](const ClInst& s, int64_t Ab, int32_t wl) -> int64_t {
+    if (wl >= s.wtail) return kNever;
+    return arrival[__ldcg(&ar.rid[Ab + wl])] + run.overhead_ticks;
+  };
+  // every landing at `now`: the new landed end is computed in registers and
+  // stored warp-uniformly (no lane reads a value another lane is writing)
+  auto land_at = [&](ClInst& s, int64_t Ab, int64_t now) {
+    int32_t wl = s.wland;
+    while (next_land(s, Ab, wl) == now) ++wl;
+    __syncwarp();
+    s.wland = wl;
+    __syncwarp();
   };
   // close the instant tc (its completions and landings — events at tc after
   // that instant's arrivals — then end_of_instant's begin_step) and advance
@@ -645,14 +654,14 @@ __global__ void __launch_bounds__(kClWarps * 32, cl_min_blocks(K))
                              relief ? &S.cand_min : nullptr);
         last_done = max(last_done, tc);
       }
-      while (next_land(s, Ab) == tc) s.wland += 1;
+      land_at(s, Ab, tc);
       if (!s.mid && (s.n > 0 || s.whead < s.wland)) {
         const int32_t e = live_begin<K, POW2>(live_cfg, ar, Rb, Ab, s, tc, outs, &S.preempts);
         if (e != BSG_OK) return e;
       }
     }
     for (;;) {
-      const int64_t tl = next_land(s, Ab);
+      const int64_t tl = next_land(s, Ab, s.wland);
       const int64_t td = s.mid ? s.t_done : kNever;
       const int64_t now = min(tl, td);
       if (now >= t) break;
@@ -660,7 +669,7 @@ __global__ void __launch_bounds__(kClWarps * 32, cl_min_blocks(K))
         live_finish<K, POW2>(cfg, ar, Rb, s, now, outs, run.threshold_s, relief_after,
                              relief ? &S.cand_min : nullptr);
       }
-      while (next_land(s, Ab) == now) s.wland += 1;
+      land_at(s, Ab, now);
       last_done = max(last_done, now);
       if (!s.mid && (s.n > 0 || s.whead < s.wland)) {
         const int32_t e = live_begin<K, POW2>(live_cfg, ar, Rb, Ab, s, now, outs, &S.preempts);

@@ -35,4 +35,18 @@ fl.snapshot(0)
 fl.finish(len(p))
 cells, _ = sweep.make_cells([2], sweep.load_profiles(), request_cap=60, qps_max=6, slo=1.0)
 native.sweep_run(0, cells, threads=2)
+# round 2: KV-pressure what-ifs with admit / self-preempt cycle absorption (the
+# wide K=2 kernel and the trace kernel compile the cycle windows), heuristic
+# policies and the dispatch-overhead mode in K5, run_sweep / run_capacity
+w3 = abi.make_workload(count=1000, prompt_median=600, output_median=600, qps=5.0, arrival_seed=1)
+_, _, c3 = ctx.replay(w3, cfg, abi.make_replay_spec(12))
+ctx.set_configs(cfg)
+tail = c3.compact(np.arange(len(c3) - 256, len(c3)))
+ctx.predict_batch(tail)
+ctx.trace(tail, 255, cap=1 << 14)
+runs = [(w, abi.make_replay_spec(4, policy=pol, capture=0, policy_seed=2, dispatch_overhead_s=ov), 0)
+        for pol, ov in ((0, 0.0), (2, 0.3), (3, 0.0), (4, 0.05), (5, 0.2))]
+ctx.replay_device(runs)
+native.run_sweep(0, abi.make_workload(count=60), cfg, abi.make_replay_spec(3, capture=0), [1, 5], [4.0], [1])
+native.run_capacity(0, abi.make_workload(count=60), cfg, abi.make_replay_spec(3, capture=0), [5], 4, 1, 1, 4, 3.0)
 print("sanitize workload done")
