@@ -182,3 +182,52 @@ def test_reference_sweep_equals_capacity_search(ref):
         if st == abi.OK:
             assert o["result"].tolist() == exp.tolist()
     assert (got["status"] == abi.NO_CAPACITY).any() and (got["status"] == abi.OK).any()
+
+
+def test_reference_run_sweep_rows_equal_run_experiment(ref):
+    """ref_run_sweep (the reference's own run_sweep, driver.cpp:333-390) —
+    pinned cell by cell to spec_for_cell + run_experiment + aggregate through
+    the shim, so the GPU table is checked against the real thing."""
+    cfg = abi.make_config()
+    w = abi.make_workload(count=150)
+    spec = abi.make_replay_spec(3, capture=0)
+    pols, qps, seeds = [abi.POLICY_ROUND_ROBIN, abi.POLICY_LLUMNIX_MINUS], [5.0, 12.5], [2, 9]
+    rows = ref.run_sweep(w, cfg, spec, pols, qps, seeds, jobs=4)
+    assert len(rows) == 8
+    i = 0
+    for p in pols:
+        for q in qps:
+            for s in seeds:  # the reference's cell order: policy, qps, seed
+                cw = w.copy()
+                cw["qps"], cw["arrival_seed"], cw["estimator_seed"] = q, s, s
+                sp = spec.copy()
+                sp["policy"], sp["policy_seed"] = p, s
+                rep = ref.run_report(cw, cfg, sp)
+                r = rows[i]
+                assert (int(r["policy"]), float(r["qps"]), int(r["seed"]), int(r["ok"])) == (p, q, s, 1)
+                for f in ("mean_ttft_s", "p99_ttft_s", "mean_e2e_s", "p99_e2e_s", "throughput_rps",
+                          "total_preemptions", "finished_requests", "free_blocks_var_avg"):
+                    assert r[f] == rep[f], (i, f)
+                i += 1
+
+
+def test_reference_run_capacity_gains_format(ref):
+    """ref_run_capacity (run_capacity, driver.cpp:392-427): the baseline is
+    appended when absent, rows equal capacity_search per policy, and the gains
+    are format_percent of (c - c_base) / c_base."""
+    cfg = abi.make_config()
+    w = abi.make_workload(count=120)
+    spec = abi.make_replay_spec(3, capture=0)
+    pols, base = [abi.POLICY_BLOCK_PREDICTIVE, abi.POLICY_ROUND_ROBIN], abi.POLICY_LLUMNIX_MINUS
+    st, rows, bcap = ref.run_capacity(w, cfg, spec, pols, base, 2, 1, 10, 3.0)
+    assert st == 0 and [int(p) for p in rows["policy"]] == pols + [base]
+    for r in rows:
+        sp = spec.copy()
+        sp["policy"] = r["policy"]
+        cst, exp, _ = ref.capacity_search(w, cfg, sp, 2, 1, 10, 3.0)
+        assert cst == 0 and r["result"].tolist() == exp.tolist()
+    assert bcap == float(rows["result"]["capacity_qps"][-1])
+    for r in rows[:-1]:
+        g = (float(r["result"]["capacity_qps"]) - bcap) / bcap
+        assert r["gain_text"].decode() == "%.1f%%" % (g * 100.0)
+    assert rows[-1]["has_gain"] == 0
