@@ -120,3 +120,46 @@ def test_run_capacity_matches_reference(ref):
     for f in ("policy", "result", "has_gain", "gain_text"):
         assert got[f].tobytes() == exp[f].tobytes(), (f, got[f], exp[f])
     assert any(got["has_gain"])
+
+
+@pytest.mark.parametrize("cfg_kw", [
+    dict(local_policy=1, total_blocks=260, max_batch_size=40, block_size=8,       # prefill priority
+         _wl=dict(max_prompt_tokens=1024, max_output_tokens=1024)),              # under KV pressure
+    dict(block_size=12, total_blocks=1500, max_batch_size=100, chunk_budget=600),  # K = 4, non-pow2
+    dict(cache_mode=2, context_bucket=128, total_blocks=400),                      # bucketed what-ifs
+])
+def test_policies_and_overhead_across_configs(ctx, ref, cfg_kw):
+    """Every policy with and without dispatch overhead, and preempt / relief
+    provisioning, on instance configs beyond the default: K5 and the host loop
+    against run_experiment + aggregate."""
+    cfg_kw = dict(cfg_kw)
+    wl = cfg_kw.pop("_wl", {})
+    cfg = abi.make_config(**cfg_kw)
+    cases = []
+    for i, pol in enumerate(HEURISTICS + [abi.POLICY_BLOCK_PREDICTIVE]):
+        w = abi.make_workload(count=200, qps=10.0 + 4 * i, arrival_seed=i + 1, **wl)
+        cases.append((w, abi.make_replay_spec(3 + i % 3, policy=pol, capture=0, policy_seed=i,
+                                              dispatch_overhead_s=(0.0, 0.15, 1.2)[i % 3])))
+    w = abi.make_workload(count=250, qps=20.0, arrival_seed=9, **wl)
+    cases.append((w, abi.make_replay_spec(2, policy=abi.POLICY_LLUMNIX_MINUS, capture=0, dispatch_overhead_s=0.2,
+                                          provision_kind=abi.PROVISION_PREEMPT, max_instances=5,
+                                          threshold_s=6.0, cold_start_s=2.0, cooldown_s=1.0)))
+    cases.append((w, abi.make_replay_spec(2, policy=abi.POLICY_BLOCK_PREDICTIVE, capture=0,
+                                          dispatch_overhead_s=0.05, provision_kind=2, max_instances=5,
+                                          threshold_s=6.0, cold_start_s=2.0, cooldown_s=0.0)))
+    check_runs(ctx, ref, cfg, cases)
+
+
+def test_run_sweep_with_overhead_and_provisioning(ref):
+    """run_sweep over a base spec with dispatch overhead and preempt
+    provisioning (spec_for_cell keeps both), every row equal."""
+    cfg = abi.make_config()
+    w = abi.make_workload(count=200)
+    spec = abi.make_replay_spec(3, capture=0, dispatch_overhead_s=0.1, provision_kind=abi.PROVISION_PREEMPT,
+                                max_instances=6, threshold_s=8.0, cold_start_s=3.0, cooldown_s=2.0)
+    pols = [abi.POLICY_RANDOM, abi.POLICY_INFAAS_PP, abi.POLICY_BLOCK_PREDICTIVE]
+    got = native.run_sweep(0, w, cfg, spec, pols, [6.0, 20.0], [3], threads=THREADS)
+    exp = ref.run_sweep(w, cfg, spec, pols, [6.0, 20.0], [3], jobs=THREADS)
+    for f in got.dtype.names:
+        if f != "status":
+            assert np.array_equal(got[f], exp[f]), (f, got[f], exp[f])
