@@ -10,6 +10,7 @@
 #include <array>
 #include <cstdlib>
 #include <cstdio>
+#include <chrono>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -716,6 +717,12 @@ bsg_status bsg_ctx_create(int device, bsg_ctx** out) {
       return BSG_CUDA_ERROR;
     }
   }
+  for (int i = 0; i < bsg_ctx::kPieces; ++i) {
+    if (cudaEventCreateWithFlags(&ctx->piece_ev[i], cudaEventDisableTiming) != cudaSuccess) {
+      delete ctx;
+      return BSG_CUDA_ERROR;
+    }
+  }
   *out = ctx;
   return BSG_OK;
 }
@@ -731,6 +738,9 @@ void bsg_ctx_destroy(bsg_ctx* ctx) {
       cudaStreamDestroy(ctx->pipe[i]);
     }
     if (ctx->pipe_done[i]) cudaEventDestroy(ctx->pipe_done[i]);
+  }
+  for (int i = 0; i < bsg_ctx::kPieces; ++i) {
+    if (ctx->piece_ev[i]) cudaEventDestroy(ctx->piece_ev[i]);
   }
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   delete ctx;
@@ -824,9 +834,9 @@ bsg_status bsg_predict_batch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n
   auto* dsc = static_cast<bsg_scenario*>(ctx->scen.p);
   auto* dres = static_cast<bsg_result*>(ctx->res.p);
   // Chunked pipeline (measured on cfg2, pinned buffers: 3 chunks of 20k cut the
-  // call from 1.05 to 0.75 ms; H2D is PCIe-bound): chunk c (a contiguous scenario range) copies only the
-  // entry range its scenarios reference, runs, and copies its results back on
-  // stream c % 3, so H2D(c+1) overlaps the kernel on c and D2H(c-1).
+  // call from 1.05 to 0.75 ms; H2D is PCIe-bound): chunk c (a contiguous
+  // scenario range) runs and copies its results back while later chunks' bytes
+  // are still in flight.
   const char* env_chunk = std::getenv("BSG_PIPE_CHUNK");
   const int64_t target_chunk = env_chunk ? std::max<int64_t>(1, std::atoll(env_chunk)) : 20000;
   const int64_t nchunks0 = std::min<int64_t>(16, std::max<int64_t>(1, n / target_chunk));
@@ -853,11 +863,53 @@ bsg_status bsg_predict_batch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n
     bounds.push_back(n);
   }
   const int64_t nchunks = static_cast<int64_t>(bounds.size()) - 1;
+  // BSG_PIPE_PROFILE=1 (diagnostics): host timestamps and per-chunk CUDA events to stderr
+  const bool pipe_prof = std::getenv("BSG_PIPE_PROFILE") != nullptr;
+  std::vector<cudaEvent_t> pev;
+  std::vector<double> host_us;
+  const auto h0 = std::chrono::steady_clock::now();
+  auto hnow = [&]() { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count(); };
+  auto mark = [&](cudaStream_t st) {
+    if (!pipe_prof) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    pev.push_back(e);
+    host_us.push_back(hnow());
+  };
+  mark(ctx->pipe[0]);
   auto cols_h = std::array<const int32_t*, 4>{entries->prompt, entries->est, entries->prefill,
                                               entries->decoded};
   auto cols_d = std::array<int32_t*, 4>{static_cast<int32_t*>(ctx->prompt.p), static_cast<int32_t*>(ctx->est.p),
                                         static_cast<int32_t*>(ctx->prefill.p),
                                         static_cast<int32_t*>(ctx->decoded.p)};
+  // The scenario rows and then the entry columns stream in pieces (one per
+  // chunk) on pipe[0] from the start of the call — no host scan in front of the
+  // first byte; scenario chunk c runs on pipe[1 + c % 2] once the piece holding
+  // its last entry has landed, while the host scans the next chunk. Measured on
+  // cfg2 (tools/pipeprobe.py): 0.60 ms vs 0.68 ms for per-chunk copies behind
+  // each chunk's scan (BSG_PIPE=1); more pieces than chunks cost more in copy
+  // calls than they gain (6 pieces 0.66 ms, 12 pieces 0.77 ms).
+  const char* env_pipe = std::getenv("BSG_PIPE");
+  const bool v2 = !(env_pipe && std::atoi(env_pipe) == 1);
+  const char* env_pieces = std::getenv("BSG_PIPE_PIECES");
+  const int np = static_cast<int>(std::min<int64_t>(
+      bsg_ctx::kPieces, std::max<int64_t>(1, env_pieces ? std::atoll(env_pieces) : nchunks)));
+  std::vector<int64_t> pe(np + 1);
+  if (v2) {
+    // the scenario rows first (1.9 MB at cfg2): every chunk needs its rows before its entries
+    BSG_CUDA(ctx, cudaMemcpyAsync(dsc, scenarios, n * sizeof(bsg_scenario), cudaMemcpyHostToDevice,
+                                  ctx->pipe[0]));
+    for (int k = 0; k <= np; ++k) pe[k] = n_entries * k / np;
+    for (int k = 0; k < np; ++k) {
+      if (pe[k + 1] > pe[k])
+        for (int q = 0; q < 4; ++q)
+          BSG_CUDA(ctx, cudaMemcpyAsync(cols_d[q] + pe[k], cols_h[q] + pe[k], (pe[k + 1] - pe[k]) * 4,
+                                        cudaMemcpyHostToDevice, ctx->pipe[0]));
+      BSG_CUDA(ctx, cudaEventRecord(ctx->piece_ev[k], ctx->pipe[0]));
+    }
+    mark(ctx->pipe[0]);
+  }
   for (int64_t c = 0; c < nchunks; ++c) {
     const int64_t s0 = bounds[c], s1 = bounds[c + 1];
     if (s0 >= s1) continue;
@@ -883,23 +935,52 @@ bsg_status bsg_predict_batch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n
       ctx->last_error = "scenario references entries outside [0, n_entries)";
       return BSG_INVALID_ARGUMENT;
     }
-    cudaStream_t st = ctx->pipe[c % 3];
-    if (c >= 3) BSG_CUDA(ctx, cudaStreamWaitEvent(st, ctx->pipe_done[c % 3], 0));
-    if (hi > lo) {
-      for (int q = 0; q < 4; ++q)
-        BSG_CUDA(ctx, cudaMemcpyAsync(cols_d[q] + lo, cols_h[q] + lo, (hi - lo) * 4,
-                                      cudaMemcpyHostToDevice, st));
+    cudaStream_t st = v2 ? ctx->pipe[1 + c % 2] : ctx->pipe[c % 3];
+    if (v2) {
+      if (hi > lo) {  // the piece holding entry hi - 1 (pieces land in order)
+        int k = 0;
+        while (k + 1 < np && pe[k + 1] < hi) ++k;
+        BSG_CUDA(ctx, cudaStreamWaitEvent(st, ctx->piece_ev[k], 0));
+      }
+    } else {
+      if (c >= 3) BSG_CUDA(ctx, cudaStreamWaitEvent(st, ctx->pipe_done[c % 3], 0));
+      if (hi > lo) {
+        for (int q = 0; q < 4; ++q)
+          BSG_CUDA(ctx, cudaMemcpyAsync(cols_d[q] + lo, cols_h[q] + lo, (hi - lo) * 4,
+                                        cudaMemcpyHostToDevice, st));
+      }
     }
-    BSG_CUDA(ctx, cudaMemcpyAsync(dsc + s0, scenarios + s0, (s1 - s0) * sizeof(bsg_scenario),
-                                  cudaMemcpyHostToDevice, st));
+    if (!v2)
+      BSG_CUDA(ctx, cudaMemcpyAsync(dsc + s0, scenarios + s0, (s1 - s0) * sizeof(bsg_scenario),
+                                    cudaMemcpyHostToDevice, st));
+    else if (hi <= lo)  // no entries: still after the scenario rows
+      BSG_CUDA(ctx, cudaStreamWaitEvent(st, ctx->piece_ev[0], 0));
+    mark(st);  // H2D of chunk c done
     const int k = capacity_k(need);
     const bsg_status ls = launch_predict_k(ctx, k == 0 ? 8 : k, s1 - s0, dev, dsc + s0, dres + s0, st, &used);
     if (ls != BSG_OK) return ls;
+    mark(st);  // kernels of chunk c done
     BSG_CUDA(ctx, cudaMemcpyAsync(out + s0, dres + s0, (s1 - s0) * sizeof(bsg_result),
                                   cudaMemcpyDeviceToHost, st));
+    mark(st);  // D2H of chunk c done
     BSG_CUDA(ctx, cudaEventRecord(ctx->pipe_done[c % 3], st));
   }
   for (int i = 0; i < 3; ++i) BSG_CUDA(ctx, cudaStreamSynchronize(ctx->pipe[i]));
+  if (pipe_prof && v2) {  // the piece copies' completion first, then the chunks
+    std::rotate(pev.begin() + 1, pev.begin() + 2, pev.end());
+    std::rotate(host_us.begin() + 1, host_us.begin() + 2, host_us.end());
+  }
+  if (pipe_prof) {
+    std::string line = "pipe: host_end " + std::to_string(static_cast<int>(hnow())) + " us;";
+    for (size_t i = 1; i < pev.size(); ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, pev[0], pev[i]);
+      line += " [c" + std::to_string((i - 1) / 3) + (((i - 1) % 3) == 0 ? " h2d " : ((i - 1) % 3) == 1 ? " ker " : " d2h ") +
+              std::to_string(static_cast<int>(ms * 1000)) + " enq@" + std::to_string(static_cast<int>(host_us[i])) + "]";
+    }
+    std::fprintf(stderr, "%s\n", line.c_str());
+    for (cudaEvent_t e : pev) cudaEventDestroy(e);
+  }
   return BSG_OK;
 }
 

@@ -36,6 +36,8 @@ struct bsg_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};  // chunked host-buffer pipeline
   cudaEvent_t pipe_done[3] = {nullptr, nullptr, nullptr};
+  static constexpr int kPieces = 16;
+  cudaEvent_t piece_ev[kPieces] = {};  // entry pieces landed (host-buffer pipeline)
   std::string last_error;
   std::string last_launch;  // the simulation kernel(s) the last call launched
   int64_t launches = 0;
