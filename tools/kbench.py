@@ -1,6 +1,6 @@
 """Kernel timing probe: device-timed predict over a captured set (L2 flushed
 between launches), plus the per-launch kernel mix.
-usage: [BSG_LIB_PATH=<so>] python tools/kbench.py [cfg2|cfg3|cfg3q|cfg1 ...] [--steps N]"""
+usage: [BSG_LIB_PATH=<so>] python tools/kbench.py [cfg2|cfg3|cfg3q|cfg1 ...] [--steps N] [--noflush]"""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
@@ -14,6 +14,7 @@ SETS = {
 }
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
 steps = 10
+noflush = "--noflush" in sys.argv
 for i, a in enumerate(sys.argv):
     if a == "--steps":
         steps = int(sys.argv[i + 1])
@@ -41,7 +42,8 @@ for name in args or ["cfg2", "cfg3"]:
     res = np.frombuffer(out.cpu().numpy().tobytes(), dtype=abi.result_dtype).copy()
     ts = []
     for _ in range(steps):
-        flush.zero_()
+        if not noflush:
+            flush.zero_()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(st)
