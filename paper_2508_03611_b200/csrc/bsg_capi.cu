@@ -42,9 +42,12 @@ constexpr int kPredictWarps = BSG_WPB;
 #ifndef BSG_OPT_WARPS_PER_SM
 #define BSG_OPT_WARPS_PER_SM 32
 #endif
-// ... and for the 64-member kernels (KV-pressure sets with deep waiting queues)
+// ... and for the 64-member kernels: they run small sets (below the queue
+// threshold: one wave, bound by the longest scenario) and the optimistic
+// passes' retries, so registers beat warps — 16 warps/SM, 119 registers, no
+// spills (24 warps: 80 registers, 154/192 B spills): cfg1 200 -> 176 us, cfg3 flat.
 #ifndef BSG_K2_WARPS_PER_SM
-#define BSG_K2_WARPS_PER_SM 24
+#define BSG_K2_WARPS_PER_SM 16
 #endif
 constexpr int min_blocks(int k, bool opt = false) {
   return opt ? BSG_OPT_WARPS_PER_SM / kPredictWarps
