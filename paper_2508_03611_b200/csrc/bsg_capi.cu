@@ -222,9 +222,9 @@ __global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K, OPT))
                    const int32_t* __restrict__ prefill, const int32_t* __restrict__ decoded,
                    const bsg_scenario* __restrict__ scen, int64_t n, WorkQueue* __restrict__ q,
                    bsg_result* __restrict__ out) {
-  __shared__ int32_t smem_all[kPredictWarps * smem_words(K)];
+  __shared__ int32_t smem_all[kPredictWarps * smem_words(K, WJ)];
   const int warp = threadIdx.x >> 5;
-  int32_t* smem = smem_all + warp * smem_words(K);
+  int32_t* smem = smem_all + warp * smem_words(K, WJ);
   if constexpr (OPT) {  // two optimistic passes are launched; the vote keeps one
     static_assert(BSG_WIN_J_WIDE != BSG_WIN_J_PREDICT, "the two optimistic passes need distinct widths");
     // use_wide = the vote chose wide (BSG_WIN_J_PREDICT-step) windows; else the
@@ -265,9 +265,9 @@ __global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K))
                          const int32_t* __restrict__ prefill, const int32_t* __restrict__ decoded,
                          const bsg_scenario* __restrict__ scen, int64_t n, WorkQueue* __restrict__ q,
                          bsg_result* __restrict__ out) {
-  __shared__ int32_t smem_all[kPredictWarps * smem_words(K)];
+  __shared__ int32_t smem_all[kPredictWarps * smem_words(K, BSG_WIN_J_WIDE)];
   const int warp = threadIdx.x >> 5;
-  int32_t* smem = smem_all + warp * smem_words(K);
+  int32_t* smem = smem_all + warp * smem_words(K, BSG_WIN_J_WIDE);
   const int32_t cnt = __ldcg(&q->retry_count);
   const int32_t* rl = retry_list(q, n);
   for (int64_t j = static_cast<int64_t>(blockIdx.x) * kPredictWarps + warp; j < cnt;
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(32)
                  const int32_t* __restrict__ est, const int32_t* __restrict__ prefill,
                  const int32_t* __restrict__ decoded, const bsg_scenario* __restrict__ scen,
                  bsg_result* __restrict__ out, bsg_step_record* rec, int64_t cap) {
-  __shared__ int32_t smem[smem_words(K)];
+  __shared__ int32_t smem[smem_words(K, WJ)];
   const bsg_scenario sc = scen[0];
   const DevCfg cfg = cfgs[sc.cfg];
   simulate_scenario<K, true, false, POW2, true, false, WJ, CYC>(cfg, prompt, est, prefill, decoded, sc, smem,
@@ -365,8 +365,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   if (w >= static_cast<int64_t>(n_inst) * n_req) return;
   const int32_t r = static_cast<int32_t>(w / n_inst);
   const int32_t Sp = SAMPLE ? pow2_ceil(S) : S;
-  int32_t* smem = dsm + warp * (smem_words(K) + Sp);
-  int32_t* len = smem + smem_words(K);
+  int32_t* smem = dsm + warp * (smem_words(K, BSG_WIN_J_LATENCY) + Sp);
+  int32_t* len = smem + smem_words(K, BSG_WIN_J_LATENCY);
   const bsg_scenario sc = scen[w];
   if constexpr (SAMPLE) {
     stage_mc_samples(len, sc.cand_est, smp.request_id[r], S, smp.seed, smp.scale,
@@ -1018,8 +1018,9 @@ bsg_status bsg_trace(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries
   auto* res = static_cast<bsg_result*>(ctx->res.p);
   auto* sc = static_cast<const bsg_scenario*>(ctx->scen.p);
   auto* cf = static_cast<const DevCfg*>(ctx->cfgs.p);
-  // the window width under test: the kernels use 1 (wide / KV-pressure sets) and
-  // 4 (32-member sets, latency path); BSG_TRACE_J picks which per-step trace to emit
+  // the window width under test: the kernels use 1 (wide / KV-pressure sets), 4
+  // (32-member sets) and 8 (latency path, no cycle absorption); BSG_TRACE_J picks
+  // which per-step trace to emit
   const char* tj = std::getenv("BSG_TRACE_J");
   const int wj = tj ? std::atoi(tj) : 1;
   // BSG_TRACE_CYC=0 traces the windows without admit/self-preempt cycle absorption
@@ -1033,7 +1034,10 @@ bsg_status bsg_trace(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_entries
   }
 #define BSG_TRACE_LAUNCH(KK)                                                                     \
   {                                                                                              \
-    if (wj == 4) {                                                                               \
+    if (wj == 8) {                                                                               \
+      if (ctx->all_pow2) trace_kernel<KK, true, 8, false><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap); \
+      else trace_kernel<KK, false, 8, false><<<1, 32, 0, ctx->stream>>>(cf, dev.prompt, dev.est, dev.prefill, dev.decoded, sc, res, rec, cap); \
+    } else if (wj == 4) {                                                                        \
       if (ctx->all_pow2) BSG_TRACE_LAUNCH_C(KK, true, 4) else BSG_TRACE_LAUNCH_C(KK, false, 4)   \
     } else {                                                                                     \
       if (ctx->all_pow2) BSG_TRACE_LAUNCH_C(KK, true, 1) else BSG_TRACE_LAUNCH_C(KK, false, 1)   \
@@ -1225,7 +1229,7 @@ bsg_status dispatch_fused(bsg_ctx* ctx, const bsg_entries* entries, int64_t n_en
   const int32_t Sp = sample ? pow2_ceil(n_samples) : n_samples;
 #define BSG_LAUNCH_MC2(KK, P2, SM)                                                              \
   {                                                                                             \
-    const size_t sm = static_cast<size_t>(kWarpsPerBlock) * (smem_words(KK) + Sp) * 4;        \
+    const size_t sm = static_cast<size_t>(kWarpsPerBlock) * (smem_words(KK, BSG_WIN_J_LATENCY) + Sp) * 4; \
     if (sm > 48 * 1024)                                                                         \
       cudaFuncSetAttribute(dispatch_mc_kernel<KK, P2, SM>,                                      \
                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));  \

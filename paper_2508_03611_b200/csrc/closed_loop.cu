@@ -389,7 +389,7 @@ template <int K>
 struct ClShared {
   ClInst inst[kClMaxInst];
   bsg_result res[kClMaxInst];
-  int32_t scratch[kClWarps][smem_words(K)];
+  int32_t scratch[kClWarps][smem_words(K, BSG_WIN_J_CLOSED)];
   int64_t pend[kClMaxInst];     // provision-complete times, non-decreasing
   unsigned long long preempts;
   unsigned long long end_ticks;
@@ -1036,8 +1036,8 @@ __global__ void __launch_bounds__(kFleetWarps * 32)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t i = blockIdx.x * kFleetWarps + warp;
   if (i >= n_inst) return;
-  int32_t* smem = fsm + warp * (smem_words(K) + pow2_ceil(S));
-  int32_t* len = smem + smem_words(K);
+  int32_t* smem = fsm + warp * (smem_words(K, BSG_WIN_J_LATENCY) + pow2_ceil(S));
+  int32_t* len = smem + smem_words(K, BSG_WIN_J_LATENCY);
   const DevCfg cfg = cfgs[cfg_index];
   DevCfg live_cfg = cfg;
   live_cfg.cache_mode = BSG_CACHE_OFF;  // live steps use batch_latency itself
@@ -1349,7 +1349,7 @@ namespace {
 // Enqueues the fleet kernel on the context stream; inputs come from f->dparams.
 template <int K, bool POW2, bool MC>
 cudaError_t launch_fleet(bsg_fleet* f, int32_t S) {
-  const size_t sm = static_cast<size_t>(kFleetWarps) * (smem_words(K) + pow2_ceil(S)) * 4;
+  const size_t sm = static_cast<size_t>(kFleetWarps) * (smem_words(K, BSG_WIN_J_LATENCY) + pow2_ceil(S)) * 4;
   if (sm > 48 * 1024)
     cudaFuncSetAttribute(fleet_dispatch_kernel<K, POW2, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sm));

@@ -39,7 +39,7 @@ constexpr unsigned kFull = 0xffffffffu;
 // DESIGN.md): wide windows for decode-dominated throughput sets and for the
 // latency path, narrow ones where events keep windows short.
 #ifndef BSG_MAX_WIN_J
-#define BSG_MAX_WIN_J 4
+#define BSG_MAX_WIN_J 8
 #endif
 constexpr int kMaxWinJ = BSG_MAX_WIN_J;
 #ifndef BSG_WIN_J_PREDICT
@@ -49,8 +49,8 @@ constexpr int kMaxWinJ = BSG_MAX_WIN_J;
 #define BSG_WIN_J_WIDE 1      // K1 for wide / KV-pressure sets (and their optimistic pass)
 #endif
 #ifndef BSG_WIN_J_LATENCY
-#define BSG_WIN_J_LATENCY 4   // per-request dispatch (dispatch_mc, fleet)
-#endif
+#define BSG_WIN_J_LATENCY 8   // per-request dispatch (dispatch_mc, fleet): one wave, the longest
+#endif                        // simulation is the latency (cfg4 p99 113 -> 100 us vs 128-step windows)
 #ifndef BSG_WIN_J_CLOSED
 #define BSG_WIN_J_CLOSED 1    // K5 closed-loop what-ifs
 #endif
@@ -65,10 +65,11 @@ constexpr int kMaxWinJ = BSG_MAX_WIN_J;
 #ifndef BSG_CYC_CLOSED
 #define BSG_CYC_CLOSED 0
 #endif
-// Per-warp shared-memory words of simulate_scenario: the completion-compaction
-// area (5 x 32K) / the window histograms (4 x 32 x kMaxWinJ), whichever is larger.
-__host__ __device__ constexpr int smem_words(int K) {
-  return (5 * 32 * K > 4 * 32 * kMaxWinJ ? 5 * 32 * K : 4 * 32 * kMaxWinJ);
+// Per-warp shared-memory words of simulate_scenario with window width WJ: the
+// completion-compaction area (5 x 32K) / the window histograms and cycle arrays
+// (4 x 32 x WJ), whichever is larger.
+__host__ __device__ constexpr int smem_words(int K, int WJ = kMaxWinJ) {
+  return (5 * 32 * K > 4 * 32 * WJ ? 5 * 32 * K : 4 * 32 * WJ);
 }
 constexpr int64_t kMaxSimulatedSteps = 50000000LL;  // predictor.cpp:11
 
@@ -275,7 +276,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
                                   const int32_t* __restrict__ g_est,
                                   const int32_t* __restrict__ g_prefill,
                                   const int32_t* __restrict__ g_decoded, const bsg_scenario sc,
-                                  // smem_words(K) int32 per warp. Not __restrict__: lanes
+                                  // smem_words(K, WJ) int32 per warp. Not __restrict__: lanes
                                   // exchange values through it across __syncwarp(), which
                                   // a restrict-qualified pointer lets the compiler reorder
                                   // loads across (the barrier does not take the pointer)

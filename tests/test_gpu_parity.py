@@ -36,7 +36,7 @@ def test_gpu_matches_reference_fuzz(ctx, ref, seed):
     assert bad.sum() == 0, [(i, got[i], exp[i]) for i in np.nonzero(bad)[0][:5]]
 
 
-@pytest.mark.parametrize("win_j,cyc", [("1", "1"), ("4", "1"), ("4", "0"), ("1", "0")])
+@pytest.mark.parametrize("win_j,cyc", [("1", "1"), ("4", "1"), ("4", "0"), ("1", "0"), ("8", "0")])
 def test_gpu_trace_matches_reference(ctx, ref, monkeypatch, win_j, cyc):
     """Per-step batch composition, allocations, preemption victims, first
     tokens, completions and durations (bsg_step_record) for every step — with
