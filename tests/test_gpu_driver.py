@@ -163,3 +163,37 @@ def test_run_sweep_with_overhead_and_provisioning(ref):
     for f in got.dtype.names:
         if f != "status":
             assert np.array_equal(got[f], exp[f]), (f, got[f], exp[f])
+
+
+def test_sweep_and_capacity_error_semantics(ref):
+    """An unservable workload (a request needs more blocks than an instance has):
+    run_sweep records every cell as failed (the reference's ok = false), and
+    run_capacity fails as a whole (the reference throws out of run_capacity).
+    A policy with no capacity at qps_min: its row says NO_CAPACITY (the
+    reference's capacity_search throws NoCapacityError for it), the others are
+    the reference's capacity_search results."""
+    cfg = abi.make_config(total_blocks=40)
+    w = abi.make_workload(count=100)
+    spec = abi.make_replay_spec(3, capture=0)
+    got = native.run_sweep(0, w, cfg, spec, [abi.POLICY_ROUND_ROBIN, abi.POLICY_BLOCK_PREDICTIVE], [5.0], [1])
+    exp = ref.run_sweep(w, cfg, spec, [abi.POLICY_ROUND_ROBIN, abi.POLICY_BLOCK_PREDICTIVE], [5.0], [1])
+    assert (got["ok"] == 0).all() and (exp["ok"] == 0).all()
+    assert (got["status"] == abi.TOO_LARGE_CANDIDATE).all()
+    with pytest.raises(native.BsgError):
+        native.run_capacity(0, w, cfg, spec, [abi.POLICY_BLOCK_PREDICTIVE], abi.POLICY_LLUMNIX_MINUS, 1, 1, 4, 3.0)
+    assert ref.run_capacity(w, cfg, spec, [abi.POLICY_BLOCK_PREDICTIVE], abi.POLICY_LLUMNIX_MINUS, 1, 1, 4, 3.0)[0] < 0
+    # no capacity at qps_min for some policies (tight SLO, high qps_min)
+    cfg = abi.make_config()
+    w = abi.make_workload(count=300)
+    pols = [abi.POLICY_BLOCK_PREDICTIVE, abi.POLICY_RANDOM, abi.POLICY_INFAAS_PP]
+    rows, _ = native.run_capacity(0, w, cfg, spec, pols, abi.POLICY_LLUMNIX_MINUS, 2, 8, 14, 0.5, threads=THREADS)
+    statuses = set()
+    for r in rows:
+        sp = spec.copy()
+        sp["policy"] = r["policy"]
+        st, res, _ = ref.capacity_search(w, cfg, sp, 2, 8, 14, 0.5)
+        assert int(r["status"]) == st, (int(r["policy"]), int(r["status"]), st)
+        if st == abi.OK:
+            assert r["result"].tolist() == res.tolist()
+        statuses.add(st)
+    assert abi.NO_CAPACITY in statuses, statuses
