@@ -78,6 +78,8 @@ struct ClInst {
   int64_t t_done;      // completion time of the current step
   int32_t mid;         // mid-step
   int32_t wland;       // end of the landed waiting requests
+  int32_t held;        // the status snapshot's sum of blocks_needed(stored) over running
+  int32_t pad;         //   (backend.cpp:357-365), kept by live_begin / live_finish
 };
 
 // Instance i of a run: R at base, A at base + maxb (A's first maxb slots are
@@ -303,9 +305,14 @@ __device__ int32_t live_begin(const DevCfg& cfg, const Arena& ar, int64_t Rb, in
   }
   const int32_t n_dec = count<K>(ds);
   const int64_t dur = step_ticks(cfg, warp_sum<K>(pt), n_dec, warp_sum<K>(ctx));
+  int32_t hs[K];  // the surviving members' blocks at their pre-step stored tokens
+#pragma unroll
+  for (int k = 0; k < K; ++k) hs[k] = (lane * K + k) < e_star ? bnt<POW2>(stored[k], cfg) : 0;
+  const int32_t held = warp_sum<K>(hs);
   // every lane writes the (warp-uniform) new state: no lane ever reads a value
   // another lane stored, so the state may live in registers, shared or global
   __syncwarp();
+  st.held = held;
   st.n = e_star;
   st.whead = new_whead;
   st.free_blocks = free_blocks;
@@ -363,6 +370,10 @@ __device__ void live_finish(const DevCfg& cfg, const Arena& ar, int64_t Rb, ClIn
   }
   const int32_t kept = excl_scan<K>(keep, dst);
   const int32_t rel = warp_sum<K>(freed);
+  int32_t hk[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) hk[k] = keep[k] ? bnt<POW2>(prefill[k] + decoded[k], cfg) : 0;
+  const int32_t held = warp_sum<K>(hk);
   __syncwarp();
 #pragma unroll
   for (int k = 0; k < K; ++k) {  // stable erase of completed members (backend.cpp:319-322)
@@ -380,6 +391,7 @@ __device__ void live_finish(const DevCfg& cfg, const Arena& ar, int64_t Rb, ClIn
   const int32_t nf = st.free_blocks + rel;  // warp-uniform state update, every lane
   __syncwarp();
   st.n = kept;
+  st.held = held;
   st.free_blocks = nf;
   st.mid = 0;
   __syncwarp();
@@ -597,6 +609,7 @@ __global__ void __launch_bounds__(kClWarps * 32, cl_min_blocks(K))
     s.whead = maxb;
     s.wtail = maxb;
     s.wland = maxb;
+    s.held = 0;
     s.free_blocks = cfg.total_blocks;
     s.t_done = 0;
     s.mid = 0;
@@ -725,8 +738,19 @@ __global__ void __launch_bounds__(kClWarps * 32, cl_min_blocks(K))
     relief_after = S.last_prov >= 0 ? S.last_prov + run.cooldown_ticks : 0;
   };
   int64_t t_prev = -1;
+#ifdef BSG_CL_TIMING
+  unsigned long long ph_adv = 0, ph_wif = 0, ph_t = 0;  // debug: advance / what-if phase ns
+  auto gtime = [] {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    return v;
+  };
+#endif
   for (int32_t k = 0; k < N; ++k) {
     const int64_t t = arrival[k];
+#ifdef BSG_CL_TIMING
+    if (threadIdx.x == 0) ph_t = gtime();
+#endif
     if (t != t_prev) {
       const int32_t I = S.active;
       for (int32_t i = warp; i < I; i += kClWarps) {
@@ -737,6 +761,13 @@ __global__ void __launch_bounds__(kClWarps * 32, cl_min_blocks(K))
         }
       }
       __syncthreads();
+#ifdef BSG_CL_TIMING
+      if (threadIdx.x == 0) {
+        const unsigned long long g = gtime();
+        ph_adv += g - ph_t;
+        ph_t = g;
+      }
+#endif
       if (S.err != BSG_OK) break;
       if (relief) relief_round(t);
       // ProvisionComplete events before this instant (arrivals at an equal time go first)
@@ -784,13 +815,7 @@ __global__ void __launch_bounds__(kClWarps * 32, cl_min_blocks(K))
       if (i >= I) break;
       const ClInst& s = S.inst[i];
       if (need_stats) {  // the snapshot's free blocks (backend.cpp:357-365): total - sum held(stored)
-        int32_t held = 0;
-        for (int32_t p = lane; p < s.n; p += 32) {
-          const int64_t g = run.arena_off + i * stride + p;
-          held += bnt<POW2>(__ldcg(&ar.prefill[g]) + __ldcg(&ar.decoded[g]), cfg);
-        }
-        held = static_cast<int32_t>(__reduce_add_sync(kFull, static_cast<uint32_t>(held)));
-        const int32_t snap_free = cfg.total_blocks - held;
+        const int32_t snap_free = cfg.total_blocks - s.held;
         if (lane == 0) S.snap_free[i] = snap_free;
         if (!bp) {
           // load_infaas / load_llumnix (scheduler.cpp:33-46) over the snapshot
@@ -827,6 +852,12 @@ __global__ void __launch_bounds__(kClWarps * 32, cl_min_blocks(K))
           TraceSink{nullptr, 0});
     }
     __syncthreads();
+#ifdef BSG_CL_TIMING
+    if (threadIdx.x == 0) {
+      const unsigned long long g = gtime();
+      ph_wif += g - ph_t;
+    }
+#endif
     if (bp && S.idle_rep < I) {
       const int32_t r0 = S.idle_rep;
       for (int32_t i = threadIdx.x; i < I; i += blockDim.x)
@@ -980,6 +1011,10 @@ __global__ void __launch_bounds__(kClWarps * 32, cl_min_blocks(K))
 #endif
     sm.instances_provisioned = S.n_pend;
     sm.final_instance_count = S.active;
+#ifdef BSG_CL_TIMING
+    sm.total_preemptions = static_cast<int64_t>(ph_adv);                 // debug: advance ns
+    sm.instances_provisioned = static_cast<int32_t>(ph_wif / 1000);      // debug: stats + what-if us
+#endif
     summaries[blockIdx.x] = sm;
   }
   if (reports && S.err == BSG_OK) {
@@ -1440,7 +1475,7 @@ extern "C" bsg_status bsg_fleet_create(bsg_ctx* ctx, int32_t cfg, int32_t n_inst
   p += b_sc;
   f->dparams = reinterpret_cast<FleetParams*>(p);
   std::vector<ClInst> init(static_cast<size_t>(n_instances));
-  for (auto& x : init) x = ClInst{0, c.max_batch_size, c.max_batch_size, c.total_blocks, 0, 0, c.max_batch_size};
+  for (auto& x : init) x = ClInst{0, c.max_batch_size, c.max_batch_size, c.total_blocks, 0, 0, c.max_batch_size, 0, 0};
   FleetDev fd0{-1, 0, 0, -1, BSG_OK, 0};
   bool ok = cudaHostAlloc(&f->pinned, 64 + static_cast<size_t>(n_instances) * 8, cudaHostAllocDefault) == cudaSuccess;
   ok = ok && cudaHostAlloc(reinterpret_cast<void**>(&f->hparams), sizeof(FleetParams), cudaHostAllocDefault) == cudaSuccess;

@@ -27,6 +27,10 @@ for rep in range(2):
     got = ctx.replay_device(runs)
     wall = time.perf_counter() - t0
 ns = np.array([int(g[2]["end_ticks"]) for g in got])
+adv = np.array([int(g[2]["total_preemptions"]) for g in got])
+wif = np.array([int(g[2]["instances_provisioned"]) * 1000 for g in got])
+if os.environ.get("CLPROBE_SAVE"):
+    np.save(os.environ["CLPROBE_SAVE"], np.array([(t[0], t[1], t[2], v) for t, v in zip(tags, ns)]))
 print(f"{len(runs)} runs, call wall {wall*1e3:.1f} ms, longest block {ns.max()/1e6:.1f} ms, "
       f"median {np.median(ns)/1e6:.2f} ms, sum {ns.sum()/1e9:.2f} s")
 order = np.argsort(-ns)
@@ -34,4 +38,5 @@ for i in order[:12]:
     print("  inst %3d cell %d qps %2d: %.2f ms" % (*tags[i], ns[i] / 1e6))
 for ni in sorted(set(t[0] for t in tags)):
     m = np.array([t[0] == ni for t in tags])
-    print(f"instances {ni}: runs {m.sum()}, max {ns[m].max()/1e6:.2f} ms, mean {ns[m].mean()/1e6:.2f} ms")
+    print(f"instances {ni}: runs {m.sum()}, max {ns[m].max()/1e6:.2f} ms, mean {ns[m].mean()/1e6:.2f} ms, "
+          f"advance {adv[m].sum()/ns[m].sum():.2f}, stats+what-ifs {wif[m].sum()/ns[m].sum():.2f} of block time")
