@@ -197,3 +197,37 @@ def test_sweep_and_capacity_error_semantics(ref):
             assert r["result"].tolist() == res.tolist()
         statuses.add(st)
     assert abi.NO_CAPACITY in statuses, statuses
+
+
+def test_closed_loop_fuzz_matches_reference(ctx, ref):
+    """Seeded random closed loops — instance configs (block size, blocks, batch,
+    budget, scheduling policy, latency cache), workloads (shape, estimator, load),
+    dispatch policies, dispatch overhead and provisioning — on K5 in one batched
+    launch per config, against run_experiment + aggregate."""
+    rng = np.random.default_rng(20261017)
+    for case in range(16):
+        bs = int(rng.choice([8, 12, 16, 32]))
+        cfg = abi.make_config(block_size=bs, total_blocks=int(rng.integers(3000, 9000)) // bs,
+                              max_batch_size=int(rng.choice([8, 24, 48, 64, 100, 160])),
+                              chunk_budget=int(rng.choice([256, 512, 1024])),
+                              local_policy=int(rng.integers(0, 2)), cache_mode=int(rng.choice([0, 1, 2])),
+                              context_bucket=int(rng.choice([64, 256])))
+        cases = []
+        for _ in range(4):
+            w = abi.make_workload(count=int(rng.integers(80, 220)), qps=float(rng.uniform(2, 30)),
+                                  arrival_seed=int(rng.integers(1, 1 << 30)),
+                                  prompt_median=float(rng.uniform(100, 400)),
+                                  output_median=float(rng.uniform(60, 300)),
+                                  max_prompt_tokens=1024, max_output_tokens=1024,
+                                  estimator_kind=int(rng.choice([0, 2])),
+                                  estimator_seed=int(rng.integers(1, 1000)))
+            kind = int(rng.choice([0, 0, 1, 2]))
+            ni = int(rng.integers(1, 7))
+            sp = abi.make_replay_spec(ni, policy=int(rng.integers(0, 6)), objective=int(rng.integers(0, 2)),
+                                      capture=0, policy_seed=int(rng.integers(0, 1 << 30)),
+                                      provision_kind=kind, max_instances=ni + int(rng.integers(0, 4)),
+                                      threshold_s=float(rng.uniform(2, 20)), cold_start_s=float(rng.uniform(0, 5)),
+                                      cooldown_s=float(rng.choice([0.0, 1.0, 3.0])),
+                                      dispatch_overhead_s=float(rng.choice([0.0, 0.0, 0.05, 0.7])))
+            cases.append((w, sp))
+        check_runs(ctx, ref, cfg, cases, host=(case % 2 == 0))
