@@ -122,7 +122,9 @@ def test_c_struct_layouts_match_numpy(tmp_path):
              ("bsg_workload", abi.workload_dtype), ("bsg_replay_spec", abi.replay_spec_dtype),
              ("bsg_replay_summary", abi.summary_dtype), ("bsg_request_outcome", abi.outcome_dtype),
              ("bsg_run_report", abi.report_dtype), ("bsg_capacity_result", abi.capacity_dtype),
-             ("bsg_sweep_cell", abi.sweep_cell_dtype), ("bsg_sweep_out", abi.sweep_out_dtype)]
+             ("bsg_sweep_cell", abi.sweep_cell_dtype), ("bsg_sweep_out", abi.sweep_out_dtype),
+             ("bsg_closed_loop_run", abi.closed_loop_run_dtype), ("bsg_sweep_row", abi.sweep_row_dtype),
+             ("bsg_capacity_row", abi.capacity_row_dtype)]
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "blocksim_b200.h"',
              'int main(void) {']
     for cname, dt in pairs:
@@ -223,3 +225,18 @@ def test_wire_check_error_bodies_match_reference(lib, ref):
         else:  # simulated by the reference (200 / 422): simulated here too
             assert st == 0, (body, code, exp, got)
     assert n_err > 60
+
+
+def test_sweep_driver_argument_checks_without_device(lib):
+    """run_sweep / run_capacity reject bad policies and arguments before any
+    device work (a host check, so it holds on this GPU-less container too)."""
+    cfg, w, spec = abi.make_config(), abi.make_workload(count=10), abi.make_replay_spec(2, capture=0)
+    with pytest.raises(native.BsgError) as e:
+        native.run_sweep(0, w, cfg, spec, [9], [1.0], [1])
+    assert e.value.status == abi.BAD_CONFIG
+    with pytest.raises(native.BsgError) as e:
+        native.run_capacity(0, w, cfg, spec, [abi.POLICY_BLOCK_PREDICTIVE], 7, 1, 1, 2, 3.0)
+    assert e.value.status == abi.BAD_CONFIG
+    rows = np.zeros(1, abi.sweep_row_dtype)
+    assert lib.bsg_run_sweep(0, abi.ptr(w), abi.ptr(cfg), abi.ptr(spec), None, 1, None, 0, None, 0, 1,
+                             abi.ptr(rows)) == abi.INVALID_ARGUMENT
