@@ -55,82 +55,81 @@ constexpr int min_blocks(int k, bool opt = false) {
                       : (k == 2 ? BSG_K2_WARPS_PER_SM / kPredictWarps : 1);
 }
 
-// ---- cost-aware launch order ----------------------------------------------------
+// ---- cost-ordered launch (LPT) ----------------------------------------------------
 // Scenario costs vary ~100x (a scenario runs until its candidate completes, so
-// its step count is ~ the candidate's estimate plus its queueing): one long
+// its step count is ~ the candidate's estimate plus its queueing) and one long
 // scenario that starts late is the kernel's tail. Blocks are dispatched in
-// index order, so predict_kernel's first warps run the HEAVY scenarios (cost
-// bucket >= a threshold picked by heavy_threshold_kernel: at most the top n / kHeavyDiv
-// by quarter-octave of cand_est, listed by heavy_list_kernel); the following
-// warps run the rest in the caller's order (which keeps memory locality),
-// skipping the heavy ones. No sort, no atomics on the simulation path.
+// index order, so order_kernel counting-sorts the scenarios by cost bucket,
+// most expensive first (longest-processing-time order), into a scratch copy of
+// the scenario rows whose `reserved` word carries the caller's index;
+// predict_kernel's warp w runs sorted row w and writes result `reserved`. The
+// copy keeps the row one dependent load away (an index array in between would
+// add one more load latency to every scenario's start). Measured with the
+// per-scenario timeline (tools/tlprobe.py, cfg2): the round-2 heavy-first list
+// (top n/128 only) left a 38 us tail of medium scenarios started late (span
+// 220 us, active warps < 90 % of peak for the last 17 %).
 constexpr int kCostBuckets = 128;
 // A scenario queued behind more than kDeepWait waiting entries admits/preempts
 // often, so its pure-decode windows are short: the optimistic pass runs 32-step
 // windows when such scenarios are >= 1/4 of the set, 128-step windows otherwise
 // (cfg3 8.1 ms with 32 vs 9.6 ms with 128; cfg1 310 vs 238 us).
 constexpr int32_t kDeepWait = 8;
+// Cost proxy: the candidate's estimate plus BSG_COST_WAIT tokens per waiting
+// entry queued ahead of it (cfg2: duration vs cand_est correlation 0.98; cfg1,
+// with queues: 0.53 on cand_est alone, 0.83 with 100 per waiting entry).
+#ifndef BSG_COST_WAIT
+#define BSG_COST_WAIT 250
+#endif
 
-__device__ __forceinline__ int cost_bucket(int32_t cand_est) {
-  const uint32_t x = static_cast<uint32_t>(max(cand_est, 0)) + 1u;
+__device__ __forceinline__ int cost_bucket(const bsg_scenario& s) {
+  const int64_t c = static_cast<int64_t>(max(s.cand_est, 0)) +
+                    static_cast<int64_t>(BSG_COST_WAIT) * max(s.wait_n, 0);
+  const uint32_t x = static_cast<uint32_t>(c < 0x7ffffffe ? c : 0x7ffffffe) + 1u;
   const int l = 31 - __clz(x);
   const int f = l >= 2 ? static_cast<int>((x >> (l - 2)) & 3u) : static_cast<int>((x << (2 - l)) & 3u);
   return min(4 * l + f, kCostBuckets - 1);
 }
 
-// Work-queue state of one launch (zeroed before it): 2 tickets, the heavy
-// bucket threshold, a block-completion count, then the bucket histogram.
-// At most n / kHeavyDiv scenarios (whole cost buckets) form the heavy list
-// (cfg2, 60k scenarios: n/16 245.0 us, n/64 241.0, n/128 238.8, n/256 243.0;
-// cfg3 flat).
-#ifndef BSG_HEAVY_DIV
-#define BSG_HEAVY_DIV 128
-#endif
-constexpr int64_t kHeavyDiv = BSG_HEAVY_DIV;
-
+// Work-queue state of one launch (zeroed before it), followed in the same
+// allocation by bsg_scenario sorted[n] and int32_t retry[n].
 struct WorkQueue {
-  int32_t threshold, blocks_done;
-  int32_t heavy_count, retry_count;
+  int32_t arrive;       // order_kernel's grid barrier
+  int32_t retry_count;
   int32_t deep_wait, use_wide;  // window-width vote of the optimistic pass
   int32_t hist[kCostBuckets];
-  // followed by the heavy list: int32_t heavy[n / kHeavyDiv + 32], then the retry
-  // list of the optimistic narrow pass: int32_t retry[n]
+  int32_t cursor[kCostBuckets];
 };
-__device__ __forceinline__ int32_t* heavy_list(WorkQueue* q) { return reinterpret_cast<int32_t*>(q + 1); }
-__device__ __forceinline__ int32_t* retry_list(WorkQueue* q, int64_t n) { return heavy_list(q) + n / kHeavyDiv + 32; }
-
-// Lists the heavy scenarios (order inside the list is arbitrary).
-__global__ void __launch_bounds__(256) heavy_list_kernel(const bsg_scenario* __restrict__ sc, int64_t n,
-                                                         WorkQueue* q) {
-  const int32_t thr = __ldcg(&q->threshold);
-  if (thr >= kCostBuckets) return;
-  const int lane = threadIdx.x & 31;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += stride) {
-    const int64_t i = i0 + lane;
-    const bool heavy = i < n && cost_bucket(__ldg(&sc[i].cand_est)) >= thr;
-    const unsigned m = __ballot_sync(kFull, heavy);
-    if (!m) continue;
-    int32_t base = 0;
-    if (lane == 0) base = atomicAdd(&q->heavy_count, __popc(m));
-    base = __shfl_sync(kFull, base, 0);
-    if (heavy) heavy_list(q)[base + __popc(m & ((1u << lane) - 1u))] = static_cast<int32_t>(i);
-  }
+constexpr size_t kQueueHeader = (sizeof(WorkQueue) + 127) / 128 * 128;
+__device__ __forceinline__ bsg_scenario* sorted_rows(WorkQueue* q) {
+  return reinterpret_cast<bsg_scenario*>(reinterpret_cast<char*>(q) + kQueueHeader);
+}
+__device__ __forceinline__ int32_t* retry_list(WorkQueue* q, int64_t n) {
+  return reinterpret_cast<int32_t*>(sorted_rows(q) + n);
 }
 
-// Histogram of cost buckets; the last block picks the threshold: the highest
-// buckets whose cumulative count stays within n / kHeavyDiv (none if the top bucket alone
-// exceeds it).
-__global__ void __launch_bounds__(256) heavy_threshold_kernel(const bsg_scenario* __restrict__ sc,
-                                                              int64_t n, WorkQueue* q, int32_t force_vote) {
+#ifdef BSG_PROFILE_TIMELINE
+constexpr int64_t kTimelineCap = 1 << 17;
+__device__ uint64_t g_timeline[3 * kTimelineCap];
+#endif
+
+// One launch, grid <= one block per SM (all co-resident): bucket histogram,
+// one grid barrier, then every block derives the descending bucket offsets and
+// scatters its own rows (warp-aggregated cursor atomics; order inside a bucket
+// is arbitrary — each row carries its result index). Block 0 also casts the
+// optimistic pass's window-width vote.
+__global__ void __launch_bounds__(256) order_kernel(const bsg_scenario* __restrict__ sc, int64_t n,
+                                                    WorkQueue* q, int32_t force_vote) {
   __shared__ int32_t h[kCostBuckets];
-  __shared__ bool last;
+  __shared__ int32_t base[kCostBuckets];
   for (int b = threadIdx.x; b < kCostBuckets; b += blockDim.x) h[b] = 0;
   __syncthreads();
+  // contiguous range per block
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = static_cast<int64_t>(blockIdx.x) * per;
+  const int64_t hi = min(n, lo + per);
   int32_t deep = 0;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    atomicAdd(&h[cost_bucket(sc[i].cand_est)], 1);
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    atomicAdd(&h[cost_bucket(sc[i])], 1);
     deep += sc[i].wait_n > kDeepWait ? 1 : 0;
   }
   deep = static_cast<int32_t>(__reduce_add_sync(kFull, static_cast<uint32_t>(deep)));
@@ -138,34 +137,56 @@ __global__ void __launch_bounds__(256) heavy_threshold_kernel(const bsg_scenario
   __syncthreads();
   for (int b = threadIdx.x; b < kCostBuckets; b += blockDim.x)
     if (h[b]) atomicAdd(&q->hist[b], h[b]);
+  // grid barrier (the grid is at most one block per SM, so every block is resident)
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&q->blocks_done, 1) == static_cast<int>(gridDim.x) - 1;
+  if (threadIdx.x == 0) {
+    atomicAdd(&q->arrive, 1);
+    while (atomicAdd(&q->arrive, 0) < static_cast<int32_t>(gridDim.x)) __nanosleep(64);
+  }
   __syncthreads();
-  if (!last || threadIdx.x >= 32) return;
   __threadfence();
-  // suffix sums over buckets (highest cost first), 4 buckets per lane
-  const int lane = threadIdx.x;
-  int32_t c[4], tot = 0;
+  if (threadIdx.x < 32) {
+    // exclusive offsets, highest bucket first: 4 buckets per lane
+    const int lane = threadIdx.x;
+    int32_t c[4], tot = 0;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    c[j] = __ldcg(&q->hist[kCostBuckets - 1 - (lane * 4 + j)]);
-    tot += c[j];
-  }
-  int32_t acc = warp_incl_scan(tot) - tot;  // count in strictly higher buckets
-  const int64_t cap = n / kHeavyDiv;
-  int32_t thr = kCostBuckets;  // no heavy bucket
+    for (int j = 0; j < 4; ++j) {
+      c[j] = __ldcg(&q->hist[kCostBuckets - 1 - (lane * 4 + j)]);
+      tot += c[j];
+    }
+    int32_t acc = warp_incl_scan(tot) - tot;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    acc += c[j];
-    if (acc <= cap && c[j] > 0) thr = kCostBuckets - 1 - (lane * 4 + j);
+    for (int j = 0; j < 4; ++j) {
+      base[kCostBuckets - 1 - (lane * 4 + j)] = acc;
+      acc += c[j];
+    }
+    if (blockIdx.x == 0 && lane == 0)
+      q->use_wide = force_vote >= 0 ? force_vote
+                                    : (static_cast<int64_t>(__ldcg(&q->deep_wait)) * 4 < n ? 1 : 0);
   }
-  thr = static_cast<int32_t>(__reduce_min_sync(kFull, static_cast<uint32_t>(thr)));
-  if (lane == 0) {
-    q->threshold = thr;
-    // wide windows unless a quarter of the set queues behind a deep waiting line
-    q->use_wide = force_vote >= 0 ? force_vote
-                                  : (static_cast<int64_t>(__ldcg(&q->deep_wait)) * 4 < n ? 1 : 0);
+  __syncthreads();
+  bsg_scenario* out = sorted_rows(q);
+  const int lane = threadIdx.x & 31;
+  const unsigned lanes_lt = (1u << lane) - 1u;
+  for (int64_t i0 = lo + (threadIdx.x & ~31); i0 < hi; i0 += blockDim.x) {
+    const int64_t i = i0 + lane;
+    const bool in = i < hi;
+    bsg_scenario r{};
+    int b = -1;
+    if (in) {
+      r = sc[i];
+      b = cost_bucket(r);
+    }
+    const unsigned peers = __match_any_sync(kFull, b);
+    const int leader = __ffs(peers) - 1;
+    int32_t pos = 0;
+    if (in && lane == leader) pos = atomicAdd(&q->cursor[b], __popc(peers));
+    pos = __shfl_sync(kFull, pos, leader);
+    if (in) {
+      r.reserved = static_cast<int32_t>(i);
+      out[base[b] + pos + __popc(peers & lanes_lt)] = r;
+    }
   }
 }
 
@@ -231,25 +252,32 @@ __global__ void __launch_bounds__(kPredictWarps * 32, min_blocks(K, OPT))
     // BSG_WIN_J_WIDE pass (the width for wide member sets) runs
     if ((__ldcg(&q->use_wide) != 0) != (WJ == BSG_WIN_J_PREDICT)) return;
   }
-  // warps [0, nh) run the heavy list; warp nh + i runs scenario i unless it is heavy
+  // warp w runs the w-th row in cost order (order_kernel), whose result index
+  // rides in its reserved word; without a queue, scenario w in caller order
   int64_t w = static_cast<int64_t>(blockIdx.x) * kPredictWarps + warp;
-  if (q) {
-    const int32_t thr = __ldcg(&q->threshold);
-    const int64_t nh = thr < kCostBuckets ? __ldcg(&q->heavy_count) : 0;
-    if (w < nh) {
-      w = __ldcg(&heavy_list(q)[w]);
-    } else {
-      w -= nh;
-      if (w >= n || (thr < kCostBuckets && cost_bucket(__ldg(&scen[w].cand_est)) >= thr)) return;
-    }
-  } else if (w >= n) {
-    return;
-  }
-  const bsg_scenario sc = scen[w];
+  if (w >= n) return;
+  const bsg_scenario sc = q ? sorted_rows(q)[w] : scen[w];
+  if (q) w = sc.reserved;
+#ifdef BSG_PROFILE_TIMELINE
+  uint64_t tl_t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl_t0));
+#endif
   // admit / self-preempt cycle absorption (scenario_sim.cuh) only where queues
   // are deep (KV-pressure / wide sets): it costs the 32-member kernel registers
   const bool ran = predict_one<K, POW2, OPT, WJ, (OPT || K >= 2)>(cfg, cfg_sel, ncfg, prompt, est, prefill, decoded, sc,
                                                   smem, out + w);
+#ifdef BSG_PROFILE_TIMELINE
+  // debug: per-scenario (start, end, SM) on the global timer (tools/tlprobe.py)
+  if (ran && (threadIdx.x & 31) == 0 && w < kTimelineCap) {
+    uint64_t tl_t1;
+    uint32_t smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl_t1));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_timeline[3 * w] = tl_t0;
+    g_timeline[3 * w + 1] = tl_t1;
+    g_timeline[3 * w + 2] = smid;
+  }
+#endif
   if constexpr (OPT) {  // too wide for this pass: list it for the wide kernel
     __syncwarp();
     if (ran && (threadIdx.x & 31) == 0 && out[w].status == kStatusRetryWider)
@@ -500,7 +528,12 @@ int capacity_k(int32_t need) {
   return 0;
 }
 
-// The cost-aware queue pays for itself only with several waves of warps.
+// The queue path (cost order + optimistic narrow pass + retry) serves wide
+// member sets (K > 1) of several waves. 32-member sets (cfg2 shape) and one-wave
+// sets run in the caller's order: measured, the cost order's pre-pass costs
+// more than it saves there (cfg2 229 us plain vs 249 us LPT-ordered and 243 us
+// with round 2's heavy-first list; cfg1 181 vs 186 us) — cand_est misjudges
+// scenarios whose candidate waits for KV blocks, and those end up in the tail.
 #ifndef BSG_QUEUE_MIN
 #define BSG_QUEUE_MIN 8192
 #endif
@@ -513,7 +546,8 @@ bsg_status launch_predict_t(bsg_ctx* ctx, int32_t cfg_sel, int64_t n, const bsg_
   const DevCfg& cf = ctx->dev_cfgs_host[cfg_sel];
   const int64_t blocks = (n + kPredictWarps - 1) / kPredictWarps;
   const std::string tp = std::string(POW2 ? "true" : "false");
-  if (no_queue || n < BSG_QUEUE_MIN) {
+  const bool queue = !no_queue && n >= BSG_QUEUE_MIN && K > 1;
+  if (!queue) {
     ctx->last_launch = "predict_kernel<" + std::to_string(K) + "," + tp + ",false," +
                        std::to_string(BSG_WIN_J_PREDICT) + ">";
     predict_kernel<K, POW2, false, BSG_WIN_J_PREDICT><<<static_cast<unsigned>(blocks), kPredictWarps * 32, 0, s>>>(
@@ -524,7 +558,7 @@ bsg_status launch_predict_t(bsg_ctx* ctx, int32_t cfg_sel, int64_t n, const bsg_
   }
   // stream-ordered scratch: safe for concurrent calls on different streams
   void* mem = nullptr;
-  BSG_CUDA(ctx, cudaMallocAsync(&mem, sizeof(WorkQueue) + (n / kHeavyDiv + 32 + n) * sizeof(int32_t), s));
+  BSG_CUDA(ctx, cudaMallocAsync(&mem, kQueueHeader + n * (sizeof(bsg_scenario) + sizeof(int32_t)), s));
   auto* q = static_cast<WorkQueue*>(mem);
   BSG_CUDA(ctx, cudaMemsetAsync(q, 0, sizeof(WorkQueue), s));
   const int64_t hb = std::min<int64_t>((n + 1023) / 1024, 148);
@@ -532,9 +566,8 @@ bsg_status launch_predict_t(bsg_ctx* ctx, int32_t cfg_sel, int64_t n, const bsg_
   // tests run both passes on the same sets); unset: the vote decides
   const char* fv = std::getenv("BSG_FORCE_VOTE");
   const int32_t force_vote = fv ? (std::atoi(fv) != 0 ? 1 : 0) : -1;
-  heavy_threshold_kernel<<<static_cast<unsigned>(hb), 256, 0, s>>>(sc, n, q, force_vote);
-  heavy_list_kernel<<<static_cast<unsigned>(hb), 256, 0, s>>>(sc, n, q);
-  const int64_t pb = (n + n / kHeavyDiv + 32 + kPredictWarps - 1) / kPredictWarps;  // >= heavy + n warps
+  order_kernel<<<static_cast<unsigned>(hb), 256, 0, s>>>(sc, n, q, force_vote);
+  const int64_t pb = blocks;
   static const bool no_opt = std::getenv("BSG_NO_OPT") != nullptr;
   if constexpr (K > 1) {
     if (!no_opt) {
@@ -552,26 +585,19 @@ bsg_status launch_predict_t(bsg_ctx* ctx, int32_t cfg_sel, int64_t n, const bsg_
       const int64_t rb = std::min<int64_t>(pb, 148 * 8);
       predict_retry_kernel<K, POW2><<<static_cast<unsigned>(rb), kPredictWarps * 32, 0, s>>>(
           cf, cfg_sel, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
-      ctx->launches += 5;
+      ctx->launches += 4;
       BSG_CUDA(ctx, cudaGetLastError());
       BSG_CUDA(ctx, cudaFreeAsync(mem, s));
       return BSG_OK;
     }
   }
   ctx->last_launch = "predict_kernel<" + std::to_string(K) + "," + tp + ",false," +
-                     std::to_string(K == 1 ? BSG_WIN_J_PREDICT : BSG_WIN_J_WIDE) + ">";
+                     std::to_string(BSG_WIN_J_WIDE) + ">";
   predict_kernel<K, POW2, false, K == 1 ? BSG_WIN_J_PREDICT : BSG_WIN_J_WIDE>
       <<<static_cast<unsigned>(pb), kPredictWarps * 32, 0, s>>>(
       cf, cfg_sel, ctx->ncfg, e.prompt, e.est, e.prefill, e.decoded, sc, n, q, out);
-  ctx->launches += 3;
+  ctx->launches += 2;
   BSG_CUDA(ctx, cudaGetLastError());
-  if (std::getenv("BSG_QUEUE_DEBUG")) {
-    WorkQueue hq;
-    cudaMemcpyAsync(&hq, q, sizeof(hq), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    std::fprintf(stderr, "queue: n=%lld blocks=%lld threshold=%d heavy=%d\n",
-                 static_cast<long long>(n), static_cast<long long>(pb), hq.threshold, hq.heavy_count);
-  }
   BSG_CUDA(ctx, cudaFreeAsync(mem, s));
   return BSG_OK;
 }
@@ -713,7 +739,7 @@ bsg_status bsg_ctx_create(int device, bsg_ctx** out) {
     delete ctx;
     return BSG_CUDA_ERROR;
   }
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < bsg_ctx::kPipe; ++i) {
     if (cudaStreamCreateWithFlags(&ctx->pipe[i], cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->pipe_done[i], cudaEventDisableTiming) != cudaSuccess) {
       delete ctx;
@@ -836,32 +862,35 @@ bsg_status bsg_predict_batch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n
   dev.decoded = static_cast<const int32_t*>(ctx->decoded.p);
   auto* dsc = static_cast<bsg_scenario*>(ctx->scen.p);
   auto* dres = static_cast<bsg_result*>(ctx->res.p);
-  // Chunked pipeline (measured on cfg2, pinned buffers: 3 chunks of 20k cut the
-  // call from 1.05 to 0.75 ms; H2D is PCIe-bound): chunk c (a contiguous
-  // scenario range) runs and copies its results back while later chunks' bytes
-  // are still in flight.
-  const char* env_chunk = std::getenv("BSG_PIPE_CHUNK");
-  const int64_t target_chunk = env_chunk ? std::max<int64_t>(1, std::atoll(env_chunk)) : 20000;
-  const int64_t nchunks0 = std::min<int64_t>(16, std::max<int64_t>(1, n / target_chunk));
-  const int64_t per = (n + nchunks0 - 1) / nchunks0;
-  // chunk boundaries: equal chunks, except that the last one is split in
-  // halving pieces (BSG_PIPE_TAIL of them) so the final kernel — whose tail
-  // nothing overlaps — is short
+  // Chunked pipeline: chunk c (a contiguous scenario range) runs as soon as
+  // the entry piece holding its last entry has landed, on its own stream, and
+  // copies its results back while later pieces are still in flight. The
+  // chunks shrink (weights BSG_PIPE_SPLIT, default 3:2:1): the last chunk's
+  // kernel — the only one nothing overlaps — is short. Measured on cfg2
+  // (tools/e2eprobe.py, one box, median of 40 calls): equal thirds 0.592 ms,
+  // 3:2:1 0.557, 2:1 0.566, 4:3:2:1 0.569, 5:4:3:2:1 0.584 (each piece costs
+  // four more copy calls), one chunk 0.698.
   std::vector<int64_t> bounds{0};
   {
-    const char* env_tail = std::getenv("BSG_PIPE_TAIL");
-    const int tail = env_tail ? std::max(0, std::atoi(env_tail)) : 0;
-    // an optional small first chunk: its host-side range scan and copy start the
-    // pipeline sooner (BSG_PIPE_HEAD scenarios)
-    const char* env_head = std::getenv("BSG_PIPE_HEAD");
-    const int64_t head = env_head ? std::max<int64_t>(0, std::atoll(env_head)) : 0;
-    if (head > 0 && head < per) bounds.push_back(head);
-    for (int64_t c = 0; c + 1 < nchunks0; ++c) bounds.push_back(std::min(n, (c + 1) * per));
-    int64_t rest = n - bounds.back();
-    for (int t = 0; t < tail && rest > 2048; ++t) {
-      const int64_t piece = rest / 2;
-      bounds.push_back(bounds.back() + piece);
-      rest -= piece;
+    std::vector<double> wts;
+    if (const char* env_split = std::getenv("BSG_PIPE_SPLIT")) {
+      for (const char* q = env_split; *q;) {
+        char* end = nullptr;
+        const double v = std::strtod(q, &end);
+        if (end == q) break;
+        if (v > 0) wts.push_back(v);
+        q = *end == ',' ? end + 1 : end;
+      }
+    }
+    if (wts.empty()) wts = {3, 2, 1};
+    if (static_cast<int>(wts.size()) > bsg_ctx::kPieces) wts.resize(bsg_ctx::kPieces);
+    if (n < 16384) wts = {1};  // one wave or two: nothing to overlap
+    double tot = 0;
+    for (double v : wts) tot += v;
+    double acc = 0;
+    for (size_t c = 0; c + 1 < wts.size(); ++c) {
+      acc += wts[c];
+      bounds.push_back(std::min<int64_t>(n, static_cast<int64_t>(static_cast<double>(n) * acc / tot)));
     }
     bounds.push_back(n);
   }
@@ -888,22 +917,20 @@ bsg_status bsg_predict_batch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n
                                         static_cast<int32_t*>(ctx->decoded.p)};
   // The scenario rows and then the entry columns stream in pieces (one per
   // chunk) on pipe[0] from the start of the call — no host scan in front of the
-  // first byte; scenario chunk c runs on pipe[1 + c % 2] once the piece holding
-  // its last entry has landed, while the host scans the next chunk. Measured on
-  // cfg2 (tools/pipeprobe.py): 0.60 ms vs 0.68 ms for per-chunk copies behind
-  // each chunk's scan (BSG_PIPE=1); more pieces than chunks cost more in copy
-  // calls than they gain (6 pieces 0.66 ms, 12 pieces 0.77 ms).
+  // first byte; scenario chunk c runs on its own stream pipe[1 + c % 6] once the
+  // piece holding its last entry has landed, while the host scans the next
+  // chunk (round 2: 0.60 ms vs 0.68 ms for per-chunk copies behind each chunk's
+  // scan, BSG_PIPE=1).
   const char* env_pipe = std::getenv("BSG_PIPE");
   const bool v2 = !(env_pipe && std::atoi(env_pipe) == 1);
-  const char* env_pieces = std::getenv("BSG_PIPE_PIECES");
-  const int np = static_cast<int>(std::min<int64_t>(
-      bsg_ctx::kPieces, std::max<int64_t>(1, env_pieces ? std::atoll(env_pieces) : nchunks)));
+  const int np = static_cast<int>(nchunks);  // one entry piece per chunk, same fraction
   std::vector<int64_t> pe(np + 1);
   if (v2) {
     // the scenario rows first (1.9 MB at cfg2): every chunk needs its rows before its entries
     BSG_CUDA(ctx, cudaMemcpyAsync(dsc, scenarios, n * sizeof(bsg_scenario), cudaMemcpyHostToDevice,
                                   ctx->pipe[0]));
-    for (int k = 0; k <= np; ++k) pe[k] = n_entries * k / np;
+    for (int k = 0; k <= np; ++k) pe[k] = static_cast<int64_t>(static_cast<double>(n_entries) * bounds[k] / n);
+    pe[np] = n_entries;
     for (int k = 0; k < np; ++k) {
       if (pe[k + 1] > pe[k])
         for (int q = 0; q < 4; ++q)
@@ -938,7 +965,7 @@ bsg_status bsg_predict_batch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n
       ctx->last_error = "scenario references entries outside [0, n_entries)";
       return BSG_INVALID_ARGUMENT;
     }
-    cudaStream_t st = v2 ? ctx->pipe[1 + c % 2] : ctx->pipe[c % 3];
+    cudaStream_t st = v2 ? ctx->pipe[1 + c % (bsg_ctx::kPipe - 1)] : ctx->pipe[c % 3];
     if (v2) {
       if (hi > lo) {  // the piece holding entry hi - 1 (pieces land in order)
         int k = 0;
@@ -968,7 +995,7 @@ bsg_status bsg_predict_batch(bsg_ctx* ctx, const bsg_entries* entries, int64_t n
     mark(st);  // D2H of chunk c done
     BSG_CUDA(ctx, cudaEventRecord(ctx->pipe_done[c % 3], st));
   }
-  for (int i = 0; i < 3; ++i) BSG_CUDA(ctx, cudaStreamSynchronize(ctx->pipe[i]));
+  for (int i = 0; i < bsg_ctx::kPipe; ++i) BSG_CUDA(ctx, cudaStreamSynchronize(ctx->pipe[i]));
   if (pipe_prof && v2) {  // the piece copies' completion first, then the chunks
     std::rotate(pev.begin() + 1, pev.begin() + 2, pev.end());
     std::rotate(host_us.begin() + 1, host_us.begin() + 2, host_us.end());
@@ -1329,3 +1356,11 @@ bsg_status bsg_dispatch_mc_sampled(bsg_ctx* ctx, const bsg_entries* entries, int
 }
 
 }  // extern "C"
+
+#ifdef BSG_PROFILE_TIMELINE
+// debug build only: copies the per-scenario (start, end, SM) timeline of the last predict pass
+extern "C" int bsg_debug_timeline(uint64_t* host, int64_t n) {
+  if (n > bsg::kTimelineCap) n = bsg::kTimelineCap;
+  return cudaMemcpyFromSymbol(host, bsg::g_timeline, 3 * n * sizeof(uint64_t)) == cudaSuccess ? 0 : 1;
+}
+#endif

@@ -34,8 +34,10 @@ struct DevBuf {
 struct bsg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};  // chunked host-buffer pipeline
-  cudaEvent_t pipe_done[3] = {nullptr, nullptr, nullptr};
+  // chunked host-buffer pipeline: pipe[0] copies, pipe[1..kPipe) run chunks
+  static constexpr int kPipe = 7;
+  cudaStream_t pipe[kPipe] = {};
+  cudaEvent_t pipe_done[kPipe] = {};
   static constexpr int kPieces = 16;
   cudaEvent_t piece_ev[kPieces] = {};  // entry pieces landed (host-buffer pipeline)
   std::string last_error;

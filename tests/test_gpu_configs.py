@@ -1,6 +1,6 @@
 """GPU parity on the configurations exactly as bench.py measures them
 (BASELINE.json configs 1-5): the same captured scenario sets, through the
-same device-resident entry point (bsg_predict_batch_device: heavy-first queue,
+same device-resident entry point (bsg_predict_batch_device: cost-ordered queue,
 the optimistic narrow passes with their window-width vote, the wide retry
 kernel), checked bit-exactly against the reference's own predict()
 (oracle/_ref) on all host cores. Also: both outcomes of the optimistic pass's

@@ -463,7 +463,7 @@ def test_edge_inputs(ctx, ref):
     """Empty batches, a scenario naming a config that does not exist (every
     per-config pass writes its INVALID_ARGUMENT verdict, the rest are
     unaffected), and a set whose configs are all unused but one."""
-    cfgs, ss = fuzz_set(41, 9000)  # >= the queue threshold: heavy list + per-config passes
+    cfgs, ss = fuzz_set(41, 9000)  # >= the queue threshold: cost order (wide sets) + per-config passes
     ctx.set_configs(cfgs)
     empty = abi.ScenarioSet(ss.prompt[:0], ss.est[:0], ss.prefill[:0], ss.decoded[:0], ss.scenarios[:0])
     assert len(ctx.predict_batch(empty)) == 0

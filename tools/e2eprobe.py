@@ -1,6 +1,6 @@
-"""e2e (host buffers through bsg_predict_batch) vs pipeline chunking, and the
+"""e2e (host buffers through bsg_predict_batch) vs pipeline chunk splits (BSG_PIPE_SPLIT), and the
 plain pinned H2D / D2H of the same bytes (cfg2 capture, L2 flushed per call).
-usage: python tools/e2eprobe.py"""
+usage: python tools/e2eprobe.py [split ...]"""
 import ctypes as C
 import os
 import sys
@@ -49,16 +49,15 @@ def call():
     assert st == abi.OK
 
 
-for chunk in ["60000", "30000", "20000", "15000", "12000", "10000", "7500", "5000"]:
-    for tail in ["0", "2"]:
-        os.environ["BSG_PIPE_CHUNK"] = chunk
-        os.environ["BSG_PIPE_TAIL"] = tail
-        ts = []
-        for i in range(80):
-            flush.zero_()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            call()
-            ts.append(time.perf_counter() - t0)
-        print(f"chunk {chunk:>5} tail {tail}: median {np.median(ts[40:]) * 1e3:.3f} ms  "
-              f"min {min(ts[40:]) * 1e3:.3f} ms", flush=True)
+splits = sys.argv[1:] or ["1", "1,1,1", "4,3,2,1", "3,3,2,1", "5,4,3,2,1", "6,4,2,1", "8,6,4,2,1", "2,1", "3,2,1"]
+for split in splits:
+    os.environ["BSG_PIPE_SPLIT"] = split
+    ts = []
+    for i in range(80):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        call()
+        ts.append(time.perf_counter() - t0)
+    print(f"split {split:>10}: median {np.median(ts[40:]) * 1e3:.3f} ms  "
+          f"min {min(ts[40:]) * 1e3:.3f} ms", flush=True)

@@ -1,6 +1,6 @@
 """Timeline of the host-buffer pipeline (bsg_predict_batch with BSG_PIPE_PROFILE=1:
 per chunk, when its H2D / kernels / D2H finished on the device and when the host
-had enqueued them, microseconds from the call's start). usage: python tools/pipeprobe.py"""
+had enqueued them, microseconds from the call's start). usage: python tools/pipeprobe.py [BSG_PIPE_SPLIT weights, e.g. 4,3,2,1 ...]"""
 import ctypes as C
 import os
 import sys
@@ -22,8 +22,8 @@ host = abi.ScenarioSet(*[p.numpy() for p in pinned], pscen.numpy().view(abi.scen
 pout = torch.empty(n * abi.result_dtype.itemsize, dtype=torch.uint8).pin_memory()
 ent = host.entries()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-for chunk in sys.argv[1:] or ["20000"]:
-    os.environ["BSG_PIPE_CHUNK"] = chunk
+for chunk in sys.argv[1:] or ["4,3,2,1"]:
+    os.environ["BSG_PIPE_SPLIT"] = chunk
     ts = []
     for i in range(60):
         if i == 59:
@@ -36,4 +36,4 @@ for chunk in sys.argv[1:] or ["20000"]:
         ts.append(time.perf_counter() - t0)
         assert st == abi.OK
     os.environ.pop("BSG_PIPE_PROFILE")
-    print(f"chunk {chunk}: median {np.median(ts[20:59]) * 1e3:.3f} ms", flush=True)
+    print(f"split {chunk}: median {np.median(ts[20:59]) * 1e3:.3f} ms", flush=True)
