@@ -65,6 +65,12 @@ constexpr int kMaxWinJ = BSG_MAX_WIN_J;
 #ifndef BSG_CYC_CLOSED
 #define BSG_CYC_CLOSED 0
 #endif
+// Drain pass (simulate_scenario): once nothing can be admitted any more, the
+// steps up to the candidate's completion are priced in one pass (BSG_DRAIN=0:
+// windows only, for A/B measurements).
+#ifndef BSG_DRAIN
+#define BSG_DRAIN 1
+#endif
 // Per-warp shared-memory words of simulate_scenario with window width WJ: the
 // completion-compaction area (5 x 32K) / the window histograms and cycle arrays
 // (4 x 32 x WJ), whichever is larger.
@@ -665,7 +671,139 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
 #ifdef BSG_PROFILE_T0
     bool prof_entered = false;
 #endif
-    if (win) {
+    // ---------------- drain: the rest of the run in one pass ----------------
+    // Nothing is waiting (no victim, the snapshot's queue consumed, the
+    // candidate admitted) and every running member decodes: no admission can
+    // happen any more, so the steps up to the candidate's completion are pure
+    // decode and only completions change the batch — unless the decode block
+    // demand runs out of free blocks. If the members' total demand up to the
+    // candidate's completion fits in the free blocks now (releases only add),
+    // no step preempts, and the run ends at step T = r_cand + 1 with
+    //   D(t) = #{p : r_p >= t},  C(t) = sum_{p : r_p >= t} (stored_p + t),
+    // the window's formulas (below) without its 32*WJ-step cap. Members are
+    // ranked by r_p into shared memory; lane l prices steps
+    // [T*l/32, T*(l+1)/32), walking the completions in order. (Reference:
+    // backend.cpp:113-182 with an empty waiting_ is a decode-all plan;
+    // 263-288 allocates without eviction while demand <= free.)
+    bool drained = false;
+    if constexpr (!TRACE && !MC && BSG_DRAIN) {
+      if (win && !cyc0 && L == n && h >= wait_n && !cand_tail) {
+        int32_t rk[K], rc = 0x7fffffff;
+        int64_t dem = 0;
+        const int32_t rcl = [&] {
+          int32_t m = 0x7fffffff;
+#pragma unroll
+          for (int k = 0; k < K; ++k)
+            if (lane * K + k < n && org[k] == (kCandOrg | kEverBit)) m = target[k] - decoded[k] - 1;
+          return m;
+        }();
+        rc = static_cast<int32_t>(__reduce_min_sync(kFull, static_cast<uint32_t>(rcl)));
+        const int64_t lim = kMaxSimulatedSteps + 1 - steps;
+        const int32_t Td = rc + 1;  // steps to the candidate's completion (inclusive)
+        if (rc != 0x7fffffff && Td <= lim) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            rk[k] = lane * K + k < n ? target[k] - decoded[k] - 1 : 0x7fffffff;
+            if (lane * K + k < n) {
+              const int32_t rl = rk[k] < Td - 1 ? rk[k] : Td - 1;
+              dem += bnt<POW2>(stored[k] + rl + 1, cfg) - bnt<POW2>(stored[k], cfg);
+            }
+          }
+          dem = warp_sum_i64(dem);
+          if (dem <= free_blocks) {
+            drained = true;
+            T = Td;
+            // rank members by (r, position) and store (r, stored) in that order
+            int32_t rank[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) rank[k] = 0;
+            for (int src = 0; src < 32; ++src) {
+#pragma unroll
+              for (int kk = 0; kk < K; ++kk) {
+                const int32_t rq = __shfl_sync(kFull, rk[kk], src);
+                const int32_t q = src * K + kk;
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+                  rank[k] += (rq < rk[k] || (rq == rk[k] && q < lane * K + k)) ? 1 : 0;
+              }
+            }
+            int32_t* s_r = smem;
+            int32_t* s_s = smem + CAP;
+            int32_t* s_p = smem + 2 * CAP;
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              if (lane * K + k < n) {
+                s_r[rank[k]] = rk[k];
+                s_s[rank[k]] = stored[k];
+              }
+            }
+            __syncwarp();
+            int32_t sv[K], sp[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) sv[k] = lane * K + k < n ? s_s[lane * K + k] : 0;
+            const int32_t s_tot = excl_scan<K>(sv, sp);
+#pragma unroll
+            for (int k = 0; k < K; ++k) s_p[lane * K + k] = sp[k];
+            __syncwarp();
+            const int32_t t0 = static_cast<int32_t>((static_cast<int64_t>(Td) * lane) >> 5);
+            const int32_t t1 = static_cast<int32_t>((static_cast<int64_t>(Td) * (lane + 1)) >> 5);
+            int32_t lo = 0, hi = n;  // idx = #{members with r < t0}
+            while (lo < hi) {
+              const int32_t mid = (lo + hi) >> 1;
+              if (s_r[mid] < t0) lo = mid + 1;
+              else hi = mid;
+            }
+            int32_t idx = lo;
+            int32_t S = idx < n ? s_tot - s_p[idx] : 0;  // stored tokens of the members alive at t
+            int32_t nxt = idx < n ? s_r[idx] : 0x7fffffff;
+            // step_ticks(cfg, 0, D, C) split at its D term (same operations, same order)
+            auto xd_of = [&](int32_t D) {
+              const double x = __dadd_rn(cfg.c0, __dmul_rn(cfg.cp, 0.0));
+              return __dadd_rn(x, __dmul_rn(cfg.cd, static_cast<double>(D)));
+            };
+            double xd = xd_of(n - idx);
+            int64_t sum = 0, msum = 0;
+            for (int32_t t = t0; t < t1; ++t) {
+              if (nxt < t) {
+                do {
+                  S -= s_s[idx];
+                  ++idx;
+                  nxt = idx < n ? s_r[idx] : 0x7fffffff;
+                } while (nxt < t);
+                xd = xd_of(n - idx);
+              }
+              const int32_t D = n - idx;
+              int64_t ctx = S + t * D;
+              if (cfg.cache_mode == BSG_CACHE_BUCKETED) {
+                const int64_t b = cfg.context_bucket < 1 ? 1 : cfg.context_bucket;
+                ctx = (ctx + b / 2) / b * b;
+              }
+              const double x = __dadd_rn(xd, __dmul_rn(cfg.cc, static_cast<double>(ctx)));
+              sum += llround(__dmul_rn(x, 1e9));
+              msum += D + 1;
+            }
+            elapsed += warp_sum_i64(sum);
+            steps += T;
+            res.member_steps += warp_sum_i64(msum);
+            free_blocks -= static_cast<int32_t>(dem);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              const int32_t p = lane * K + k;
+              dec_s[k] = p < n;
+              pre_s[k] = false;
+              first_tok[k] = false;
+              if (p < n) decoded[k] += rk[k] < T ? rk[k] + 1 : T;
+              done[k] = p < n && decoded[k] >= target[k];
+              freed[k] = done[k] ? bnt<POW2>(prefill[k] + decoded[k], cfg) : 0;
+              if (org[k] == (kCandOrg | kEverBit)) cand_done |= done[k];
+            }
+            __syncwarp();
+          }
+        }
+      }
+    }
+    if (win && !drained) {
 #ifdef BSG_PROFILE_T0
       prof_entered = true;
 #endif
