@@ -686,7 +686,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
     // backend.cpp:113-182 with an empty waiting_ is a decode-all plan;
     // 263-288 allocates without eviction while demand <= free.)
     bool drained = false;
-    if constexpr (!TRACE && !MC && BSG_DRAIN) {
+    if constexpr (BSG_DRAIN) {
       if (win && !cyc0 && L == n && h >= wait_n && !cand_tail) {
         int32_t rk[K], rc = 0x7fffffff;
         int64_t dem = 0;
@@ -764,6 +764,21 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
             };
             double xd = xd_of(n - idx);
             int64_t sum = 0, msum = 0;
+            // MC: sample j (sorted) ends at step L_j - dec0 - 1; this lane's
+            // samples are those ending in [t0, t1), recorded at their step with
+            // the lane-local prefix, rebased after the walk
+            const int32_t dec0 = cand_target - 1 - rc;  // the candidate's decoded count now
+            int32_t jp = 0, j0 = 0;
+            int64_t part = 0;
+            if constexpr (MC) {
+              int32_t a0 = mc_ptr, b0 = mc.S;
+              while (a0 < b0) {
+                const int32_t mid = (a0 + b0) >> 1;
+                if (mc.len[mid] - dec0 - 1 < t0) a0 = mid + 1;
+                else b0 = mid;
+              }
+              jp = j0 = a0;
+            }
             for (int32_t t = t0; t < t1; ++t) {
               if (nxt < t) {
                 do {
@@ -782,6 +797,77 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
               const double x = __dadd_rn(xd, __dmul_rn(cfg.cc, static_cast<double>(ctx)));
               sum += llround(__dmul_rn(x, 1e9));
               msum += D + 1;
+              if constexpr (MC) {
+                while (jp < mc.S && mc.len[jp] - dec0 - 1 == t) {
+                  part += sum;
+                  if (mc.sample_e2e) mc.sample_e2e[jp] = sum;
+                  ++jp;
+                }
+              }
+            }
+            if constexpr (MC) {
+              // elapsed before this lane's first step: exclusive scan of the lane sums
+              int64_t pre = sum;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const int64_t y = __shfl_up_sync(kFull, pre, o);
+                if (lane >= o) pre += y;
+              }
+              const int64_t base = elapsed + (pre - sum);
+              mc_sum += part + static_cast<int64_t>(jp - j0) * base;
+              if (mc.sample_e2e)
+                for (int32_t j = j0; j < jp; ++j) mc.sample_e2e[j] += base;
+              mc_ptr = mc.S;  // the candidate completes in this pass: every sample is done
+              cand_hi = cand_target;
+            }
+            if constexpr (TRACE) {
+              // per-step records (bsg_trace), as the window writes them
+              int32_t fcur = free_blocks;
+              for (int32_t t = 0; t < T && steps + t < trace.cap; ++t) {
+                int32_t al[K], ral[K], cp[K], rcp[K], z[K], rz[K], cx[K], dm[K], fr[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                  const bool in = lane * K + k < n;
+                  al[k] = in && rk[k] >= t ? 1 : 0;
+                  cp[k] = in && rk[k] == t ? 1 : 0;
+                  z[k] = in && t == 0 && decoded[k] == 0 ? 1 : 0;
+                  cx[k] = al[k] ? stored[k] + t : 0;
+                  dm[k] = al[k] && modt<POW2>(stored[k] + t, cfg) == 0 ? 1 : 0;
+                  fr[k] = cp[k] ? bnt<POW2>(stored[k] + t + 1, cfg) : 0;
+                }
+                const int32_t nd = excl_scan<K>(al, ral);
+                const int32_t ncp = excl_scan<K>(cp, rcp);
+                excl_scan<K>(z, rz);
+                uint64_t hplan = 0, hev = 0;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                  const int32_t o = org_origin(org[k]);
+                  if (al[k]) hplan += hash_term(BSG_TAG_PLAN, ral[k], o, 0);
+                  if (z[k]) hev += hash_term(BSG_TAG_FIRST, rz[k], o, 0);
+                  if (cp[k]) hev += hash_term(BSG_TAG_COMPLETED, rcp[k], o, 0);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                  hplan += __shfl_xor_sync(kFull, hplan, o);
+                  hev += __shfl_xor_sync(kFull, hev, o);
+                }
+                const int32_t ct = warp_sum<K>(cx);
+                fcur += warp_sum<K>(fr) - warp_sum<K>(dm);
+                if (lane == 0) {
+                  bsg_step_record& rec = trace.rec[steps + t];
+                  rec.duration_ticks = step_ticks(cfg, 0, nd, ct);
+                  rec.context_tokens = ct;
+                  rec.n_decode = nd;
+                  rec.prefill_tokens = 0;
+                  rec.n_prefill = 0;
+                  rec.n_preempted = 0;
+                  rec.n_completed = ncp;
+                  rec.free_blocks_after = fcur;
+                  rec.plan_hash = hplan;
+                  rec.event_hash = hev;
+                }
+              }
+              __syncwarp();
             }
             elapsed += warp_sum_i64(sum);
             steps += T;
