@@ -8,9 +8,9 @@
 set -x
 mkdir -p gpurun_out
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-  --log-file gpurun_out/launches_r2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-latency \
+  --log-file gpurun_out/launches_r2b.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-latency \
   > gpurun_out/ncu_launches_bench.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:predict_kernel -c 1 \
-  -o gpurun_out/prof_r2_cfg2 python tools/kbench.py cfg2 --steps 1 > gpurun_out/ncu_full_cfg2.log 2>&1
+  -o gpurun_out/prof_r2b_cfg2 python tools/kbench.py cfg2 --steps 1 > gpurun_out/ncu_full_cfg2.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:predict_kernel --launch-skip 1 -c 1 \
-  -o gpurun_out/prof_r2_cfg3 python tools/kbench.py cfg3 --steps 1 > gpurun_out/ncu_full_cfg3.log 2>&1
+  -o gpurun_out/prof_r2b_cfg3 python tools/kbench.py cfg3 --steps 1 > gpurun_out/ncu_full_cfg3.log 2>&1
