@@ -713,29 +713,51 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
           if (dem <= free_blocks) {
             drained = true;
             T = Td;
-            // rank members by (r, position) and store (r, stored) in that order
-            int32_t rank[K];
-#pragma unroll
-            for (int k = 0; k < K; ++k) rank[k] = 0;
-            for (int src = 0; src < 32; ++src) {
-#pragma unroll
-              for (int kk = 0; kk < K; ++kk) {
-                const int32_t rq = __shfl_sync(kFull, rk[kk], src);
-                const int32_t q = src * K + kk;
-#pragma unroll
-                for (int k = 0; k < K; ++k)
-                  rank[k] += (rq < rk[k] || (rq == rk[k] && q < lane * K + k)) ? 1 : 0;
-              }
-            }
             int32_t* s_r = smem;
             int32_t* s_s = smem + CAP;
             int32_t* s_p = smem + 2 * CAP;
             __syncwarp();
+            if constexpr (K == 1) {
+              // bitonic sort of (r, stored) across the 32 lanes, ascending r
+              int32_t key = rk[0], val = stored[0];
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-              if (lane * K + k < n) {
-                s_r[rank[k]] = rk[k];
-                s_s[rank[k]] = stored[k];
+              for (int kb = 2; kb <= 32; kb <<= 1) {
+#pragma unroll
+                for (int j = kb >> 1; j > 0; j >>= 1) {
+                  const int32_t ko = __shfl_xor_sync(kFull, key, j);
+                  const int32_t vo = __shfl_xor_sync(kFull, val, j);
+                  const bool keep_min = ((lane & j) == 0) == ((lane & kb) == 0);
+                  if (keep_min ? ko < key : ko > key) {
+                    key = ko;
+                    val = vo;
+                  }
+                }
+              }
+              if (lane < n) {
+                s_r[lane] = key;
+                s_s[lane] = val;
+              }
+            } else {
+              // rank members by (r, position) and store (r, stored) in that order
+              int32_t rank[K];
+#pragma unroll
+              for (int k = 0; k < K; ++k) rank[k] = 0;
+              for (int src = 0; src < 32; ++src) {
+#pragma unroll
+                for (int kk = 0; kk < K; ++kk) {
+                  const int32_t rq = __shfl_sync(kFull, rk[kk], src);
+                  const int32_t q = src * K + kk;
+#pragma unroll
+                  for (int k = 0; k < K; ++k)
+                    rank[k] += (rq < rk[k] || (rq == rk[k] && q < lane * K + k)) ? 1 : 0;
+                }
+              }
+#pragma unroll
+              for (int k = 0; k < K; ++k) {
+                if (lane * K + k < n) {
+                  s_r[rank[k]] = rk[k];
+                  s_s[rank[k]] = stored[k];
+                }
               }
             }
             __syncwarp();

@@ -460,8 +460,12 @@ class Context:
             raise BsgError(st, "bsg_set_configs", f"config {bi.value} field {fc.value}")
         self.cfgs = cfgs
 
-    def predict_batch(self, ss: abi.ScenarioSet) -> np.ndarray:
-        out = np.zeros(len(ss), abi.result_dtype)
+    def predict_batch(self, ss: abi.ScenarioSet, out: np.ndarray | None = None) -> np.ndarray:
+        """out: optional result array to fill (e.g. a view of pinned host memory:
+        32-member chunks then store their results straight into it)."""
+        if out is None:
+            out = np.zeros(len(ss), abi.result_dtype)
+        assert out.dtype == abi.result_dtype and len(out) >= len(ss) and out.flags.c_contiguous
         e = ss.entries()
         self._check(self.L.bsg_predict_batch(self.h, C.byref(e), ss.n_entries, _p(ss.scenarios),
                                              len(ss), _p(out)), "bsg_predict_batch")

@@ -107,6 +107,26 @@ def test_gpu_matches_reference_on_replay_captures(ctx, ref, cfgname, kw, n_inst)
     assert compare_to_ref(got, exp).sum() == 0
 
 
+def test_pinned_host_buffers_match_reference(ctx, ref):
+    """The e2e path as bench.py drives it: bsg_predict_batch over pinned host
+    buffers (pipelined pieces, 3:2:1 chunks, one stream per chunk) equals the
+    reference and the pageable-buffer call on the cfg2 capture."""
+    import torch
+    cfg = abi.make_config()
+    w = abi.make_workload(count=5000, estimator_kind=0, qps=27, arrival_seed=1)
+    _, _, ss = ref.replay(w, cfg, abi.make_replay_spec(12))
+    ctx.set_configs(cfg)
+    pinned = [torch.from_numpy(c).pin_memory() for c in (ss.prompt, ss.est, ss.prefill, ss.decoded)]
+    pscen = torch.from_numpy(ss.scenarios.view(np.uint8)).pin_memory()
+    host = abi.ScenarioSet(*[p.numpy() for p in pinned], pscen.numpy().view(abi.scenario_dtype))
+    pout = torch.full((len(ss) * abi.result_dtype.itemsize,), 0xAB, dtype=torch.uint8).pin_memory()
+    out = pout.numpy().view(abi.result_dtype)
+    ctx.predict_batch(host, out=out)
+    exp = ref.predict_batch(cfg, ss, threads=8)
+    assert compare_to_ref(out, exp).sum() == 0
+    assert np.array_equal(out, ctx.predict_batch(ss))
+
+
 @pytest.mark.parametrize("kw,n_inst,policy", [
     (dict(count=1000, estimator_kind=2, estimator_seed=1, qps=10, arrival_seed=1), 4,
      abi.POLICY_BLOCK_PREDICTIVE),

@@ -1,7 +1,7 @@
 """Per-scenario timeline of one predict pass (debug build with -DBSG_PROFILE_TIMELINE):
 active warps over time, the tail after the last scenario starts, and how well
 cand_est predicts a scenario's duration.
-usage: tools/variant.sh "-DBSG_PROFILE_TIMELINE" tools/tlprobe.py [cfg2|cfg1|cfg3q]"""
+usage: tools/mkvariant.sh tl "-DBSG_PROFILE_TIMELINE"; BSG_LIB_PATH=build/var_tl/libblocksim_b200.so python tools/tlprobe.py [cfg2|cfg1|cfg3|cfg3q]"""
 import ctypes, os, sys
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
