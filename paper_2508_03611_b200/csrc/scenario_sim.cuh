@@ -382,6 +382,9 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
   const int32_t wait_n = sc.wait_n;
   const bool chunked = cfg.local_policy == BSG_CHUNKED_PREFILL;
   const int32_t maxb = cfg.max_batch_size;
+#ifdef BSG_PROFILE_DRAIN
+  int32_t prof_dr_ok = 0, prof_dr_fail = 0;
+#endif
 #ifdef BSG_PROFILE_ITERS
   int64_t prof_gen = 0, prof_win = 0, prof_adm = 0, prof_pre = 0, prof_prf = 0;
 #endif
@@ -710,6 +713,11 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
             }
           }
           dem = warp_sum_i64(dem);
+#ifdef BSG_PROFILE_DRAIN
+          // debug: drain attempts that pass / fail the demand check (tools/drainprobe.py)
+          if (dem <= free_blocks) prof_dr_ok += 1;
+          else prof_dr_fail += 1;
+#endif
           if (dem <= free_blocks) {
             drained = true;
             T = Td;
@@ -1697,6 +1705,9 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
     }
   }
   res.steps = steps;
+#ifdef BSG_PROFILE_DRAIN
+  res.detail = prof_dr_ok + 1000 * prof_dr_fail;
+#endif
 #ifdef BSG_PROFILE_ITERS
   // debug build only (tools/iterprobe.py): loop iterations by kind
   res.detail = static_cast<int32_t>(prof_gen);
