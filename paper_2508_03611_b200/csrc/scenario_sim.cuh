@@ -713,12 +713,59 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
             }
           }
           dem = warp_sum_i64(dem);
+          bool fits = dem <= free_blocks;
+          // 32-member lists: (r, stored) bitonic-sorted across the lanes, ascending r
+          int32_t key = rk[0], val = stored[0];
+          bool sorted = false;
+          auto sort_members = [&]() {
+#pragma unroll
+            for (int kb = 2; kb <= 32; kb <<= 1) {
+#pragma unroll
+              for (int j = kb >> 1; j > 0; j >>= 1) {
+                const int32_t ko = __shfl_xor_sync(kFull, key, j);
+                const int32_t vo = __shfl_xor_sync(kFull, val, j);
+                const bool keep_min = ((lane & j) == 0) == ((lane & kb) == 0);
+                if (keep_min ? ko < key : ko > key) {
+                  key = ko;
+                  val = vo;
+                }
+              }
+            }
+            sorted = true;
+          };
+          if constexpr (K == 1 && !OPT) {  // (KV-pressure sets: the bound rarely holds, cfg3 +3 %)
+            if (!fits) {
+              // With the releases: step t needs free + R(t) >= Dc(t) (cumulative
+              // demand vs the blocks of members completed before t). R grows only
+              // at completions, so checking t = r_(k) at each distinct r suffices;
+              // there Dc(t) <= (full demand of members sorted up to k) + (members
+              // after k) * ceil((t + 1) / block_size) — one block per block_size
+              // steps at most — and R(t) is the exclusive prefix of releases.
+              int64_t rel = lane < n && rk[0] < Td - 1 ? bnt<POW2>(stored[0] + rk[0] + 1, cfg) : 0;
+              rel = warp_sum_i64(rel);
+              if (dem <= free_blocks + rel) {
+                sort_members();
+                const bool alive = lane < n;
+                const int32_t tk = key < Td - 1 ? key : Td - 1;
+                const int32_t dfull = alive ? bnt<POW2>(val + tk + 1, cfg) - bnt<POW2>(val, cfg) : 0;
+                const int32_t fr = alive && key < Td - 1 ? bnt<POW2>(val + key + 1, cfg) : 0;
+                const uint64_t pk = static_cast<uint32_t>(dfull) | (static_cast<uint64_t>(static_cast<uint32_t>(fr)) << 32);
+                const uint64_t incl = warp_incl_scan_u64(pk);  // halves < 2^31 each: no carry
+                const int64_t P = static_cast<int64_t>(static_cast<uint32_t>(incl));
+                const int64_t R = static_cast<int64_t>(incl >> 32) - fr;
+                const int32_t kprev = __shfl_up_sync(kFull, key, 1);
+                const bool start = alive && (lane == 0 || kprev < key);
+                const int64_t bound = P + static_cast<int64_t>(n - lane - 1) * divt<POW2>(tk + cfg.block_size, cfg);
+                fits = __all_sync(kFull, !start || free_blocks + R >= bound);
+              }
+            }
+          }
 #ifdef BSG_PROFILE_DRAIN
           // debug: drain attempts that pass / fail the demand check (tools/drainprobe.py)
-          if (dem <= free_blocks) prof_dr_ok += 1;
+          if (fits) prof_dr_ok += 1;
           else prof_dr_fail += 1;
 #endif
-          if (dem <= free_blocks) {
+          if (fits) {
             drained = true;
             T = Td;
             int32_t* s_r = smem;
@@ -726,21 +773,7 @@ __device__ void simulate_scenario(const DevCfg& cfg, const int32_t* __restrict__
             int32_t* s_p = smem + 2 * CAP;
             __syncwarp();
             if constexpr (K == 1) {
-              // bitonic sort of (r, stored) across the 32 lanes, ascending r
-              int32_t key = rk[0], val = stored[0];
-#pragma unroll
-              for (int kb = 2; kb <= 32; kb <<= 1) {
-#pragma unroll
-                for (int j = kb >> 1; j > 0; j >>= 1) {
-                  const int32_t ko = __shfl_xor_sync(kFull, key, j);
-                  const int32_t vo = __shfl_xor_sync(kFull, val, j);
-                  const bool keep_min = ((lane & j) == 0) == ((lane & kb) == 0);
-                  if (keep_min ? ko < key : ko > key) {
-                    key = ko;
-                    val = vo;
-                  }
-                }
-              }
+              if (!sorted) sort_members();
               if (lane < n) {
                 s_r[lane] = key;
                 s_s[lane] = val;
