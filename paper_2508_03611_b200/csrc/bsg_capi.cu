@@ -546,7 +546,10 @@ bsg_status launch_predict_t(bsg_ctx* ctx, int32_t cfg_sel, int64_t n, const bsg_
   const DevCfg& cf = ctx->dev_cfgs_host[cfg_sel];
   const int64_t blocks = (n + kPredictWarps - 1) / kPredictWarps;
   const std::string tp = std::string(POW2 ? "true" : "false");
-  const bool queue = !no_queue && n >= BSG_QUEUE_MIN && K > 1;
+#ifndef BSG_QUEUE_K1
+#define BSG_QUEUE_K1 0  // 1: cost order for 32-member sets too (A/B builds)
+#endif
+  const bool queue = !no_queue && n >= BSG_QUEUE_MIN && (K > 1 || BSG_QUEUE_K1);
   if (!queue) {
     ctx->last_launch = "predict_kernel<" + std::to_string(K) + "," + tp + ",false," +
                        std::to_string(BSG_WIN_J_PREDICT) + ">";

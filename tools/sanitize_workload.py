@@ -10,7 +10,7 @@ from paper_2508_03611_b200 import abi, native, sweep
 from scenarios import fuzz_set
 
 ctx = native.Context(0)
-cfgs, ss = fuzz_set(3, 9000)            # > BSG_QUEUE_MIN: heavy-first launch order
+cfgs, ss = fuzz_set(3, 9000)            # > BSG_QUEUE_MIN: cost-ordered queue path for the wide passes
 ctx.set_configs(cfgs)
 ctx.predict_batch(ss)
 ctx.trace(ss, 0, cap=2048)
